@@ -1,0 +1,167 @@
+/* include/dem.h — C-ABI of the B200-native clump-DEM hot path (libdem_b200.so).
+ *
+ * The library advances a system of clumps — rigid unions of overlapping spheres
+ * (Fig. 2 caption P:135) whose spheres each carry their own material
+ * (E, nu, mu, CoR) — by explicit time steps of size h under gravity.
+ * One dem_step = the per-step hot path of PAPER.md Sec. 2 in the "traditional"
+ * per-step-rebuild mode:
+ *   (a1) sphere world poses          c = X + R(q) o
+ *   (a2) broad phase: multi-insert uniform-grid binning by counting sort
+ *   (a3) narrow phase: directed per-sphere contact rows, sorted by partner key
+ *   (a4) tangential-history remap by contact key
+ *   (a5-a8) contact kinematics + Hertz-Mindlin forces, walls     (Eqs. 1a-3c)
+ *   (a9) deterministic per-clump force/torque reduction           (Eq. 4 RHS)
+ *   (a10) semi-implicit Euler of position and orientation         (Eq. 4a-4b)
+ * The exact arithmetic and every reading of the paper is in DESIGN.md §3.
+ *
+ * Conventions
+ *   - SI units, fp64 everywhere.  Quaternions (w,x,y,z), Hamilton product, body->world.
+ *   - Clump velocity V is world-frame, angular velocity Omega is body-frame (principal axes).
+ *   - Keys: sphere key = clump_gid * 64 + component (<= 64 components per template);
+ *     plane key = INT64_MAX - plane_index.  A contact (key_a, key_b) has key_a < key_b; the
+ *     normal n points from a to b, and the reported force is the force ON b (-F acts on a).
+ *     u_t is oriented a->b (it changes sign if a and b are swapped).
+ *   - Pointers: "host" arrays are caller-owned and only read/written during the call; the
+ *     library never keeps a caller pointer.  Device memory is owned by the library and is
+ *     obtained from params.alloc (e.g. the PyTorch caching allocator) or cudaMallocAsync.
+ *   - Streams: all device work runs on the stream passed to dem_create (borrowed; it must
+ *     outlive the system).  One system per host thread at a time; no global state.
+ *   - Errors: argument errors are returned synchronously.  Device-detected errors (sphere out
+ *     of domain, non-finite wrench, coincident centres) are latched in a device status word and
+ *     returned by the next call that synchronises (dem_step returns after its last step has
+ *     been checked); dem_last_error() names the clump/contact key and the step.  Capacity
+ *     overflows (bins, contact rows) are handled internally by regrowing and re-running the
+ *     aborted steps; a contact list is never silently truncated.
+ */
+#ifndef DEM_B200_H
+#define DEM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  DEM_OK = 0,
+  DEM_ERR_INVALID_ARG = -1,
+  DEM_ERR_CUDA = -2,
+  DEM_ERR_OOM = -3,
+  DEM_ERR_NCCL = -4,
+  DEM_ERR_BAD_MATERIAL = -5,      /* E > 0, 0 <= nu < 0.5, mu >= 0, 0 < CoR <= 1   */
+  DEM_ERR_BAD_TEMPLATE = -6,      /* 1..64 comps, r > 0, mass > 0, inertia > 0          */
+  DEM_ERR_OUT_OF_DOMAIN = -10,    /* a sphere centre left [domain_lo, domain_hi]       */
+  DEM_ERR_NONFINITE = -11,        /* non-finite wrench/state                          */
+  DEM_ERR_DEGENERATE_CONTACT = -12, /* coincident sphere centres in a contact         */
+  DEM_ERR_CAPACITY = -14          /* a buffer could not be grown (device memory exhausted)   */
+} dem_status;
+
+/* One sphere material.  Pair parameters of two materials follow DESIGN.md §3 R4:
+ * 1/E* = sum (1-nu^2)/E, 1/G* = sum 2(2-nu)(1+nu)/E, CoR = min, mu = min. */
+typedef struct {
+  double E, nu, mu, cor;
+} dem_material;
+
+/* One clump template: component spheres in the principal body frame with the
+ * COM at the origin; mass and principal inertia of the union are inputs (computed by the
+ * caller, e.g. by voxelisation).  Arrays are read during dem_create only. */
+typedef struct {
+  int32_t n_comp;            /* 1..64 */
+  const double* offset;      /* [3*n_comp] body-frame centres */
+  const double* radius;      /* [n_comp] */
+  const int32_t* material;   /* [n_comp] indices into the material table */
+  double mass;               /* kg */
+  double inertia[3];         /* principal moments, kg m^2 */
+} dem_template;
+
+/* A fixed analytic plane (flat-wall limit: R_bar = r, m_bar = clump mass). */
+typedef struct {
+  double point[3];
+  double normal[3];          /* unit, pointing into the domain */
+  int32_t material;
+} dem_plane;
+
+typedef void* (*dem_alloc_fn)(size_t bytes, void* ctx, void* stream);
+typedef void (*dem_free_fn)(void* ptr, size_t bytes, void* ctx, void* stream);
+
+typedef struct {
+  double h;                  /* time step [s] */
+  double gravity[3];         /* [m/s^2]; tilt it for inclines */
+  double margin;             /* total contact-detection enlargement [m]; 0 for per-step rebuild */
+  int32_t cd_every;          /* steps per contact-set rebuild; must be 1 in this version */
+  double domain_lo[3], domain_hi[3]; /* every sphere centre must stay inside */
+  double cell_size;          /* bin edge [m]; 0 = automatic */
+  int32_t record_contacts;   /* 1: keep per-contact force/point/normal/delta for dem_get_contacts */
+  dem_alloc_fn alloc;        /* NULL: cudaMallocAsync on the system stream */
+  dem_free_fn free;
+  void* alloc_ctx;
+} dem_params;
+
+typedef struct {
+  int64_t steps;             /* steps completed since dem_set_state */
+  int64_t n_clumps, n_spheres;
+  int64_t n_entries;         /* directed contact-row entries of the last step (2 per sphere pair + walls) */
+  int64_t n_contacts;        /* canonical contacts of the last step (sphere pairs + sphere-wall) */
+  int64_t n_inserts;         /* bin inserts of the last step */
+  int64_t n_cells;
+  double cell_size;
+  int64_t regrows;           /* capacity regrows so far */
+  int64_t kernel_launches_per_step;
+} dem_stats;
+
+typedef struct dem_system dem_system;
+
+/* Create a system.  cuda_stream is a cudaStream_t (NULL = legacy default stream). */
+dem_status dem_create(const dem_params* params, const dem_material* materials, int32_t n_mat,
+                      const dem_template* templates, int32_t n_tmpl, const dem_plane* planes,
+                      int32_t n_planes, void* cuda_stream, dem_system** out);
+
+/* Replace the clump state (n clumps; gids unique, >= 0, < 2^56).  pos/vel/omega are [3n],
+ * quat [4n] (normalised by the caller), all row-major (x,y,z per clump).  on_device = 1 means
+ * the pointers are device pointers.  Clears the tangential history. */
+dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* clump_gid, const int32_t* template_id,
+                         const double* pos, const double* quat, const double* vel, const double* omega,
+                         int32_t on_device);
+
+/* Replace the tangential history carried into the next step (host arrays; u_t [3n], oriented
+ * key_a -> key_b, key_a < key_b).  Keys whose spheres are not in the system are ignored. */
+dem_status dem_set_contact_history(dem_system* sys, int64_t n, const int64_t* key_a, const int64_t* key_b,
+                                   const double* u_t);
+
+/* Advance n_steps steps on the system stream (CUDA-graph launches).  Returns after checking the
+ * device status word once at the end (one stream synchronisation per call). */
+dem_status dem_step(dem_system* sys, int64_t n_steps);
+
+dem_status dem_synchronize(dem_system* sys);
+
+/* Copy the state out in the order of the last dem_set_state.  cap = capacity in clumps; *n
+ * receives the clump count.  Any output pointer may be NULL.  on_device as in dem_set_state. */
+dem_status dem_get_state(dem_system* sys, int64_t cap, int64_t* n, int64_t* clump_gid, int32_t* template_id,
+                         double* pos, double* quat, double* vel, double* omega, int32_t on_device);
+
+/* Canonical contact list of the last step (built from the state at that step's start), sorted by
+ * (key_a, key_b): force on b, contact point, normal a->b, u_t after the step, penetration delta.
+ * Force/point/normal/delta need params.record_contacts = 1 (else DEM_ERR_INVALID_ARG if requested).
+ * Call with cap = 0 to query *n. */
+dem_status dem_get_contacts(dem_system* sys, int64_t cap, int64_t* n, int64_t* key_a, int64_t* key_b,
+                            double* force_on_b, double* point, double* normal, double* u_t, double* delta);
+
+dem_status dem_get_stats(dem_system* sys, dem_stats* out);
+
+/* Stage profiling.  With enable = 1, dem_step launches the step kernels directly (no graph) with
+ * CUDA events between the stages on the system stream and accumulates each stage's device time;
+ * enable resets the accumulators.  dem_get_stage_times returns the mean ms per step of each stage,
+ * in the order: pose+bin-count, bin-offset scan, bin scatter, narrow count, row-offset scan,
+ * narrow fill + row sort, force (remap + contact forces + per-sphere sums), reduce + integrate. */
+dem_status dem_set_profiling(dem_system* sys, int32_t enable);
+dem_status dem_get_stage_times(dem_system* sys, int32_t n_stages, double* ms);
+
+const char* dem_status_string(dem_status s);
+dem_status dem_last_error(const dem_system* sys, char* buf, size_t len);
+void dem_destroy(dem_system* sys);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DEM_B200_H */

@@ -58,6 +58,7 @@ struct orc_sys {
   int32_t* s_comp;
   int64_t* s_key;
   double* s_pos;
+  double* s_rad;
   /* history and last contacts */
   int64_t nh;
   hist_rec* hist;
@@ -241,7 +242,8 @@ orc_sys* orc_create(double h, const double gravity[3], double margin, const doub
 static void free_state(orc_sys* s) {
   free(s->gid); free(s->tid); free(s->X); free(s->Q); free(s->V); free(s->W);
   free(s->Fc); free(s->Tc);
-  free(s->s_clump); free(s->s_comp); free(s->s_key); free(s->s_pos);
+  free(s->s_clump); free(s->s_comp); free(s->s_key); free(s->s_pos); free(s->s_rad);
+  s->s_rad = NULL;
   s->gid = NULL; s->tid = NULL; s->X = s->Q = s->V = s->W = s->Fc = s->Tc = NULL;
   s->s_clump = NULL; s->s_comp = NULL; s->s_key = NULL; s->s_pos = NULL;
 }
@@ -287,6 +289,7 @@ int orc_set_state(orc_sys* s, int64_t n, const int64_t* gid, const int32_t* tid,
   s->s_comp = (int32_t*)xcalloc(ns, sizeof(int32_t));
   s->s_key = (int64_t*)xcalloc(ns, sizeof(int64_t));
   s->s_pos = (double*)xcalloc(3 * ns, sizeof(double));
+  s->s_rad = (double*)xcalloc(ns, sizeof(double));
   int64_t k = 0;
   for (c = 0; c < n; ++c) {
     int j;
@@ -294,6 +297,7 @@ int orc_set_state(orc_sys* s, int64_t n, const int64_t* gid, const int32_t* tid,
       s->s_clump[k] = c;
       s->s_comp[k] = j;
       s->s_key[k] = gid[c] * KEY_STRIDE + j;
+      s->s_rad[k] = s->rad[s->coff[tid[c]] + j];
       ++k;
     }
   }
@@ -363,15 +367,13 @@ static int sphere_pair_candidate(const orc_sys* s, int64_t a, int64_t b) {
   const double* ca = s->s_pos + 3 * a;
   const double* cb = s->s_pos + 3 * b;
   double dx = cb[0] - ca[0], dy = cb[1] - ca[1], dz = cb[2] - ca[2];
-  double ra = s->rad[s->coff[s->tid[s->s_clump[a]]] + s->s_comp[a]];
-  double rb = s->rad[s->coff[s->tid[s->s_clump[b]]] + s->s_comp[b]];
+  double ra = s->s_rad[a];
+  double rb = s->s_rad[b];
   double sum = (ra + rb) + s->margin;
   return dx * dx + dy * dy + dz * dz <= sum * sum;
 }
 
-static double sphere_radius(const orc_sys* s, int64_t a) {
-  return s->rad[s->coff[s->tid[s->s_clump[a]]] + s->s_comp[a]];
-}
+static double sphere_radius(const orc_sys* s, int64_t a) { return s->s_rad[a]; }
 
 static void detect_brute(orc_sys* s) {
   int64_t a, b;
@@ -380,15 +382,19 @@ static void detect_brute(orc_sys* s) {
       if (s->s_clump[a] != s->s_clump[b] && sphere_pair_candidate(s, a, b)) push_contact(s, a, b);
 }
 
-/* simple uniform grid: cell >= 2 r_max + margin, spheres binned by centre, 27-cell stencil */
+/* simple uniform grid: spheres binned by centre into cells of side 2 r_min + margin.  Each
+ * unordered pair is tested once, from its larger sphere (ties: lower index), so sphere a scans
+ * the cells within its reach 2 r_a + margin (>= r_a + r_b + margin for every r_b <= r_a), with
+ * the same predicate as the brute force. */
 static void detect_grid(orc_sys* s) {
-  double rmax = 0.0, lo[3], hi[3];
+  double rmin = INFINITY, lo[3], hi[3];
   int64_t a;
   int d, t;
-  for (t = 0; t < s->coff[s->n_tmpl]; ++t)
-    if (s->rad[t] > rmax) rmax = s->rad[t];
-  double cell = 2.0 * rmax + s->margin;
-  cell *= 1.0 + 1e-9;
+  for (t = 0; t < s->coff[s->n_tmpl]; ++t) {
+
+    if (s->rad[t] < rmin) rmin = s->rad[t];
+  }
+  double cell = (2.0 * rmin + s->margin) * (1.0 + 1e-6);
   for (d = 0; d < 3; ++d) {
     lo[d] = INFINITY;
     hi[d] = -INFINITY;
@@ -421,16 +427,21 @@ static void detect_grid(orc_sys* s) {
   for (a = 0; a < s->ns; ++a) items[cstart[cidx[a]] + fill[cidx[a]]++] = a;
   for (a = 0; a < s->ns; ++a) {
     int64_t x, y, z;
-    for (z = cc[3 * a + 2] - 1; z <= cc[3 * a + 2] + 1; ++z) {
+    /* |floor(u) - floor(v)| <= ceil(|u - v|): bins within ceil(reach / cell) hold every partner
+     * (the 1e-9 relative slack covers the rounding of the bin coordinates) */
+    double ra = s->s_rad[a];
+    int64_t reach = (int64_t)ceil((2.0 * ra + s->margin) * (1.0 + 1e-9) / cell);
+    for (z = cc[3 * a + 2] - reach; z <= cc[3 * a + 2] + reach; ++z) {
       if (z < 0 || z >= dim[2]) continue;
-      for (y = cc[3 * a + 1] - 1; y <= cc[3 * a + 1] + 1; ++y) {
+      for (y = cc[3 * a + 1] - reach; y <= cc[3 * a + 1] + reach; ++y) {
         if (y < 0 || y >= dim[1]) continue;
-        for (x = cc[3 * a] - 1; x <= cc[3 * a] + 1; ++x) {
+        for (x = cc[3 * a] - reach; x <= cc[3 * a] + reach; ++x) {
           if (x < 0 || x >= dim[0]) continue;
           int64_t cid = (z * dim[1] + y) * dim[0] + x, k;
           for (k = cstart[cid]; k < cstart[cid + 1]; ++k) {
             int64_t b = items[k];
-            if (b <= a) continue;
+            double rb = s->s_rad[b];
+            if (rb > ra || (rb == ra && b <= a)) continue;
             if (s->s_clump[a] != s->s_clump[b] && sphere_pair_candidate(s, a, b)) push_contact(s, a, b);
           }
         }

@@ -1,0 +1,7 @@
+"""B200-native clump-DEM hot path (arXiv 2307.03445): CUDA library + thin ctypes binding.
+
+The product is `libdem_b200.so` (hand-written sm_100a CUDA behind the C-ABI in
+include/dem.h); `binding` marshals arguments and provides PyTorch's allocator and stream.
+"""
+from .binding import (DEM_STATUS, EXPORTS, LIB_PATH, STAGES, DemError, System, load_library,  # noqa: F401
+                      system_from_scene)

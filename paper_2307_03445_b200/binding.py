@@ -1,0 +1,272 @@
+"""Thin ctypes binding of libdem_b200.so (include/dem.h) — argument marshalling only.
+
+Every step of the hot path runs in the CUDA library; this module converts numpy arrays
+to the C structs, hands the library PyTorch's caching allocator and current CUDA stream
+(PyTorch is plumbing here: device memory and streams), and raises on error statuses.
+There is no CPU fallback: importing this module on a machine without the built library,
+or creating a system without a CUDA device, raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdem_b200.so")
+
+DEM_STATUS = {0: "ok", -1: "invalid argument", -2: "CUDA error", -3: "out of device memory", -4: "NCCL error",
+              -5: "bad material", -6: "bad template", -10: "sphere out of domain", -11: "non-finite wrench",
+              -12: "degenerate contact", -14: "capacity"}
+
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+
+
+class dem_material(C.Structure):
+    _fields_ = [("E", C.c_double), ("nu", C.c_double), ("mu", C.c_double), ("cor", C.c_double)]
+
+
+class dem_template(C.Structure):
+    _fields_ = [("n_comp", C.c_int32), ("offset", C.POINTER(C.c_double)), ("radius", C.POINTER(C.c_double)),
+                ("material", C.POINTER(C.c_int32)), ("mass", C.c_double), ("inertia", C.c_double * 3)]
+
+
+class dem_plane(C.Structure):
+    _fields_ = [("point", C.c_double * 3), ("normal", C.c_double * 3), ("material", C.c_int32)]
+
+
+class dem_params(C.Structure):
+    _fields_ = [("h", C.c_double), ("gravity", C.c_double * 3), ("margin", C.c_double), ("cd_every", C.c_int32),
+                ("domain_lo", C.c_double * 3), ("domain_hi", C.c_double * 3), ("cell_size", C.c_double),
+                ("record_contacts", C.c_int32), ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_ctx", C.c_void_p)]
+
+
+class dem_stats(C.Structure):
+    _fields_ = [("steps", C.c_int64), ("n_clumps", C.c_int64), ("n_spheres", C.c_int64), ("n_entries", C.c_int64),
+                ("n_contacts", C.c_int64), ("n_inserts", C.c_int64), ("n_cells", C.c_int64),
+                ("cell_size", C.c_double), ("regrows", C.c_int64), ("kernel_launches_per_step", C.c_int64)]
+
+
+EXPORTS = ["dem_create", "dem_set_state", "dem_set_contact_history", "dem_step", "dem_synchronize",
+           "dem_get_state", "dem_get_contacts", "dem_get_stats", "dem_set_profiling", "dem_get_stage_times",
+           "dem_status_string", "dem_last_error", "dem_destroy"]
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libdem_b200.so (raises if it was not built — there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = C.CDLL(path)
+    P, I64, I32 = C.c_void_p, C.c_int64, C.c_int32
+    L.dem_create.argtypes = [C.POINTER(dem_params), P, I32, P, I32, P, I32, P, C.POINTER(P)]
+    L.dem_set_state.argtypes = [P, I64, P, P, P, P, P, P, I32]
+    L.dem_set_contact_history.argtypes = [P, I64, P, P, P]
+    L.dem_step.argtypes = [P, I64]
+    L.dem_synchronize.argtypes = [P]
+    L.dem_get_state.argtypes = [P, I64, C.POINTER(I64), P, P, P, P, P, P, I32]
+    L.dem_get_contacts.argtypes = [P, I64, C.POINTER(I64), P, P, P, P, P, P, P]
+    L.dem_get_stats.argtypes = [P, C.POINTER(dem_stats)]
+    L.dem_set_profiling.argtypes = [P, I32]
+    L.dem_get_stage_times.argtypes = [P, I32, P]
+    L.dem_status_string.restype = C.c_char_p
+    L.dem_status_string.argtypes = [C.c_int]
+    L.dem_last_error.argtypes = [P, C.c_char_p, C.c_size_t]
+    L.dem_destroy.argtypes = [P]
+    L.dem_destroy.restype = None
+    for f in EXPORTS:
+        if f not in ("dem_destroy", "dem_status_string"):
+            getattr(L, f).restype = C.c_int
+    _lib = L
+    return L
+
+
+class DemError(RuntimeError):
+    def __init__(self, status, msg=""):
+        super().__init__(f"{DEM_STATUS.get(status, status)} ({status}): {msg}")
+        self.status = status
+
+
+def _ptr(a):
+    return C.c_void_p(a.ctypes.data) if a is not None and a.size else None
+
+
+def _f64(a, shape=None):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a if shape is None else a.reshape(shape)
+
+
+STAGES = ["pose+bin_count", "bin_scan", "bin_scatter", "narrow_count", "row_scan", "narrow_fill", "force",
+          "integrate"]
+
+
+class System:
+    """One dem_system on the current CUDA device and PyTorch's current stream."""
+
+    def __init__(self, materials, templates, planes=(), *, h, gravity=(0.0, 0.0, -9.81), domain_lo, domain_hi,
+                 margin=0.0, cell_size=0.0, record_contacts=False, use_torch_allocator=True, stream=None):
+        import torch  # plumbing only: device memory and streams
+
+        if not torch.cuda.is_available():
+            raise DemError(-2, "no CUDA device: the DEM hot path runs only on the GPU")
+        L = load_library()
+        self._torch = torch
+        self.device = torch.cuda.current_device()
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        mats = (dem_material * len(materials))(*[dem_material(*map(float, m)) for m in materials])
+        self._keep = []
+        tpls = (dem_template * len(templates))()
+        for k, t in enumerate(templates):
+            off, rad, mat = _f64(t["offsets"]).reshape(-1), _f64(t["radius"]), np.ascontiguousarray(t["material"],
+                                                                                                    np.int32)
+            self._keep += [off, rad, mat]
+            tpls[k].n_comp = rad.shape[0]
+            tpls[k].offset = off.ctypes.data_as(C.POINTER(C.c_double))
+            tpls[k].radius = rad.ctypes.data_as(C.POINTER(C.c_double))
+            tpls[k].material = mat.ctypes.data_as(C.POINTER(C.c_int32))
+            tpls[k].mass = float(t["mass"])
+            tpls[k].inertia[:] = [float(x) for x in t["inertia"]]
+        pls = (dem_plane * max(1, len(planes)))()
+        for k, (pt, nrm, m) in enumerate(planes):
+            pls[k].point[:] = [float(x) for x in pt]
+            pls[k].normal[:] = [float(x) for x in nrm]
+            pls[k].material = int(m)
+        p = dem_params()
+        p.h = h
+        p.gravity[:] = [float(x) for x in gravity]
+        p.margin = margin
+        p.cd_every = 1
+        p.domain_lo[:] = [float(x) for x in domain_lo]
+        p.domain_hi[:] = [float(x) for x in domain_hi]
+        p.cell_size = cell_size
+        p.record_contacts = 1 if record_contacts else 0
+        if use_torch_allocator:
+            dev = self.device
+
+            def _alloc(nbytes, ctx, stream):
+                return torch.cuda.caching_allocator_alloc(int(nbytes), dev, stream or 0)
+
+            def _free(ptr, nbytes, ctx, stream):
+                torch.cuda.caching_allocator_delete(ptr)
+
+            self._alloc_cb, self._free_cb = ALLOC_FN(_alloc), FREE_FN(_free)
+            p.alloc, p.free = self._alloc_cb, self._free_cb
+        self.record = record_contacts
+        self.sys = C.c_void_p()
+        rc = L.dem_create(C.byref(p), mats, len(materials), tpls, len(templates), pls, len(planes),
+                          C.c_void_p(self.stream.cuda_stream), C.byref(self.sys))
+        if rc:
+            raise DemError(rc, "dem_create")
+        self.n = 0
+
+    # ------------------------------------------------------------------ plumbing
+    def _check(self, rc, what=""):
+        if rc:
+            buf = C.create_string_buffer(512)
+            load_library().dem_last_error(self.sys, buf, 512)
+            raise DemError(rc, f"{what}: {buf.value.decode()}")
+
+    def close(self):
+        if getattr(self, "sys", None):
+            load_library().dem_destroy(self.sys)
+            self.sys = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------ C-ABI calls
+    def dem_set_state(self, gid, tid, pos, quat, vel, omega):
+        """Host numpy arrays (row-major).  For device tensors use `dem_set_state_device`."""
+        gid = np.ascontiguousarray(gid, np.int64)
+        tid = np.ascontiguousarray(tid, np.int32)
+        arr = [_f64(pos), _f64(quat), _f64(vel), _f64(omega)]
+        self.n = gid.shape[0]
+        self._check(load_library().dem_set_state(self.sys, self.n, _ptr(gid), _ptr(tid), *[_ptr(a) for a in arr], 0),
+                    "dem_set_state")
+
+    def dem_set_state_device(self, gid, tid, pos, quat, vel, omega):
+        """torch CUDA tensors (int64, int32, float64 x4), contiguous."""
+        ts = [gid, tid, pos, quat, vel, omega]
+        self.n = gid.shape[0]
+        self._check(load_library().dem_set_state(self.sys, self.n, *[C.c_void_p(t.data_ptr()) for t in ts], 1),
+                    "dem_set_state")
+
+    def dem_set_contact_history(self, key_a, key_b, u_t):
+        ka, kb = np.ascontiguousarray(key_a, np.int64), np.ascontiguousarray(key_b, np.int64)
+        ut = _f64(u_t)
+        self._check(load_library().dem_set_contact_history(self.sys, ka.shape[0], _ptr(ka), _ptr(kb), _ptr(ut)),
+                    "dem_set_contact_history")
+
+    def dem_step(self, n_steps=1):
+        self._check(load_library().dem_step(self.sys, int(n_steps)), "dem_step")
+
+    def dem_synchronize(self):
+        self._check(load_library().dem_synchronize(self.sys), "dem_synchronize")
+
+    def dem_get_state(self):
+        n = self.n
+        out = dict(gid=np.zeros(n, np.int64), tid=np.zeros(n, np.int32), pos=np.zeros((n, 3)), quat=np.zeros((n, 4)),
+                   vel=np.zeros((n, 3)), omega=np.zeros((n, 3)))
+        nn = C.c_int64()
+        self._check(load_library().dem_get_state(self.sys, n, C.byref(nn), *[_ptr(out[k]) for k in
+                                                                            ("gid", "tid", "pos", "quat", "vel",
+                                                                             "omega")], 0), "dem_get_state")
+        return out
+
+    def dem_get_state_device(self, out):
+        """Copy into torch CUDA tensors: dict with gid, tid, pos, quat, vel, omega."""
+        nn = C.c_int64()
+        ks = ("gid", "tid", "pos", "quat", "vel", "omega")
+        self._check(load_library().dem_get_state(self.sys, self.n, C.byref(nn),
+                                                 *[C.c_void_p(out[k].data_ptr()) for k in ks], 1), "dem_get_state")
+        return out
+
+    def dem_get_contacts(self, full=None):
+        full = self.record if full is None else full
+        L = load_library()
+        nn = C.c_int64()
+        self._check(L.dem_get_contacts(self.sys, 0, C.byref(nn), None, None, None, None, None, None, None),
+                    "dem_get_contacts")
+        m = nn.value
+        out = dict(key_a=np.zeros(m, np.int64), key_b=np.zeros(m, np.int64), u_t=np.zeros((m, 3)))
+        if full:
+            out.update(force_b=np.zeros((m, 3)), point=np.zeros((m, 3)), normal=np.zeros((m, 3)), delta=np.zeros(m))
+        g = lambda k: _ptr(out[k]) if k in out else None  # noqa: E731
+        if m:
+            self._check(L.dem_get_contacts(self.sys, m, C.byref(nn), g("key_a"), g("key_b"), g("force_b"),
+                                           g("point"), g("normal"), g("u_t"), g("delta")), "dem_get_contacts")
+        return out
+
+    def dem_get_stats(self):
+        st = dem_stats()
+        self._check(load_library().dem_get_stats(self.sys, C.byref(st)), "dem_get_stats")
+        return {k: getattr(st, k) for k, _ in dem_stats._fields_}
+
+    def dem_set_profiling(self, enable=True):
+        self._check(load_library().dem_set_profiling(self.sys, 1 if enable else 0), "dem_set_profiling")
+
+    def dem_get_stage_times(self):
+        ms = np.zeros(len(STAGES))
+        self._check(load_library().dem_get_stage_times(self.sys, len(STAGES), _ptr(ms)), "dem_get_stage_times")
+        return dict(zip(STAGES, ms.tolist()))
+
+
+def system_from_scene(scene, record_contacts=False, cell_size=None, margin=None, **kw) -> System:
+    """Build a System from a workloads.Scene-like object (duck-typed; no import of workloads)."""
+    templates = [dict(offsets=t.offsets, radius=t.radius, material=t.material, mass=t.mass, inertia=t.inertia)
+                 for t in scene.templates]
+    planes = [(p.point, p.normal, p.material) for p in scene.planes]
+    s = System(scene.materials, templates, planes, h=scene.h, gravity=scene.gravity, domain_lo=scene.domain_lo,
+               domain_hi=scene.domain_hi, margin=scene.margin if margin is None else margin,
+               cell_size=scene.cell_size if cell_size is None else cell_size, record_contacts=record_contacts, **kw)
+    s.dem_set_state(scene.gid, scene.tid, scene.pos, scene.quat, scene.vel, scene.omega)
+    return s

@@ -1,0 +1,173 @@
+// dem_device.cuh — device data layout and helpers of the B200 clump-DEM hot path.
+//
+// Product code (libdem_b200.so).  Independent of oracle/: nothing here is shared with
+// or derived from the CPU checker; the formulas are restated from PAPER.md Sec. 2.1
+// and DESIGN.md §3.
+//
+// HBM layout:
+//   clump state   SoA fp64, 13 arrays (x,y,z, qw,qx,qy,qz, vx,vy,vz, wx,wy,wz), ping-pong
+//   clump aux     tid (i32), gid (i64), sphere offset (i32, n+1), omega_world (3 x fp64, per step)
+//   sphere        clump (i32), template-component (i32), key (i64), centre (3 x fp64 SoA),
+//                 partial force/torque (3+3 fp64 SoA)
+//   bins          cell_count (i32, ncell), cell_start (i32, ncell+1), items (i32, n_inserts)
+//   rows (x2)     CSR by own sphere: row_ptr (i32, ns+1), partner (i32), key (i64), u_t (3 fp64 AoS)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace dem {
+
+constexpr int kKeyStride = 64;
+constexpr int kMaxPlanes = 16;
+constexpr int kMaxRowSort = 64;  // rows longer than this are sorted in place in global memory
+
+// device status word (host reads it after each dem_step)
+struct Ctl {
+  int abort;          // set on capacity overflow or error: later kernels become no-ops
+  int err_code;       // first device error (dem_status value), 0 = none
+  long long err_key;  // sphere key / clump gid / contact key naming the error
+  long long err_key2;
+  long long err_step;
+  long long step;     // steps completed since dem_set_state
+  long long need_inserts;
+  long long need_entries;
+};
+
+struct Tables {
+  const double* tc_off;   // [3 * n_tc] body-frame offsets, AoS
+  const double* tc_rad;   // [n_tc]
+  const int* tc_mat;      // [n_tc]
+  const int* tpl_coff;    // [n_tmpl]
+  const double* tpl_mass;
+  const double* tpl_inertia;  // [3 * n_tmpl]
+  const double* pair;     // [n_mat * n_mat * 4]: E*, G*, beta, mu (symmetric)
+  int n_mat;
+  int n_planes;
+  double plane_pt[kMaxPlanes][3];
+  double plane_n[kMaxPlanes][3];
+  int plane_mat[kMaxPlanes];
+};
+
+struct State {
+  double *x, *y, *z, *qw, *qx, *qy, *qz, *vx, *vy, *vz, *wx, *wy, *wz;
+};
+
+struct Grid {
+  double lo[3];
+  double inv_cell;
+  double cell;
+  double dom_lo[3], dom_hi[3];
+  int n[3];
+  double pad;  // r + pad is the half-extent of a sphere's bin AABB (margin/2 + eps)
+};
+
+struct Rows {
+  int* row_ptr;     // [ns + 1]
+  int* partner;     // [cap] local sphere index, or -1 - plane
+  long long* key;   // [cap] partner key
+  double* ut;       // [3 * cap] AoS, oriented own -> partner
+};
+
+struct Record {
+  double* F;        // [3 * cap] force on partner (own = i)
+  double* p;        // [3 * cap]
+  double* n;        // [3 * cap]
+  double* delta;    // [cap]
+};
+
+struct StepArgs {
+  // sizes
+  int n;            // clumps
+  int ns;           // spheres
+  long long ncell;
+  long long cap_inserts;
+  long long cap_entries;
+  double h;
+  double g[3];
+  double margin;
+  Tables tab;
+  Grid grid;
+  State cur, nxt;
+  const int* tid;
+  const long long* gid;
+  const int* sph_off;
+  double *wwx, *wwy, *wwz;   // omega_world of cur
+  const int* s_clump;
+  const int* s_tc;
+  const long long* s_key;
+  double *sx, *sy, *sz;      // sphere centres
+  double *sfx, *sfy, *sfz, *stx, *sty, *stz;  // per-sphere force / torque (world, about COM)
+  int* cell_count;
+  int* cell_start;
+  int* items;
+  int* row_cnt;
+  Rows rows, prev;
+  Record rec;
+  int record;
+  Ctl* ctl;
+};
+
+// ---------------------------------------------------------------- error latch
+__device__ __forceinline__ void raise_error(Ctl* ctl, int code, long long key, long long key2) {
+  if (atomicCAS(&ctl->err_code, 0, code) == 0) {
+    ctl->err_key = key;
+    ctl->err_key2 = key2;
+    ctl->err_step = ctl->step;
+  }
+  atomicExch(&ctl->abort, 1);
+}
+
+// ---------------------------------------------------------------- exact-rounding helpers
+// Sphere centres and the candidate predicate are evaluated with explicitly rounded
+// operations (no FMA contraction) in the order written in DESIGN.md §3 R14/R22, so the
+// contact set is a function of the fp64 state alone.
+__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+
+// R(q) for q = (w,x,y,z), Hamilton, body -> world; row-major R[0..8]
+__device__ __forceinline__ void quat_R(double w, double x, double y, double z, double R[9]) {
+  double xx = mul(x, x), yy = mul(y, y), zz = mul(z, z);
+  double xy = mul(x, y), xz = mul(x, z), yz = mul(y, z);
+  double wx = mul(w, x), wy = mul(w, y), wz = mul(w, z);
+  R[0] = sub(1.0, mul(2.0, add(yy, zz)));
+  R[1] = mul(2.0, sub(xy, wz));
+  R[2] = mul(2.0, add(xz, wy));
+  R[3] = mul(2.0, add(xy, wz));
+  R[4] = sub(1.0, mul(2.0, add(xx, zz)));
+  R[5] = mul(2.0, sub(yz, wx));
+  R[6] = mul(2.0, sub(xz, wy));
+  R[7] = mul(2.0, add(yz, wx));
+  R[8] = sub(1.0, mul(2.0, add(xx, yy)));
+}
+
+// (R v)_row = (R0 v0 + R1 v1) + R2 v2, each product rounded
+__device__ __forceinline__ double row_dot(const double* R, double a, double b, double c) {
+  return add(add(mul(R[0], a), mul(R[1], b)), mul(R[2], c));
+}
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// bin-index range of the sphere's enlarged AABB along one axis (clamped to the grid)
+__device__ __forceinline__ void cell_range(const Grid& g, int d, double c, double r, int& lo, int& hi) {
+  double e = r + g.pad;
+  lo = clampi(__double2int_rd((c - e - g.lo[d]) * g.inv_cell), 0, g.n[d] - 1);
+  hi = clampi(__double2int_rd((c + e - g.lo[d]) * g.inv_cell), 0, g.n[d] - 1);
+}
+
+__device__ __forceinline__ int cell_lo(const Grid& g, int d, double c, double r) {
+  double e = r + g.pad;
+  return clampi(__double2int_rd((c - e - g.lo[d]) * g.inv_cell), 0, g.n[d] - 1);
+}
+
+// velocity of a body point: V + omega x r, written with explicit roundings so the
+// own-side and partner-side evaluations of one contact are bitwise mirror images
+__device__ __forceinline__ void point_velocity(double Vx, double Vy, double Vz, double wx, double wy,
+                                               double wz, double rx, double ry, double rz, double& ox,
+                                               double& oy, double& oz) {
+  ox = __dadd_rn(Vx, __fma_rn(wy, rz, -__dmul_rn(wz, ry)));
+  oy = __dadd_rn(Vy, __fma_rn(wz, rx, -__dmul_rn(wx, rz)));
+  oz = __dadd_rn(Vz, __fma_rn(wx, ry, -__dmul_rn(wy, rx)));
+}
+
+}  // namespace dem

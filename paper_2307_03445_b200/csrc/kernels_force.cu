@@ -1,0 +1,254 @@
+// kernels_force.cu — (a4) history remap, (a5-a8) contact forces, (a9) reduction, (a10) integration.
+//
+// PAPER.md Sec. 2.1: Eq. 1a-1e, Eq. 2a-2c, Eq. 3a-3c,
+// Eq. 4a-4b.  Readings: R1 force on j with n from i to j;
+// R2/R3 Hertz coefficients S_n = 2E*sqrt(R d), k_n = 2/3 S_n, c_n = 2 sqrt(5/6) beta
+// sqrt(S_n m), k_t = 8 G* sqrt(R d), c_t = 2 sqrt(5/6) beta sqrt(k_t m); R5 m from clump
+// masses, R from sphere radii; R6 contact point = middle of the overlap; R7 Eq. 3c literal;
+// R8 no tension clamp; R9 u_t = 0 once delta <= 0; R11 torque r x (F_n + F_t) with the
+// gyroscopic term; R12 semi-implicit Euler + exponential-map quaternion update.
+//
+// Directed "pull" rows: every sphere evaluates each of its contacts with itself as body i
+// and writes only its own partial wrench.  The two evaluations of one sphere pair are
+// bitwise mirror images (every operation is sign-symmetric under i <-> j and the
+// asymmetric point velocities use explicit roundings), so Newton's third law holds
+// exactly without atomics, and sums run in a canonical order (partner key, then
+// component) independent of storage order.
+#include "dem_device.cuh"
+
+namespace dem {
+
+__global__ void __launch_bounds__(128) k_force(StepArgs a) {
+  if (a.ctl->abort) return;
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.ns) return;
+  const int ci = a.s_clump[i];
+  const int tci = a.s_tc[i];
+  const double cx = a.sx[i], cy = a.sy[i], cz = a.sz[i];
+  const double ri = a.tab.tc_rad[tci];
+  const int mi = a.tab.tc_mat[tci];
+  const double Xx = a.cur.x[ci], Xy = a.cur.y[ci], Xz = a.cur.z[ci];
+  const double Vx = a.cur.vx[ci], Vy = a.cur.vy[ci], Vz = a.cur.vz[ci];
+  const double Wx = a.wwx[ci], Wy = a.wwy[ci], Wz = a.wwz[ci];
+  const double Mi = a.tab.tpl_mass[a.tid[ci]];
+  const double h = a.h;
+  const double k56 = 2.0 * sqrt(5.0 / 6.0);
+
+  const int beg = a.rows.row_ptr[i], end = a.rows.row_ptr[i + 1];
+  int pj = a.prev.row_ptr[i];
+  const int pend = a.prev.row_ptr[i + 1];
+
+  double fsx = 0.0, fsy = 0.0, fsz = 0.0, tsx = 0.0, tsy = 0.0, tsz = 0.0;
+  for (int e = beg; e < end; ++e) {
+    const long long key = a.rows.key[e];
+    const int t = a.rows.partner[e];
+    // (a4) history remap: both rows are sorted by partner key
+    while (pj < pend && a.prev.key[pj] < key) ++pj;
+    double ux = 0.0, uy = 0.0, uz = 0.0;
+    if (pj < pend && a.prev.key[pj] == key) {
+      ux = a.prev.ut[3 * pj];
+      uy = a.prev.ut[3 * pj + 1];
+      uz = a.prev.ut[3 * pj + 2];
+    }
+    // (a5) geometry: n from i (own) to j (partner)
+    double nx, ny, nz, px, py, pz, delta, rbar, mbar;
+    double Xjx = 0, Xjy = 0, Xjz = 0, Vjx = 0, Vjy = 0, Vjz = 0, Wjx = 0, Wjy = 0, Wjz = 0;
+    int mj;
+    bool wall = t < 0;
+    if (!wall) {
+      const int cj = a.s_clump[t];
+      const int tcj = a.s_tc[t];
+      const double rj = a.tab.tc_rad[tcj];
+      mj = a.tab.tc_mat[tcj];
+      const double dx = a.sx[t] - cx, dy = a.sy[t] - cy, dz = a.sz[t] - cz;
+      const double dist = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+      if (dist == 0.0) {
+        raise_error(a.ctl, -12, a.s_key[i], key);
+        return;
+      }
+      delta = (ri + rj) - dist;
+      nx = dx / dist;
+      ny = dy / dist;
+      nz = dz / dist;
+      const double hr = 0.5 * (ri - rj);
+      px = __fma_rn(hr, nx, 0.5 * (cx + a.sx[t]));
+      py = __fma_rn(hr, ny, 0.5 * (cy + a.sy[t]));
+      pz = __fma_rn(hr, nz, 0.5 * (cz + a.sz[t]));
+      rbar = (ri * rj) / (ri + rj);
+      const double Mj = a.tab.tpl_mass[a.tid[cj]];
+      mbar = (Mi * Mj) / (Mi + Mj);
+      Xjx = a.cur.x[cj]; Xjy = a.cur.y[cj]; Xjz = a.cur.z[cj];
+      Vjx = a.cur.vx[cj]; Vjy = a.cur.vy[cj]; Vjz = a.cur.vz[cj];
+      Wjx = a.wwx[cj]; Wjy = a.wwy[cj]; Wjz = a.wwz[cj];
+    } else {
+      const int pl = -1 - t;
+      const double* pp = a.tab.plane_pt[pl];
+      const double* nw = a.tab.plane_n[pl];
+      const double dd = (cx - pp[0]) * nw[0] + (cy - pp[1]) * nw[1] + (cz - pp[2]) * nw[2];
+      delta = ri - dd;
+      nx = -nw[0];
+      ny = -nw[1];
+      nz = -nw[2];
+      const double arm = ri - 0.5 * delta;
+      px = cx + arm * nx;
+      py = cy + arm * ny;
+      pz = cz + arm * nz;
+      rbar = ri;
+      mbar = Mi;
+      mj = a.tab.plane_mat[pl];
+    }
+    double Fx = 0.0, Fy = 0.0, Fz = 0.0, nux = 0.0, nuy = 0.0, nuz = 0.0;
+    const double rix = px - Xx, riy = py - Xy, riz = pz - Xz;
+    if (delta > 0.0) {
+      // contact-point velocities (Eq. 2a)
+      double vix, viy, viz, vjx = 0.0, vjy = 0.0, vjz = 0.0;
+      point_velocity(Vx, Vy, Vz, Wx, Wy, Wz, rix, riy, riz, vix, viy, viz);
+      if (!wall) point_velocity(Vjx, Vjy, Vjz, Wjx, Wjy, Wjz, px - Xjx, py - Xjy, pz - Xjz, vjx, vjy, vjz);
+      const double vrx = vjx - vix, vry = vjy - viy, vrz = vjz - viz;
+      const double* pr = a.tab.pair + 4 * (mi * a.tab.n_mat + mj);
+      const double estar = pr[0], gstar = pr[1], beta = pr[2], mu = pr[3];
+      // (a6) normal force, Eq. 1a
+      const double sq = sqrt(rbar * delta);
+      const double Sn = 2.0 * estar * sq;
+      const double kn = (2.0 / 3.0) * Sn;
+      const double cn = k56 * beta * sqrt(Sn * mbar);
+      const double vn = vrx * nx + vry * ny + vrz * nz;
+      const double fns = kn * delta - cn * vn;
+      const double fnx = fns * nx, fny = fns * ny, fnz = fns * nz;
+      double ftx = 0.0, fty = 0.0, ftz = 0.0;
+      if (mu != 0.0) {
+        // (a7) Eq. 3a-3b, Eq. 1b, Eq. 3c
+        const double vtx = vrx - vn * nx, vty = vry - vn * ny, vtz = vrz - vn * nz;
+        const double upx = ux + h * vtx, upy = uy + h * vty, upz = uz + h * vtz;
+        const double upn = upx * nx + upy * ny + upz * nz;
+        const double utx = upx - upn * nx, uty = upy - upn * ny, utz = upz - upn * nz;
+        const double kt = 8.0 * gstar * sq;
+        const double ct = k56 * beta * sqrt(kt * mbar);
+        const double trx = -kt * utx - ct * vtx, try_ = -kt * uty - ct * vty, trz = -kt * utz - ct * vtz;
+        const double cap = mu * sqrt(fnx * fnx + fny * fny + fnz * fnz);
+        const double tmag = sqrt(trx * trx + try_ * try_ + trz * trz);
+        if (tmag <= cap) {
+          ftx = trx; fty = try_; ftz = trz;
+          nux = utx; nuy = uty; nuz = utz;
+        } else {
+          const double um = sqrt(utx * utx + uty * uty + utz * utz);
+          if (um > 0.0) {
+            const double dxu = utx / um, dyu = uty / um, dzu = utz / um;
+            const double s = cap / kt;
+            nux = s * dxu; nuy = s * dyu; nuz = s * dzu;
+            ftx = -cap * dxu; fty = -cap * dyu; ftz = -cap * dzu;
+          }
+        }
+      }
+      Fx = fnx + ftx;
+      Fy = fny + fty;
+      Fz = fnz + ftz;
+    }
+    a.rows.ut[3 * e] = nux;
+    a.rows.ut[3 * e + 1] = nuy;
+    a.rows.ut[3 * e + 2] = nuz;
+    if (a.record) {
+      a.rec.F[3 * e] = Fx; a.rec.F[3 * e + 1] = Fy; a.rec.F[3 * e + 2] = Fz;
+      a.rec.p[3 * e] = px; a.rec.p[3 * e + 1] = py; a.rec.p[3 * e + 2] = pz;
+      a.rec.n[3 * e] = nx; a.rec.n[3 * e + 1] = ny; a.rec.n[3 * e + 2] = nz;
+      a.rec.delta[e] = delta;
+    }
+    // force on own sphere is -F, torque r_i x (-F) (Eq. 4, reading R11)
+    const double fx = -Fx, fy = -Fy, fz = -Fz;
+    fsx += fx; fsy += fy; fsz += fz;
+    tsx += __fma_rn(riy, fz, -__dmul_rn(riz, fy));
+    tsy += __fma_rn(riz, fx, -__dmul_rn(rix, fz));
+    tsz += __fma_rn(rix, fy, -__dmul_rn(riy, fx));
+  }
+  a.sfx[i] = fsx; a.sfy[i] = fsy; a.sfz[i] = fsz;
+  a.stx[i] = tsx; a.sty[i] = tsy; a.stz[i] = tsz;
+}
+
+// (a9) + (a10): one thread per clump.  F = sum_k f_k + M g; tau_body = R^T sum_k tau_k;
+// V += h F/M; X += h V; Omega += h I^-1 (tau - Omega x I Omega); q <- normalize(q (x) exp).
+__global__ void __launch_bounds__(256) k_integrate(StepArgs a) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a.ctl->abort) {
+    // capacity abort / error: carry the state forward unchanged so the ping-pong stays valid
+    if (c < a.n) {
+      a.nxt.x[c] = a.cur.x[c]; a.nxt.y[c] = a.cur.y[c]; a.nxt.z[c] = a.cur.z[c];
+      a.nxt.qw[c] = a.cur.qw[c]; a.nxt.qx[c] = a.cur.qx[c]; a.nxt.qy[c] = a.cur.qy[c]; a.nxt.qz[c] = a.cur.qz[c];
+      a.nxt.vx[c] = a.cur.vx[c]; a.nxt.vy[c] = a.cur.vy[c]; a.nxt.vz[c] = a.cur.vz[c];
+      a.nxt.wx[c] = a.cur.wx[c]; a.nxt.wy[c] = a.cur.wy[c]; a.nxt.wz[c] = a.cur.wz[c];
+    }
+    return;
+  }
+  if (c == 0) a.ctl->step += 1;  // read by no other thread of this launch
+  if (c >= a.n) return;
+  const int t = a.tid[c];
+  const double M = a.tab.tpl_mass[t];
+  const double I0 = a.tab.tpl_inertia[3 * t], I1 = a.tab.tpl_inertia[3 * t + 1], I2 = a.tab.tpl_inertia[3 * t + 2];
+  double Fx = 0.0, Fy = 0.0, Fz = 0.0, Tx = 0.0, Ty = 0.0, Tz = 0.0;
+  for (int s = a.sph_off[c], e = a.sph_off[c + 1]; s < e; ++s) {
+    Fx += a.sfx[s]; Fy += a.sfy[s]; Fz += a.sfz[s];
+    Tx += a.stx[s]; Ty += a.sty[s]; Tz += a.stz[s];
+  }
+  Fx = __dadd_rn(Fx, __dmul_rn(M, a.g[0]));
+  Fy = __dadd_rn(Fy, __dmul_rn(M, a.g[1]));
+  Fz = __dadd_rn(Fz, __dmul_rn(M, a.g[2]));
+  double qw = a.cur.qw[c], qx = a.cur.qx[c], qy = a.cur.qy[c], qz = a.cur.qz[c];
+  double R[9];
+  quat_R(qw, qx, qy, qz, R);
+  const double tbx = R[0] * Tx + R[3] * Ty + R[6] * Tz;
+  const double tby = R[1] * Tx + R[4] * Ty + R[7] * Tz;
+  const double tbz = R[2] * Tx + R[5] * Ty + R[8] * Tz;
+  if (!isfinite(Fx) || !isfinite(Fy) || !isfinite(Fz) || !isfinite(tbx) || !isfinite(tby) || !isfinite(tbz)) {
+    raise_error(a.ctl, -11, a.gid[c], 0);
+  }
+  const double h = a.h;
+  const double vx = a.cur.vx[c] + h * (Fx / M), vy = a.cur.vy[c] + h * (Fy / M), vz = a.cur.vz[c] + h * (Fz / M);
+  a.nxt.vx[c] = vx; a.nxt.vy[c] = vy; a.nxt.vz[c] = vz;
+  a.nxt.x[c] = a.cur.x[c] + h * vx;
+  a.nxt.y[c] = a.cur.y[c] + h * vy;
+  a.nxt.z[c] = a.cur.z[c] + h * vz;
+  const double w0 = a.cur.wx[c], w1 = a.cur.wy[c], w2 = a.cur.wz[c];
+  const double L0 = I0 * w0, L1 = I1 * w1, L2 = I2 * w2;
+  const double g0 = w1 * L2 - w2 * L1, g1 = w2 * L0 - w0 * L2, g2 = w0 * L1 - w1 * L0;
+  const double n0 = w0 + h * ((tbx - g0) / I0);
+  const double n1 = w1 + h * ((tby - g1) / I1);
+  const double n2 = w2 + h * ((tbz - g2) / I2);
+  a.nxt.wx[c] = n0; a.nxt.wy[c] = n1; a.nxt.wz[c] = n2;
+  const double wn = sqrt(n0 * n0 + n1 * n1 + n2 * n2);
+  double dw = 1.0, dx = 0.0, dy = 0.0, dz = 0.0;
+  if (wn > 0.0) {
+    double sh, ch;
+    sincos(0.5 * (h * wn), &sh, &ch);
+    const double sn = sh / wn;
+    dw = ch; dx = n0 * sn; dy = n1 * sn; dz = n2 * sn;
+  }
+  const double rw = qw * dw - qx * dx - qy * dy - qz * dz;
+  const double rx = qw * dx + qx * dw + qy * dz - qz * dy;
+  const double ry = qw * dy - qx * dz + qy * dw + qz * dx;
+  const double rz = qw * dz + qx * dy - qy * dx + qz * dw;
+  const double nrm = sqrt(rw * rw + rx * rx + ry * ry + rz * rz);
+  a.nxt.qw[c] = rw / nrm; a.nxt.qx[c] = rx / nrm; a.nxt.qy[c] = ry / nrm; a.nxt.qz[c] = rz / nrm;
+}
+
+void launch_force(const StepArgs& a, cudaStream_t s) {
+  if (a.ns) k_force<<<(a.ns + 127) / 128, 128, 0, s>>>(a);
+}
+void launch_integrate(const StepArgs& a, cudaStream_t s) {
+  k_integrate<<<(a.n + 255) / 256 > 0 ? (a.n + 255) / 256 : 1, 256, 0, s>>>(a);
+}
+
+}  // namespace dem
+
+namespace dem {
+// wall entries of a row set (for dem_get_stats: canonical contacts = walls + pairs/2)
+__global__ void k_count_walls(Rows r, int ns, unsigned long long* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long c = 0;
+  if (i < ns)
+    for (int e = r.row_ptr[i]; e < r.row_ptr[i + 1]; ++e) c += r.key[e] > (0x7fffffffffffffffLL - kMaxPlanes);
+  c = __reduce_add_sync(0xffffffffu, (unsigned)c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+void launch_count_walls(const Rows& r, int ns, unsigned long long* out, cudaStream_t s) {
+  if (ns) k_count_walls<<<(ns + 255) / 256, 256, 0, s>>>(r, ns, out);
+}
+}  // namespace dem

@@ -1,0 +1,901 @@
+// system.cu — host runtime and C-ABI (include/dem.h) of the B200 clump-DEM hot path.
+//
+// Owns device memory (through the caller's allocator callback, e.g. the PyTorch caching
+// allocator, or cudaMallocAsync), captures one CUDA graph per state parity for the
+// 10-launch step sequence, checks the device status word once per dem_step call, and
+// regrows bin/row capacity transparently (the aborted steps are re-run).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "dem.h"
+#include "dem_device.cuh"
+
+namespace dem {
+void launch_pose_count(const StepArgs&, cudaStream_t);
+void launch_bin_scatter(const StepArgs&, cudaStream_t);
+void launch_narrow_count(const StepArgs&, cudaStream_t);
+void launch_narrow_fill(const StepArgs&, cudaStream_t);
+void launch_force(const StepArgs&, cudaStream_t);
+void launch_integrate(const StepArgs&, cudaStream_t);
+long long scan_tiles_needed(long long n);
+void launch_excl_scan(const int* in, int* out, long long n, int* tmp, const int* abort, cudaStream_t s);
+void launch_count_walls(const Rows& r, int ns, unsigned long long* out, cudaStream_t s);
+}  // namespace dem
+
+using namespace dem;
+
+static constexpr int kStages = 8;
+
+struct RowBuf {
+  int* row_ptr = nullptr;
+  int* partner = nullptr;
+  long long* key = nullptr;
+  double* ut = nullptr;
+};
+
+struct dem_system {
+  dem_params P{};
+  cudaStream_t stream = nullptr;
+  cudaStream_t cap_stream = nullptr;
+  std::string err;
+  // host tables
+  int n_mat = 0, n_tmpl = 0, n_planes = 0;
+  std::vector<int> tpl_ncomp, tpl_coff, tc_mat;
+  std::vector<double> tc_off, tc_rad, tpl_mass, tpl_inertia, pair;
+  std::vector<dem_plane> planes;
+  double rmin = 0, rmax = 0;
+  // device tables
+  double *d_tc_off = nullptr, *d_tc_rad = nullptr, *d_tpl_mass = nullptr, *d_tpl_inertia = nullptr,
+         *d_pair = nullptr;
+  int *d_tc_mat = nullptr, *d_tpl_coff = nullptr;
+  // state
+  int64_t n = 0, ns = 0;
+  std::vector<long long> h_gid;
+  std::vector<int> h_tid, h_sph_off, h_s_tc;
+  std::vector<long long> h_s_key;
+  long long* d_gid = nullptr;
+  int *d_tid = nullptr, *d_sph_off = nullptr;
+  double* d_state[2] = {nullptr, nullptr};
+  double* d_ww = nullptr;
+  int *d_s_clump = nullptr, *d_s_tc = nullptr;
+  long long* d_s_key = nullptr;
+  double *d_spos = nullptr, *d_sft = nullptr;
+  // bins
+  Grid grid{};
+  long long ncell = 0, cap_inserts = 0;
+  int *d_cell_count = nullptr, *d_cell_start = nullptr, *d_items = nullptr;
+  int *d_row_cnt = nullptr, *d_scan_tmp = nullptr;
+  // rows
+  RowBuf rows[2];
+  long long cap_entries = 0;
+  Record rec{};
+  Ctl* d_ctl = nullptr;
+  Ctl* h_ctl = nullptr;
+  unsigned long long* d_counter = nullptr;
+  // graphs
+  cudaGraphExec_t graph[2] = {nullptr, nullptr};
+  bool graphs_valid = false;
+  int64_t launched = 0;  // steps launched since dem_set_state (selects the parity)
+  int64_t steps_done = 0;
+  int64_t regrows = 0;
+  long long last_entries = 0, last_inserts = 0;
+  // profiling
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev;
+  double stage_ms[kStages] = {0};
+  int64_t prof_steps = 0;
+  std::unordered_map<void*, size_t> allocs;
+};
+
+// ------------------------------------------------------------------ helpers
+#define CK(call)                                                                  \
+  do {                                                                            \
+    cudaError_t e_ = (call);                                                      \
+    if (e_ != cudaSuccess) {                                                      \
+      sys->err = std::string(#call) + ": " + cudaGetErrorString(e_);              \
+      return e_ == cudaErrorMemoryAllocation ? DEM_ERR_OOM : DEM_ERR_CUDA;        \
+    }                                                                             \
+  } while (0)
+
+static void* dalloc(dem_system* sys, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  void* p = nullptr;
+  if (sys->P.alloc) {
+    p = sys->P.alloc(bytes, sys->P.alloc_ctx, (void*)sys->stream);
+  } else {
+    if (cudaMallocAsync(&p, bytes, sys->stream) != cudaSuccess) p = nullptr;
+  }
+  if (p) sys->allocs[p] = bytes;
+  return p;
+}
+
+static void dfree(dem_system* sys, void* p) {
+  if (!p) return;
+  auto it = sys->allocs.find(p);
+  size_t bytes = it == sys->allocs.end() ? 0 : it->second;
+  if (it != sys->allocs.end()) sys->allocs.erase(it);
+  if (sys->P.free)
+    sys->P.free(p, bytes, sys->P.alloc_ctx, (void*)sys->stream);
+  else
+    cudaFreeAsync(p, sys->stream);
+}
+
+template <class T>
+static dem_status alloc_arr(dem_system* sys, T** out, size_t count) {
+  dfree(sys, *out);
+  *out = (T*)dalloc(sys, sizeof(T) * count);
+  if (!*out) {
+    sys->err = "device allocation of " + std::to_string(sizeof(T) * count) + " bytes failed";
+    return DEM_ERR_OOM;
+  }
+  return DEM_OK;
+}
+
+#define TRY(x)                      \
+  do {                              \
+    dem_status s_ = (x);            \
+    if (s_ != DEM_OK) return s_;    \
+  } while (0)
+
+static void free_graphs(dem_system* sys) {
+  for (int p = 0; p < 2; ++p)
+    if (sys->graph[p]) {
+      cudaGraphExecDestroy(sys->graph[p]);
+      sys->graph[p] = nullptr;
+    }
+  sys->graphs_valid = false;
+}
+
+static StepArgs make_args(dem_system* sys, int p) {
+  StepArgs a{};
+  a.n = (int)sys->n;
+  a.ns = (int)sys->ns;
+  a.ncell = sys->ncell;
+  a.cap_inserts = sys->cap_inserts;
+  a.cap_entries = sys->cap_entries;
+  a.h = sys->P.h;
+  for (int d = 0; d < 3; ++d) a.g[d] = sys->P.gravity[d];
+  a.margin = sys->P.margin;
+  Tables& t = a.tab;
+  t.tc_off = sys->d_tc_off;
+  t.tc_rad = sys->d_tc_rad;
+  t.tc_mat = sys->d_tc_mat;
+  t.tpl_coff = sys->d_tpl_coff;
+  t.tpl_mass = sys->d_tpl_mass;
+  t.tpl_inertia = sys->d_tpl_inertia;
+  t.pair = sys->d_pair;
+  t.n_mat = sys->n_mat;
+  t.n_planes = sys->n_planes;
+  for (int k = 0; k < sys->n_planes; ++k) {
+    for (int d = 0; d < 3; ++d) {
+      t.plane_pt[k][d] = sys->planes[k].point[d];
+      t.plane_n[k][d] = sys->planes[k].normal[d];
+    }
+    t.plane_mat[k] = sys->planes[k].material;
+  }
+  a.grid = sys->grid;
+  auto soa = [&](double* base) {
+    State s;
+    size_t n = (size_t)sys->n;
+    double* f[13];
+    for (int k = 0; k < 13; ++k) f[k] = base + k * n;
+    s.x = f[0]; s.y = f[1]; s.z = f[2]; s.qw = f[3]; s.qx = f[4]; s.qy = f[5]; s.qz = f[6];
+    s.vx = f[7]; s.vy = f[8]; s.vz = f[9]; s.wx = f[10]; s.wy = f[11]; s.wz = f[12];
+    return s;
+  };
+  a.cur = soa(sys->d_state[p]);
+  a.nxt = soa(sys->d_state[p ^ 1]);
+  a.tid = sys->d_tid;
+  a.gid = sys->d_gid;
+  a.sph_off = sys->d_sph_off;
+  a.wwx = sys->d_ww;
+  a.wwy = sys->d_ww + sys->n;
+  a.wwz = sys->d_ww + 2 * sys->n;
+  a.s_clump = sys->d_s_clump;
+  a.s_tc = sys->d_s_tc;
+  a.s_key = sys->d_s_key;
+  size_t ns = (size_t)sys->ns;
+  a.sx = sys->d_spos;
+  a.sy = sys->d_spos + ns;
+  a.sz = sys->d_spos + 2 * ns;
+  a.sfx = sys->d_sft;
+  a.sfy = sys->d_sft + ns;
+  a.sfz = sys->d_sft + 2 * ns;
+  a.stx = sys->d_sft + 3 * ns;
+  a.sty = sys->d_sft + 4 * ns;
+  a.stz = sys->d_sft + 5 * ns;
+  a.cell_count = sys->d_cell_count;
+  a.cell_start = sys->d_cell_start;
+  a.items = sys->d_items;
+  a.row_cnt = sys->d_row_cnt;
+  const RowBuf& R = sys->rows[p];
+  const RowBuf& Q = sys->rows[p ^ 1];
+  a.rows = Rows{R.row_ptr, R.partner, R.key, R.ut};
+  a.prev = Rows{Q.row_ptr, Q.partner, Q.key, Q.ut};
+  a.rec = sys->rec;
+  a.record = sys->P.record_contacts ? 1 : 0;
+  a.ctl = sys->d_ctl;
+  return a;
+}
+
+// the step sequence; ev (optional) receives kStages+1 events around the stages
+static void enqueue_step(dem_system* sys, int p, cudaStream_t s, cudaEvent_t* ev) {
+  StepArgs a = make_args(sys, p);
+  const int* abort = &sys->d_ctl->abort;
+  if (ev) cudaEventRecord(ev[0], s);
+  launch_pose_count(a, s);
+  if (ev) cudaEventRecord(ev[1], s);
+  launch_excl_scan(sys->d_cell_count, sys->d_cell_start, sys->ncell, sys->d_scan_tmp, abort, s);
+  if (ev) cudaEventRecord(ev[2], s);
+  launch_bin_scatter(a, s);
+  if (ev) cudaEventRecord(ev[3], s);
+  launch_narrow_count(a, s);
+  if (ev) cudaEventRecord(ev[4], s);
+  launch_excl_scan(sys->d_row_cnt, sys->rows[p].row_ptr, sys->ns, sys->d_scan_tmp, abort, s);
+  if (ev) cudaEventRecord(ev[5], s);
+  launch_narrow_fill(a, s);
+  if (ev) cudaEventRecord(ev[6], s);
+  launch_force(a, s);
+  if (ev) cudaEventRecord(ev[7], s);
+  launch_integrate(a, s);
+  if (ev) cudaEventRecord(ev[8], s);
+}
+
+static dem_status capture_graphs(dem_system* sys) {
+  free_graphs(sys);
+  for (int p = 0; p < 2; ++p) {
+    cudaGraph_t g;
+    CK(cudaStreamBeginCapture(sys->cap_stream, cudaStreamCaptureModeThreadLocal));
+    enqueue_step(sys, p, sys->cap_stream, nullptr);
+    CK(cudaStreamEndCapture(sys->cap_stream, &g));
+    cudaError_t e = cudaGraphInstantiate(&sys->graph[p], g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+      sys->err = std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e);
+      return DEM_ERR_CUDA;
+    }
+  }
+  sys->graphs_valid = true;
+  return DEM_OK;
+}
+
+// ------------------------------------------------------------------ validation / tables
+static bool material_ok(const dem_material& m) {
+  return m.E > 0 && m.nu >= 0 && m.nu < 0.5 && m.mu >= 0 && m.cor > 0 && m.cor <= 1 && std::isfinite(m.E);
+}
+
+// pair parameters (DESIGN.md §3 R4): series E*, G*; min CoR -> beta; min mu
+static void pair_params(const dem_material& A, const dem_material& B, double out[4]) {
+  double ie = (1.0 - A.nu * A.nu) / A.E + (1.0 - B.nu * B.nu) / B.E;
+  double ig = 2.0 * (2.0 - A.nu) * (1.0 + A.nu) / A.E + 2.0 * (2.0 - B.nu) * (1.0 + B.nu) / B.E;
+  double e = std::min(A.cor, B.cor);
+  double beta = 0.0;
+  if (e < 1.0) {
+    double le = std::log(e);
+    beta = -le / std::sqrt(le * le + M_PI * M_PI);
+  }
+  out[0] = 1.0 / ie;
+  out[1] = 1.0 / ig;
+  out[2] = beta;
+  out[3] = std::min(A.mu, B.mu);
+}
+
+extern "C" const char* dem_status_string(dem_status s) {
+  switch (s) {
+    case DEM_OK: return "ok";
+    case DEM_ERR_INVALID_ARG: return "invalid argument";
+    case DEM_ERR_CUDA: return "CUDA error";
+    case DEM_ERR_OOM: return "out of device memory";
+    case DEM_ERR_NCCL: return "NCCL error";
+    case DEM_ERR_BAD_MATERIAL: return "bad material";
+    case DEM_ERR_BAD_TEMPLATE: return "bad template";
+    case DEM_ERR_OUT_OF_DOMAIN: return "sphere out of domain";
+    case DEM_ERR_NONFINITE: return "non-finite wrench";
+    case DEM_ERR_DEGENERATE_CONTACT: return "degenerate contact (coincident centres)";
+    case DEM_ERR_CAPACITY: return "capacity";
+  }
+  return "unknown";
+}
+
+extern "C" dem_status dem_last_error(const dem_system* sys, char* buf, size_t len) {
+  if (!sys || !buf || !len) return DEM_ERR_INVALID_ARG;
+  std::snprintf(buf, len, "%s", sys->err.c_str());
+  return DEM_OK;
+}
+
+extern "C" dem_status dem_create(const dem_params* params, const dem_material* materials, int32_t n_mat,
+                                 const dem_template* templates, int32_t n_tmpl, const dem_plane* planes,
+                                 int32_t n_planes, void* cuda_stream, dem_system** out) {
+  if (!params || !out || n_mat <= 0 || n_tmpl <= 0 || n_planes < 0 || n_planes > kMaxPlanes || !materials ||
+      !templates || (n_planes && !planes))
+    return DEM_ERR_INVALID_ARG;
+  if (!(params->h > 0) || params->margin < 0 || params->cd_every != 1 || params->cell_size < 0)
+    return DEM_ERR_INVALID_ARG;
+  for (int d = 0; d < 3; ++d)
+    if (!(params->domain_hi[d] > params->domain_lo[d])) return DEM_ERR_INVALID_ARG;
+  for (int m = 0; m < n_mat; ++m)
+    if (!material_ok(materials[m])) return DEM_ERR_BAD_MATERIAL;
+  for (int p = 0; p < n_planes; ++p) {
+    const double* nv = planes[p].normal;
+    double nn = std::sqrt(nv[0] * nv[0] + nv[1] * nv[1] + nv[2] * nv[2]);
+    if (std::fabs(nn - 1.0) > 1e-9 || planes[p].material < 0 || planes[p].material >= n_mat)
+      return DEM_ERR_INVALID_ARG;
+  }
+  for (int t = 0; t < n_tmpl; ++t) {
+    const dem_template& T = templates[t];
+    if (T.n_comp < 1 || T.n_comp > kKeyStride || !T.offset || !T.radius || !T.material || !(T.mass > 0) ||
+        !(T.inertia[0] > 0) || !(T.inertia[1] > 0) || !(T.inertia[2] > 0))
+      return DEM_ERR_BAD_TEMPLATE;
+    for (int k = 0; k < T.n_comp; ++k)
+      if (!(T.radius[k] > 0) || T.material[k] < 0 || T.material[k] >= n_mat) return DEM_ERR_BAD_TEMPLATE;
+  }
+  dem_system* sys = new dem_system();
+  sys->P = *params;
+  sys->stream = (cudaStream_t)cuda_stream;
+  sys->n_mat = n_mat;
+  sys->n_tmpl = n_tmpl;
+  sys->n_planes = n_planes;
+  sys->planes.assign(planes, planes + n_planes);
+  sys->rmin = 1e300;
+  sys->rmax = 0;
+  for (int t = 0; t < n_tmpl; ++t) {
+    const dem_template& T = templates[t];
+    sys->tpl_coff.push_back((int)sys->tc_rad.size());
+    sys->tpl_ncomp.push_back(T.n_comp);
+    sys->tpl_mass.push_back(T.mass);
+    for (int d = 0; d < 3; ++d) sys->tpl_inertia.push_back(T.inertia[d]);
+    for (int k = 0; k < T.n_comp; ++k) {
+      for (int d = 0; d < 3; ++d) sys->tc_off.push_back(T.offset[3 * k + d]);
+      sys->tc_rad.push_back(T.radius[k]);
+      sys->tc_mat.push_back(T.material[k]);
+      sys->rmin = std::min(sys->rmin, T.radius[k]);
+      sys->rmax = std::max(sys->rmax, T.radius[k]);
+    }
+  }
+  sys->pair.assign((size_t)n_mat * n_mat * 4, 0.0);
+  for (int i = 0; i < n_mat; ++i)
+    for (int j = i; j < n_mat; ++j) {
+      double o[4];
+      pair_params(materials[i], materials[j], o);
+      for (int q = 0; q < 4; ++q) {
+        sys->pair[4 * (i * n_mat + j) + q] = o[q];
+        sys->pair[4 * (j * n_mat + i) + q] = o[q];
+      }
+    }
+  cudaError_t e = cudaStreamCreateWithFlags(&sys->cap_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete sys;
+    return DEM_ERR_CUDA;
+  }
+  auto up = [&](auto** dst, const auto& vec) -> dem_status {
+    using T = std::remove_reference_t<decltype(**dst)>;
+    TRY(alloc_arr(sys, dst, vec.size()));
+    if (cudaMemcpyAsync(*dst, vec.data(), sizeof(T) * vec.size(), cudaMemcpyHostToDevice, sys->stream) !=
+        cudaSuccess)
+      return DEM_ERR_CUDA;
+    return DEM_OK;
+  };
+  dem_status st = DEM_OK;
+  if ((st = up(&sys->d_tc_off, sys->tc_off)) || (st = up(&sys->d_tc_rad, sys->tc_rad)) ||
+      (st = up(&sys->d_tc_mat, sys->tc_mat)) || (st = up(&sys->d_tpl_coff, sys->tpl_coff)) ||
+      (st = up(&sys->d_tpl_mass, sys->tpl_mass)) || (st = up(&sys->d_tpl_inertia, sys->tpl_inertia)) ||
+      (st = up(&sys->d_pair, sys->pair))) {
+    dem_destroy(sys);
+    return st;
+  }
+  if ((st = alloc_arr(sys, &sys->d_ctl, 1)) || (st = alloc_arr(sys, &sys->d_counter, 1))) {
+    dem_destroy(sys);
+    return st;
+  }
+  if (cudaMallocHost(&sys->h_ctl, sizeof(Ctl)) != cudaSuccess) {
+    dem_destroy(sys);
+    return DEM_ERR_CUDA;
+  }
+  std::memset(sys->h_ctl, 0, sizeof(Ctl));
+  cudaMemcpyAsync(sys->d_ctl, sys->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, sys->stream);
+  if (cudaStreamSynchronize(sys->stream) != cudaSuccess) {
+    dem_destroy(sys);
+    return DEM_ERR_CUDA;
+  }
+  *out = sys;
+  return DEM_OK;
+}
+
+extern "C" void dem_destroy(dem_system* sys) {
+  if (!sys) return;
+  cudaStreamSynchronize(sys->stream);
+  free_graphs(sys);
+  std::vector<void*> ptrs;
+  for (auto& kv : sys->allocs) ptrs.push_back(kv.first);
+  for (void* p : ptrs) dfree(sys, p);
+  cudaStreamSynchronize(sys->stream);
+  if (sys->h_ctl) cudaFreeHost(sys->h_ctl);
+  for (auto e : sys->ev) cudaEventDestroy(e);
+  if (sys->cap_stream) cudaStreamDestroy(sys->cap_stream);
+  delete sys;
+}
+
+// ------------------------------------------------------------------ capacity
+static dem_status alloc_rows(dem_system* sys, long long cap) {
+  // grow both row buffers to cap entries, preserving the contents of both
+  for (int p = 0; p < 2; ++p) {
+    RowBuf nb;
+    nb.row_ptr = sys->rows[p].row_ptr;
+    nb.partner = (int*)dalloc(sys, sizeof(int) * cap);
+    nb.key = (long long*)dalloc(sys, sizeof(long long) * cap);
+    nb.ut = (double*)dalloc(sys, sizeof(double) * 3 * cap);
+    if (!nb.partner || !nb.key || !nb.ut) {
+      sys->err = "row buffer allocation failed";
+      return DEM_ERR_OOM;
+    }
+    if (sys->rows[p].key && sys->cap_entries) {
+      size_t m = (size_t)std::min(cap, sys->cap_entries);
+      cudaMemcpyAsync(nb.partner, sys->rows[p].partner, sizeof(int) * m, cudaMemcpyDeviceToDevice, sys->stream);
+      cudaMemcpyAsync(nb.key, sys->rows[p].key, sizeof(long long) * m, cudaMemcpyDeviceToDevice, sys->stream);
+      cudaMemcpyAsync(nb.ut, sys->rows[p].ut, sizeof(double) * 3 * m, cudaMemcpyDeviceToDevice, sys->stream);
+    }
+    dfree(sys, sys->rows[p].partner);
+    dfree(sys, sys->rows[p].key);
+    dfree(sys, sys->rows[p].ut);
+    sys->rows[p] = nb;
+  }
+  if (sys->P.record_contacts) {
+    TRY(alloc_arr(sys, &sys->rec.F, 3 * cap));
+    TRY(alloc_arr(sys, &sys->rec.p, 3 * cap));
+    TRY(alloc_arr(sys, &sys->rec.n, 3 * cap));
+    TRY(alloc_arr(sys, &sys->rec.delta, cap));
+  }
+  sys->cap_entries = cap;
+  free_graphs(sys);
+  return DEM_OK;
+}
+
+// ------------------------------------------------------------------ state
+extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* gid, const int32_t* tid,
+                                    const double* pos, const double* quat, const double* vel, const double* omega,
+                                    int32_t on_device) {
+  if (!sys || n < 0 || (n > 0 && (!gid || !tid || !pos || !quat || !vel || !omega))) return DEM_ERR_INVALID_ARG;
+  if (n > (1LL << 30)) return DEM_ERR_INVALID_ARG;
+  CK(cudaStreamSynchronize(sys->stream));
+  std::vector<long long> g(n);
+  std::vector<int> t(n);
+  std::vector<double> in[4];
+  const double* src[4] = {pos, quat, vel, omega};
+  const int width[4] = {3, 4, 3, 3};
+  if (on_device) {
+    if (n) {
+      CK(cudaMemcpy(g.data(), gid, sizeof(long long) * n, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(t.data(), tid, sizeof(int) * n, cudaMemcpyDeviceToHost));
+    }
+    for (int k = 0; k < 4; ++k) {
+      in[k].resize((size_t)width[k] * n);
+      if (n) CK(cudaMemcpy(in[k].data(), src[k], sizeof(double) * width[k] * n, cudaMemcpyDeviceToHost));
+      src[k] = in[k].data();
+    }
+  } else {
+    for (int64_t c = 0; c < n; ++c) {
+      g[c] = gid[c];
+      t[c] = tid[c];
+    }
+  }
+  int64_t ns = 0;
+  for (int64_t c = 0; c < n; ++c) {
+    if (t[c] < 0 || t[c] >= sys->n_tmpl || g[c] < 0 || g[c] >= (1LL << 56)) {
+      sys->err = "clump " + std::to_string(c) + ": bad template id or gid";
+      return DEM_ERR_INVALID_ARG;
+    }
+    ns += sys->tpl_ncomp[t[c]];
+  }
+  if (ns > (1LL << 30)) return DEM_ERR_INVALID_ARG;
+  free_graphs(sys);
+  sys->n = n;
+  sys->ns = ns;
+  sys->h_gid = g;
+  sys->h_tid = t;
+  sys->h_sph_off.assign(n + 1, 0);
+  std::vector<int> s_clump(ns);
+  sys->h_s_tc.assign(ns, 0);
+  sys->h_s_key.assign(ns, 0);
+  int64_t k = 0;
+  for (int64_t c = 0; c < n; ++c) {
+    sys->h_sph_off[c] = (int)k;
+    for (int j = 0; j < sys->tpl_ncomp[t[c]]; ++j, ++k) {
+      s_clump[k] = (int)c;
+      sys->h_s_tc[k] = sys->tpl_coff[t[c]] + j;
+      sys->h_s_key[k] = g[c] * kKeyStride + j;
+    }
+  }
+  sys->h_sph_off[n] = (int)k;
+  // SoA state on the host, one upload
+  std::vector<double> st((size_t)13 * n);
+  for (int64_t c = 0; c < n; ++c) {
+    for (int d = 0; d < 3; ++d) st[(0 + d) * n + c] = src[0][3 * c + d];
+    for (int d = 0; d < 4; ++d) st[(3 + d) * n + c] = src[1][4 * c + d];
+    for (int d = 0; d < 3; ++d) st[(7 + d) * n + c] = src[2][3 * c + d];
+    for (int d = 0; d < 3; ++d) st[(10 + d) * n + c] = src[3][3 * c + d];
+    for (int d = 0; d < 3; ++d)
+      if (!std::isfinite(src[0][3 * c + d]) || !std::isfinite(src[2][3 * c + d]) || !std::isfinite(src[3][3 * c + d]))
+        return DEM_ERR_NONFINITE;
+  }
+  // grid: cell edge (auto: 4 x mean sphere radius + margin, at least 2 r_min + margin)
+  double rsum = 0;
+  for (int64_t s = 0; s < ns; ++s) rsum += sys->tc_rad[sys->h_s_tc[s]];
+  double rmean = ns ? rsum / ns : sys->rmax;
+  double cell = sys->P.cell_size > 0 ? sys->P.cell_size : std::max(4.0 * rmean, 2.0 * sys->rmin) + sys->P.margin;
+  Grid& G = sys->grid;
+  G.cell = cell;
+  G.inv_cell = 1.0 / cell;
+  G.pad = 0.5 * sys->P.margin + 1e-9;
+  long long ncell = 1;
+  for (int d = 0; d < 3; ++d) {
+    G.lo[d] = sys->P.domain_lo[d];
+    G.dom_lo[d] = sys->P.domain_lo[d];
+    G.dom_hi[d] = sys->P.domain_hi[d];
+    double ext = sys->P.domain_hi[d] - sys->P.domain_lo[d];
+    long long nd = (long long)std::ceil(ext / cell) + 1;
+    if (nd > (1LL << 20)) {
+      sys->err = "grid too fine for the domain";
+      return DEM_ERR_INVALID_ARG;
+    }
+    G.n[d] = (int)nd;
+    ncell *= nd;
+  }
+  if (ncell > (1LL << 31) - 2) {
+    sys->err = "too many bins; increase cell_size";
+    return DEM_ERR_INVALID_ARG;
+  }
+  sys->ncell = ncell;
+  // upper bound of bin inserts: (floor(2e / cell) + 2)^3 per sphere
+  long long ins = 0;
+  for (int64_t s = 0; s < ns; ++s) {
+    double e = sys->tc_rad[sys->h_s_tc[s]] + G.pad;
+    long long m = (long long)std::floor(2.0 * e / cell) + 2;
+    ins += m * m * m;
+  }
+  if (ins > (1LL << 31) - 2) ins = (1LL << 31) - 2;
+  sys->cap_inserts = ins;
+  // device arrays
+  TRY(alloc_arr(sys, &sys->d_gid, n));
+  TRY(alloc_arr(sys, &sys->d_tid, n));
+  TRY(alloc_arr(sys, &sys->d_sph_off, n + 1));
+  TRY(alloc_arr(sys, &sys->d_state[0], 13 * n));
+  TRY(alloc_arr(sys, &sys->d_state[1], 13 * n));
+  TRY(alloc_arr(sys, &sys->d_ww, 3 * n));
+  TRY(alloc_arr(sys, &sys->d_s_clump, ns));
+  TRY(alloc_arr(sys, &sys->d_s_tc, ns));
+  TRY(alloc_arr(sys, &sys->d_s_key, ns));
+  TRY(alloc_arr(sys, &sys->d_spos, 3 * ns));
+  TRY(alloc_arr(sys, &sys->d_sft, 6 * ns));
+  TRY(alloc_arr(sys, &sys->d_cell_count, ncell));
+  TRY(alloc_arr(sys, &sys->d_cell_start, ncell + 1));
+  TRY(alloc_arr(sys, &sys->d_items, ins));
+  TRY(alloc_arr(sys, &sys->d_row_cnt, ns + 1));
+  TRY(alloc_arr(sys, &sys->d_scan_tmp, std::max(scan_tiles_needed(ncell), scan_tiles_needed(ns)) + 1));
+  for (int p = 0; p < 2; ++p) TRY(alloc_arr(sys, &sys->rows[p].row_ptr, ns + 1));
+  long long cap = std::max<long long>(1024, 8 * ns);
+  sys->cap_entries = 0;
+  for (int p = 0; p < 2; ++p) {
+    dfree(sys, sys->rows[p].partner); sys->rows[p].partner = nullptr;
+    dfree(sys, sys->rows[p].key); sys->rows[p].key = nullptr;
+    dfree(sys, sys->rows[p].ut); sys->rows[p].ut = nullptr;
+  }
+  TRY(alloc_rows(sys, cap));
+  cudaStream_t s = sys->stream;
+  CK(cudaMemcpyAsync(sys->d_gid, g.data(), sizeof(long long) * n, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(sys->d_tid, t.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(sys->d_sph_off, sys->h_sph_off.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(sys->d_state[0], st.data(), sizeof(double) * 13 * n, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(sys->d_s_clump, s_clump.data(), sizeof(int) * ns, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(sys->d_s_tc, sys->h_s_tc.data(), sizeof(int) * ns, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(sys->d_s_key, sys->h_s_key.data(), sizeof(long long) * ns, cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(sys->d_cell_count, 0, sizeof(int) * ncell, s));
+  for (int p = 0; p < 2; ++p) CK(cudaMemsetAsync(sys->rows[p].row_ptr, 0, sizeof(int) * (ns + 1), s));
+  std::memset(sys->h_ctl, 0, sizeof(Ctl));
+  CK(cudaMemcpyAsync(sys->d_ctl, sys->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));
+  sys->launched = 0;
+  sys->steps_done = 0;
+  sys->last_entries = 0;
+  sys->err.clear();
+  return DEM_OK;
+}
+
+extern "C" dem_status dem_set_contact_history(dem_system* sys, int64_t n, const int64_t* key_a,
+                                              const int64_t* key_b, const double* u_t) {
+  if (!sys || n < 0 || (n && (!key_a || !key_b || !u_t))) return DEM_ERR_INVALID_ARG;
+  std::unordered_map<long long, int> idx;
+  idx.reserve((size_t)sys->ns * 2);
+  for (int64_t s = 0; s < sys->ns; ++s) idx[sys->h_s_key[s]] = (int)s;
+  struct E {
+    long long key;
+    double u[3];
+  };
+  std::vector<std::vector<E>> per(sys->ns);
+  for (int64_t r = 0; r < n; ++r) {
+    if (!(key_a[r] < key_b[r])) return DEM_ERR_INVALID_ARG;
+    auto ia = idx.find(key_a[r]);
+    if (ia != idx.end()) per[ia->second].push_back(E{key_b[r], {u_t[3 * r], u_t[3 * r + 1], u_t[3 * r + 2]}});
+    auto ib = idx.find(key_b[r]);
+    if (ib != idx.end()) per[ib->second].push_back(E{key_a[r], {-u_t[3 * r], -u_t[3 * r + 1], -u_t[3 * r + 2]}});
+  }
+  std::vector<int> rp(sys->ns + 1, 0);
+  std::vector<long long> keys;
+  std::vector<double> ut;
+  std::vector<int> partner;
+  for (int64_t s = 0; s < sys->ns; ++s) {
+    auto& v = per[s];
+    std::sort(v.begin(), v.end(), [](const E& x, const E& y) { return x.key < y.key; });
+    for (auto& e : v) {
+      keys.push_back(e.key);
+      partner.push_back(-1);
+      for (int d = 0; d < 3; ++d) ut.push_back(e.u[d]);
+    }
+    rp[s + 1] = (int)keys.size();
+  }
+  long long m = (long long)keys.size();
+  if (m > sys->cap_entries) TRY(alloc_rows(sys, m + m / 4 + 1024));
+  int prev = (int)((sys->launched & 1) ^ 1);
+  cudaStream_t s = sys->stream;
+  RowBuf& R = sys->rows[prev];
+  CK(cudaMemcpyAsync(R.row_ptr, rp.data(), sizeof(int) * (sys->ns + 1), cudaMemcpyHostToDevice, s));
+  if (m) {
+    CK(cudaMemcpyAsync(R.key, keys.data(), sizeof(long long) * m, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(R.partner, partner.data(), sizeof(int) * m, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(R.ut, ut.data(), sizeof(double) * 3 * m, cudaMemcpyHostToDevice, s));
+  }
+  CK(cudaStreamSynchronize(s));
+  return DEM_OK;
+}
+
+// ------------------------------------------------------------------ stepping
+static dem_status read_ctl(dem_system* sys) {
+  CK(cudaMemcpyAsync(sys->h_ctl, sys->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, sys->stream));
+  CK(cudaStreamSynchronize(sys->stream));
+  return DEM_OK;
+}
+
+static dem_status device_error(dem_system* sys) {
+  const Ctl& c = *sys->h_ctl;
+  char buf[256];
+  switch (c.err_code) {
+    case DEM_ERR_OUT_OF_DOMAIN:
+      std::snprintf(buf, sizeof buf, "sphere %lld of clump gid %lld left the domain at step %lld", c.err_key,
+                    c.err_key2, c.err_step);
+      break;
+    case DEM_ERR_NONFINITE:
+      std::snprintf(buf, sizeof buf, "non-finite wrench on clump gid %lld at step %lld", c.err_key, c.err_step);
+      break;
+    case DEM_ERR_DEGENERATE_CONTACT:
+      std::snprintf(buf, sizeof buf, "coincident centres of spheres %lld and %lld at step %lld", c.err_key,
+                    c.err_key2, c.err_step);
+      break;
+    default:
+      std::snprintf(buf, sizeof buf, "device error %d at step %lld", c.err_code, c.err_step);
+  }
+  sys->err = buf;
+  return (dem_status)c.err_code;
+}
+
+static dem_status ensure_events(dem_system* sys, int64_t steps) {
+  size_t need = (size_t)steps * (kStages + 1);
+  while (sys->ev.size() < need) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    sys->ev.push_back(e);
+  }
+  return DEM_OK;
+}
+
+extern "C" dem_status dem_step(dem_system* sys, int64_t n_steps) {
+  if (!sys || n_steps < 0) return DEM_ERR_INVALID_ARG;
+  if (sys->h_ctl->err_code) return (dem_status)sys->h_ctl->err_code;
+  int64_t remaining = n_steps;
+  int guard = 0;
+  while (remaining > 0) {
+    if (!sys->profiling && !sys->graphs_valid) TRY(capture_graphs(sys));
+    const int64_t launched_before = sys->launched;
+    const int64_t done_before = sys->h_ctl->step;
+    if (sys->profiling) {
+      TRY(ensure_events(sys, remaining));
+      for (int64_t k = 0; k < remaining; ++k) {
+        enqueue_step(sys, (int)(sys->launched & 1), sys->stream, &sys->ev[(size_t)k * (kStages + 1)]);
+        sys->launched++;
+      }
+    } else {
+      for (int64_t k = 0; k < remaining; ++k) {
+        CK(cudaGraphLaunch(sys->graph[sys->launched & 1], sys->stream));
+        sys->launched++;
+      }
+    }
+    TRY(read_ctl(sys));
+    const int64_t done = sys->h_ctl->step - done_before;
+    if (sys->profiling) {
+      for (int64_t k = 0; k < done; ++k)
+        for (int st = 0; st < kStages; ++st) {
+          float ms = 0;
+          cudaEventElapsedTime(&ms, sys->ev[(size_t)k * (kStages + 1) + st],
+                               sys->ev[(size_t)k * (kStages + 1) + st + 1]);
+          sys->stage_ms[st] += ms;
+        }
+      sys->prof_steps += done;
+    }
+    sys->steps_done = sys->h_ctl->step;
+    if (sys->h_ctl->err_code) return device_error(sys);
+    remaining -= done;
+    if (!sys->h_ctl->abort) break;
+    // capacity abort: regrow and re-run the steps that did not complete
+    if (++guard > 8) {
+      sys->err = "capacity regrow did not converge";
+      return DEM_ERR_CAPACITY;
+    }
+    sys->regrows++;
+    // rows of the last successful step must become the next step's "prev" side
+    const int valid = (int)((launched_before + done - 1) & 1);
+    const int want_prev = (int)((sys->launched & 1) ^ 1);
+    if (valid != want_prev) std::swap(sys->rows[0], sys->rows[1]);
+    if (sys->h_ctl->need_entries > sys->cap_entries) {
+      long long need = sys->h_ctl->need_entries;
+      TRY(alloc_rows(sys, need + need / 4 + 1024));
+    }
+    if (sys->h_ctl->need_inserts > sys->cap_inserts) {
+      long long need = sys->h_ctl->need_inserts;
+      sys->cap_inserts = need + need / 4 + 1024;
+      TRY(alloc_arr(sys, &sys->d_items, sys->cap_inserts));
+    }
+    free_graphs(sys);
+    sys->h_ctl->abort = 0;
+    sys->h_ctl->need_entries = 0;
+    sys->h_ctl->need_inserts = 0;
+    CK(cudaMemcpyAsync(sys->d_ctl, sys->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, sys->stream));
+  }
+  return DEM_OK;
+}
+
+extern "C" dem_status dem_synchronize(dem_system* sys) {
+  if (!sys) return DEM_ERR_INVALID_ARG;
+  TRY(read_ctl(sys));
+  if (sys->h_ctl->err_code) return device_error(sys);
+  return DEM_OK;
+}
+
+extern "C" dem_status dem_get_state(dem_system* sys, int64_t cap, int64_t* n, int64_t* gid, int32_t* tid,
+                                    double* pos, double* quat, double* vel, double* omega, int32_t on_device) {
+  if (!sys) return DEM_ERR_INVALID_ARG;
+  if (n) *n = sys->n;
+  if (cap < sys->n) return (pos || quat || vel || omega || gid || tid) ? DEM_ERR_INVALID_ARG : DEM_OK;
+  CK(cudaStreamSynchronize(sys->stream));
+  const int64_t N = sys->n;
+  std::vector<double> st((size_t)13 * N);
+  if (N)
+    CK(cudaMemcpy(st.data(), sys->d_state[sys->launched & 1], sizeof(double) * 13 * N, cudaMemcpyDeviceToHost));
+  std::vector<double> out[4];
+  double* dst[4] = {pos, quat, vel, omega};
+  const int width[4] = {3, 4, 3, 3}, first[4] = {0, 3, 7, 10};
+  for (int k = 0; k < 4; ++k) {
+    if (!dst[k]) continue;
+    double* o = dst[k];
+    if (on_device) {
+      out[k].resize((size_t)width[k] * N);
+      o = out[k].data();
+    }
+    for (int64_t c = 0; c < N; ++c)
+      for (int d = 0; d < width[k]; ++d) o[width[k] * c + d] = st[(first[k] + d) * N + c];
+    if (on_device && N) CK(cudaMemcpy(dst[k], o, sizeof(double) * width[k] * N, cudaMemcpyHostToDevice));
+  }
+  if (gid) {
+    if (on_device)
+      CK(cudaMemcpy(gid, sys->h_gid.data(), sizeof(long long) * N, cudaMemcpyHostToDevice));
+    else
+      std::memcpy(gid, sys->h_gid.data(), sizeof(long long) * N);
+  }
+  if (tid) {
+    if (on_device)
+      CK(cudaMemcpy(tid, sys->h_tid.data(), sizeof(int) * N, cudaMemcpyHostToDevice));
+    else
+      std::memcpy(tid, sys->h_tid.data(), sizeof(int) * N);
+  }
+  return DEM_OK;
+}
+
+extern "C" dem_status dem_get_contacts(dem_system* sys, int64_t cap, int64_t* n, int64_t* key_a, int64_t* key_b,
+                                       double* force_on_b, double* point, double* normal, double* u_t,
+                                       double* delta) {
+  if (!sys || !n) return DEM_ERR_INVALID_ARG;
+  if ((force_on_b || point || normal || delta) && !sys->P.record_contacts) {
+    sys->err = "force/point/normal/delta need params.record_contacts = 1";
+    return DEM_ERR_INVALID_ARG;
+  }
+  CK(cudaStreamSynchronize(sys->stream));
+  if (sys->launched == 0 || sys->ns == 0) {
+    *n = 0;
+    return DEM_OK;
+  }
+  const RowBuf& R = sys->rows[(sys->launched - 1) & 1];
+  const int64_t ns = sys->ns;
+  std::vector<int> rp(ns + 1);
+  CK(cudaMemcpy(rp.data(), R.row_ptr, sizeof(int) * (ns + 1), cudaMemcpyDeviceToHost));
+  const int64_t m = rp[ns];
+  std::vector<long long> keys(m);
+  if (m) CK(cudaMemcpy(keys.data(), R.key, sizeof(long long) * m, cudaMemcpyDeviceToHost));
+  // canonical entries: own key < partner key
+  std::vector<std::pair<int64_t, int64_t>> sel;  // (own sphere, entry)
+  for (int64_t s = 0; s < ns; ++s)
+    for (int e = rp[s]; e < rp[s + 1]; ++e)
+      if (sys->h_s_key[s] < keys[e]) sel.emplace_back(s, e);
+  std::sort(sel.begin(), sel.end(), [&](const auto& x, const auto& y) {
+    long long ax = sys->h_s_key[x.first], ay = sys->h_s_key[y.first];
+    if (ax != ay) return ax < ay;
+    return keys[x.second] < keys[y.second];
+  });
+  *n = (int64_t)sel.size();
+  if (cap == 0) return DEM_OK;
+  if (cap < (int64_t)sel.size()) return DEM_ERR_INVALID_ARG;
+  auto fetch3 = [&](const double* dev, double* out) -> dem_status {
+    if (!out) return DEM_OK;
+    std::vector<double> buf((size_t)3 * m);
+    if (m) CK(cudaMemcpy(buf.data(), dev, sizeof(double) * 3 * m, cudaMemcpyDeviceToHost));
+    for (size_t k = 0; k < sel.size(); ++k)
+      for (int d = 0; d < 3; ++d) out[3 * k + d] = buf[3 * sel[k].second + d];
+    return DEM_OK;
+  };
+  for (size_t k = 0; k < sel.size(); ++k) {
+    if (key_a) key_a[k] = sys->h_s_key[sel[k].first];
+    if (key_b) key_b[k] = keys[sel[k].second];
+  }
+  TRY(fetch3(R.ut, u_t));
+  TRY(fetch3(sys->rec.F, force_on_b));
+  TRY(fetch3(sys->rec.p, point));
+  TRY(fetch3(sys->rec.n, normal));
+  if (delta) {
+    std::vector<double> buf(m);
+    if (m) CK(cudaMemcpy(buf.data(), sys->rec.delta, sizeof(double) * m, cudaMemcpyDeviceToHost));
+    for (size_t k = 0; k < sel.size(); ++k) delta[k] = buf[sel[k].second];
+  }
+  return DEM_OK;
+}
+
+extern "C" dem_status dem_get_stats(dem_system* sys, dem_stats* out) {
+  if (!sys || !out) return DEM_ERR_INVALID_ARG;
+  std::memset(out, 0, sizeof *out);
+  out->steps = sys->steps_done;
+  out->n_clumps = sys->n;
+  out->n_spheres = sys->ns;
+  out->n_cells = sys->ncell;
+  out->cell_size = sys->grid.cell;
+  out->regrows = sys->regrows;
+  out->kernel_launches_per_step = 12;
+  if (sys->launched > 0 && sys->ns > 0) {
+    const RowBuf& R = sys->rows[(sys->launched - 1) & 1];
+    int tot = 0, ins = 0;
+    CK(cudaMemcpyAsync(&tot, R.row_ptr + sys->ns, sizeof(int), cudaMemcpyDeviceToHost, sys->stream));
+    CK(cudaMemcpyAsync(&ins, sys->d_cell_start + sys->ncell, sizeof(int), cudaMemcpyDeviceToHost, sys->stream));
+    CK(cudaMemsetAsync(sys->d_counter, 0, sizeof(unsigned long long), sys->stream));
+    launch_count_walls(Rows{R.row_ptr, R.partner, R.key, R.ut}, (int)sys->ns, sys->d_counter, sys->stream);
+    unsigned long long walls = 0;
+    CK(cudaMemcpyAsync(&walls, sys->d_counter, sizeof(walls), cudaMemcpyDeviceToHost, sys->stream));
+    CK(cudaStreamSynchronize(sys->stream));
+    out->n_entries = tot;
+    out->n_inserts = ins;
+    out->n_contacts = (int64_t)walls + ((int64_t)tot - (int64_t)walls) / 2;
+  }
+  return DEM_OK;
+}
+
+extern "C" dem_status dem_set_profiling(dem_system* sys, int32_t enable) {
+  if (!sys) return DEM_ERR_INVALID_ARG;
+  sys->profiling = enable != 0;
+  for (int s = 0; s < kStages; ++s) sys->stage_ms[s] = 0;
+  sys->prof_steps = 0;
+  return DEM_OK;
+}
+
+extern "C" dem_status dem_get_stage_times(dem_system* sys, int32_t n_stages, double* ms) {
+  if (!sys || !ms) return DEM_ERR_INVALID_ARG;
+  for (int s = 0; s < n_stages && s < kStages; ++s) ms[s] = sys->prof_steps ? sys->stage_ms[s] / sys->prof_steps : 0.0;
+  return DEM_OK;
+}

@@ -303,6 +303,65 @@ def rsa_bed(seed: int, n_clumps: int, lo, hi, per_comp_mat: bool = False, vz: fl
                  omega=om, name=f"rsa-bed-{n_clumps}")
 
 
+def rsa_bed_exact(seed: int, n_clumps: int, lo, hi, per_comp_mat: bool = False, vz: float = 0.0,
+                  h: float = 1e-6, clearance: float = 0.05e-3, max_tries: int = 5000) -> Scene:
+    """RSA with the clumps' actual component spheres (not bounding spheres): denser spawn.
+
+    Clumps are placed largest type first at uniform random poses inside [lo, hi]; a pose
+    is accepted when every component sphere clears every placed sphere by `clearance`
+    and stays inside the box.  Sphere centres for the test use scipy's Rotation, so
+    this module still holds none of the method's own arithmetic.
+    """
+    from scipy.spatial.transform import Rotation
+
+    rng = np.random.default_rng(seed)
+    templates = ds_templates(per_component_materials=per_comp_mat)
+    counts = ds_type_counts(n_clumps)
+    types = np.concatenate([np.full(c, t, dtype=np.int32) for t, c in enumerate(counts)])
+    lo, hi = np.asarray(lo, float), np.asarray(hi, float)
+    n_sph = int(sum(templates[t].n_comp for t in types))
+    S = np.full((n_sph, 3), 1e9)
+    Sr = np.zeros(n_sph)
+    ns = 0
+    P = np.zeros((n_clumps, 3))
+    Q = np.zeros((n_clumps, 4))
+    for k, t in enumerate(types):
+        tpl = templates[t]
+        rb = tpl.bounding_radius
+        ok = False
+        for _ in range(max_tries):
+            p = rng.uniform(lo + rb * np.array([0.3, 0.3, 0.3]), hi - rb * np.array([0.3, 0.3, 0.3]))
+            q = random_quaternions(rng, 1)[0]
+            c = p + Rotation.from_quat(q[[1, 2, 3, 0]]).apply(tpl.offsets)
+            r = tpl.radius
+            if np.any(c - r[:, None] < lo + clearance) or np.any(c + r[:, None] > hi - clearance):
+                continue
+            if ns:
+                near = np.all(np.abs(S[:ns] - p) < rb + 3.7e-3 + clearance, axis=1)
+                if near.any():
+                    d = np.linalg.norm(S[:ns][near][None, :, :] - c[:, None, :], axis=-1)
+                    if np.any(d < r[:, None] + Sr[:ns][near][None, :] + clearance):
+                        continue
+            ok = True
+            break
+        if not ok:
+            raise RuntimeError(f"RSA could not place clump {k} of {n_clumps}")
+        S[ns:ns + tpl.n_comp] = c
+        Sr[ns:ns + tpl.n_comp] = tpl.radius
+        ns += tpl.n_comp
+        P[k], Q[k] = p, q
+    gid, tid, pos, quat, vel, om = _mk_state(n_clumps)
+    perm = rng.permutation(n_clumps)
+    tid[:] = types[perm]
+    pos[:] = P[perm]
+    quat[:] = Q[perm]
+    vel[:, 2] = vz
+    mats = C4_MATERIALS if per_comp_mat else [M0]
+    return Scene(materials=np.array(mats), templates=templates, planes=box_planes(lo, hi, 0, top=False), h=h,
+                 gravity=np.array([0.0, 0.0, -9.81]), domain_lo=lo - 1e-3, domain_hi=hi + np.array([1e-3, 1e-3, 0.05]),
+                 gid=gid, tid=tid, pos=pos, quat=quat, vel=vel, omega=om, name=f"rsa-exact-{n_clumps}")
+
+
 def c3_repose(seed: int = 3, n_clumps: int = 100_000, h: float = 1e-6) -> Scene:
     """Config 3: 100k DS clumps in a vertical cylinder r = 0.06 m above the plane z = 0,
     solid fraction of bounding spheres ~0.25 (column ~0.57 m); far walls at +-0.3 m."""
