@@ -1,0 +1,298 @@
+#!/usr/bin/env python
+"""Benchmark of the clump-DEM hot path: sphere-steps/s on the VIPER-scale bed (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5|c4|c3|c1] [--impl ours|reference]
+
+A "step" is one pass of the whole per-step hot path (poses,
+binning, narrow phase, history remap, forces, reduction, integration) over every sphere
+of the bed, contact set rebuilt every step (k = 1).  At N = 1 the workload is
+config 5, the ~11.34M-clump / ~34.7M-sphere bed the metric is quoted on (it fits one
+B200).  Inputs are resident in HBM when the timed region starts; the state and contact
+rows (> 10 GB) are far larger than L2, so no L2 flush is needed.  Rank 0 prints one
+JSON line.  `--impl reference` times the CPU oracle (test infrastructure) on a bounded
+crop of the same bed instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sphere-steps/sec (device-timed, max over ranks) at 1/2/4/8 B200; % HBM roofline"
+UNIT = "sphere-steps/s"
+FALLBACK_HBM = 6650.0  # B200_PROFILING.md fallback, GB/s
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+# ---------------------------------------------------------------- workloads
+def make_scene(name: str):
+    import workloads as w
+    from workloads import beds
+
+    if name == "c5":
+        return beds.c5_bed()
+    if name == "c4":
+        return beds.c4_bed()
+    if name == "c3":
+        return w.c3_repose()
+    if name == "c1":
+        return w.c1_box()
+    raise ValueError(name)
+
+
+def sample_crop(scene, side=0.03):
+    """A bounded sample of the bed for the CPU oracle: one full-depth side x side column."""
+    from workloads import beds
+
+    c = 0.5 * (scene.domain_lo + scene.domain_hi)
+    lo = np.array([c[0] - side / 2, c[1] - side / 2, -1.0])
+    hi = np.array([c[0] + side / 2, c[1] + side / 2, 10.0])
+    return beds.crop(scene, lo, hi)
+
+
+def oracle_rate(scene, budget_s=15.0, warm=2):
+    """sphere-steps/s of the CPU oracle (single thread, as it stands) on `scene`."""
+    import oracle
+
+    o = oracle.Oracle(scene, detect=1)
+    o.step(warm)
+    t0 = time.perf_counter()
+    o.step(1)
+    t1 = time.perf_counter() - t0
+    steps = max(1, int(budget_s / max(t1, 1e-4)))
+    t0 = time.perf_counter()
+    o.step(steps)
+    dt = time.perf_counter() - t0
+    return scene.n_spheres * steps / dt, steps, dt
+
+
+# ---------------------------------------------------------------- algorithmic bytes
+def stage_bytes(st):
+    """Minimum DRAM bytes each stage must move for its function, per launch."""
+    n, ns, nc = st["n_clumps"], st["n_spheres"], st["n_cells"]
+    ins, ent = st["n_inserts"], st["n_entries"]
+    pairs = ent - st["n_contacts"]  # entries = walls + 2 pairs, contacts = walls + pairs
+    return {
+        "pose+bin_count": n * 188 + ns * 44 + nc * 8,
+        "bin_scan": nc * 8,
+        "bin_scatter": ns * 32 + nc * 12 + ins * 4,
+        "pairs": nc * 4 + ins * 40 + pairs * 16,
+        "row_scan": ns * 8,
+        "rows_scatter": pairs * 72,
+        "rows_finish": ns * 40 + ent * 24,
+        "force": ns * (32 + 8 + 16 + 48) + n * 80 + ent * 68,
+        "integrate": n * (104 + 104 + 8) + ns * 48,
+    }
+
+
+def survey_bytes_per_sphere_step(c, k=1):
+    """B(c,k) = 69.3 + 56 c + (31.6 + 16 c)/k bytes per sphere-step."""
+    return 69.3 + 56.0 * c + (31.6 + 16.0 * c) / k
+
+
+# ---------------------------------------------------------------- clocks
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.p = None
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if not self.p:
+            return None
+        time.sleep(0.3)
+        self.p.terminate()
+        out = self.p.communicate(timeout=10)[0]
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for nme, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nme)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    scene = make_scene(a.config)
+    crop = sample_crop(scene) if a.config in ("c5", "c4", "c3") else scene
+    import oracle
+
+    o = oracle.Oracle(crop, detect=1)
+    o.step(a.warmup)
+    t0 = time.perf_counter()
+    o.step(a.steps)
+    dt = time.perf_counter() - t0
+    v = crop.n_spheres * a.steps / dt
+    sample = f"{crop.n_clumps} clumps / {crop.n_spheres} spheres: 30x30 mm full-depth column of {scene.name}"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": dt / a.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": scene.name, "sample": sample, "parallelism": "cpu-1thread"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(a):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world,
+                              "error": "multi-GPU slab decomposition is not built yet (round 1: single GPU)"}))
+        return
+    import paper_2307_03445_b200 as dem
+
+    torch.cuda.set_device(0)
+    t_setup = time.perf_counter()
+    scene = make_scene(a.config)
+    sys_ = dem.system_from_scene(scene, record_contacts=False, cell_size=a.cell_size)
+    stream = sys_.stream
+    sys_.dem_step(a.warmup)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t_setup
+
+    # ---------------- timed region: K steps, stage events on the system stream
+    sys_.dem_set_profiling(True)
+    clk = Clocks(0)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    sys_.dem_step(a.steps)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    clocks = clk.stop()
+    stages = sys_.dem_get_stage_times()
+    sys_.dem_set_profiling(False)
+    st = sys_.dem_get_stats()
+    ns = st["n_spheres"]
+    value = ns * a.steps / (ms * 1e-3)
+
+    # ---------------- roofline of the dominant kernel
+    peak, peak_kind = peaks()
+    sb = stage_bytes(st)
+    dom = max(stages, key=stages.get)
+    achieved = sb[dom] / (stages[dom] * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(a.config, {}).get(dom)
+        except Exception:
+            traffic = None
+    c = st["n_contacts"] / max(ns, 1)
+    step_bytes = survey_bytes_per_sphere_step(c) * ns
+
+    # ---------------- e2e through the C-ABI with host buffers (pinned)
+    pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()  # noqa: E731
+    hs = {k: pin(getattr(scene, k)) for k in ("gid", "tid", "pos", "quat", "vel", "omega")}
+    h2d = sum(v.nbytes for v in hs.values())
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    sys_.dem_set_state(hs["gid"], hs["tid"], hs["pos"], hs["quat"], hs["vel"], hs["omega"])
+    sys_.dem_step(a.steps)
+    out = sys_.dem_get_state()
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    d2h = sum(v.nbytes for v in out.values())
+    e2e = {"value": ns * a.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d / a.steps,
+           "d2h_bytes_per_step": d2h / a.steps,
+           "note": "dem_set_state(host) + dem_step(K) + dem_get_state(host), wall clock, per-step bytes = total/K"}
+
+    # ---------------- CPU oracle baseline on a bounded sample of the same bed
+    cpu = None
+    if not a.no_cpu_baseline:
+        crop = sample_crop(scene) if a.config in ("c5", "c4", "c3") else scene
+        v_cpu, steps_cpu, dt_cpu = oracle_rate(crop, budget_s=a.cpu_budget)
+        cpu = {"value": v_cpu, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{steps_cpu} oracle steps ({dt_cpu:.1f} s) of a 30x30 mm full-depth column "
+                         f"({crop.n_clumps} clumps / {crop.n_spheres} spheres) of the same bed"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": scene.name, "clumps": st["n_clumps"], "spheres": ns,
+                   "contacts_per_sphere": c, "directed_entries": st["n_entries"], "bin_inserts": st["n_inserts"],
+                   "cell_size_m": st["cell_size"], "rebuild_every": 1, "h": scene.h,
+                   "l2": "inputs larger than L2 (state + rows > 10 GB); no flush",
+                   "parallelism": "single-gpu", "setup_s": round(setup_s, 1)},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "alg_bytes_per_launch": sb[dom], "avg_launch_ms": stages[dom]},
+        "step_roofline": {"bytes_per_sphere_step": survey_bytes_per_sphere_step(c),
+                          "achieved_gbs": step_bytes / (ms / a.steps * 1e-3) / 1e9,
+                          "frac": step_bytes / (ms / a.steps * 1e-3) / 1e9 / peak},
+        "stage_ms": stages,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": int(st["kernel_launches_per_step"]) * a.steps,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="c5", choices=["c5", "c4", "c3", "c1"])
+    ap.add_argument("--cell-size", type=float, default=0.0)
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    a = ap.parse_args()
+    if a.warmup < 3:
+        a.warmup = 3
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

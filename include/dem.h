@@ -152,8 +152,9 @@ dem_status dem_get_stats(dem_system* sys, dem_stats* out);
 /* Stage profiling.  With enable = 1, dem_step launches the step kernels directly (no graph) with
  * CUDA events between the stages on the system stream and accumulates each stage's device time;
  * enable resets the accumulators.  dem_get_stage_times returns the mean ms per step of each stage,
- * in the order: pose+bin-count, bin-offset scan, bin scatter, narrow count, row-offset scan,
- * narrow fill + row sort, force (remap + contact forces + per-sphere sums), reduce + integrate. */
+ * in the order: pose+bin-count, bin-offset scan, bin scatter, per-bin pair tests, row-offset scan,
+ * row scatter, wall entries + row sort, force (remap + contact forces + per-sphere sums),
+ * reduce + integrate. */
 dem_status dem_set_profiling(dem_system* sys, int32_t enable);
 dem_status dem_get_stage_times(dem_system* sys, int32_t n_stages, double* ms);
 

@@ -102,8 +102,8 @@ def _f64(a, shape=None):
     return a if shape is None else a.reshape(shape)
 
 
-STAGES = ["pose+bin_count", "bin_scan", "bin_scatter", "narrow_count", "row_scan", "narrow_fill", "force",
-          "integrate"]
+STAGES = ["pose+bin_count", "bin_scan", "bin_scatter", "pairs", "row_scan", "rows_scatter", "rows_finish",
+          "force", "integrate"]
 
 
 class System:

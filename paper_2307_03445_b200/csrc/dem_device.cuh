@@ -7,9 +7,11 @@
 // HBM layout:
 //   clump state   SoA fp64, 13 arrays (x,y,z, qw,qx,qy,qz, vx,vy,vz, wx,wy,wz), ping-pong
 //   clump aux     tid (i32), gid (i64), sphere offset (i32, n+1), omega_world (3 x fp64, per step)
-//   sphere        clump (i32), template-component (i32), key (i64), centre (3 x fp64 SoA),
+//   clump kin     packed per step: X, V, omega_world, mass (10 fp64 AoS) for coalesced partner gathers
+//   sphere        clump (i32), template-component (i32), key (i64), (x,y,z,r) (double4 AoS),
 //                 partial force/torque (3+3 fp64 SoA)
 //   bins          cell_count (i32, ncell), cell_start (i32, ncell+1), items (i32, n_inserts)
+//   pairs         unordered candidate pairs of the step (int2), built by the per-bin warps
 //   rows (x2)     CSR by own sphere: row_ptr (i32, ns+1), partner (i32), key (i64), u_t (3 fp64 AoS)
 #pragma once
 #include <cstdint>
@@ -31,7 +33,10 @@ struct Ctl {
   long long step;     // steps completed since dem_set_state
   long long need_inserts;
   long long need_entries;
+  long long need_pairs;
 };
+
+constexpr int kKin = 10;  // doubles per clump in the packed kinematics record
 
 struct Tables {
   const double* tc_off;   // [3 * n_tc] body-frame offsets, AoS
@@ -91,16 +96,19 @@ struct StepArgs {
   const int* tid;
   const long long* gid;
   const int* sph_off;
-  double *wwx, *wwy, *wwz;   // omega_world of cur
   const int* s_clump;
   const int* s_tc;
   const long long* s_key;
-  double *sx, *sy, *sz;      // sphere centres
+  double4* spos;             // sphere (x, y, z, r), written by the pose kernel each step
+  double* kin;               // per clump [kKin]: X(3), V(3), omega_world(3), mass
   double *sfx, *sfy, *sfz, *stx, *sty, *stz;  // per-sphere force / torque (world, about COM)
   int* cell_count;
   int* cell_start;
   int* items;
-  int* row_cnt;
+  int* row_cnt;              // walls + sphere partners per sphere (built by atomics each step)
+  int2* pairs;               // unordered candidate pairs of the step
+  unsigned long long* pair_cursor;
+  long long cap_pairs;
   Rows rows, prev;
   Record rec;
   int record;

@@ -1,38 +1,55 @@
-// kernels_detect.cu — (a1) sphere poses, (a2) multi-insert binning, (a3) narrow phase.
+// kernels_detect.cu — (a1) sphere poses, (a2) multi-insert binning, (a3) narrow phase + rows.
 //
 // PAPER.md:142 ("identifying the active set represents a significant computational
 // bottleneck"), P:145 (per-step rebuild), P:69 (binning CD following hammadTobyDan2012:
-// every body is inserted into each bin its AABB overlaps).  Readings: DESIGN.md §3
-// R14 (predicate d.d <= (r_a + r_b + margin)^2 in fp64, no FMA), R15 (no intra-clump
-// pairs), R22 (sphere centre c = X + R(q) o).
+// every body is inserted into each bin its AABB overlaps, pairs are tested per bin).
+// Readings: DESIGN.md §3 R14 (predicate d.d <= (r_a + r_b + margin)^2 in fp64, no FMA),
+// R15 (no intra-clump pairs), R22 (sphere centre c = X + R(q) o, explicit roundings).
+//
+// Pipeline of one rebuild:
+//   k_pose_count    per sphere: centre, (x,y,z,r) record, wall candidates -> row_cnt,
+//                   bin counts; component 0 packs the clump kinematics record
+//   scan            bin offsets
+//   k_bin_scatter   per sphere: bin item lists (slots by decrementing the counts)
+//   k_pairs         one warp per bin: members staged in shared memory, every unordered
+//                   pair of the bin tested once by one lane, kept only in the bin of the
+//                   minimum corner of the two AABBs' bin-range intersection (so each pair
+//                   is found exactly once grid-wide); hits compacted with warp ballots
+//                   into a per-warp shared buffer, flushed with one atomic per 128 pairs
+//   scan            row offsets
+//   k_rows_scatter  per pair: both directed entries placed into their rows
+//   k_rows_finish   per sphere: wall entries + row sorted by partner key
 #include "dem_device.cuh"
 
 namespace dem {
 
 // ---------------------------------------------------------------- (a1) + bin count
-// One thread per sphere: c = X + R(q) o (explicit roundings), store the centre, count
-// the bins its enlarged AABB overlaps.  Component 0 also stores omega_world = R Omega.
 __global__ void __launch_bounds__(256) k_pose_count(StepArgs a) {
   if (a.ctl->abort) return;
   int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) *a.pair_cursor = 0ull;
   if (i >= a.ns) return;
-  int c = a.s_clump[i];
-  int tc = a.s_tc[i];
-  double qw = a.cur.qw[c], qx = a.cur.qx[c], qy = a.cur.qy[c], qz = a.cur.qz[c];
+  const int c = a.s_clump[i];
+  const int tc = a.s_tc[i];
+  const double qw = a.cur.qw[c], qx = a.cur.qx[c], qy = a.cur.qy[c], qz = a.cur.qz[c];
   double R[9];
   quat_R(qw, qx, qy, qz, R);
-  double ox = a.tab.tc_off[3 * tc], oy = a.tab.tc_off[3 * tc + 1], oz = a.tab.tc_off[3 * tc + 2];
-  double cx = add(a.cur.x[c], row_dot(R, ox, oy, oz));
-  double cy = add(a.cur.y[c], row_dot(R + 3, ox, oy, oz));
-  double cz = add(a.cur.z[c], row_dot(R + 6, ox, oy, oz));
-  a.sx[i] = cx;
-  a.sy[i] = cy;
-  a.sz[i] = cz;
+  const double ox = a.tab.tc_off[3 * tc], oy = a.tab.tc_off[3 * tc + 1], oz = a.tab.tc_off[3 * tc + 2];
+  const double X = a.cur.x[c], Y = a.cur.y[c], Z = a.cur.z[c];
+  const double cx = add(X, row_dot(R, ox, oy, oz));
+  const double cy = add(Y, row_dot(R + 3, ox, oy, oz));
+  const double cz = add(Z, row_dot(R + 6, ox, oy, oz));
+  const double r = a.tab.tc_rad[tc];
+  a.spos[i] = make_double4(cx, cy, cz, r);
   if (tc == a.tab.tpl_coff[a.tid[c]]) {
-    double wx = a.cur.wx[c], wy = a.cur.wy[c], wz = a.cur.wz[c];
-    a.wwx[c] = R[0] * wx + R[1] * wy + R[2] * wz;
-    a.wwy[c] = R[3] * wx + R[4] * wy + R[5] * wz;
-    a.wwz[c] = R[6] * wx + R[7] * wy + R[8] * wz;
+    const double wx = a.cur.wx[c], wy = a.cur.wy[c], wz = a.cur.wz[c];
+    double* k = a.kin + (size_t)kKin * c;
+    k[0] = X; k[1] = Y; k[2] = Z;
+    k[3] = a.cur.vx[c]; k[4] = a.cur.vy[c]; k[5] = a.cur.vz[c];
+    k[6] = R[0] * wx + R[1] * wy + R[2] * wz;
+    k[7] = R[3] * wx + R[4] * wy + R[5] * wz;
+    k[8] = R[6] * wx + R[7] * wy + R[8] * wz;
+    k[9] = a.tab.tpl_mass[a.tid[c]];
   }
   const Grid& g = a.grid;
   if (!(cx >= g.dom_lo[0] && cx <= g.dom_hi[0] && cy >= g.dom_lo[1] && cy <= g.dom_hi[1] &&
@@ -40,14 +57,22 @@ __global__ void __launch_bounds__(256) k_pose_count(StepArgs a) {
     raise_error(a.ctl, -10, a.s_key[i], a.gid[c]);
     return;
   }
-  double r = a.tab.tc_rad[tc];
+  // sphere-plane candidates: (r + margin) - (c - p_w).n_w >= 0
+  int walls = 0;
+  for (int p = 0; p < a.tab.n_planes; ++p) {
+    const double* pp = a.tab.plane_pt[p];
+    const double* nw = a.tab.plane_n[p];
+    const double dd = add(add(mul(sub(cx, pp[0]), nw[0]), mul(sub(cy, pp[1]), nw[1])), mul(sub(cz, pp[2]), nw[2]));
+    walls += sub(add(r, a.margin), dd) >= 0.0;
+  }
+  a.row_cnt[i] = walls;
   int lx, hx, ly, hy, lz, hz;
   cell_range(g, 0, cx, r, lx, hx);
   cell_range(g, 1, cy, r, ly, hy);
   cell_range(g, 2, cz, r, lz, hz);
   for (int z = lz; z <= hz; ++z)
     for (int y = ly; y <= hy; ++y) {
-      long long base = ((long long)z * g.n[1] + y) * g.n[0];
+      const long long base = ((long long)z * g.n[1] + y) * g.n[0];
       for (int x = lx; x <= hx; ++x) atomicAdd(&a.cell_count[base + x], 1);
     }
 }
@@ -57,115 +82,202 @@ __global__ void __launch_bounds__(256) k_pose_count(StepArgs a) {
 // next step.  The order inside a bin is irrelevant: rows are sorted by partner key.
 __global__ void __launch_bounds__(256) k_bin_scatter(StepArgs a) {
   if (a.ctl->abort) return;
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.ns) return;
-  bool fits = (long long)a.cell_start[a.ncell] <= a.cap_inserts;
-  double r = a.tab.tc_rad[a.s_tc[i]];
+  const bool fits = (long long)a.cell_start[a.ncell] <= a.cap_inserts;
+  const double4 s = a.spos[i];
   const Grid& g = a.grid;
   int lx, hx, ly, hy, lz, hz;
-  cell_range(g, 0, a.sx[i], r, lx, hx);
-  cell_range(g, 1, a.sy[i], r, ly, hy);
-  cell_range(g, 2, a.sz[i], r, lz, hz);
+  cell_range(g, 0, s.x, s.w, lx, hx);
+  cell_range(g, 1, s.y, s.w, ly, hy);
+  cell_range(g, 2, s.z, s.w, lz, hz);
   for (int z = lz; z <= hz; ++z)
     for (int y = ly; y <= hy; ++y) {
-      long long base = ((long long)z * g.n[1] + y) * g.n[0];
+      const long long base = ((long long)z * g.n[1] + y) * g.n[0];
       for (int x = lx; x <= hx; ++x) {
-        long long cid = base + x;
-        int slot = atomicSub(&a.cell_count[cid], 1) - 1;
+        const long long cid = base + x;
+        const int slot = atomicSub(&a.cell_count[cid], 1) - 1;
         if (fits) a.items[a.cell_start[cid] + slot] = i;
       }
     }
 }
 
-// ---------------------------------------------------------------- (a3) narrow phase
-// Every candidate pair (a, b) is reported by thread a exactly once: in the bin that
-// holds the minimum corner of the two AABBs' bin-range intersection (so both directed
-// rows a->b and b->a are produced, by threads a and b, with the same predicate).
-template <bool kFill>
-__device__ __forceinline__ int narrow_row(const StepArgs& a, int i, int* out_partner, long long* out_key) {
-  const Grid& g = a.grid;
-  int ci = a.s_clump[i];
-  double cx = a.sx[i], cy = a.sy[i], cz = a.sz[i];
-  double r = a.tab.tc_rad[a.s_tc[i]];
-  int lx, hx, ly, hy, lz, hz;
-  cell_range(g, 0, cx, r, lx, hx);
-  cell_range(g, 1, cy, r, ly, hy);
-  cell_range(g, 2, cz, r, lz, hz);
-  int cnt = 0;
-  for (int z = lz; z <= hz; ++z)
-    for (int y = ly; y <= hy; ++y) {
-      long long base = ((long long)z * g.n[1] + y) * g.n[0];
-      for (int x = lx; x <= hx; ++x) {
-        long long cid = base + x;
-        int k0 = a.cell_start[cid], k1 = a.cell_start[cid + 1];
-        for (int k = k0; k < k1; ++k) {
-          int b = a.items[k];
-          if (b == i || a.s_clump[b] == ci) continue;
-          double bx = a.sx[b], by = a.sy[b], bz = a.sz[b];
-          double rb = a.tab.tc_rad[a.s_tc[b]];
-          // dedupe: only in the bin of the range intersection's minimum corner
-          if (max(lx, cell_lo(g, 0, bx, rb)) != x || max(ly, cell_lo(g, 1, by, rb)) != y ||
-              max(lz, cell_lo(g, 2, bz, rb)) != z)
-            continue;
-          double dx = sub(bx, cx), dy = sub(by, cy), dz = sub(bz, cz);
-          double d2 = add(add(mul(dx, dx), mul(dy, dy)), mul(dz, dz));
-          double s = add(add(r, rb), a.margin);
-          if (d2 <= mul(s, s)) {
-            if (kFill) {
-              out_partner[cnt] = b;
-              out_key[cnt] = a.s_key[b];
-            }
-            ++cnt;
-          }
-        }
-      }
-    }
-  // sphere-plane candidates: (r + margin) - (c - p_w).n_w >= 0
-  for (int p = 0; p < a.tab.n_planes; ++p) {
-    const double* pp = a.tab.plane_pt[p];
-    const double* nw = a.tab.plane_n[p];
-    double dd = add(add(mul(sub(cx, pp[0]), nw[0]), mul(sub(cy, pp[1]), nw[1])), mul(sub(cz, pp[2]), nw[2]));
-    if (sub(add(r, a.margin), dd) >= 0.0) {
-      if (kFill) {
-        out_partner[cnt] = -1 - p;
-        out_key[cnt] = (long long)(0x7fffffffffffffffLL - p);
-      }
-      ++cnt;
-    }
-  }
-  return cnt;
+// ---------------------------------------------------------------- (a3) per-bin pair tests
+constexpr int kPairWarps = 8;
+constexpr int kPairBuf = 128;
+
+struct Member {
+  double4 p;  // x, y, z, r
+  int clump;
+  int idx;
+  int lo[3];
+  int pad;
+};
+
+__device__ __forceinline__ void load_member(const StepArgs& a, Member& m, int idx) {
+  const double4 p = a.spos[idx];
+  m.p = p;
+  m.idx = idx;
+  m.clump = a.s_clump[idx];
+  m.lo[0] = cell_lo(a.grid, 0, p.x, p.w);
+  m.lo[1] = cell_lo(a.grid, 1, p.y, p.w);
+  m.lo[2] = cell_lo(a.grid, 2, p.z, p.w);
 }
 
-__global__ void __launch_bounds__(256) k_narrow_count(StepArgs a) {
+// p -> (i, j), 0 <= i < j, p = j (j - 1) / 2 + i
+__device__ __forceinline__ void decode_tri(int p, int& i, int& j) {
+  int jj = (int)((1.0f + sqrtf(1.0f + 8.0f * (float)p)) * 0.5f);
+  while (jj * (jj - 1) / 2 > p) --jj;
+  while ((jj + 1) * jj / 2 <= p) ++jj;
+  j = jj;
+  i = p - jj * (jj - 1) / 2;
+}
+
+__device__ __forceinline__ void flush_pairs(const StepArgs& a, int2* bf, int n, int lane) {
+  __syncwarp();
+  if (n == 0) return;
+  unsigned long long off = 0;
+  if (lane == 0) off = atomicAdd(a.pair_cursor, (unsigned long long)n);
+  off = __shfl_sync(0xffffffffu, off, 0);
+  for (int k = lane; k < n; k += 32)
+    if ((long long)(off + k) < a.cap_pairs) a.pairs[off + k] = bf[k];
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(kPairWarps * 32) k_pairs(StepArgs a) {
+  __shared__ Member smA[kPairWarps][32];
+  __shared__ Member smB[kPairWarps][32];
+  __shared__ int2 sbuf[kPairWarps][kPairBuf];
   if (a.ctl->abort) return;
   if ((long long)a.cell_start[a.ncell] > a.cap_inserts) {
     a.ctl->need_inserts = a.cell_start[a.ncell];
     atomicExch(&a.ctl->abort, 1);
     return;
   }
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.ns) return;
-  a.row_cnt[i] = narrow_row<false>(a, i, nullptr, nullptr);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  Member* A = smA[w];
+  Member* B = smB[w];
+  int2* bf = sbuf[w];
+  int nbuf = 0;  // warp-uniform
+  const Grid& g = a.grid;
+  const long long nw = (long long)gridDim.x * kPairWarps;
+  for (long long cid = (long long)blockIdx.x * kPairWarps + w; cid < a.ncell; cid += nw) {
+    const int k0 = a.cell_start[cid];
+    const int m = a.cell_start[cid + 1] - k0;
+    if (m < 2) continue;
+    const int cx = (int)(cid % g.n[0]);
+    const long long rest = cid / g.n[0];
+    const int cy = (int)(rest % g.n[1]);
+    const int cz = (int)(rest / g.n[1]);
+    for (int ib = 0; ib < m; ib += 32) {
+      const int mi = min(32, m - ib);
+      __syncwarp();
+      if (lane < mi) load_member(a, A[lane], a.items[k0 + ib + lane]);
+      for (int jb = ib; jb < m; jb += 32) {
+        const int mj = min(32, m - jb);
+        const bool same = jb == ib;
+        const Member* Bp = same ? A : B;
+        if (!same) {
+          __syncwarp();
+          if (lane < mj) load_member(a, B[lane], a.items[k0 + jb + lane]);
+        }
+        __syncwarp();
+        const int np = same ? mi * (mi - 1) / 2 : mi * mj;
+        for (int base = 0; base < np; base += 32) {
+          const int p = base + lane;
+          bool hit = false;
+          int ia = 0, ibx = 0;
+          if (p < np) {
+            int i, j;
+            if (same) {
+              decode_tri(p, i, j);
+            } else {
+              i = p / mj;
+              j = p - i * mj;
+            }
+            const Member& u = A[i];
+            const Member& v = Bp[j];
+            if (u.clump != v.clump && max(u.lo[0], v.lo[0]) == cx && max(u.lo[1], v.lo[1]) == cy &&
+                max(u.lo[2], v.lo[2]) == cz) {
+              const double dx = sub(v.p.x, u.p.x), dy = sub(v.p.y, u.p.y), dz = sub(v.p.z, u.p.z);
+              const double d2 = add(add(mul(dx, dx), mul(dy, dy)), mul(dz, dz));
+              const double s = add(add(u.p.w, v.p.w), a.margin);
+              hit = d2 <= mul(s, s);
+              ia = u.idx;
+              ibx = v.idx;
+            }
+          }
+          const unsigned mask = __ballot_sync(0xffffffffu, hit);
+          if (mask) {
+            const int cnt = __popc(mask);
+            if (nbuf + cnt > kPairBuf) {
+              flush_pairs(a, bf, nbuf, lane);
+              nbuf = 0;
+            }
+            if (hit) {
+              bf[nbuf + __popc(mask & ((1u << lane) - 1u))] = make_int2(ia, ibx);
+              atomicAdd(&a.row_cnt[ia], 1);
+              atomicAdd(&a.row_cnt[ibx], 1);
+            }
+            nbuf += cnt;
+          }
+        }
+      }
+    }
+  }
+  flush_pairs(a, bf, nbuf, lane);
 }
 
-__global__ void __launch_bounds__(256) k_narrow_fill(StepArgs a) {
+// ---------------------------------------------------------------- rows
+// per pair: both directed entries, slots taken by decrementing row_cnt (walls stay in front)
+__global__ void __launch_bounds__(256) k_rows_scatter(StepArgs a) {
   if (a.ctl->abort) return;
-  int total = a.rows.row_ptr[a.ns];
-  if ((long long)total > a.cap_entries) {
-    a.ctl->need_entries = total;
+  const unsigned long long np = *a.pair_cursor;
+  const int total = a.rows.row_ptr[a.ns];
+  if ((long long)np > a.cap_pairs || (long long)total > a.cap_entries) {
+    if ((long long)np > a.cap_pairs) a.ctl->need_pairs = (long long)np;
+    if ((long long)total > a.cap_entries) a.ctl->need_entries = total;
     atomicExch(&a.ctl->abort, 1);
     return;
   }
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < (long long)np; t += stride) {
+    const int2 pr = a.pairs[t];
+    const int sa = atomicSub(&a.row_cnt[pr.x], 1) - 1;
+    const int sb = atomicSub(&a.row_cnt[pr.y], 1) - 1;
+    const int ea = a.rows.row_ptr[pr.x] + sa;
+    const int eb = a.rows.row_ptr[pr.y] + sb;
+    a.rows.partner[ea] = pr.y;
+    a.rows.key[ea] = a.s_key[pr.y];
+    a.rows.partner[eb] = pr.x;
+    a.rows.key[eb] = a.s_key[pr.x];
+  }
+}
+
+// per sphere: wall entries in front, then the whole row sorted by partner key
+__global__ void __launch_bounds__(256) k_rows_finish(StepArgs a) {
+  if (a.ctl->abort) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.ns) return;
-  int beg = a.rows.row_ptr[i];
+  const int beg = a.rows.row_ptr[i];
+  const int m = a.rows.row_ptr[i + 1] - beg;
   int* P = a.rows.partner + beg;
   long long* K = a.rows.key + beg;
-  int m = narrow_row<true>(a, i, P, K);
-  // insertion sort of the row by partner key (rows are short: ~2c + walls entries)
+  const double4 s = a.spos[i];
+  int w = 0;
+  for (int p = 0; p < a.tab.n_planes; ++p) {
+    const double* pp = a.tab.plane_pt[p];
+    const double* nw = a.tab.plane_n[p];
+    const double dd = add(add(mul(sub(s.x, pp[0]), nw[0]), mul(sub(s.y, pp[1]), nw[1])), mul(sub(s.z, pp[2]), nw[2]));
+    if (sub(add(s.w, a.margin), dd) >= 0.0) {
+      P[w] = -1 - p;
+      K[w] = (long long)(0x7fffffffffffffffLL - p);
+      ++w;
+    }
+  }
   for (int u = 1; u < m; ++u) {
-    long long kk = K[u];
-    int pp = P[u];
+    const long long kk = K[u];
+    const int pp = P[u];
     int v = u - 1;
     while (v >= 0 && K[v] > kk) {
       K[v + 1] = K[v];
@@ -179,16 +291,24 @@ __global__ void __launch_bounds__(256) k_narrow_fill(StepArgs a) {
 
 // host launchers
 void launch_pose_count(const StepArgs& a, cudaStream_t s) {
-  if (a.ns) k_pose_count<<<(a.ns + 255) / 256, 256, 0, s>>>(a);
+  k_pose_count<<<a.ns ? (a.ns + 255) / 256 : 1, 256, 0, s>>>(a);
 }
 void launch_bin_scatter(const StepArgs& a, cudaStream_t s) {
   if (a.ns) k_bin_scatter<<<(a.ns + 255) / 256, 256, 0, s>>>(a);
 }
-void launch_narrow_count(const StepArgs& a, cudaStream_t s) {
-  if (a.ns) k_narrow_count<<<(a.ns + 255) / 256, 256, 0, s>>>(a);
+void launch_pairs(const StepArgs& a, cudaStream_t s, int n_sm) {
+  long long warps = a.ncell;
+  long long blocks = (warps + kPairWarps - 1) / kPairWarps;
+  long long cap = (long long)n_sm * 8 * 16;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  k_pairs<<<(unsigned)blocks, kPairWarps * 32, 0, s>>>(a);
 }
-void launch_narrow_fill(const StepArgs& a, cudaStream_t s) {
-  if (a.ns) k_narrow_fill<<<(a.ns + 255) / 256, 256, 0, s>>>(a);
+void launch_rows_scatter(const StepArgs& a, cudaStream_t s, int n_sm) {
+  k_rows_scatter<<<n_sm * 16, 256, 0, s>>>(a);
+}
+void launch_rows_finish(const StepArgs& a, cudaStream_t s) {
+  if (a.ns) k_rows_finish<<<(a.ns + 255) / 256, 256, 0, s>>>(a);
 }
 
 }  // namespace dem

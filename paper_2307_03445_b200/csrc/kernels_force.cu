@@ -24,13 +24,15 @@ __global__ void __launch_bounds__(128) k_force(StepArgs a) {
   if (i >= a.ns) return;
   const int ci = a.s_clump[i];
   const int tci = a.s_tc[i];
-  const double cx = a.sx[i], cy = a.sy[i], cz = a.sz[i];
-  const double ri = a.tab.tc_rad[tci];
+  const double4 own = a.spos[i];
+  const double cx = own.x, cy = own.y, cz = own.z;
+  const double ri = own.w;
   const int mi = a.tab.tc_mat[tci];
-  const double Xx = a.cur.x[ci], Xy = a.cur.y[ci], Xz = a.cur.z[ci];
-  const double Vx = a.cur.vx[ci], Vy = a.cur.vy[ci], Vz = a.cur.vz[ci];
-  const double Wx = a.wwx[ci], Wy = a.wwy[ci], Wz = a.wwz[ci];
-  const double Mi = a.tab.tpl_mass[a.tid[ci]];
+  const double* ki = a.kin + (size_t)kKin * ci;
+  const double Xx = ki[0], Xy = ki[1], Xz = ki[2];
+  const double Vx = ki[3], Vy = ki[4], Vz = ki[5];
+  const double Wx = ki[6], Wy = ki[7], Wz = ki[8];
+  const double Mi = ki[9];
   const double h = a.h;
   const double k56 = 2.0 * sqrt(5.0 / 6.0);
 
@@ -58,9 +60,10 @@ __global__ void __launch_bounds__(128) k_force(StepArgs a) {
     if (!wall) {
       const int cj = a.s_clump[t];
       const int tcj = a.s_tc[t];
-      const double rj = a.tab.tc_rad[tcj];
+      const double4 pj = a.spos[t];
+      const double rj = pj.w;
       mj = a.tab.tc_mat[tcj];
-      const double dx = a.sx[t] - cx, dy = a.sy[t] - cy, dz = a.sz[t] - cz;
+      const double dx = pj.x - cx, dy = pj.y - cy, dz = pj.z - cz;
       const double dist = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
       if (dist == 0.0) {
         raise_error(a.ctl, -12, a.s_key[i], key);
@@ -71,15 +74,16 @@ __global__ void __launch_bounds__(128) k_force(StepArgs a) {
       ny = dy / dist;
       nz = dz / dist;
       const double hr = 0.5 * (ri - rj);
-      px = __fma_rn(hr, nx, 0.5 * (cx + a.sx[t]));
-      py = __fma_rn(hr, ny, 0.5 * (cy + a.sy[t]));
-      pz = __fma_rn(hr, nz, 0.5 * (cz + a.sz[t]));
+      px = __fma_rn(hr, nx, 0.5 * (cx + pj.x));
+      py = __fma_rn(hr, ny, 0.5 * (cy + pj.y));
+      pz = __fma_rn(hr, nz, 0.5 * (cz + pj.z));
       rbar = (ri * rj) / (ri + rj);
-      const double Mj = a.tab.tpl_mass[a.tid[cj]];
+      const double* kj = a.kin + (size_t)kKin * cj;
+      const double Mj = kj[9];
       mbar = (Mi * Mj) / (Mi + Mj);
-      Xjx = a.cur.x[cj]; Xjy = a.cur.y[cj]; Xjz = a.cur.z[cj];
-      Vjx = a.cur.vx[cj]; Vjy = a.cur.vy[cj]; Vjz = a.cur.vz[cj];
-      Wjx = a.wwx[cj]; Wjy = a.wwy[cj]; Wjz = a.wwz[cj];
+      Xjx = kj[0]; Xjy = kj[1]; Xjz = kj[2];
+      Vjx = kj[3]; Vjy = kj[4]; Vjz = kj[5];
+      Wjx = kj[6]; Wjy = kj[7]; Wjz = kj[8];
     } else {
       const int pl = -1 - t;
       const double* pp = a.tab.plane_pt[pl];

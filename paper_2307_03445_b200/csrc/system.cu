@@ -18,8 +18,9 @@
 namespace dem {
 void launch_pose_count(const StepArgs&, cudaStream_t);
 void launch_bin_scatter(const StepArgs&, cudaStream_t);
-void launch_narrow_count(const StepArgs&, cudaStream_t);
-void launch_narrow_fill(const StepArgs&, cudaStream_t);
+void launch_pairs(const StepArgs&, cudaStream_t, int n_sm);
+void launch_rows_scatter(const StepArgs&, cudaStream_t, int n_sm);
+void launch_rows_finish(const StepArgs&, cudaStream_t);
 void launch_force(const StepArgs&, cudaStream_t);
 void launch_integrate(const StepArgs&, cudaStream_t);
 long long scan_tiles_needed(long long n);
@@ -29,7 +30,8 @@ void launch_count_walls(const Rows& r, int ns, unsigned long long* out, cudaStre
 
 using namespace dem;
 
-static constexpr int kStages = 8;
+static constexpr int kStages = 9;
+static constexpr int kLaunchesPerStep = 13;  // 7 stage kernels + 2 x 3 scan kernels
 
 struct RowBuf {
   int* row_ptr = nullptr;
@@ -58,13 +60,19 @@ struct dem_system {
   std::vector<long long> h_gid;
   std::vector<int> h_tid, h_sph_off, h_s_tc;
   std::vector<long long> h_s_key;
+  std::vector<int64_t> h_perm;  // storage index -> caller index
   long long* d_gid = nullptr;
   int *d_tid = nullptr, *d_sph_off = nullptr;
   double* d_state[2] = {nullptr, nullptr};
-  double* d_ww = nullptr;
+  double* d_kin = nullptr;
   int *d_s_clump = nullptr, *d_s_tc = nullptr;
   long long* d_s_key = nullptr;
-  double *d_spos = nullptr, *d_sft = nullptr;
+  double4* d_spos = nullptr;
+  double* d_sft = nullptr;
+  int2* d_pairs = nullptr;
+  unsigned long long* d_pair_cursor = nullptr;
+  long long cap_pairs = 0;
+  int n_sm = 148;
   // bins
   Grid grid{};
   long long ncell = 0, cap_inserts = 0;
@@ -193,16 +201,15 @@ static StepArgs make_args(dem_system* sys, int p) {
   a.tid = sys->d_tid;
   a.gid = sys->d_gid;
   a.sph_off = sys->d_sph_off;
-  a.wwx = sys->d_ww;
-  a.wwy = sys->d_ww + sys->n;
-  a.wwz = sys->d_ww + 2 * sys->n;
+  a.kin = sys->d_kin;
   a.s_clump = sys->d_s_clump;
   a.s_tc = sys->d_s_tc;
   a.s_key = sys->d_s_key;
   size_t ns = (size_t)sys->ns;
-  a.sx = sys->d_spos;
-  a.sy = sys->d_spos + ns;
-  a.sz = sys->d_spos + 2 * ns;
+  a.spos = sys->d_spos;
+  a.pairs = sys->d_pairs;
+  a.pair_cursor = sys->d_pair_cursor;
+  a.cap_pairs = sys->cap_pairs;
   a.sfx = sys->d_sft;
   a.sfy = sys->d_sft + ns;
   a.sfz = sys->d_sft + 2 * ns;
@@ -234,16 +241,18 @@ static void enqueue_step(dem_system* sys, int p, cudaStream_t s, cudaEvent_t* ev
   if (ev) cudaEventRecord(ev[2], s);
   launch_bin_scatter(a, s);
   if (ev) cudaEventRecord(ev[3], s);
-  launch_narrow_count(a, s);
+  launch_pairs(a, s, sys->n_sm);
   if (ev) cudaEventRecord(ev[4], s);
   launch_excl_scan(sys->d_row_cnt, sys->rows[p].row_ptr, sys->ns, sys->d_scan_tmp, abort, s);
   if (ev) cudaEventRecord(ev[5], s);
-  launch_narrow_fill(a, s);
+  launch_rows_scatter(a, s, sys->n_sm);
   if (ev) cudaEventRecord(ev[6], s);
-  launch_force(a, s);
+  launch_rows_finish(a, s);
   if (ev) cudaEventRecord(ev[7], s);
-  launch_integrate(a, s);
+  launch_force(a, s);
   if (ev) cudaEventRecord(ev[8], s);
+  launch_integrate(a, s);
+  if (ev) cudaEventRecord(ev[9], s);
 }
 
 static dem_status capture_graphs(dem_system* sys) {
@@ -388,9 +397,16 @@ extern "C" dem_status dem_create(const dem_params* params, const dem_material* m
     dem_destroy(sys);
     return st;
   }
-  if ((st = alloc_arr(sys, &sys->d_ctl, 1)) || (st = alloc_arr(sys, &sys->d_counter, 1))) {
+  if ((st = alloc_arr(sys, &sys->d_ctl, 1)) || (st = alloc_arr(sys, &sys->d_counter, 1)) ||
+      (st = alloc_arr(sys, &sys->d_pair_cursor, 1))) {
     dem_destroy(sys);
     return st;
+  }
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sys->n_sm, cudaDevAttrMultiProcessorCount, dev);
+    if (sys->n_sm <= 0) sys->n_sm = 148;
   }
   if (cudaMallocHost(&sys->h_ctl, sizeof(Ctl)) != cudaSuccess) {
     dem_destroy(sys);
@@ -493,38 +509,10 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
   }
   if (ns > (1LL << 30)) return DEM_ERR_INVALID_ARG;
   free_graphs(sys);
-  sys->n = n;
-  sys->ns = ns;
-  sys->h_gid = g;
-  sys->h_tid = t;
-  sys->h_sph_off.assign(n + 1, 0);
-  std::vector<int> s_clump(ns);
-  sys->h_s_tc.assign(ns, 0);
-  sys->h_s_key.assign(ns, 0);
-  int64_t k = 0;
-  for (int64_t c = 0; c < n; ++c) {
-    sys->h_sph_off[c] = (int)k;
-    for (int j = 0; j < sys->tpl_ncomp[t[c]]; ++j, ++k) {
-      s_clump[k] = (int)c;
-      sys->h_s_tc[k] = sys->tpl_coff[t[c]] + j;
-      sys->h_s_key[k] = g[c] * kKeyStride + j;
-    }
-  }
-  sys->h_sph_off[n] = (int)k;
-  // SoA state on the host, one upload
-  std::vector<double> st((size_t)13 * n);
-  for (int64_t c = 0; c < n; ++c) {
-    for (int d = 0; d < 3; ++d) st[(0 + d) * n + c] = src[0][3 * c + d];
-    for (int d = 0; d < 4; ++d) st[(3 + d) * n + c] = src[1][4 * c + d];
-    for (int d = 0; d < 3; ++d) st[(7 + d) * n + c] = src[2][3 * c + d];
-    for (int d = 0; d < 3; ++d) st[(10 + d) * n + c] = src[3][3 * c + d];
-    for (int d = 0; d < 3; ++d)
-      if (!std::isfinite(src[0][3 * c + d]) || !std::isfinite(src[2][3 * c + d]) || !std::isfinite(src[3][3 * c + d]))
-        return DEM_ERR_NONFINITE;
-  }
   // grid: cell edge (auto: 4 x mean sphere radius + margin, at least 2 r_min + margin)
   double rsum = 0;
-  for (int64_t s = 0; s < ns; ++s) rsum += sys->tc_rad[sys->h_s_tc[s]];
+  for (int64_t c = 0; c < n; ++c)
+    for (int j = 0; j < sys->tpl_ncomp[t[c]]; ++j) rsum += sys->tc_rad[sys->tpl_coff[t[c]] + j];
   double rmean = ns ? rsum / ns : sys->rmax;
   double cell = sys->P.cell_size > 0 ? sys->P.cell_size : std::max(4.0 * rmean, 2.0 * sys->rmin) + sys->P.margin;
   Grid& G = sys->grid;
@@ -550,6 +538,62 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
     return DEM_ERR_INVALID_ARG;
   }
   sys->ncell = ncell;
+  // storage order: clumps sorted by the bin of their COM (spatial locality for every gather);
+  // results do not depend on it (keys, canonical sums).  h_perm maps storage -> caller order.
+  {
+    std::vector<long long> ckey(n);
+    for (int64_t c = 0; c < n; ++c) {
+      long long id[3];
+      for (int d = 0; d < 3; ++d) {
+        double v = (src[0][3 * c + d] - G.lo[d]) * G.inv_cell;
+        long long q = std::isfinite(v) ? (long long)std::floor(v) : 0;
+        id[d] = std::min<long long>(std::max<long long>(q, 0), G.n[d] - 1);
+      }
+      ckey[c] = (id[2] * G.n[1] + id[1]) * G.n[0] + id[0];
+    }
+    sys->h_perm.resize(n);
+    for (int64_t c = 0; c < n; ++c) sys->h_perm[c] = c;
+    std::stable_sort(sys->h_perm.begin(), sys->h_perm.end(),
+                     [&](int64_t x, int64_t y) { return ckey[x] < ckey[y]; });
+    std::vector<long long> g2(n);
+    std::vector<int> t2(n);
+    for (int64_t c = 0; c < n; ++c) {
+      g2[c] = g[sys->h_perm[c]];
+      t2[c] = t[sys->h_perm[c]];
+    }
+    g.swap(g2);
+    t.swap(t2);
+  }
+  sys->n = n;
+  sys->ns = ns;
+  sys->h_gid = g;
+  sys->h_tid = t;
+  sys->h_sph_off.assign(n + 1, 0);
+  std::vector<int> s_clump(ns);
+  sys->h_s_tc.assign(ns, 0);
+  sys->h_s_key.assign(ns, 0);
+  int64_t k = 0;
+  for (int64_t c = 0; c < n; ++c) {
+    sys->h_sph_off[c] = (int)k;
+    for (int j = 0; j < sys->tpl_ncomp[t[c]]; ++j, ++k) {
+      s_clump[k] = (int)c;
+      sys->h_s_tc[k] = sys->tpl_coff[t[c]] + j;
+      sys->h_s_key[k] = g[c] * kKeyStride + j;
+    }
+  }
+  sys->h_sph_off[n] = (int)k;
+  // SoA state on the host, one upload
+  std::vector<double> st((size_t)13 * n);
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t c = sys->h_perm[i];
+    for (int d = 0; d < 3; ++d) st[(0 + d) * n + i] = src[0][3 * c + d];
+    for (int d = 0; d < 4; ++d) st[(3 + d) * n + i] = src[1][4 * c + d];
+    for (int d = 0; d < 3; ++d) st[(7 + d) * n + i] = src[2][3 * c + d];
+    for (int d = 0; d < 3; ++d) st[(10 + d) * n + i] = src[3][3 * c + d];
+    for (int d = 0; d < 3; ++d)
+      if (!std::isfinite(src[0][3 * c + d]) || !std::isfinite(src[2][3 * c + d]) || !std::isfinite(src[3][3 * c + d]))
+        return DEM_ERR_NONFINITE;
+  }
   // upper bound of bin inserts: (floor(2e / cell) + 2)^3 per sphere
   long long ins = 0;
   for (int64_t s = 0; s < ns; ++s) {
@@ -565,11 +609,13 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
   TRY(alloc_arr(sys, &sys->d_sph_off, n + 1));
   TRY(alloc_arr(sys, &sys->d_state[0], 13 * n));
   TRY(alloc_arr(sys, &sys->d_state[1], 13 * n));
-  TRY(alloc_arr(sys, &sys->d_ww, 3 * n));
+  TRY(alloc_arr(sys, &sys->d_kin, (size_t)kKin * n));
   TRY(alloc_arr(sys, &sys->d_s_clump, ns));
   TRY(alloc_arr(sys, &sys->d_s_tc, ns));
   TRY(alloc_arr(sys, &sys->d_s_key, ns));
-  TRY(alloc_arr(sys, &sys->d_spos, 3 * ns));
+  TRY(alloc_arr(sys, &sys->d_spos, ns));
+  sys->cap_pairs = std::max<long long>(1024, 4 * ns);
+  TRY(alloc_arr(sys, &sys->d_pairs, sys->cap_pairs));
   TRY(alloc_arr(sys, &sys->d_sft, 6 * ns));
   TRY(alloc_arr(sys, &sys->d_cell_count, ncell));
   TRY(alloc_arr(sys, &sys->d_cell_start, ncell + 1));
@@ -747,10 +793,16 @@ extern "C" dem_status dem_step(dem_system* sys, int64_t n_steps) {
       sys->cap_inserts = need + need / 4 + 1024;
       TRY(alloc_arr(sys, &sys->d_items, sys->cap_inserts));
     }
+    if (sys->h_ctl->need_pairs > sys->cap_pairs) {
+      long long need = sys->h_ctl->need_pairs;
+      sys->cap_pairs = need + need / 4 + 1024;
+      TRY(alloc_arr(sys, &sys->d_pairs, sys->cap_pairs));
+    }
     free_graphs(sys);
     sys->h_ctl->abort = 0;
     sys->h_ctl->need_entries = 0;
     sys->h_ctl->need_inserts = 0;
+    sys->h_ctl->need_pairs = 0;
     CK(cudaMemcpyAsync(sys->d_ctl, sys->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, sys->stream));
   }
   return DEM_OK;
@@ -783,21 +835,29 @@ extern "C" dem_status dem_get_state(dem_system* sys, int64_t cap, int64_t* n, in
       out[k].resize((size_t)width[k] * N);
       o = out[k].data();
     }
-    for (int64_t c = 0; c < N; ++c)
-      for (int d = 0; d < width[k]; ++d) o[width[k] * c + d] = st[(first[k] + d) * N + c];
+    for (int64_t i = 0; i < N; ++i) {
+      const int64_t c = sys->h_perm[i];
+      for (int d = 0; d < width[k]; ++d) o[width[k] * c + d] = st[(first[k] + d) * N + i];
+    }
     if (on_device && N) CK(cudaMemcpy(dst[k], o, sizeof(double) * width[k] * N, cudaMemcpyHostToDevice));
+  }
+  std::vector<long long> go(N);
+  std::vector<int> to(N);
+  for (int64_t i = 0; i < N; ++i) {
+    go[sys->h_perm[i]] = sys->h_gid[i];
+    to[sys->h_perm[i]] = sys->h_tid[i];
   }
   if (gid) {
     if (on_device)
-      CK(cudaMemcpy(gid, sys->h_gid.data(), sizeof(long long) * N, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(gid, go.data(), sizeof(long long) * N, cudaMemcpyHostToDevice));
     else
-      std::memcpy(gid, sys->h_gid.data(), sizeof(long long) * N);
+      std::memcpy(gid, go.data(), sizeof(long long) * N);
   }
   if (tid) {
     if (on_device)
-      CK(cudaMemcpy(tid, sys->h_tid.data(), sizeof(int) * N, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(tid, to.data(), sizeof(int) * N, cudaMemcpyHostToDevice));
     else
-      std::memcpy(tid, sys->h_tid.data(), sizeof(int) * N);
+      std::memcpy(tid, to.data(), sizeof(int) * N);
   }
   return DEM_OK;
 }
@@ -868,7 +928,7 @@ extern "C" dem_status dem_get_stats(dem_system* sys, dem_stats* out) {
   out->n_cells = sys->ncell;
   out->cell_size = sys->grid.cell;
   out->regrows = sys->regrows;
-  out->kernel_launches_per_step = 12;
+  out->kernel_launches_per_step = kLaunchesPerStep;
   if (sys->launched > 0 && sys->ns > 0) {
     const RowBuf& R = sys->rows[(sys->launched - 1) & 1];
     int tot = 0, ins = 0;

@@ -1,0 +1,115 @@
+"""Benchmark beds C4/C5: the oracle-settled DS patch copy-pasted to millions of clumps.
+
+The patch (`data/ds_patch_30mm.npz`) is written by `workloads/make_patch.py`, which calls
+only `oracle/`.  Tiles are laid out on an x-y lattice with a small gap and each tile is
+turned by a seeded multiple of 90 degrees about its own vertical axis, so the bed is not
+a pure translation copy.  Extra clumps are trimmed from the top of the bed to hit the
+target count exactly.  Nothing here computes forces or motion.
+"""
+from __future__ import annotations
+
+import math
+import os
+
+import numpy as np
+
+from .ds import C4_MATERIALS, M0, ds_templates
+from .scenes import Scene, box_planes
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+PATCH = os.path.join(HERE, "data", "ds_patch_30mm.npz")
+
+C5_CLUMPS = 11_336_638  # P:574, VIPER-scale bed
+C4_CLUMPS = 2_000_000
+
+
+def _qmul(a, b):
+    w1, x1, y1, z1 = a.T
+    w2, x2, y2, z2 = b.T
+    return np.stack([w1 * w2 - x1 * x2 - y1 * y2 - z1 * z2, w1 * x2 + x1 * w2 + y1 * z2 - z1 * y2,
+                     w1 * y2 - x1 * z2 + y1 * w2 + z1 * x2, w1 * z2 + x1 * y2 - y1 * x2 + z1 * w2], axis=1)
+
+
+def load_patch(path: str = PATCH) -> Scene:
+    from .scenes import load_scene
+
+    if not os.path.exists(path):
+        raise FileNotFoundError(f"{path} missing: run `python -m workloads.make_patch` (oracle-only settling)")
+    return load_scene(path)
+
+
+def tiled_bed(n_target: int, footprint=(2.48, 1.0), seed: int = 574, per_comp_mat: bool = False,
+              gap: float = 0.2e-3, patch: Scene | None = None, vel_jitter: float = 0.0) -> Scene:
+    """Tile the settled patch over `footprint` (rounded up to whole tiles) and trim to n_target clumps."""
+    p = load_patch() if patch is None else patch
+    side_x = max(pl.point[0] for pl in p.planes if pl.normal[0] < 0)
+    side_y = max(pl.point[1] for pl in p.planes if pl.normal[1] < 0)
+    Lx, Ly = side_x + gap, side_y + gap
+    nx = max(1, math.ceil(footprint[0] / Lx))
+    ny = max(1, math.ceil(footprint[1] / Ly))
+    while nx * ny * p.n_clumps < n_target:  # footprint too small for the count: widen along x
+        nx += 1
+    rng = np.random.default_rng(seed)
+    m = p.n_clumps
+    T = nx * ny
+    rot = rng.integers(0, 4, size=T)
+    cx, cy = 0.5 * side_x, 0.5 * side_y
+    pos = np.empty((T, m, 3))
+    quat = np.empty((T, m, 4))
+    vel = np.empty((T, m, 3))
+    for k in range(4):
+        sel = np.nonzero(rot == k)[0]
+        if sel.size == 0:
+            continue
+        a = 0.5 * math.pi * k
+        c, s = math.cos(a), math.sin(a)
+        x, y = p.pos[:, 0] - cx, p.pos[:, 1] - cy
+        pr = np.stack([c * x - s * y + cx, s * x + c * y + cy, p.pos[:, 2]], axis=1)
+        qz = np.array([[math.cos(a / 2), 0.0, 0.0, math.sin(a / 2)]])
+        qr = _qmul(np.repeat(qz, m, 0), p.quat)
+        vr = np.stack([c * p.vel[:, 0] - s * p.vel[:, 1], s * p.vel[:, 0] + c * p.vel[:, 1], p.vel[:, 2]], axis=1)
+        pos[sel], quat[sel], vel[sel] = pr, qr, vr
+    ti, tj = np.divmod(np.arange(T), ny)
+    pos[:, :, 0] += (ti * Lx)[:, None]
+    pos[:, :, 1] += (tj * Ly)[:, None]
+    pos = pos.reshape(-1, 3)
+    quat = quat.reshape(-1, 4)
+    vel = vel.reshape(-1, 3)
+    om = np.tile(p.omega, (T, 1))
+    tid = np.tile(p.tid, T).astype(np.int32)
+    if n_target < pos.shape[0]:
+        keep = np.sort(np.argsort(pos[:, 2], kind="stable")[:n_target])
+        pos, quat, vel, om, tid = pos[keep], quat[keep], vel[keep], om[keep], tid[keep]
+    if vel_jitter:
+        vel = vel + rng.uniform(-vel_jitter, vel_jitter, size=vel.shape)
+    quat /= np.linalg.norm(quat, axis=1, keepdims=True)
+    n = pos.shape[0]
+    lo = np.array([0.0, 0.0, 0.0])
+    hi = np.array([nx * Lx - gap, ny * Ly - gap, float(pos[:, 2].max()) + 0.01])
+    templates = ds_templates(per_component_materials=per_comp_mat)
+    mats = np.array(C4_MATERIALS if per_comp_mat else [M0])
+    return Scene(materials=mats, templates=templates, planes=box_planes(lo, hi, 0, top=False), h=p.h,
+                 gravity=np.array([0.0, 0.0, -9.81]), domain_lo=lo - 1e-3, domain_hi=hi + np.array([1e-3, 1e-3, 0.05]),
+                 gid=np.arange(n, dtype=np.int64), tid=tid, pos=pos, quat=quat, vel=vel, omega=om,
+                 name=f"tiled-{nx}x{ny}-{n}")
+
+
+def c5_bed(**kw) -> Scene:
+    """Config 5: VIPER-scale bed, 11,336,638 DS clumps, footprint ~2.48 x 1.0 m, M0."""
+    s = tiled_bed(C5_CLUMPS, footprint=(2.48, 1.0), **kw)
+    s.name = "C5-viper-bed"
+    return s
+
+
+def c4_bed(**kw) -> Scene:
+    """Config 4: GRC-1 DS bed, 2,000,000 clumps, footprint 0.66 x 0.66 m, per-sphere materials M_{k mod 4}."""
+    s = tiled_bed(C4_CLUMPS, footprint=(0.66, 0.66), per_comp_mat=True, **kw)
+    s.name = "C4-grc1-bed"
+    return s
+
+
+def crop(scene: Scene, lo, hi) -> Scene:
+    """Clumps whose COM lies in the box [lo, hi] (a bounded sample of a bed)."""
+    lo, hi = np.asarray(lo), np.asarray(hi)
+    sel = np.nonzero(np.all((scene.pos >= lo) & (scene.pos <= hi), axis=1))[0]
+    return scene.subset(sel)
