@@ -92,9 +92,9 @@ def stage_bytes(st):
         "pose+bin_count": n * 188 + ns * 44 + nc * 8,
         "bin_scan": nc * 8,
         "bin_scatter": ns * 32 + nc * 12 + ins * 4,
-        "pairs": nc * 4 + ins * 40 + pairs * 16,
+        "pairs": nc * 4 + ins * 40 + pairs * (16 + 16),
         "row_scan": ns * 8,
-        "rows_scatter": pairs * 72,
+        "rows_scatter": pairs * 64,
         "rows_finish": ns * 40 + ent * 24,
         "force": ns * (32 + 8 + 16 + 48) + n * 80 + ent * 68,
         "integrate": n * (104 + 104 + 8) + ns * 48,

@@ -106,7 +106,7 @@ struct StepArgs {
   int* cell_start;
   int* items;
   int* row_cnt;              // walls + sphere partners per sphere (built by atomics each step)
-  int2* pairs;               // unordered candidate pairs of the step
+  int4* pairs;               // candidate pairs of the step: (a, b, slot in row a, slot in row b)
   unsigned long long* pair_cursor;
   long long cap_pairs;
   Rows rows, prev;

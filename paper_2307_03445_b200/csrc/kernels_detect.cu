@@ -106,22 +106,23 @@ __global__ void __launch_bounds__(256) k_bin_scatter(StepArgs a) {
 constexpr int kPairWarps = 8;
 constexpr int kPairBuf = 128;
 
-struct Member {
-  double4 p;  // x, y, z, r
-  int clump;
-  int idx;
-  int lo[3];
-  int pad;
+// Shared-memory member of a bin.  Both spheres of a pair overlap the bin C, so their
+// lowest bins satisfy lo <= C on every axis and max(lo_a, lo_b) == C  <=>  on every axis
+// lo_a == C or lo_b == C.  Each member therefore carries a 3-bit mask "C is my lowest bin
+// along axis d" (bits 29..31 of meta.y, the sphere index in bits 0..28), and the pair is
+// kept iff (mask_a | mask_b) == 7.
+struct Members {
+  double4 p[32];  // x, y, z, r
+  int2 meta[32];  // (clump, idx | mask << 29)
 };
 
-__device__ __forceinline__ void load_member(const StepArgs& a, Member& m, int idx) {
+__device__ __forceinline__ void load_member(const StepArgs& a, Members& M, int slot, int idx, int cx, int cy,
+                                            int cz) {
   const double4 p = a.spos[idx];
-  m.p = p;
-  m.idx = idx;
-  m.clump = a.s_clump[idx];
-  m.lo[0] = cell_lo(a.grid, 0, p.x, p.w);
-  m.lo[1] = cell_lo(a.grid, 1, p.y, p.w);
-  m.lo[2] = cell_lo(a.grid, 2, p.z, p.w);
+  M.p[slot] = p;
+  const int mask = (cell_lo(a.grid, 0, p.x, p.w) == cx ? 1 : 0) | (cell_lo(a.grid, 1, p.y, p.w) == cy ? 2 : 0) |
+                   (cell_lo(a.grid, 2, p.z, p.w) == cz ? 4 : 0);
+  M.meta[slot] = make_int2(a.s_clump[idx], idx | (mask << 29));
 }
 
 // p -> (i, j), 0 <= i < j, p = j (j - 1) / 2 + i
@@ -133,7 +134,7 @@ __device__ __forceinline__ void decode_tri(int p, int& i, int& j) {
   i = p - jj * (jj - 1) / 2;
 }
 
-__device__ __forceinline__ void flush_pairs(const StepArgs& a, int2* bf, int n, int lane) {
+__device__ __forceinline__ void flush_pairs(const StepArgs& a, int4* bf, int n, int lane) {
   __syncwarp();
   if (n == 0) return;
   unsigned long long off = 0;
@@ -145,9 +146,9 @@ __device__ __forceinline__ void flush_pairs(const StepArgs& a, int2* bf, int n, 
 }
 
 __global__ void __launch_bounds__(kPairWarps * 32) k_pairs(StepArgs a) {
-  __shared__ Member smA[kPairWarps][32];
-  __shared__ Member smB[kPairWarps][32];
-  __shared__ int2 sbuf[kPairWarps][kPairBuf];
+  __shared__ Members smA[kPairWarps];
+  __shared__ Members smB[kPairWarps];
+  __shared__ int4 sbuf[kPairWarps][kPairBuf];
   if (a.ctl->abort) return;
   if ((long long)a.cell_start[a.ncell] > a.cap_inserts) {
     a.ctl->need_inserts = a.cell_start[a.ncell];
@@ -155,9 +156,9 @@ __global__ void __launch_bounds__(kPairWarps * 32) k_pairs(StepArgs a) {
     return;
   }
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  Member* A = smA[w];
-  Member* B = smB[w];
-  int2* bf = sbuf[w];
+  Members& A = smA[w];
+  Members& B = smB[w];
+  int4* bf = sbuf[w];
   int nbuf = 0;  // warp-uniform
   const Grid& g = a.grid;
   const long long nw = (long long)gridDim.x * kPairWarps;
@@ -172,14 +173,14 @@ __global__ void __launch_bounds__(kPairWarps * 32) k_pairs(StepArgs a) {
     for (int ib = 0; ib < m; ib += 32) {
       const int mi = min(32, m - ib);
       __syncwarp();
-      if (lane < mi) load_member(a, A[lane], a.items[k0 + ib + lane]);
+      if (lane < mi) load_member(a, A, lane, a.items[k0 + ib + lane], cx, cy, cz);
       for (int jb = ib; jb < m; jb += 32) {
         const int mj = min(32, m - jb);
         const bool same = jb == ib;
-        const Member* Bp = same ? A : B;
+        const Members& Bp = same ? A : B;
         if (!same) {
           __syncwarp();
-          if (lane < mj) load_member(a, B[lane], a.items[k0 + jb + lane]);
+          if (lane < mj) load_member(a, B, lane, a.items[k0 + jb + lane], cx, cy, cz);
         }
         __syncwarp();
         const int np = same ? mi * (mi - 1) / 2 : mi * mj;
@@ -195,16 +196,17 @@ __global__ void __launch_bounds__(kPairWarps * 32) k_pairs(StepArgs a) {
               i = p / mj;
               j = p - i * mj;
             }
-            const Member& u = A[i];
-            const Member& v = Bp[j];
-            if (u.clump != v.clump && max(u.lo[0], v.lo[0]) == cx && max(u.lo[1], v.lo[1]) == cy &&
-                max(u.lo[2], v.lo[2]) == cz) {
-              const double dx = sub(v.p.x, u.p.x), dy = sub(v.p.y, u.p.y), dz = sub(v.p.z, u.p.z);
+            const int2 mu = A.meta[i];
+            const int2 mv = Bp.meta[j];
+            if (mu.x != mv.x && (((unsigned)(mu.y | mv.y) >> 29) == 7u)) {
+              const double4 u = A.p[i];
+              const double4 v = Bp.p[j];
+              const double dx = sub(v.x, u.x), dy = sub(v.y, u.y), dz = sub(v.z, u.z);
               const double d2 = add(add(mul(dx, dx), mul(dy, dy)), mul(dz, dz));
-              const double s = add(add(u.p.w, v.p.w), a.margin);
+              const double s = add(add(u.w, v.w), a.margin);
               hit = d2 <= mul(s, s);
-              ia = u.idx;
-              ibx = v.idx;
+              ia = mu.y & 0x1fffffff;
+              ibx = mv.y & 0x1fffffff;
             }
           }
           const unsigned mask = __ballot_sync(0xffffffffu, hit);
@@ -215,9 +217,10 @@ __global__ void __launch_bounds__(kPairWarps * 32) k_pairs(StepArgs a) {
               nbuf = 0;
             }
             if (hit) {
-              bf[nbuf + __popc(mask & ((1u << lane) - 1u))] = make_int2(ia, ibx);
-              atomicAdd(&a.row_cnt[ia], 1);
-              atomicAdd(&a.row_cnt[ibx], 1);
+              // the counting atomics hand out each entry's slot in its row (walls come first)
+              const int sa = atomicAdd(&a.row_cnt[ia], 1);
+              const int sb = atomicAdd(&a.row_cnt[ibx], 1);
+              bf[nbuf + __popc(mask & ((1u << lane) - 1u))] = make_int4(ia, ibx, sa, sb);
             }
             nbuf += cnt;
           }
@@ -229,7 +232,7 @@ __global__ void __launch_bounds__(kPairWarps * 32) k_pairs(StepArgs a) {
 }
 
 // ---------------------------------------------------------------- rows
-// per pair: both directed entries, slots taken by decrementing row_cnt (walls stay in front)
+// per pair: both directed entries at the slots handed out in k_pairs (walls stay in front)
 __global__ void __launch_bounds__(256) k_rows_scatter(StepArgs a) {
   if (a.ctl->abort) return;
   const unsigned long long np = *a.pair_cursor;
@@ -242,11 +245,9 @@ __global__ void __launch_bounds__(256) k_rows_scatter(StepArgs a) {
   }
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < (long long)np; t += stride) {
-    const int2 pr = a.pairs[t];
-    const int sa = atomicSub(&a.row_cnt[pr.x], 1) - 1;
-    const int sb = atomicSub(&a.row_cnt[pr.y], 1) - 1;
-    const int ea = a.rows.row_ptr[pr.x] + sa;
-    const int eb = a.rows.row_ptr[pr.y] + sb;
+    const int4 pr = a.pairs[t];
+    const int ea = a.rows.row_ptr[pr.x] + pr.z;
+    const int eb = a.rows.row_ptr[pr.y] + pr.w;
     a.rows.partner[ea] = pr.y;
     a.rows.key[ea] = a.s_key[pr.y];
     a.rows.partner[eb] = pr.x;

@@ -9,163 +9,213 @@
 // gyroscopic term; R12 semi-implicit Euler + exponential-map quaternion update.
 //
 // Directed "pull" rows: every sphere evaluates each of its contacts with itself as body i
-// and writes only its own partial wrench.  The two evaluations of one sphere pair are
+// and produces only its own partial wrench.  The two evaluations of one sphere pair are
 // bitwise mirror images (every operation is sign-symmetric under i <-> j and the
 // asymmetric point velocities use explicit roundings), so Newton's third law holds
 // exactly without atomics, and sums run in a canonical order (partner key, then
 // component) independent of storage order.
+//
+// Parallel layout of k_force: a CTA owns kFS consecutive spheres, whose rows are one
+// contiguous range of the CSR arrays.  One thread per directed entry evaluates a contact
+// (no serial per-sphere chains, so gathers of many entries are in flight at once), writes
+// its partial wrench to shared memory, and one thread per sphere then adds its entries in
+// row order — the same sequential sum, bit for bit, as a thread-per-sphere loop.
 #include "dem_device.cuh"
 
 namespace dem {
 
-__global__ void __launch_bounds__(128) k_force(StepArgs a) {
+constexpr int kFS = 128;   // spheres per CTA
+constexpr int kFT = 128;   // threads per CTA (= entries per chunk)
+static_assert(kFS <= kFT, "one summing thread per sphere");
+
+__global__ void __launch_bounds__(kFT, 5) k_force(StepArgs a) {
+  __shared__ int rp[kFS + 1], prp[kFS + 1];
+  __shared__ double4 own_p[kFS];
+  __shared__ double own_k[kFS][kKin];
+  __shared__ int own_mat[kFS];
+  __shared__ double part[6][kFT];
   if (a.ctl->abort) return;
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.ns) return;
-  const int ci = a.s_clump[i];
-  const int tci = a.s_tc[i];
-  const double4 own = a.spos[i];
-  const double cx = own.x, cy = own.y, cz = own.z;
-  const double ri = own.w;
-  const int mi = a.tab.tc_mat[tci];
-  const double* ki = a.kin + (size_t)kKin * ci;
-  const double Xx = ki[0], Xy = ki[1], Xz = ki[2];
-  const double Vx = ki[3], Vy = ki[4], Vz = ki[5];
-  const double Wx = ki[6], Wy = ki[7], Wz = ki[8];
-  const double Mi = ki[9];
+  const int tid = threadIdx.x;
+  const int s0 = blockIdx.x * kFS;
+  const int nsph = min(kFS, a.ns - s0);
+  for (int k = tid; k <= nsph; k += kFT) {
+    rp[k] = a.rows.row_ptr[s0 + k];
+    prp[k] = a.prev.row_ptr[s0 + k];
+  }
+  if (tid < nsph) {
+    const int i = s0 + tid;
+    own_p[tid] = a.spos[i];
+    own_mat[tid] = a.tab.tc_mat[a.s_tc[i]];
+    const double* k = a.kin + (size_t)kKin * a.s_clump[i];
+#pragma unroll
+    for (int q = 0; q < kKin; ++q) own_k[tid][q] = k[q];
+  }
+  __syncthreads();
   const double h = a.h;
   const double k56 = 2.0 * sqrt(5.0 / 6.0);
-
-  const int beg = a.rows.row_ptr[i], end = a.rows.row_ptr[i + 1];
-  int pj = a.prev.row_ptr[i];
-  const int pend = a.prev.row_ptr[i + 1];
-
-  double fsx = 0.0, fsy = 0.0, fsz = 0.0, tsx = 0.0, tsy = 0.0, tsz = 0.0;
-  for (int e = beg; e < end; ++e) {
-    const long long key = a.rows.key[e];
-    const int t = a.rows.partner[e];
-    // (a4) history remap: both rows are sorted by partner key
-    while (pj < pend && a.prev.key[pj] < key) ++pj;
-    double ux = 0.0, uy = 0.0, uz = 0.0;
-    if (pj < pend && a.prev.key[pj] == key) {
-      ux = a.prev.ut[3 * pj];
-      uy = a.prev.ut[3 * pj + 1];
-      uz = a.prev.ut[3 * pj + 2];
-    }
-    // (a5) geometry: n from i (own) to j (partner)
-    double nx, ny, nz, px, py, pz, delta, rbar, mbar;
-    double Xjx = 0, Xjy = 0, Xjz = 0, Vjx = 0, Vjy = 0, Vjz = 0, Wjx = 0, Wjy = 0, Wjz = 0;
-    int mj;
-    bool wall = t < 0;
-    if (!wall) {
-      const int cj = a.s_clump[t];
-      const int tcj = a.s_tc[t];
-      const double4 pj = a.spos[t];
-      const double rj = pj.w;
-      mj = a.tab.tc_mat[tcj];
-      const double dx = pj.x - cx, dy = pj.y - cy, dz = pj.z - cz;
-      const double dist = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
-      if (dist == 0.0) {
-        raise_error(a.ctl, -12, a.s_key[i], key);
-        return;
+  const int E0 = rp[0], E1 = rp[nsph];
+  double fsx = 0.0, fsy = 0.0, fsz = 0.0, tsx = 0.0, tsy = 0.0, tsz = 0.0;  // sphere s0 + tid
+  for (int c0 = E0; c0 < E1; c0 += kFT) {
+    const int e = c0 + tid;
+    if (e < E1) {
+      // owner: last ls with rp[ls] <= e
+      int lo = 0, hi = nsph - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (rp[mid] <= e) lo = mid; else hi = mid - 1;
       }
-      delta = (ri + rj) - dist;
-      nx = dx / dist;
-      ny = dy / dist;
-      nz = dz / dist;
-      const double hr = 0.5 * (ri - rj);
-      px = __fma_rn(hr, nx, 0.5 * (cx + pj.x));
-      py = __fma_rn(hr, ny, 0.5 * (cy + pj.y));
-      pz = __fma_rn(hr, nz, 0.5 * (cz + pj.z));
-      rbar = (ri * rj) / (ri + rj);
-      const double* kj = a.kin + (size_t)kKin * cj;
-      const double Mj = kj[9];
-      mbar = (Mi * Mj) / (Mi + Mj);
-      Xjx = kj[0]; Xjy = kj[1]; Xjz = kj[2];
-      Vjx = kj[3]; Vjy = kj[4]; Vjz = kj[5];
-      Wjx = kj[6]; Wjy = kj[7]; Wjz = kj[8];
-    } else {
-      const int pl = -1 - t;
-      const double* pp = a.tab.plane_pt[pl];
-      const double* nw = a.tab.plane_n[pl];
-      const double dd = (cx - pp[0]) * nw[0] + (cy - pp[1]) * nw[1] + (cz - pp[2]) * nw[2];
-      delta = ri - dd;
-      nx = -nw[0];
-      ny = -nw[1];
-      nz = -nw[2];
-      const double arm = ri - 0.5 * delta;
-      px = cx + arm * nx;
-      py = cy + arm * ny;
-      pz = cz + arm * nz;
-      rbar = ri;
-      mbar = Mi;
-      mj = a.tab.plane_mat[pl];
-    }
-    double Fx = 0.0, Fy = 0.0, Fz = 0.0, nux = 0.0, nuy = 0.0, nuz = 0.0;
-    const double rix = px - Xx, riy = py - Xy, riz = pz - Xz;
-    if (delta > 0.0) {
-      // contact-point velocities (Eq. 2a)
-      double vix, viy, viz, vjx = 0.0, vjy = 0.0, vjz = 0.0;
-      point_velocity(Vx, Vy, Vz, Wx, Wy, Wz, rix, riy, riz, vix, viy, viz);
-      if (!wall) point_velocity(Vjx, Vjy, Vjz, Wjx, Wjy, Wjz, px - Xjx, py - Xjy, pz - Xjz, vjx, vjy, vjz);
-      const double vrx = vjx - vix, vry = vjy - viy, vrz = vjz - viz;
-      const double* pr = a.tab.pair + 4 * (mi * a.tab.n_mat + mj);
-      const double estar = pr[0], gstar = pr[1], beta = pr[2], mu = pr[3];
-      // (a6) normal force, Eq. 1a
-      const double sq = sqrt(rbar * delta);
-      const double Sn = 2.0 * estar * sq;
-      const double kn = (2.0 / 3.0) * Sn;
-      const double cn = k56 * beta * sqrt(Sn * mbar);
-      const double vn = vrx * nx + vry * ny + vrz * nz;
-      const double fns = kn * delta - cn * vn;
-      const double fnx = fns * nx, fny = fns * ny, fnz = fns * nz;
-      double ftx = 0.0, fty = 0.0, ftz = 0.0;
-      if (mu != 0.0) {
-        // (a7) Eq. 3a-3b, Eq. 1b, Eq. 3c
-        const double vtx = vrx - vn * nx, vty = vry - vn * ny, vtz = vrz - vn * nz;
-        const double upx = ux + h * vtx, upy = uy + h * vty, upz = uz + h * vtz;
-        const double upn = upx * nx + upy * ny + upz * nz;
-        const double utx = upx - upn * nx, uty = upy - upn * ny, utz = upz - upn * nz;
-        const double kt = 8.0 * gstar * sq;
-        const double ct = k56 * beta * sqrt(kt * mbar);
-        const double trx = -kt * utx - ct * vtx, try_ = -kt * uty - ct * vty, trz = -kt * utz - ct * vtz;
-        const double cap = mu * sqrt(fnx * fnx + fny * fny + fnz * fnz);
-        const double tmag = sqrt(trx * trx + try_ * try_ + trz * trz);
-        if (tmag <= cap) {
-          ftx = trx; fty = try_; ftz = trz;
-          nux = utx; nuy = uty; nuz = utz;
-        } else {
-          const double um = sqrt(utx * utx + uty * uty + utz * utz);
-          if (um > 0.0) {
-            const double dxu = utx / um, dyu = uty / um, dzu = utz / um;
-            const double s = cap / kt;
-            nux = s * dxu; nuy = s * dyu; nuz = s * dzu;
-            ftx = -cap * dxu; fty = -cap * dyu; ftz = -cap * dzu;
-          }
+      const int ls = lo;
+      const double4 own = own_p[ls];
+      const double cx = own.x, cy = own.y, cz = own.z, ri = own.w;
+      const double* ki = own_k[ls];
+      const double Xx = ki[0], Xy = ki[1], Xz = ki[2];
+      const double Mi = ki[9];
+      const long long key = a.rows.key[e];
+      const int t = a.rows.partner[e];
+      // (a4) history remap: binary search of the key in the sphere's previous (sorted) row
+      double ux = 0.0, uy = 0.0, uz = 0.0;
+      {
+        int l = prp[ls], r = prp[ls + 1];
+        while (l < r) {
+          const int mid = (l + r) >> 1;
+          if (a.prev.key[mid] < key) l = mid + 1; else r = mid;
+        }
+        if (l < prp[ls + 1] && a.prev.key[l] == key) {
+          ux = a.prev.ut[3 * l];
+          uy = a.prev.ut[3 * l + 1];
+          uz = a.prev.ut[3 * l + 2];
         }
       }
-      Fx = fnx + ftx;
-      Fy = fny + fty;
-      Fz = fnz + ftz;
+      // (a5) geometry: n from i (own) to j (partner)
+      double nx, ny, nz, px, py, pz, delta, rbar, mbar;
+      double Xjx = 0, Xjy = 0, Xjz = 0, Vjx = 0, Vjy = 0, Vjz = 0, Wjx = 0, Wjy = 0, Wjz = 0;
+      int mj;
+      const bool wall = t < 0;
+      bool degenerate = false;
+      if (!wall) {
+        const double4 pj = a.spos[t];
+        const double* kj = a.kin + (size_t)kKin * a.s_clump[t];
+        mj = a.tab.tc_mat[a.s_tc[t]];
+        const double rj = pj.w;
+        const double dx = pj.x - cx, dy = pj.y - cy, dz = pj.z - cz;
+        const double dist = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+        degenerate = dist == 0.0;
+        delta = (ri + rj) - dist;
+        nx = dx / dist;
+        ny = dy / dist;
+        nz = dz / dist;
+        const double hr = 0.5 * (ri - rj);
+        px = __fma_rn(hr, nx, 0.5 * (cx + pj.x));
+        py = __fma_rn(hr, ny, 0.5 * (cy + pj.y));
+        pz = __fma_rn(hr, nz, 0.5 * (cz + pj.z));
+        rbar = (ri * rj) / (ri + rj);
+        const double Mj = kj[9];
+        mbar = (Mi * Mj) / (Mi + Mj);
+        Xjx = kj[0]; Xjy = kj[1]; Xjz = kj[2];
+        Vjx = kj[3]; Vjy = kj[4]; Vjz = kj[5];
+        Wjx = kj[6]; Wjy = kj[7]; Wjz = kj[8];
+      } else {
+        const int pl = -1 - t;
+        const double* pp = a.tab.plane_pt[pl];
+        const double* nw = a.tab.plane_n[pl];
+        const double dd = (cx - pp[0]) * nw[0] + (cy - pp[1]) * nw[1] + (cz - pp[2]) * nw[2];
+        delta = ri - dd;
+        nx = -nw[0];
+        ny = -nw[1];
+        nz = -nw[2];
+        const double arm = ri - 0.5 * delta;
+        px = cx + arm * nx;
+        py = cy + arm * ny;
+        pz = cz + arm * nz;
+        rbar = ri;
+        mbar = Mi;
+        mj = a.tab.plane_mat[pl];
+      }
+      if (degenerate) {
+        raise_error(a.ctl, -12, a.s_key[s0 + ls], key);
+        delta = 0.0;
+      }
+      double Fx = 0.0, Fy = 0.0, Fz = 0.0, nux = 0.0, nuy = 0.0, nuz = 0.0;
+      const double rix = px - Xx, riy = py - Xy, riz = pz - Xz;
+      if (delta > 0.0) {
+        // contact-point velocities (Eq. 2a)
+        double vix, viy, viz, vjx = 0.0, vjy = 0.0, vjz = 0.0;
+        point_velocity(ki[3], ki[4], ki[5], ki[6], ki[7], ki[8], rix, riy, riz, vix, viy, viz);
+        if (!wall) point_velocity(Vjx, Vjy, Vjz, Wjx, Wjy, Wjz, px - Xjx, py - Xjy, pz - Xjz, vjx, vjy, vjz);
+        const double vrx = vjx - vix, vry = vjy - viy, vrz = vjz - viz;
+        const double* pr = a.tab.pair + 4 * (own_mat[ls] * a.tab.n_mat + mj);
+        const double estar = pr[0], gstar = pr[1], beta = pr[2], mu = pr[3];
+        // (a6) normal force, Eq. 1a
+        const double sq = sqrt(rbar * delta);
+        const double Sn = 2.0 * estar * sq;
+        const double kn = (2.0 / 3.0) * Sn;
+        const double cn = k56 * beta * sqrt(Sn * mbar);
+        const double vn = vrx * nx + vry * ny + vrz * nz;
+        const double fns = kn * delta - cn * vn;
+        const double fnx = fns * nx, fny = fns * ny, fnz = fns * nz;
+        double ftx = 0.0, fty = 0.0, ftz = 0.0;
+        if (mu != 0.0) {
+          // (a7) Eq. 3a-3b, Eq. 1b, Eq. 3c
+          const double vtx = vrx - vn * nx, vty = vry - vn * ny, vtz = vrz - vn * nz;
+          const double upx = ux + h * vtx, upy = uy + h * vty, upz = uz + h * vtz;
+          const double upn = upx * nx + upy * ny + upz * nz;
+          const double utx = upx - upn * nx, uty = upy - upn * ny, utz = upz - upn * nz;
+          const double kt = 8.0 * gstar * sq;
+          const double ct = k56 * beta * sqrt(kt * mbar);
+          const double trx = -kt * utx - ct * vtx, try_ = -kt * uty - ct * vty, trz = -kt * utz - ct * vtz;
+          const double cap = mu * sqrt(fnx * fnx + fny * fny + fnz * fnz);
+          const double tmag = sqrt(trx * trx + try_ * try_ + trz * trz);
+          if (tmag <= cap) {
+            ftx = trx; fty = try_; ftz = trz;
+            nux = utx; nuy = uty; nuz = utz;
+          } else {
+            const double um = sqrt(utx * utx + uty * uty + utz * utz);
+            if (um > 0.0) {
+              const double dxu = utx / um, dyu = uty / um, dzu = utz / um;
+              const double s = cap / kt;
+              nux = s * dxu; nuy = s * dyu; nuz = s * dzu;
+              ftx = -cap * dxu; fty = -cap * dyu; ftz = -cap * dzu;
+            }
+          }
+        }
+        Fx = fnx + ftx;
+        Fy = fny + fty;
+        Fz = fnz + ftz;
+      }
+      a.rows.ut[3 * e] = nux;
+      a.rows.ut[3 * e + 1] = nuy;
+      a.rows.ut[3 * e + 2] = nuz;
+      if (a.record) {
+        a.rec.F[3 * e] = Fx; a.rec.F[3 * e + 1] = Fy; a.rec.F[3 * e + 2] = Fz;
+        a.rec.p[3 * e] = px; a.rec.p[3 * e + 1] = py; a.rec.p[3 * e + 2] = pz;
+        a.rec.n[3 * e] = nx; a.rec.n[3 * e + 1] = ny; a.rec.n[3 * e + 2] = nz;
+        a.rec.delta[e] = delta;
+      }
+      // force on own sphere is -F, torque r_i x (-F) (Eq. 4, reading R11)
+      const double fx = -Fx, fy = -Fy, fz = -Fz;
+      part[0][tid] = fx;
+      part[1][tid] = fy;
+      part[2][tid] = fz;
+      part[3][tid] = __fma_rn(riy, fz, -__dmul_rn(riz, fy));
+      part[4][tid] = __fma_rn(riz, fx, -__dmul_rn(rix, fz));
+      part[5][tid] = __fma_rn(rix, fy, -__dmul_rn(riy, fx));
     }
-    a.rows.ut[3 * e] = nux;
-    a.rows.ut[3 * e + 1] = nuy;
-    a.rows.ut[3 * e + 2] = nuz;
-    if (a.record) {
-      a.rec.F[3 * e] = Fx; a.rec.F[3 * e + 1] = Fy; a.rec.F[3 * e + 2] = Fz;
-      a.rec.p[3 * e] = px; a.rec.p[3 * e + 1] = py; a.rec.p[3 * e + 2] = pz;
-      a.rec.n[3 * e] = nx; a.rec.n[3 * e + 1] = ny; a.rec.n[3 * e + 2] = nz;
-      a.rec.delta[e] = delta;
+    __syncthreads();
+    // (a9, first level) canonical per-sphere sums: entries in row (partner-key) order
+    if (tid < nsph) {
+      const int b = max(rp[tid], c0), en = min(rp[tid + 1], c0 + kFT);
+      for (int q = b - c0; q < en - c0; ++q) {
+        fsx += part[0][q]; fsy += part[1][q]; fsz += part[2][q];
+        tsx += part[3][q]; tsy += part[4][q]; tsz += part[5][q];
+      }
     }
-    // force on own sphere is -F, torque r_i x (-F) (Eq. 4, reading R11)
-    const double fx = -Fx, fy = -Fy, fz = -Fz;
-    fsx += fx; fsy += fy; fsz += fz;
-    tsx += __fma_rn(riy, fz, -__dmul_rn(riz, fy));
-    tsy += __fma_rn(riz, fx, -__dmul_rn(rix, fz));
-    tsz += __fma_rn(rix, fy, -__dmul_rn(riy, fx));
+    __syncthreads();
   }
-  a.sfx[i] = fsx; a.sfy[i] = fsy; a.sfz[i] = fsz;
-  a.stx[i] = tsx; a.sty[i] = tsy; a.stz[i] = tsz;
+  if (tid < nsph) {
+    const int i = s0 + tid;
+    a.sfx[i] = fsx; a.sfy[i] = fsy; a.sfz[i] = fsz;
+    a.stx[i] = tsx; a.sty[i] = tsy; a.stz[i] = tsz;
+  }
 }
 
 // (a9) + (a10): one thread per clump.  F = sum_k f_k + M g; tau_body = R^T sum_k tau_k;
@@ -233,16 +283,6 @@ __global__ void __launch_bounds__(256) k_integrate(StepArgs a) {
   a.nxt.qw[c] = rw / nrm; a.nxt.qx[c] = rx / nrm; a.nxt.qy[c] = ry / nrm; a.nxt.qz[c] = rz / nrm;
 }
 
-void launch_force(const StepArgs& a, cudaStream_t s) {
-  if (a.ns) k_force<<<(a.ns + 127) / 128, 128, 0, s>>>(a);
-}
-void launch_integrate(const StepArgs& a, cudaStream_t s) {
-  k_integrate<<<(a.n + 255) / 256 > 0 ? (a.n + 255) / 256 : 1, 256, 0, s>>>(a);
-}
-
-}  // namespace dem
-
-namespace dem {
 // wall entries of a row set (for dem_get_stats: canonical contacts = walls + pairs/2)
 __global__ void k_count_walls(Rows r, int ns, unsigned long long* out) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -252,7 +292,15 @@ __global__ void k_count_walls(Rows r, int ns, unsigned long long* out) {
   c = __reduce_add_sync(0xffffffffu, (unsigned)c);
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
 }
+
+void launch_force(const StepArgs& a, cudaStream_t s) {
+  if (a.ns) k_force<<<(a.ns + kFS - 1) / kFS, kFT, 0, s>>>(a);
+}
+void launch_integrate(const StepArgs& a, cudaStream_t s) {
+  k_integrate<<<(a.n + 255) / 256 > 0 ? (a.n + 255) / 256 : 1, 256, 0, s>>>(a);
+}
 void launch_count_walls(const Rows& r, int ns, unsigned long long* out, cudaStream_t s) {
   if (ns) k_count_walls<<<(ns + 255) / 256, 256, 0, s>>>(r, ns, out);
 }
+
 }  // namespace dem

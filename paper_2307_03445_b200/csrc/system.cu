@@ -69,7 +69,7 @@ struct dem_system {
   long long* d_s_key = nullptr;
   double4* d_spos = nullptr;
   double* d_sft = nullptr;
-  int2* d_pairs = nullptr;
+  int4* d_pairs = nullptr;
   unsigned long long* d_pair_cursor = nullptr;
   long long cap_pairs = 0;
   int n_sm = 148;
@@ -507,7 +507,10 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
     }
     ns += sys->tpl_ncomp[t[c]];
   }
-  if (ns > (1LL << 30)) return DEM_ERR_INVALID_ARG;
+  if (ns >= (1LL << 29)) {  // the per-bin pair kernel packs sphere indices into 29 bits
+    sys->err = "more than 2^29 spheres per system";
+    return DEM_ERR_INVALID_ARG;
+  }
   free_graphs(sys);
   // grid: cell edge (auto: 4 x mean sphere radius + margin, at least 2 r_min + margin)
   double rsum = 0;
@@ -515,6 +518,16 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
     for (int j = 0; j < sys->tpl_ncomp[t[c]]; ++j) rsum += sys->tc_rad[sys->tpl_coff[t[c]] + j];
   double rmean = ns ? rsum / ns : sys->rmax;
   double cell = sys->P.cell_size > 0 ? sys->P.cell_size : std::max(4.0 * rmean, 2.0 * sys->rmin) + sys->P.margin;
+  // the bin edge only changes speed, never results: coarsen it while a sparse domain would
+  // need more than max(4M, 16 ns) bins
+  const long long max_cells = std::max<long long>(4LL << 20, 16 * ns);
+  auto cells_for = [&](double c) {
+    long long m = 1;
+    for (int d = 0; d < 3; ++d) m *= (long long)std::ceil((sys->P.domain_hi[d] - sys->P.domain_lo[d]) / c) + 1;
+    return m;
+  };
+  if (sys->P.cell_size <= 0)
+    while (cells_for(cell) > max_cells) cell *= 1.25;
   Grid& G = sys->grid;
   G.cell = cell;
   G.inv_cell = 1.0 / cell;
