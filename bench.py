@@ -94,10 +94,9 @@ def stage_bytes(st):
         "bin_scatter": ns * 32 + nc * 12 + ins * 4,
         "pairs": nc * 4 + ins * 40 + pairs * (16 + 16),
         "row_scan": ns * 8,
-        "rows_scatter": pairs * 64,
-        "rows_finish": ns * 40 + ent * 24,
-        "force": ns * (32 + 8 + 16 + 48) + n * 80 + ent * 68,
-        "integrate": n * (104 + 104 + 8) + ns * 48,
+        "rows_scatter": pairs * 72,
+        "rows_finish": ns * 40 + ent * 32,
+        "force+integrate": ns * (32 + 8 + 8) + n * (80 + 56 + 4 + 104) + ent * 72,
     }
 
 

@@ -153,8 +153,8 @@ dem_status dem_get_stats(dem_system* sys, dem_stats* out);
  * CUDA events between the stages on the system stream and accumulates each stage's device time;
  * enable resets the accumulators.  dem_get_stage_times returns the mean ms per step of each stage,
  * in the order: pose+bin-count, bin-offset scan, bin scatter, per-bin pair tests, row-offset scan,
- * row scatter, wall entries + row sort, force (remap + contact forces + per-sphere sums),
- * reduce + integrate. */
+ * row scatter, wall entries + row sort, force + reduce + integrate (remap, contact forces,
+ * canonical per-sphere and per-clump sums, Eq. 4 update) — 8 stages. */
 dem_status dem_set_profiling(dem_system* sys, int32_t enable);
 dem_status dem_get_stage_times(dem_system* sys, int32_t n_stages, double* ms);
 

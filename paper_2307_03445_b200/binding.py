@@ -103,7 +103,7 @@ def _f64(a, shape=None):
 
 
 STAGES = ["pose+bin_count", "bin_scan", "bin_scatter", "pairs", "row_scan", "rows_scatter", "rows_finish",
-          "force", "integrate"]
+          "force+integrate"]
 
 
 class System:

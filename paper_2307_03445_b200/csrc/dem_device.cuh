@@ -66,10 +66,15 @@ struct Grid {
   double pad;  // r + pad is the half-extent of a sphere's bin AABB (margin/2 + eps)
 };
 
+struct __align__(16) Entry {
+  long long key;    // partner key (sphere key, or INT64_MAX - plane)
+  int partner;      // partner local sphere index, or -1 - plane
+  int pad;
+};
+
 struct Rows {
   int* row_ptr;     // [ns + 1]
-  int* partner;     // [cap] local sphere index, or -1 - plane
-  long long* key;   // [cap] partner key
+  Entry* ent;       // [cap]
   double* ut;       // [3 * cap] AoS, oriented own -> partner
 };
 
@@ -101,7 +106,8 @@ struct StepArgs {
   const long long* s_key;
   double4* spos;             // sphere (x, y, z, r), written by the pose kernel each step
   double* kin;               // per clump [kKin]: X(3), V(3), omega_world(3), mass
-  double *sfx, *sfy, *sfz, *stx, *sty, *stz;  // per-sphere force / torque (world, about COM)
+  const int* cta_clump;      // [n_cta + 1] clump ranges of the fused force/integrate CTAs
+  int n_cta;
   int* cell_count;
   int* cell_start;
   int* items;

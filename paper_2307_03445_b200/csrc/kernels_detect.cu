@@ -248,10 +248,15 @@ __global__ void __launch_bounds__(256) k_rows_scatter(StepArgs a) {
     const int4 pr = a.pairs[t];
     const int ea = a.rows.row_ptr[pr.x] + pr.z;
     const int eb = a.rows.row_ptr[pr.y] + pr.w;
-    a.rows.partner[ea] = pr.y;
-    a.rows.key[ea] = a.s_key[pr.y];
-    a.rows.partner[eb] = pr.x;
-    a.rows.key[eb] = a.s_key[pr.x];
+    Entry ta, tb;
+    ta.key = a.s_key[pr.y];
+    ta.partner = pr.y;
+    ta.pad = 0;
+    tb.key = a.s_key[pr.x];
+    tb.partner = pr.x;
+    tb.pad = 0;
+    a.rows.ent[ea] = ta;
+    a.rows.ent[eb] = tb;
   }
 }
 
@@ -262,8 +267,7 @@ __global__ void __launch_bounds__(256) k_rows_finish(StepArgs a) {
   if (i >= a.ns) return;
   const int beg = a.rows.row_ptr[i];
   const int m = a.rows.row_ptr[i + 1] - beg;
-  int* P = a.rows.partner + beg;
-  long long* K = a.rows.key + beg;
+  Entry* R = a.rows.ent + beg;
   const double4 s = a.spos[i];
   int w = 0;
   for (int p = 0; p < a.tab.n_planes; ++p) {
@@ -271,22 +275,21 @@ __global__ void __launch_bounds__(256) k_rows_finish(StepArgs a) {
     const double* nw = a.tab.plane_n[p];
     const double dd = add(add(mul(sub(s.x, pp[0]), nw[0]), mul(sub(s.y, pp[1]), nw[1])), mul(sub(s.z, pp[2]), nw[2]));
     if (sub(add(s.w, a.margin), dd) >= 0.0) {
-      P[w] = -1 - p;
-      K[w] = (long long)(0x7fffffffffffffffLL - p);
-      ++w;
+      Entry e;
+      e.key = (long long)(0x7fffffffffffffffLL - p);
+      e.partner = -1 - p;
+      e.pad = 0;
+      R[w++] = e;
     }
   }
   for (int u = 1; u < m; ++u) {
-    const long long kk = K[u];
-    const int pp = P[u];
+    const Entry x = R[u];
     int v = u - 1;
-    while (v >= 0 && K[v] > kk) {
-      K[v + 1] = K[v];
-      P[v + 1] = P[v];
+    while (v >= 0 && R[v].key > x.key) {
+      R[v + 1] = R[v];
       --v;
     }
-    K[v + 1] = kk;
-    P[v + 1] = pp;
+    R[v + 1] = x;
   }
 }
 

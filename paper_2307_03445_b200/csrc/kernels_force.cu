@@ -15,48 +15,68 @@
 // exactly without atomics, and sums run in a canonical order (partner key, then
 // component) independent of storage order.
 //
-// Parallel layout of k_force: a CTA owns kFS consecutive spheres, whose rows are one
-// contiguous range of the CSR arrays.  One thread per directed entry evaluates a contact
-// (no serial per-sphere chains, so gathers of many entries are in flight at once), writes
-// its partial wrench to shared memory, and one thread per sphere then adds its entries in
-// row order — the same sequential sum, bit for bit, as a thread-per-sphere loop.
+// Parallel layout of k_force_integrate: a CTA owns a run of whole clumps, whose spheres'
+// rows are one contiguous range of the CSR arrays.  One thread per directed entry evaluates
+// a contact (no serial per-sphere chains, so gathers of many entries are in flight at
+// once) and writes its partial wrench to shared memory; one thread per sphere adds its
+// entries in row order, then one thread per clump adds its spheres in component order and
+// integrates — the canonical sums of DESIGN.md R23, with no per-sphere wrench in HBM.
 #include "dem_device.cuh"
 
 namespace dem {
 
-constexpr int kFS = 128;   // spheres per CTA
-constexpr int kFT = 128;   // threads per CTA (= entries per chunk)
-static_assert(kFS <= kFT, "one summing thread per sphere");
+constexpr int kFC = 32;     // max clumps per CTA (host partition, see system.cu)
+constexpr int kMaxS = 160;  // max spheres per CTA
+constexpr int kFT = 128;    // threads per CTA (= entries per chunk)
+int force_cta_clumps() { return kFC; }
+int force_cta_spheres() { return kMaxS; }
 
-__global__ void __launch_bounds__(kFT, 5) k_force(StepArgs a) {
-  __shared__ int rp[kFS + 1], prp[kFS + 1];
-  __shared__ double4 own_p[kFS];
-  __shared__ double own_k[kFS][kKin];
-  __shared__ int own_mat[kFS];
+// One CTA = a run of whole clumps [c0, c1) and their spheres [s0, s0 + nsph), whose rows are
+// one contiguous CSR range [E0, E1).
+__global__ void __launch_bounds__(kFT, 5) k_force_integrate(StepArgs a) {
+  __shared__ int rp[kMaxS + 1], prp[kMaxS + 1];
+  __shared__ double4 own_p[kMaxS];
+  __shared__ int own_mat[kMaxS];
+  __shared__ int own_lc[kMaxS];
+  __shared__ double ck[kFC][kKin];
   __shared__ double part[6][kFT];
-  if (a.ctl->abort) return;
+  __shared__ double acc[6][kMaxS];
   const int tid = threadIdx.x;
-  const int s0 = blockIdx.x * kFS;
-  const int nsph = min(kFS, a.ns - s0);
+  const int c0 = a.cta_clump[blockIdx.x], c1 = a.cta_clump[blockIdx.x + 1];
+  const int ncl = c1 - c0;
+  if (a.ctl->abort) {
+    // capacity abort / error: carry the state forward unchanged so the ping-pong stays valid
+    if (tid < ncl) {
+      const int c = c0 + tid;
+      a.nxt.x[c] = a.cur.x[c]; a.nxt.y[c] = a.cur.y[c]; a.nxt.z[c] = a.cur.z[c];
+      a.nxt.qw[c] = a.cur.qw[c]; a.nxt.qx[c] = a.cur.qx[c]; a.nxt.qy[c] = a.cur.qy[c]; a.nxt.qz[c] = a.cur.qz[c];
+      a.nxt.vx[c] = a.cur.vx[c]; a.nxt.vy[c] = a.cur.vy[c]; a.nxt.vz[c] = a.cur.vz[c];
+      a.nxt.wx[c] = a.cur.wx[c]; a.nxt.wy[c] = a.cur.wy[c]; a.nxt.wz[c] = a.cur.wz[c];
+    }
+    return;
+  }
+  if (blockIdx.x == 0 && tid == 0) a.ctl->step += 1;  // no other thread of this launch reads it
+  const int s0 = a.sph_off[c0];
+  const int nsph = a.sph_off[c1] - s0;
   for (int k = tid; k <= nsph; k += kFT) {
     rp[k] = a.rows.row_ptr[s0 + k];
     prp[k] = a.prev.row_ptr[s0 + k];
   }
-  if (tid < nsph) {
-    const int i = s0 + tid;
-    own_p[tid] = a.spos[i];
-    own_mat[tid] = a.tab.tc_mat[a.s_tc[i]];
-    const double* k = a.kin + (size_t)kKin * a.s_clump[i];
+  for (int ls = tid; ls < nsph; ls += kFT) {
+    const int i = s0 + ls;
+    own_p[ls] = a.spos[i];
+    own_mat[ls] = a.tab.tc_mat[a.s_tc[i]];
+    own_lc[ls] = a.s_clump[i] - c0;
 #pragma unroll
-    for (int q = 0; q < kKin; ++q) own_k[tid][q] = k[q];
+    for (int q = 0; q < 6; ++q) acc[q][ls] = 0.0;
   }
+  for (int k = tid; k < ncl * kKin; k += kFT) ck[k / kKin][k % kKin] = a.kin[(size_t)kKin * c0 + k];
   __syncthreads();
   const double h = a.h;
   const double k56 = 2.0 * sqrt(5.0 / 6.0);
   const int E0 = rp[0], E1 = rp[nsph];
-  double fsx = 0.0, fsy = 0.0, fsz = 0.0, tsx = 0.0, tsy = 0.0, tsz = 0.0;  // sphere s0 + tid
-  for (int c0 = E0; c0 < E1; c0 += kFT) {
-    const int e = c0 + tid;
+  for (int c0e = E0; c0e < E1; c0e += kFT) {
+    const int e = c0e + tid;
     if (e < E1) {
       // owner: last ls with rp[ls] <= e
       int lo = 0, hi = nsph - 1;
@@ -67,20 +87,21 @@ __global__ void __launch_bounds__(kFT, 5) k_force(StepArgs a) {
       const int ls = lo;
       const double4 own = own_p[ls];
       const double cx = own.x, cy = own.y, cz = own.z, ri = own.w;
-      const double* ki = own_k[ls];
+      const double* ki = ck[own_lc[ls]];
       const double Xx = ki[0], Xy = ki[1], Xz = ki[2];
       const double Mi = ki[9];
-      const long long key = a.rows.key[e];
-      const int t = a.rows.partner[e];
+      const Entry ent = a.rows.ent[e];
+      const long long key = ent.key;
+      const int t = ent.partner;
       // (a4) history remap: binary search of the key in the sphere's previous (sorted) row
       double ux = 0.0, uy = 0.0, uz = 0.0;
       {
         int l = prp[ls], r = prp[ls + 1];
         while (l < r) {
           const int mid = (l + r) >> 1;
-          if (a.prev.key[mid] < key) l = mid + 1; else r = mid;
+          if (a.prev.ent[mid].key < key) l = mid + 1; else r = mid;
         }
-        if (l < prp[ls + 1] && a.prev.key[l] == key) {
+        if (l < prp[ls + 1] && a.prev.ent[l].key == key) {
           ux = a.prev.ut[3 * l];
           uy = a.prev.ut[3 * l + 1];
           uz = a.prev.ut[3 * l + 2];
@@ -202,50 +223,32 @@ __global__ void __launch_bounds__(kFT, 5) k_force(StepArgs a) {
     }
     __syncthreads();
     // (a9, first level) canonical per-sphere sums: entries in row (partner-key) order
-    if (tid < nsph) {
-      const int b = max(rp[tid], c0), en = min(rp[tid + 1], c0 + kFT);
-      for (int q = b - c0; q < en - c0; ++q) {
-        fsx += part[0][q]; fsy += part[1][q]; fsz += part[2][q];
-        tsx += part[3][q]; tsy += part[4][q]; tsz += part[5][q];
+    for (int ls = tid; ls < nsph; ls += kFT) {
+      const int b = max(rp[ls], c0e), en = min(rp[ls + 1], c0e + kFT);
+      for (int q = b - c0e; q < en - c0e; ++q) {
+#pragma unroll
+        for (int d = 0; d < 6; ++d) acc[d][ls] += part[d][q];
       }
     }
     __syncthreads();
   }
-  if (tid < nsph) {
-    const int i = s0 + tid;
-    a.sfx[i] = fsx; a.sfy[i] = fsy; a.sfz[i] = fsz;
-    a.stx[i] = tsx; a.sty[i] = tsy; a.stz[i] = tsz;
-  }
-}
-
-// (a9) + (a10): one thread per clump.  F = sum_k f_k + M g; tau_body = R^T sum_k tau_k;
-// V += h F/M; X += h V; Omega += h I^-1 (tau - Omega x I Omega); q <- normalize(q (x) exp).
-__global__ void __launch_bounds__(256) k_integrate(StepArgs a) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (a.ctl->abort) {
-    // capacity abort / error: carry the state forward unchanged so the ping-pong stays valid
-    if (c < a.n) {
-      a.nxt.x[c] = a.cur.x[c]; a.nxt.y[c] = a.cur.y[c]; a.nxt.z[c] = a.cur.z[c];
-      a.nxt.qw[c] = a.cur.qw[c]; a.nxt.qx[c] = a.cur.qx[c]; a.nxt.qy[c] = a.cur.qy[c]; a.nxt.qz[c] = a.cur.qz[c];
-      a.nxt.vx[c] = a.cur.vx[c]; a.nxt.vy[c] = a.cur.vy[c]; a.nxt.vz[c] = a.cur.vz[c];
-      a.nxt.wx[c] = a.cur.wx[c]; a.nxt.wy[c] = a.cur.wy[c]; a.nxt.wz[c] = a.cur.wz[c];
-    }
-    return;
-  }
-  if (c == 0) a.ctl->step += 1;  // read by no other thread of this launch
-  if (c >= a.n) return;
+  if (tid >= ncl) return;
+  // (a9, second level) + (a10): per clump, spheres in component order.
+  // F = sum_k f_k + M g; tau_body = R^T sum_k tau_k; V += h F/M; X += h V;
+  // Omega += h I^-1 (tau - Omega x I Omega); q <- normalize(q (x) exp(h Omega)).
+  const int c = c0 + tid;
   const int t = a.tid[c];
-  const double M = a.tab.tpl_mass[t];
+  const double M = ck[tid][9];
   const double I0 = a.tab.tpl_inertia[3 * t], I1 = a.tab.tpl_inertia[3 * t + 1], I2 = a.tab.tpl_inertia[3 * t + 2];
   double Fx = 0.0, Fy = 0.0, Fz = 0.0, Tx = 0.0, Ty = 0.0, Tz = 0.0;
-  for (int s = a.sph_off[c], e = a.sph_off[c + 1]; s < e; ++s) {
-    Fx += a.sfx[s]; Fy += a.sfy[s]; Fz += a.sfz[s];
-    Tx += a.stx[s]; Ty += a.sty[s]; Tz += a.stz[s];
+  for (int s = a.sph_off[c] - s0, e = a.sph_off[c + 1] - s0; s < e; ++s) {
+    Fx += acc[0][s]; Fy += acc[1][s]; Fz += acc[2][s];
+    Tx += acc[3][s]; Ty += acc[4][s]; Tz += acc[5][s];
   }
   Fx = __dadd_rn(Fx, __dmul_rn(M, a.g[0]));
   Fy = __dadd_rn(Fy, __dmul_rn(M, a.g[1]));
   Fz = __dadd_rn(Fz, __dmul_rn(M, a.g[2]));
-  double qw = a.cur.qw[c], qx = a.cur.qx[c], qy = a.cur.qy[c], qz = a.cur.qz[c];
+  const double qw = a.cur.qw[c], qx = a.cur.qx[c], qy = a.cur.qy[c], qz = a.cur.qz[c];
   double R[9];
   quat_R(qw, qx, qy, qz, R);
   const double tbx = R[0] * Tx + R[3] * Ty + R[6] * Tz;
@@ -254,12 +257,11 @@ __global__ void __launch_bounds__(256) k_integrate(StepArgs a) {
   if (!isfinite(Fx) || !isfinite(Fy) || !isfinite(Fz) || !isfinite(tbx) || !isfinite(tby) || !isfinite(tbz)) {
     raise_error(a.ctl, -11, a.gid[c], 0);
   }
-  const double h = a.h;
-  const double vx = a.cur.vx[c] + h * (Fx / M), vy = a.cur.vy[c] + h * (Fy / M), vz = a.cur.vz[c] + h * (Fz / M);
+  const double vx = ck[tid][3] + h * (Fx / M), vy = ck[tid][4] + h * (Fy / M), vz = ck[tid][5] + h * (Fz / M);
   a.nxt.vx[c] = vx; a.nxt.vy[c] = vy; a.nxt.vz[c] = vz;
-  a.nxt.x[c] = a.cur.x[c] + h * vx;
-  a.nxt.y[c] = a.cur.y[c] + h * vy;
-  a.nxt.z[c] = a.cur.z[c] + h * vz;
+  a.nxt.x[c] = ck[tid][0] + h * vx;
+  a.nxt.y[c] = ck[tid][1] + h * vy;
+  a.nxt.z[c] = ck[tid][2] + h * vz;
   const double w0 = a.cur.wx[c], w1 = a.cur.wy[c], w2 = a.cur.wz[c];
   const double L0 = I0 * w0, L1 = I1 * w1, L2 = I2 * w2;
   const double g0 = w1 * L2 - w2 * L1, g1 = w2 * L0 - w0 * L2, g2 = w0 * L1 - w1 * L0;
@@ -270,10 +272,10 @@ __global__ void __launch_bounds__(256) k_integrate(StepArgs a) {
   const double wn = sqrt(n0 * n0 + n1 * n1 + n2 * n2);
   double dw = 1.0, dx = 0.0, dy = 0.0, dz = 0.0;
   if (wn > 0.0) {
-    double sh, ch;
-    sincos(0.5 * (h * wn), &sh, &ch);
+    double sh, chh;
+    sincos(0.5 * (h * wn), &sh, &chh);
     const double sn = sh / wn;
-    dw = ch; dx = n0 * sn; dy = n1 * sn; dz = n2 * sn;
+    dw = chh; dx = n0 * sn; dy = n1 * sn; dz = n2 * sn;
   }
   const double rw = qw * dw - qx * dx - qy * dy - qz * dz;
   const double rx = qw * dx + qx * dw + qy * dz - qz * dy;
@@ -288,16 +290,13 @@ __global__ void k_count_walls(Rows r, int ns, unsigned long long* out) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long c = 0;
   if (i < ns)
-    for (int e = r.row_ptr[i]; e < r.row_ptr[i + 1]; ++e) c += r.key[e] > (0x7fffffffffffffffLL - kMaxPlanes);
+    for (int e = r.row_ptr[i]; e < r.row_ptr[i + 1]; ++e) c += r.ent[e].key > (0x7fffffffffffffffLL - kMaxPlanes);
   c = __reduce_add_sync(0xffffffffu, (unsigned)c);
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
 }
 
-void launch_force(const StepArgs& a, cudaStream_t s) {
-  if (a.ns) k_force<<<(a.ns + kFS - 1) / kFS, kFT, 0, s>>>(a);
-}
-void launch_integrate(const StepArgs& a, cudaStream_t s) {
-  k_integrate<<<(a.n + 255) / 256 > 0 ? (a.n + 255) / 256 : 1, 256, 0, s>>>(a);
+void launch_force_integrate(const StepArgs& a, cudaStream_t s) {
+  if (a.n_cta > 0) k_force_integrate<<<a.n_cta, kFT, 0, s>>>(a);
 }
 void launch_count_walls(const Rows& r, int ns, unsigned long long* out, cudaStream_t s) {
   if (ns) k_count_walls<<<(ns + 255) / 256, 256, 0, s>>>(r, ns, out);

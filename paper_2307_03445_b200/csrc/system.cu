@@ -21,8 +21,9 @@ void launch_bin_scatter(const StepArgs&, cudaStream_t);
 void launch_pairs(const StepArgs&, cudaStream_t, int n_sm);
 void launch_rows_scatter(const StepArgs&, cudaStream_t, int n_sm);
 void launch_rows_finish(const StepArgs&, cudaStream_t);
-void launch_force(const StepArgs&, cudaStream_t);
-void launch_integrate(const StepArgs&, cudaStream_t);
+void launch_force_integrate(const StepArgs&, cudaStream_t);
+int force_cta_clumps();
+int force_cta_spheres();
 long long scan_tiles_needed(long long n);
 void launch_excl_scan(const int* in, int* out, long long n, int* tmp, const int* abort, cudaStream_t s);
 void launch_count_walls(const Rows& r, int ns, unsigned long long* out, cudaStream_t s);
@@ -30,13 +31,12 @@ void launch_count_walls(const Rows& r, int ns, unsigned long long* out, cudaStre
 
 using namespace dem;
 
-static constexpr int kStages = 9;
-static constexpr int kLaunchesPerStep = 13;  // 7 stage kernels + 2 x 3 scan kernels
+static constexpr int kStages = 8;
+static constexpr int kLaunchesPerStep = 12;  // 6 stage kernels + 2 x 3 scan kernels
 
 struct RowBuf {
   int* row_ptr = nullptr;
-  int* partner = nullptr;
-  long long* key = nullptr;
+  Entry* ent = nullptr;
   double* ut = nullptr;
 };
 
@@ -68,7 +68,8 @@ struct dem_system {
   int *d_s_clump = nullptr, *d_s_tc = nullptr;
   long long* d_s_key = nullptr;
   double4* d_spos = nullptr;
-  double* d_sft = nullptr;
+  int* d_cta_clump = nullptr;
+  int n_cta = 0;
   int4* d_pairs = nullptr;
   unsigned long long* d_pair_cursor = nullptr;
   long long cap_pairs = 0;
@@ -210,20 +211,17 @@ static StepArgs make_args(dem_system* sys, int p) {
   a.pairs = sys->d_pairs;
   a.pair_cursor = sys->d_pair_cursor;
   a.cap_pairs = sys->cap_pairs;
-  a.sfx = sys->d_sft;
-  a.sfy = sys->d_sft + ns;
-  a.sfz = sys->d_sft + 2 * ns;
-  a.stx = sys->d_sft + 3 * ns;
-  a.sty = sys->d_sft + 4 * ns;
-  a.stz = sys->d_sft + 5 * ns;
+  (void)ns;
+  a.cta_clump = sys->d_cta_clump;
+  a.n_cta = sys->n_cta;
   a.cell_count = sys->d_cell_count;
   a.cell_start = sys->d_cell_start;
   a.items = sys->d_items;
   a.row_cnt = sys->d_row_cnt;
   const RowBuf& R = sys->rows[p];
   const RowBuf& Q = sys->rows[p ^ 1];
-  a.rows = Rows{R.row_ptr, R.partner, R.key, R.ut};
-  a.prev = Rows{Q.row_ptr, Q.partner, Q.key, Q.ut};
+  a.rows = Rows{R.row_ptr, R.ent, R.ut};
+  a.prev = Rows{Q.row_ptr, Q.ent, Q.ut};
   a.rec = sys->rec;
   a.record = sys->P.record_contacts ? 1 : 0;
   a.ctl = sys->d_ctl;
@@ -249,10 +247,8 @@ static void enqueue_step(dem_system* sys, int p, cudaStream_t s, cudaEvent_t* ev
   if (ev) cudaEventRecord(ev[6], s);
   launch_rows_finish(a, s);
   if (ev) cudaEventRecord(ev[7], s);
-  launch_force(a, s);
+  launch_force_integrate(a, s);
   if (ev) cudaEventRecord(ev[8], s);
-  launch_integrate(a, s);
-  if (ev) cudaEventRecord(ev[9], s);
 }
 
 static dem_status capture_graphs(dem_system* sys) {
@@ -442,21 +438,18 @@ static dem_status alloc_rows(dem_system* sys, long long cap) {
   for (int p = 0; p < 2; ++p) {
     RowBuf nb;
     nb.row_ptr = sys->rows[p].row_ptr;
-    nb.partner = (int*)dalloc(sys, sizeof(int) * cap);
-    nb.key = (long long*)dalloc(sys, sizeof(long long) * cap);
+    nb.ent = (Entry*)dalloc(sys, sizeof(Entry) * cap);
     nb.ut = (double*)dalloc(sys, sizeof(double) * 3 * cap);
-    if (!nb.partner || !nb.key || !nb.ut) {
+    if (!nb.ent || !nb.ut) {
       sys->err = "row buffer allocation failed";
       return DEM_ERR_OOM;
     }
-    if (sys->rows[p].key && sys->cap_entries) {
+    if (sys->rows[p].ent && sys->cap_entries) {
       size_t m = (size_t)std::min(cap, sys->cap_entries);
-      cudaMemcpyAsync(nb.partner, sys->rows[p].partner, sizeof(int) * m, cudaMemcpyDeviceToDevice, sys->stream);
-      cudaMemcpyAsync(nb.key, sys->rows[p].key, sizeof(long long) * m, cudaMemcpyDeviceToDevice, sys->stream);
+      cudaMemcpyAsync(nb.ent, sys->rows[p].ent, sizeof(Entry) * m, cudaMemcpyDeviceToDevice, sys->stream);
       cudaMemcpyAsync(nb.ut, sys->rows[p].ut, sizeof(double) * 3 * m, cudaMemcpyDeviceToDevice, sys->stream);
     }
-    dfree(sys, sys->rows[p].partner);
-    dfree(sys, sys->rows[p].key);
+    dfree(sys, sys->rows[p].ent);
     dfree(sys, sys->rows[p].ut);
     sys->rows[p] = nb;
   }
@@ -629,7 +622,25 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
   TRY(alloc_arr(sys, &sys->d_spos, ns));
   sys->cap_pairs = std::max<long long>(1024, 4 * ns);
   TRY(alloc_arr(sys, &sys->d_pairs, sys->cap_pairs));
-  TRY(alloc_arr(sys, &sys->d_sft, 6 * ns));
+  // CTA partition of the fused force/integrate kernel: consecutive whole clumps, at most
+  // force_cta_clumps() clumps and force_cta_spheres() spheres per CTA
+  std::vector<int> cta{0};
+  {
+    int nc = 0, nsph = 0;
+    for (int64_t c = 0; c < n; ++c) {
+      const int m = sys->tpl_ncomp[t[c]];
+      if (nc == force_cta_clumps() || nsph + m > force_cta_spheres()) {
+        cta.push_back((int)c);
+        nc = 0;
+        nsph = 0;
+      }
+      ++nc;
+      nsph += m;
+    }
+    if (n > 0) cta.push_back((int)n);
+  }
+  sys->n_cta = (int)cta.size() - 1;
+  TRY(alloc_arr(sys, &sys->d_cta_clump, cta.size()));
   TRY(alloc_arr(sys, &sys->d_cell_count, ncell));
   TRY(alloc_arr(sys, &sys->d_cell_start, ncell + 1));
   TRY(alloc_arr(sys, &sys->d_items, ins));
@@ -639,12 +650,12 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
   long long cap = std::max<long long>(1024, 8 * ns);
   sys->cap_entries = 0;
   for (int p = 0; p < 2; ++p) {
-    dfree(sys, sys->rows[p].partner); sys->rows[p].partner = nullptr;
-    dfree(sys, sys->rows[p].key); sys->rows[p].key = nullptr;
+    dfree(sys, sys->rows[p].ent); sys->rows[p].ent = nullptr;
     dfree(sys, sys->rows[p].ut); sys->rows[p].ut = nullptr;
   }
   TRY(alloc_rows(sys, cap));
   cudaStream_t s = sys->stream;
+  CK(cudaMemcpyAsync(sys->d_cta_clump, cta.data(), sizeof(int) * cta.size(), cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(sys->d_gid, g.data(), sizeof(long long) * n, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(sys->d_tid, t.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(sys->d_sph_off, sys->h_sph_off.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice, s));
@@ -683,28 +694,29 @@ extern "C" dem_status dem_set_contact_history(dem_system* sys, int64_t n, const 
     if (ib != idx.end()) per[ib->second].push_back(E{key_a[r], {-u_t[3 * r], -u_t[3 * r + 1], -u_t[3 * r + 2]}});
   }
   std::vector<int> rp(sys->ns + 1, 0);
-  std::vector<long long> keys;
+  std::vector<Entry> ents;
   std::vector<double> ut;
-  std::vector<int> partner;
   for (int64_t s = 0; s < sys->ns; ++s) {
     auto& v = per[s];
     std::sort(v.begin(), v.end(), [](const E& x, const E& y) { return x.key < y.key; });
     for (auto& e : v) {
-      keys.push_back(e.key);
-      partner.push_back(-1);
+      Entry en;
+      en.key = e.key;
+      en.partner = -1;  // only the key and u_t of the previous rows are read
+      en.pad = 0;
+      ents.push_back(en);
       for (int d = 0; d < 3; ++d) ut.push_back(e.u[d]);
     }
-    rp[s + 1] = (int)keys.size();
+    rp[s + 1] = (int)ents.size();
   }
-  long long m = (long long)keys.size();
+  long long m = (long long)ents.size();
   if (m > sys->cap_entries) TRY(alloc_rows(sys, m + m / 4 + 1024));
   int prev = (int)((sys->launched & 1) ^ 1);
   cudaStream_t s = sys->stream;
   RowBuf& R = sys->rows[prev];
   CK(cudaMemcpyAsync(R.row_ptr, rp.data(), sizeof(int) * (sys->ns + 1), cudaMemcpyHostToDevice, s));
   if (m) {
-    CK(cudaMemcpyAsync(R.key, keys.data(), sizeof(long long) * m, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(R.partner, partner.data(), sizeof(int) * m, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(R.ent, ents.data(), sizeof(Entry) * m, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(R.ut, ut.data(), sizeof(double) * 3 * m, cudaMemcpyHostToDevice, s));
   }
   CK(cudaStreamSynchronize(s));
@@ -893,8 +905,10 @@ extern "C" dem_status dem_get_contacts(dem_system* sys, int64_t cap, int64_t* n,
   std::vector<int> rp(ns + 1);
   CK(cudaMemcpy(rp.data(), R.row_ptr, sizeof(int) * (ns + 1), cudaMemcpyDeviceToHost));
   const int64_t m = rp[ns];
+  std::vector<Entry> ents(m);
+  if (m) CK(cudaMemcpy(ents.data(), R.ent, sizeof(Entry) * m, cudaMemcpyDeviceToHost));
   std::vector<long long> keys(m);
-  if (m) CK(cudaMemcpy(keys.data(), R.key, sizeof(long long) * m, cudaMemcpyDeviceToHost));
+  for (int64_t e = 0; e < m; ++e) keys[e] = ents[e].key;
   // canonical entries: own key < partner key
   std::vector<std::pair<int64_t, int64_t>> sel;  // (own sphere, entry)
   for (int64_t s = 0; s < ns; ++s)
@@ -948,7 +962,7 @@ extern "C" dem_status dem_get_stats(dem_system* sys, dem_stats* out) {
     CK(cudaMemcpyAsync(&tot, R.row_ptr + sys->ns, sizeof(int), cudaMemcpyDeviceToHost, sys->stream));
     CK(cudaMemcpyAsync(&ins, sys->d_cell_start + sys->ncell, sizeof(int), cudaMemcpyDeviceToHost, sys->stream));
     CK(cudaMemsetAsync(sys->d_counter, 0, sizeof(unsigned long long), sys->stream));
-    launch_count_walls(Rows{R.row_ptr, R.partner, R.key, R.ut}, (int)sys->ns, sys->d_counter, sys->stream);
+    launch_count_walls(Rows{R.row_ptr, R.ent, R.ut}, (int)sys->ns, sys->d_counter, sys->stream);
     unsigned long long walls = 0;
     CK(cudaMemcpyAsync(&walls, sys->d_counter, sizeof(walls), cudaMemcpyDeviceToHost, sys->stream));
     CK(cudaStreamSynchronize(sys->stream));
