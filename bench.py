@@ -226,20 +226,22 @@ def run_ours(a):
     step_bytes = survey_bytes_per_sphere_step(c) * ns
 
     # ---------------- e2e through the C-ABI with host buffers (pinned)
-    pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()  # noqa: E731
-    hs = {k: pin(getattr(scene, k)) for k in ("gid", "tid", "pos", "quat", "vel", "omega")}
-    h2d = sum(v.nbytes for v in hs.values())
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    sys_.dem_set_state(hs["gid"], hs["tid"], hs["pos"], hs["quat"], hs["vel"], hs["omega"])
-    sys_.dem_step(a.steps)
-    out = sys_.dem_get_state()
-    torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
-    d2h = sum(v.nbytes for v in out.values())
-    e2e = {"value": ns * a.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d / a.steps,
-           "d2h_bytes_per_step": d2h / a.steps,
-           "note": "dem_set_state(host) + dem_step(K) + dem_get_state(host), wall clock, per-step bytes = total/K"}
+    e2e = None
+    if not a.no_e2e:
+        pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()  # noqa: E731
+        hs = {k: pin(getattr(scene, k)) for k in ("gid", "tid", "pos", "quat", "vel", "omega")}
+        h2d = sum(v.nbytes for v in hs.values())
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sys_.dem_set_state(hs["gid"], hs["tid"], hs["pos"], hs["quat"], hs["vel"], hs["omega"])
+        sys_.dem_step(a.steps)
+        out = sys_.dem_get_state()
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+        d2h = sum(v.nbytes for v in out.values())
+        e2e = {"value": ns * a.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d / a.steps,
+               "d2h_bytes_per_step": d2h / a.steps,
+               "note": "dem_set_state(host) + dem_step(K) + dem_get_state(host), wall clock, per-step bytes = total/K"}
 
     # ---------------- CPU oracle baseline on a bounded sample of the same bed
     cpu = None
@@ -284,6 +286,7 @@ def main():
     ap.add_argument("--cell-size", type=float, default=0.0)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer end-to-end pass (A/B runs)")
     a = ap.parse_args()
     if a.warmup < 3:
         a.warmup = 3

@@ -14,7 +14,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdem_b200.so")
+# DEM_LIB_PATH selects another build of the same library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("DEM_LIB_PATH") or os.path.join(_HERE, "libdem_b200.so")
 
 DEM_STATUS = {0: "ok", -1: "invalid argument", -2: "CUDA error", -3: "out of device memory", -4: "NCCL error",
               -5: "bad material", -6: "bad template", -10: "sphere out of domain", -11: "non-finite wrench",

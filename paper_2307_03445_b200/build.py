@@ -1,4 +1,9 @@
-"""Build libdem_b200.so in-tree with nvcc for sm_100a (no JIT cache, no torch extension)."""
+"""Build libdem_b200.so in-tree with nvcc for sm_100a (no JIT cache, no torch extension).
+
+    python paper_2307_03445_b200/build.py                 # the product library
+    python paper_2307_03445_b200/build.py -D NAME=1 -o x  # a variant (A/B timing via DEM_LIB_PATH)
+"""
+import argparse
 import os
 import subprocess
 import sys
@@ -13,22 +18,29 @@ FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-li
          "-shared", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    lib = out or LIB
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     deps = srcs + [os.path.join(CSRC, "dem_device.cuh"), os.path.join(ROOT, "include", "dem.h")]
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(d) for d in deps):
-        return LIB
-    cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp", *srcs]
+    if not force and not defines and os.path.exists(lib) and os.path.getmtime(lib) >= max(
+            os.path.getmtime(d) for d in deps):
+        return lib
+    cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-o", lib + ".tmp",
+           *srcs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libdem_b200.so")
+        raise RuntimeError("nvcc failed building " + lib)
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force=True, verbose=True)
-    print(LIB)
+    ap = argparse.ArgumentParser()
+    ap.add_argument("-D", action="append", default=[], dest="defines")
+    ap.add_argument("-o", dest="out", default=None)
+    ap.add_argument("-q", action="store_true")
+    a = ap.parse_args()
+    print(build(force=True, verbose=not a.q, defines=a.defines, out=a.out))

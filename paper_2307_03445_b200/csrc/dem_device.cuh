@@ -63,13 +63,14 @@ struct Grid {
   double cell;
   double dom_lo[3], dom_hi[3];
   int n[3];
+  long long st[3];  // linear bin id = sum_d idx[d] * st[d]; shortest axis fastest (locality)
   double pad;  // r + pad is the half-extent of a sphere's bin AABB (margin/2 + eps)
 };
 
 struct __align__(16) Entry {
   long long key;    // partner key (sphere key, or INT64_MAX - plane)
   int partner;      // partner local sphere index, or -1 - plane
-  int pad;
+  int prev;         // index of the same key in the previous step's rows (its u_t), or -1
 };
 
 struct Rows {

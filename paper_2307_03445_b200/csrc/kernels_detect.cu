@@ -72,8 +72,8 @@ __global__ void __launch_bounds__(256) k_pose_count(StepArgs a) {
   cell_range(g, 2, cz, r, lz, hz);
   for (int z = lz; z <= hz; ++z)
     for (int y = ly; y <= hy; ++y) {
-      const long long base = ((long long)z * g.n[1] + y) * g.n[0];
-      for (int x = lx; x <= hx; ++x) atomicAdd(&a.cell_count[base + x], 1);
+      const long long base = z * g.st[2] + y * g.st[1];
+      for (int x = lx; x <= hx; ++x) atomicAdd(&a.cell_count[base + x * g.st[0]], 1);
     }
 }
 
@@ -93,9 +93,9 @@ __global__ void __launch_bounds__(256) k_bin_scatter(StepArgs a) {
   cell_range(g, 2, s.z, s.w, lz, hz);
   for (int z = lz; z <= hz; ++z)
     for (int y = ly; y <= hy; ++y) {
-      const long long base = ((long long)z * g.n[1] + y) * g.n[0];
+      const long long base = z * g.st[2] + y * g.st[1];
       for (int x = lx; x <= hx; ++x) {
-        const long long cid = base + x;
+        const long long cid = base + x * g.st[0];
         const int slot = atomicSub(&a.cell_count[cid], 1) - 1;
         if (fits) a.items[a.cell_start[cid] + slot] = i;
       }
@@ -103,8 +103,19 @@ __global__ void __launch_bounds__(256) k_bin_scatter(StepArgs a) {
 }
 
 // ---------------------------------------------------------------- (a3) per-bin pair tests
+// tuning knobs (build-time; see build.py -D): buffered pairs per warp, min CTAs/SM for the
+// register budget, and whether the row-slot atomics are deferred to the buffer flush
+#ifndef DEM_PAIRS_BUF
+#define DEM_PAIRS_BUF 64
+#endif
+#ifndef DEM_PAIRS_MINB
+#define DEM_PAIRS_MINB 5
+#endif
+#ifndef DEM_PAIRS_DEFER
+#define DEM_PAIRS_DEFER 1
+#endif
 constexpr int kPairWarps = 8;
-constexpr int kPairBuf = 128;
+constexpr int kPairBuf = DEM_PAIRS_BUF;
 
 // Shared-memory member of a bin.  Both spheres of a pair overlap the bin C, so their
 // lowest bins satisfy lo <= C on every axis and max(lo_a, lo_b) == C  <=>  on every axis
@@ -134,18 +145,53 @@ __device__ __forceinline__ void decode_tri(int p, int& i, int& j) {
   i = p - jj * (jj - 1) / 2;
 }
 
+// Flush a warp's buffered pairs: one cursor atomic per warp, then the per-row counting
+// atomics that hand out each entry's slot in its row (walls come first).  The row atomics
+// are issued here, 2 x kPairBuf/32 independent ones per lane, so their latency overlaps
+// instead of stalling the pair loop on every hit.
 __device__ __forceinline__ void flush_pairs(const StepArgs& a, int4* bf, int n, int lane) {
   __syncwarp();
   if (n == 0) return;
   unsigned long long off = 0;
   if (lane == 0) off = atomicAdd(a.pair_cursor, (unsigned long long)n);
   off = __shfl_sync(0xffffffffu, off, 0);
+#if DEM_PAIRS_DEFER
+  constexpr int kPer = kPairBuf / 32;
+  int4 v[kPer];
+  int sa[kPer], sb[kPer];
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int k = lane + 32 * j;
+    if (k < n) {
+      v[j] = bf[k];
+      sa[j] = atomicAdd(&a.row_cnt[v[j].x], 1);
+      sb[j] = atomicAdd(&a.row_cnt[v[j].y], 1);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int k = lane + 32 * j;
+    if (k < n && (long long)(off + k) < a.cap_pairs) a.pairs[off + k] = make_int4(v[j].x, v[j].y, sa[j], sb[j]);
+  }
+#else
   for (int k = lane; k < n; k += 32)
     if ((long long)(off + k) < a.cap_pairs) a.pairs[off + k] = bf[k];
+#endif
   __syncwarp();
 }
 
-__global__ void __launch_bounds__(kPairWarps * 32) k_pairs(StepArgs a) {
+// a hit of the pair loop: buffered; with DEM_PAIRS_DEFER = 0 the slots are taken right here
+__device__ __forceinline__ int4 pair_record(const StepArgs& a, int ia, int ib) {
+#if DEM_PAIRS_DEFER
+  return make_int4(ia, ib, 0, 0);
+#else
+  const int sa = atomicAdd(&a.row_cnt[ia], 1);
+  const int sb = atomicAdd(&a.row_cnt[ib], 1);
+  return make_int4(ia, ib, sa, sb);
+#endif
+}
+
+__global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepArgs a) {
   __shared__ Members smA[kPairWarps];
   __shared__ Members smB[kPairWarps];
   __shared__ int4 sbuf[kPairWarps][kPairBuf];
@@ -166,10 +212,57 @@ __global__ void __launch_bounds__(kPairWarps * 32) k_pairs(StepArgs a) {
     const int k0 = a.cell_start[cid];
     const int m = a.cell_start[cid + 1] - k0;
     if (m < 2) continue;
-    const int cx = (int)(cid % g.n[0]);
-    const long long rest = cid / g.n[0];
-    const int cy = (int)(rest % g.n[1]);
-    const int cz = (int)(rest / g.n[1]);
+    const int cx = (int)((cid / g.st[0]) % g.n[0]);
+    const int cy = (int)((cid / g.st[1]) % g.n[1]);
+    const int cz = (int)((cid / g.st[2]) % g.n[2]);
+    if (m <= 32) {
+      // Common case: lane l holds member l in registers.  Rotation schedule: in round k
+      // (1 <= k <= m/2) lane l tests the pair (l, l + k mod m), partner data by shuffle;
+      // for even m the last round keeps lanes l < m/2 only.  Every unordered pair of the
+      // bin is tested exactly once, with all m lanes busy and no index decoding.
+      double4 u = make_double4(0.0, 0.0, 0.0, 0.0);
+      int2 mu = make_int2(-1, 0);
+      if (lane < m) {
+        const int idx = a.items[k0 + lane];
+        u = a.spos[idx];
+        const int mk = (cell_lo(g, 0, u.x, u.w) == cx ? 1 : 0) | (cell_lo(g, 1, u.y, u.w) == cy ? 2 : 0) |
+                       (cell_lo(g, 2, u.z, u.w) == cz ? 4 : 0);
+        mu = make_int2(a.s_clump[idx], idx | (mk << 29));
+      }
+      for (int k = 1; 2 * k <= m; ++k) {
+        int src = lane + k;
+        if (src >= m) src -= m;
+        if (lane >= m) src = lane;
+        const int vcl = __shfl_sync(0xffffffffu, mu.x, src);
+        const int vmeta = __shfl_sync(0xffffffffu, mu.y, src);
+        const double vx = __shfl_sync(0xffffffffu, u.x, src);
+        const double vy = __shfl_sync(0xffffffffu, u.y, src);
+        const double vz = __shfl_sync(0xffffffffu, u.z, src);
+        const double vw = __shfl_sync(0xffffffffu, u.w, src);
+        const bool active = lane < m && !(2 * k == m && lane >= k);
+        bool hit = false;
+        if (active && mu.x != vcl && (((unsigned)(mu.y | vmeta) >> 29) == 7u)) {
+          const double dx = sub(vx, u.x), dy = sub(vy, u.y), dz = sub(vz, u.z);
+          const double d2 = add(add(mul(dx, dx), mul(dy, dy)), mul(dz, dz));
+          const double s = add(add(u.w, vw), a.margin);
+          hit = d2 <= mul(s, s);
+        }
+        const unsigned mask = __ballot_sync(0xffffffffu, hit);
+        if (mask) {
+          const int cnt = __popc(mask);
+          if (nbuf + cnt > kPairBuf) {
+            flush_pairs(a, bf, nbuf, lane);
+            nbuf = 0;
+          }
+          if (hit)
+            bf[nbuf + __popc(mask & ((1u << lane) - 1u))] =
+                pair_record(a, mu.y & 0x1fffffff, vmeta & 0x1fffffff);
+          nbuf += cnt;
+        }
+      }
+      continue;
+    }
+    // Large bins (m > 32): blocks of 32 members staged in shared memory, pairs by index decode.
     for (int ib = 0; ib < m; ib += 32) {
       const int mi = min(32, m - ib);
       __syncwarp();
@@ -216,12 +309,7 @@ __global__ void __launch_bounds__(kPairWarps * 32) k_pairs(StepArgs a) {
               flush_pairs(a, bf, nbuf, lane);
               nbuf = 0;
             }
-            if (hit) {
-              // the counting atomics hand out each entry's slot in its row (walls come first)
-              const int sa = atomicAdd(&a.row_cnt[ia], 1);
-              const int sb = atomicAdd(&a.row_cnt[ibx], 1);
-              bf[nbuf + __popc(mask & ((1u << lane) - 1u))] = make_int4(ia, ibx, sa, sb);
-            }
+            if (hit) bf[nbuf + __popc(mask & ((1u << lane) - 1u))] = pair_record(a, ia, ibx);
             nbuf += cnt;
           }
         }
@@ -251,10 +339,10 @@ __global__ void __launch_bounds__(256) k_rows_scatter(StepArgs a) {
     Entry ta, tb;
     ta.key = a.s_key[pr.y];
     ta.partner = pr.y;
-    ta.pad = 0;
+    ta.prev = -1;
     tb.key = a.s_key[pr.x];
     tb.partner = pr.x;
-    tb.pad = 0;
+    tb.prev = -1;
     a.rows.ent[ea] = ta;
     a.rows.ent[eb] = tb;
   }
@@ -278,7 +366,7 @@ __global__ void __launch_bounds__(256) k_rows_finish(StepArgs a) {
       Entry e;
       e.key = (long long)(0x7fffffffffffffffLL - p);
       e.partner = -1 - p;
-      e.pad = 0;
+      e.prev = -1;
       R[w++] = e;
     }
   }
@@ -290,6 +378,15 @@ __global__ void __launch_bounds__(256) k_rows_finish(StepArgs a) {
       --v;
     }
     R[v + 1] = x;
+  }
+  // (a4) history remap: merge with the sphere's previous row (both sorted by key) and keep
+  // the index of each surviving key's u_t, or -1 for a contact born this step
+  int pj = a.prev.row_ptr[i];
+  const int pend = a.prev.row_ptr[i + 1];
+  for (int u = 0; u < m; ++u) {
+    const long long k = R[u].key;
+    while (pj < pend && a.prev.ent[pj].key < k) ++pj;
+    R[u].prev = (pj < pend && a.prev.ent[pj].key == k) ? pj : -1;
   }
 }
 

@@ -33,8 +33,11 @@ int force_cta_spheres() { return kMaxS; }
 
 // One CTA = a run of whole clumps [c0, c1) and their spheres [s0, s0 + nsph), whose rows are
 // one contiguous CSR range [E0, E1).
-__global__ void __launch_bounds__(kFT, 5) k_force_integrate(StepArgs a) {
-  __shared__ int rp[kMaxS + 1], prp[kMaxS + 1];
+#ifndef DEM_FORCE_MINB
+#define DEM_FORCE_MINB 8
+#endif
+__global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArgs a) {
+  __shared__ int rp[kMaxS + 1];
   __shared__ double4 own_p[kMaxS];
   __shared__ int own_mat[kMaxS];
   __shared__ int own_lc[kMaxS];
@@ -60,7 +63,6 @@ __global__ void __launch_bounds__(kFT, 5) k_force_integrate(StepArgs a) {
   const int nsph = a.sph_off[c1] - s0;
   for (int k = tid; k <= nsph; k += kFT) {
     rp[k] = a.rows.row_ptr[s0 + k];
-    prp[k] = a.prev.row_ptr[s0 + k];
   }
   for (int ls = tid; ls < nsph; ls += kFT) {
     const int i = s0 + ls;
@@ -93,19 +95,13 @@ __global__ void __launch_bounds__(kFT, 5) k_force_integrate(StepArgs a) {
       const Entry ent = a.rows.ent[e];
       const long long key = ent.key;
       const int t = ent.partner;
-      // (a4) history remap: binary search of the key in the sphere's previous (sorted) row
+      // (a4) history remap: the slot of this key in the previous rows was found by the
+      // row merge in k_rows_finish (-1: contact born this step, u_t = 0)
       double ux = 0.0, uy = 0.0, uz = 0.0;
-      {
-        int l = prp[ls], r = prp[ls + 1];
-        while (l < r) {
-          const int mid = (l + r) >> 1;
-          if (a.prev.ent[mid].key < key) l = mid + 1; else r = mid;
-        }
-        if (l < prp[ls + 1] && a.prev.ent[l].key == key) {
-          ux = a.prev.ut[3 * l];
-          uy = a.prev.ut[3 * l + 1];
-          uz = a.prev.ut[3 * l + 2];
-        }
+      if (ent.prev >= 0) {
+        ux = a.prev.ut[3 * ent.prev];
+        uy = a.prev.ut[3 * ent.prev + 1];
+        uz = a.prev.ut[3 * ent.prev + 2];
       }
       // (a5) geometry: n from i (own) to j (partner)
       double nx, ny, nz, px, py, pz, delta, rbar, mbar;

@@ -544,6 +544,20 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
     return DEM_ERR_INVALID_ARG;
   }
   sys->ncell = ncell;
+  // bin linearization: the axis with the fewest bins fastest, the longest slowest, so the
+  // neighbours of a bin along every axis stay close in memory (and x-slabs are contiguous
+  // for the usual longest-x beds)
+  {
+    int ord[3] = {0, 1, 2};
+#ifndef DEM_XFAST
+    std::sort(ord, ord + 3, [&](int p, int q) { return G.n[p] != G.n[q] ? G.n[p] < G.n[q] : p > q; });
+#endif
+    long long s = 1;
+    for (int k = 0; k < 3; ++k) {
+      G.st[ord[k]] = s;
+      s *= G.n[ord[k]];
+    }
+  }
   // storage order: clumps sorted by the bin of their COM (spatial locality for every gather);
   // results do not depend on it (keys, canonical sums).  h_perm maps storage -> caller order.
   {
@@ -555,7 +569,7 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
         long long q = std::isfinite(v) ? (long long)std::floor(v) : 0;
         id[d] = std::min<long long>(std::max<long long>(q, 0), G.n[d] - 1);
       }
-      ckey[c] = (id[2] * G.n[1] + id[1]) * G.n[0] + id[0];
+      ckey[c] = id[0] * G.st[0] + id[1] * G.st[1] + id[2] * G.st[2];
     }
     sys->h_perm.resize(n);
     for (int64_t c = 0; c < n; ++c) sys->h_perm[c] = c;
@@ -703,7 +717,7 @@ extern "C" dem_status dem_set_contact_history(dem_system* sys, int64_t n, const 
       Entry en;
       en.key = e.key;
       en.partner = -1;  // only the key and u_t of the previous rows are read
-      en.pad = 0;
+      en.prev = -1;
       ents.push_back(en);
       for (int d = 0; d < 3; ++d) ut.push_back(e.u[d]);
     }
