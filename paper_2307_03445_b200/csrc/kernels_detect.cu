@@ -114,6 +114,9 @@ __global__ void __launch_bounds__(256) k_bin_scatter(StepArgs a) {
 #ifndef DEM_PAIRS_DEFER
 #define DEM_PAIRS_DEFER 1
 #endif
+#ifndef DEM_PAIRS_CONTIG
+#define DEM_PAIRS_CONTIG 64  // bins per run (0: plain grid-stride over bins)
+#endif
 constexpr int kPairWarps = 8;
 constexpr int kPairBuf = DEM_PAIRS_BUF;
 
@@ -208,7 +211,18 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
   int nbuf = 0;  // warp-uniform
   const Grid& g = a.grid;
   const long long nw = (long long)gridDim.x * kPairWarps;
+#if DEM_PAIRS_CONTIG
+  // CTAs take spans of kPairWarps x DEM_PAIRS_CONTIG consecutive bins round-robin and their
+  // warps interleave inside the span: concurrent warps work on adjacent bins (shared L1
+  // lines of multiply-inserted spheres), and a warp's buffered pairs — so the pair list and
+  // the row scatter that follows — stay spatially local
+  constexpr long long kSpan = (long long)kPairWarps * DEM_PAIRS_CONTIG;
+  for (long long cid = (long long)blockIdx.x * kSpan + w, stop = min(a.ncell, (long long)blockIdx.x * kSpan + kSpan);
+       cid < a.ncell;
+       (cid += kPairWarps) >= stop ? (cid += (long long)(gridDim.x - 1) * kSpan, stop = min(a.ncell, stop + (long long)gridDim.x * kSpan)) : 0) {
+#else
   for (long long cid = (long long)blockIdx.x * kPairWarps + w; cid < a.ncell; cid += nw) {
+#endif
     const int k0 = a.cell_start[cid];
     const int m = a.cell_start[cid + 1] - k0;
     if (m < 2) continue;
