@@ -54,7 +54,8 @@ typedef enum {
   DEM_ERR_OUT_OF_DOMAIN = -10,    /* a sphere centre left [domain_lo, domain_hi]       */
   DEM_ERR_NONFINITE = -11,        /* non-finite wrench/state                          */
   DEM_ERR_DEGENERATE_CONTACT = -12, /* coincident sphere centres in a contact         */
-  DEM_ERR_CAPACITY = -14          /* a buffer could not be grown (device memory exhausted)   */
+  DEM_ERR_CAPACITY = -14,         /* a buffer could not be grown (device memory exhausted)   */
+  DEM_ERR_REPARTITION = -15       /* distributed: an owned clump drifted beyond drift_max    */
 } dem_status;
 
 /* One sphere material.  Pair parameters of two materials follow DESIGN.md §3 R4:
@@ -96,11 +97,29 @@ typedef struct {
   dem_alloc_fn alloc;        /* NULL: cudaMallocAsync on the system stream */
   dem_free_fn free;
   void* alloc_ctx;
+  double entries_per_sphere; /* initial contact-row capacity per sphere (0 = 8); distributed systems
+                                cannot regrow mid-run (ranks would desynchronise): size it generously */
+  /* ---- spatial slab decomposition along x.  n_ranks <= 1: one system owns all. ----
+   * dem_set_state then takes the GLOBAL state on every rank; the rank owns the clumps whose COM x
+   * is in [slab_lo, slab_hi) and keeps ghost copies of the clumps within `halo` beyond each face
+   * (owned by the neighbouring ranks rank-1 / rank+1, so halo must not exceed a neighbour's slab
+   * width).  Every step the owners' new ghost states are exchanged; contacts are evaluated by the
+   * owner of each sphere (mirror-exact, so no force exchange), and owned states are bitwise
+   * independent of the number of ranks.  halo >= 2 R_bound,max + margin + 2 drift_max; an owned
+   * COM that moves more than drift_max from its dem_set_state position raises
+   * DEM_ERR_REPARTITION (re-call dem_set_state with the gathered global state to migrate). */
+  int32_t rank, n_ranks;
+  double slab_lo, slab_hi, halo, drift_max;
+  int32_t transport;         /* DEM_TRANSPORT_NCCL or DEM_TRANSPORT_LOOPBACK */
+  unsigned char nccl_id[128];/* ncclUniqueId from dem_nccl_unique_id on rank 0, broadcast by the caller */
 } dem_params;
+
+enum { DEM_TRANSPORT_NCCL = 0, DEM_TRANSPORT_LOOPBACK = 1 };
 
 typedef struct {
   int64_t steps;             /* steps completed since dem_set_state */
-  int64_t n_clumps, n_spheres;
+  int64_t n_clumps, n_spheres; /* owned + ghost */
+  int64_t n_owned_clumps, n_owned_spheres, n_ghost_clumps;
   int64_t n_entries;         /* directed contact-row entries of the last step (2 per sphere pair + walls) */
   int64_t n_contacts;        /* canonical contacts of the last step (sphere pairs + sphere-wall) */
   int64_t n_inserts;         /* bin inserts of the last step */
@@ -136,7 +155,8 @@ dem_status dem_step(dem_system* sys, int64_t n_steps);
 dem_status dem_synchronize(dem_system* sys);
 
 /* Copy the state out in the order of the last dem_set_state.  cap = capacity in clumps; *n
- * receives the clump count.  Any output pointer may be NULL.  on_device as in dem_set_state. */
+ * receives the clump count.  Any output pointer may be NULL.  on_device as in dem_set_state.
+ * Distributed systems return their OWNED clumps only, in the order of the global input. */
 dem_status dem_get_state(dem_system* sys, int64_t cap, int64_t* n, int64_t* clump_gid, int32_t* template_id,
                          double* pos, double* quat, double* vel, double* omega, int32_t on_device);
 
@@ -157,6 +177,27 @@ dem_status dem_get_stats(dem_system* sys, dem_stats* out);
  * canonical per-sphere and per-clump sums, Eq. 4 update) — 8 stages. */
 dem_status dem_set_profiling(dem_system* sys, int32_t enable);
 dem_status dem_get_stage_times(dem_system* sys, int32_t n_stages, double* ms);
+
+/* ---- distribution ---- */
+
+/* 128-byte NCCL unique id for params.nccl_id (call on rank 0, broadcast to every rank, then each
+ * rank calls dem_create collectively).  Host only. */
+dem_status dem_nccl_unique_id(unsigned char out[128]);
+
+/* The slab partition as every rank computes it (host only, no GPU): for n clumps with COM x in
+ * pos[3c], role[c] = 0 not held, 1 owned (slab_lo <= x < slab_hi), 2 ghost from the left
+ * neighbour (slab_lo - halo <= x < slab_lo), 3 ghost from the right neighbour
+ * (slab_hi <= x < slab_hi + halo); send[c] bit 0 = owned and sent to the left neighbour
+ * (x < slab_lo + halo), bit 1 = owned and sent to the right neighbour (x >= slab_hi - halo).
+ * has_left / has_right say whether those neighbours exist.  Ghost and send lists are exchanged
+ * in ascending clump gid order. */
+dem_status dem_partition_plan(int64_t n, const double* pos, double slab_lo, double slab_hi, double halo,
+                              int32_t has_left, int32_t has_right, int8_t* role, int8_t* send);
+
+/* Step a group of LOOPBACK-transport systems (ranks 0..n-1 in order, same GPU and stream) in
+ * lockstep: per step every rank computes, then the ghost buffers are copied device-to-device
+ * between neighbours.  Lets one GPU run a P-rank decomposition (tests, scaling studies). */
+dem_status dem_step_group(dem_system* const* systems, int32_t n, int64_t n_steps);
 
 const char* dem_status_string(dem_status s);
 dem_status dem_last_error(const dem_system* sys, char* buf, size_t len);

@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("DEM_LIB_PATH") or os.path.join(_HERE, "libdem_b200.so
 
 DEM_STATUS = {0: "ok", -1: "invalid argument", -2: "CUDA error", -3: "out of device memory", -4: "NCCL error",
               -5: "bad material", -6: "bad template", -10: "sphere out of domain", -11: "non-finite wrench",
-              -12: "degenerate contact", -14: "capacity"}
+              -12: "degenerate contact", -14: "capacity", -15: "repartition needed"}
 
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
 FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
@@ -41,18 +41,25 @@ class dem_plane(C.Structure):
 class dem_params(C.Structure):
     _fields_ = [("h", C.c_double), ("gravity", C.c_double * 3), ("margin", C.c_double), ("cd_every", C.c_int32),
                 ("domain_lo", C.c_double * 3), ("domain_hi", C.c_double * 3), ("cell_size", C.c_double),
-                ("record_contacts", C.c_int32), ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_ctx", C.c_void_p)]
+                ("record_contacts", C.c_int32), ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_ctx", C.c_void_p),
+                ("entries_per_sphere", C.c_double), ("rank", C.c_int32), ("n_ranks", C.c_int32),
+                ("slab_lo", C.c_double), ("slab_hi", C.c_double), ("halo", C.c_double), ("drift_max", C.c_double),
+                ("transport", C.c_int32), ("nccl_id", C.c_ubyte * 128)]
 
 
 class dem_stats(C.Structure):
-    _fields_ = [("steps", C.c_int64), ("n_clumps", C.c_int64), ("n_spheres", C.c_int64), ("n_entries", C.c_int64),
-                ("n_contacts", C.c_int64), ("n_inserts", C.c_int64), ("n_cells", C.c_int64),
+    _fields_ = [("steps", C.c_int64), ("n_clumps", C.c_int64), ("n_spheres", C.c_int64),
+                ("n_owned_clumps", C.c_int64), ("n_owned_spheres", C.c_int64), ("n_ghost_clumps", C.c_int64),
+                ("n_entries", C.c_int64), ("n_contacts", C.c_int64), ("n_inserts", C.c_int64), ("n_cells", C.c_int64),
                 ("cell_size", C.c_double), ("regrows", C.c_int64), ("kernel_launches_per_step", C.c_int64)]
 
 
+TRANSPORT_NCCL, TRANSPORT_LOOPBACK = 0, 1
+
 EXPORTS = ["dem_create", "dem_set_state", "dem_set_contact_history", "dem_step", "dem_synchronize",
            "dem_get_state", "dem_get_contacts", "dem_get_stats", "dem_set_profiling", "dem_get_stage_times",
-           "dem_status_string", "dem_last_error", "dem_destroy"]
+           "dem_status_string", "dem_last_error", "dem_destroy", "dem_nccl_unique_id", "dem_partition_plan",
+           "dem_step_group"]
 
 _lib = None
 
@@ -81,6 +88,9 @@ def load_library(path: str = LIB_PATH):
     L.dem_last_error.argtypes = [P, C.c_char_p, C.c_size_t]
     L.dem_destroy.argtypes = [P]
     L.dem_destroy.restype = None
+    L.dem_nccl_unique_id.argtypes = [P]
+    L.dem_partition_plan.argtypes = [I64, P, C.c_double, C.c_double, C.c_double, I32, I32, P, P]
+    L.dem_step_group.argtypes = [P, I32, I64]
     for f in EXPORTS:
         if f not in ("dem_destroy", "dem_status_string"):
             getattr(L, f).restype = C.c_int
@@ -104,14 +114,17 @@ def _f64(a, shape=None):
 
 
 STAGES = ["pose+bin_count", "bin_scan", "bin_scatter", "pairs", "row_scan", "rows_scatter", "rows_finish",
-          "force+integrate"]
+          "force+integrate", "halo"]
 
 
 class System:
     """One dem_system on the current CUDA device and PyTorch's current stream."""
 
     def __init__(self, materials, templates, planes=(), *, h, gravity=(0.0, 0.0, -9.81), domain_lo, domain_hi,
-                 margin=0.0, cell_size=0.0, record_contacts=False, use_torch_allocator=True, stream=None):
+                 margin=0.0, cell_size=0.0, record_contacts=False, use_torch_allocator=True, stream=None,
+                 entries_per_sphere=0.0, dist=None):
+        """dist (optional): dict(rank, n_ranks, slab_lo, slab_hi, halo, drift_max, transport, nccl_id) —
+        the slab decomposition of dem_params (include/dem.h); nccl_id from nccl_unique_id() on rank 0."""
         import torch  # plumbing only: device memory and streams
 
         if not torch.cuda.is_available():
@@ -147,6 +160,14 @@ class System:
         p.domain_hi[:] = [float(x) for x in domain_hi]
         p.cell_size = cell_size
         p.record_contacts = 1 if record_contacts else 0
+        p.entries_per_sphere = float(entries_per_sphere)
+        if dist:
+            p.rank, p.n_ranks = int(dist["rank"]), int(dist["n_ranks"])
+            p.slab_lo, p.slab_hi = float(dist["slab_lo"]), float(dist["slab_hi"])
+            p.halo, p.drift_max = float(dist["halo"]), float(dist.get("drift_max", 0.0))
+            p.transport = int(dist.get("transport", TRANSPORT_NCCL))
+            if dist.get("nccl_id") is not None:
+                p.nccl_id[:] = list(dist["nccl_id"])
         if use_torch_allocator:
             dev = self.device
 
@@ -214,7 +235,10 @@ class System:
         self._check(load_library().dem_synchronize(self.sys), "dem_synchronize")
 
     def dem_get_state(self):
-        n = self.n
+        cnt = C.c_int64()
+        self._check(load_library().dem_get_state(self.sys, 0, C.byref(cnt), None, None, None, None, None, None, 0),
+                    "dem_get_state")
+        n = cnt.value  # owned clumps (all of them on a single system)
         out = dict(gid=np.zeros(n, np.int64), tid=np.zeros(n, np.int32), pos=np.zeros((n, 3)), quat=np.zeros((n, 4)),
                    vel=np.zeros((n, 3)), omega=np.zeros((n, 3)))
         nn = C.c_int64()
@@ -271,3 +295,54 @@ def system_from_scene(scene, record_contacts=False, cell_size=None, margin=None,
                cell_size=scene.cell_size if cell_size is None else cell_size, record_contacts=record_contacts, **kw)
     s.dem_set_state(scene.gid, scene.tid, scene.pos, scene.quat, scene.vel, scene.omega)
     return s
+
+
+# ---------------------------------------------------------------- distribution
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 creates it; the caller broadcasts it)."""
+    buf = (C.c_ubyte * 128)()
+    rc = load_library().dem_nccl_unique_id(C.cast(buf, C.c_void_p))
+    if rc:
+        raise DemError(rc, "dem_nccl_unique_id")
+    return bytes(buf)
+
+
+def partition_plan(pos, slab_lo, slab_hi, halo, has_left, has_right):
+    """Host-only slab plan of include/dem.h: (role, send) int8 arrays per clump."""
+    pos = _f64(pos).reshape(-1, 3)
+    n = pos.shape[0]
+    role, send = np.zeros(n, np.int8), np.zeros(n, np.int8)
+    rc = load_library().dem_partition_plan(n, _ptr(pos), float(slab_lo), float(slab_hi), float(halo),
+                                           int(bool(has_left)), int(bool(has_right)), _ptr(role), _ptr(send))
+    if rc:
+        raise DemError(rc, "dem_partition_plan")
+    return role, send
+
+
+def slab_bounds(x, n_ranks, lo, hi):
+    """Slab faces along x with equal clump counts (rank 0 / rank n-1 extend to the domain ends)."""
+    xs = np.sort(np.asarray(x))
+    b = [float(lo) - 1.0]
+    for r in range(1, n_ranks):
+        b.append(float(xs[int(round(r * len(xs) / n_ranks))]))
+    b.append(float(hi) + 1.0)
+    return b
+
+
+def step_group(systems, n_steps=1):
+    """Lockstep a loopback-transport group (ranks 0..n-1, same GPU and stream)."""
+    arr = (C.c_void_p * len(systems))(*[s.sys for s in systems])
+    rc = load_library().dem_step_group(arr, len(systems), int(n_steps))
+    if rc:
+        buf = C.create_string_buffer(512)
+        for s in systems:
+            load_library().dem_last_error(s.sys, buf, 512)
+            if buf.value:
+                break
+        raise DemError(rc, f"dem_step_group: {buf.value.decode()}")
+
+
+def halo_width(scene, drift_max):
+    """Ghost band: 2 x the largest bounding radius + margin + 2 drift_max (include/dem.h)."""
+    rb = max(float(np.max(np.linalg.norm(t.offsets, axis=1) + t.radius)) for t in scene.templates)
+    return 2.0 * rb + float(scene.margin) + 2.0 * drift_max

@@ -18,6 +18,15 @@ FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-li
          "-shared", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 
 
+def nccl_paths():
+    """NCCL 2.28 shipped with the torch wheel (nvidia-nccl): include dir and libnccl.so.2."""
+    import importlib.util
+
+    spec = importlib.util.find_spec("nvidia.nccl")
+    base = list(spec.submodule_search_locations)[0]
+    return os.path.join(base, "include"), os.path.join(base, "lib", "libnccl.so.2")
+
+
 def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
     lib = out or LIB
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
@@ -25,8 +34,10 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
     if not force and not defines and os.path.exists(lib) and os.path.getmtime(lib) >= max(
             os.path.getmtime(d) for d in deps):
         return lib
-    cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-o", lib + ".tmp",
-           *srcs]
+    nccl_inc, nccl_lib = nccl_paths()
+    cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-I", nccl_inc, "-o",
+           lib + ".tmp", *srcs, "-L" + os.path.dirname(nccl_lib), "-l:libnccl.so.2", "-Xlinker",
+           "-rpath=" + os.path.dirname(nccl_lib)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

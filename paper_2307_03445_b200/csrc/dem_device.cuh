@@ -109,6 +109,9 @@ struct StepArgs {
   double* kin;               // per clump [kKin]: X(3), V(3), omega_world(3), mass
   const int* cta_clump;      // [n_cta + 1] clump ranges of the fused force/integrate CTAs
   int n_cta;
+  int n_own, ns_own;         // owned clumps / spheres come first; the rest are ghosts (§8e)
+  const double* xref;        // [3 n_own] owned COMs at dem_set_state (distributed drift check)
+  double drift_max;          // 0: no check
   int* cell_count;
   int* cell_start;
   int* items;

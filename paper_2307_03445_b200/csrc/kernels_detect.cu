@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(256) k_pose_count(StepArgs a) {
     const double dd = add(add(mul(sub(cx, pp[0]), nw[0]), mul(sub(cy, pp[1]), nw[1])), mul(sub(cz, pp[2]), nw[2]));
     walls += sub(add(r, a.margin), dd) >= 0.0;
   }
-  a.row_cnt[i] = walls;
+  a.row_cnt[i] = i < a.ns_own ? walls : 0;  // ghosts get no rows (their owners evaluate them)
   int lx, hx, ly, hy, lz, hz;
   cell_range(g, 0, cx, r, lx, hx);
   cell_range(g, 1, cy, r, ly, hy);
@@ -167,8 +167,8 @@ __device__ __forceinline__ void flush_pairs(const StepArgs& a, int4* bf, int n, 
     const int k = lane + 32 * j;
     if (k < n) {
       v[j] = bf[k];
-      sa[j] = atomicAdd(&a.row_cnt[v[j].x], 1);
-      sb[j] = atomicAdd(&a.row_cnt[v[j].y], 1);
+      sa[j] = v[j].x < a.ns_own ? atomicAdd(&a.row_cnt[v[j].x], 1) : -1;  // -1: ghost, no row
+      sb[j] = v[j].y < a.ns_own ? atomicAdd(&a.row_cnt[v[j].y], 1) : -1;
     }
   }
 #pragma unroll
@@ -188,8 +188,8 @@ __device__ __forceinline__ int4 pair_record(const StepArgs& a, int ia, int ib) {
 #if DEM_PAIRS_DEFER
   return make_int4(ia, ib, 0, 0);
 #else
-  const int sa = atomicAdd(&a.row_cnt[ia], 1);
-  const int sb = atomicAdd(&a.row_cnt[ib], 1);
+  const int sa = ia < a.ns_own ? atomicAdd(&a.row_cnt[ia], 1) : -1;
+  const int sb = ib < a.ns_own ? atomicAdd(&a.row_cnt[ib], 1) : -1;
   return make_int4(ia, ib, sa, sb);
 #endif
 }
@@ -255,7 +255,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
         const double vw = __shfl_sync(0xffffffffu, u.w, src);
         const bool active = lane < m && !(2 * k == m && lane >= k);
         bool hit = false;
-        if (active && mu.x != vcl && (((unsigned)(mu.y | vmeta) >> 29) == 7u)) {
+        // different clumps, at least one owned (ghost-ghost pairs belong to other ranks), dedupe bin
+        if (active && mu.x != vcl && min(mu.x, vcl) < a.n_own && (((unsigned)(mu.y | vmeta) >> 29) == 7u)) {
           const double dx = sub(vx, u.x), dy = sub(vy, u.y), dz = sub(vz, u.z);
           const double d2 = add(add(mul(dx, dx), mul(dy, dy)), mul(dz, dz));
           const double s = add(add(u.w, vw), a.margin);
@@ -305,7 +306,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
             }
             const int2 mu = A.meta[i];
             const int2 mv = Bp.meta[j];
-            if (mu.x != mv.x && (((unsigned)(mu.y | mv.y) >> 29) == 7u)) {
+            if (mu.x != mv.x && min(mu.x, mv.x) < a.n_own && (((unsigned)(mu.y | mv.y) >> 29) == 7u)) {
               const double4 u = A.p[i];
               const double4 v = Bp.p[j];
               const double dx = sub(v.x, u.x), dy = sub(v.y, u.y), dz = sub(v.z, u.z);
@@ -348,17 +349,20 @@ __global__ void __launch_bounds__(256) k_rows_scatter(StepArgs a) {
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < (long long)np; t += stride) {
     const int4 pr = a.pairs[t];
-    const int ea = a.rows.row_ptr[pr.x] + pr.z;
-    const int eb = a.rows.row_ptr[pr.y] + pr.w;
-    Entry ta, tb;
-    ta.key = a.s_key[pr.y];
-    ta.partner = pr.y;
-    ta.prev = -1;
-    tb.key = a.s_key[pr.x];
-    tb.partner = pr.x;
-    tb.prev = -1;
-    a.rows.ent[ea] = ta;
-    a.rows.ent[eb] = tb;
+    if (pr.z >= 0) {  // slot -1: ghost sphere, evaluated by its owner
+      Entry ta;
+      ta.key = a.s_key[pr.y];
+      ta.partner = pr.y;
+      ta.prev = -1;
+      a.rows.ent[a.rows.row_ptr[pr.x] + pr.z] = ta;
+    }
+    if (pr.w >= 0) {
+      Entry tb;
+      tb.key = a.s_key[pr.x];
+      tb.partner = pr.x;
+      tb.prev = -1;
+      a.rows.ent[a.rows.row_ptr[pr.y] + pr.w] = tb;
+    }
   }
 }
 
@@ -366,7 +370,7 @@ __global__ void __launch_bounds__(256) k_rows_scatter(StepArgs a) {
 __global__ void __launch_bounds__(256) k_rows_finish(StepArgs a) {
   if (a.ctl->abort) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.ns) return;
+  if (i >= a.ns_own) return;
   const int beg = a.rows.row_ptr[i];
   const int m = a.rows.row_ptr[i + 1] - beg;
   Entry* R = a.rows.ent + beg;

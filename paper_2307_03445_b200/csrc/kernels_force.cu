@@ -255,9 +255,14 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
   }
   const double vx = ck[tid][3] + h * (Fx / M), vy = ck[tid][4] + h * (Fy / M), vz = ck[tid][5] + h * (Fz / M);
   a.nxt.vx[c] = vx; a.nxt.vy[c] = vy; a.nxt.vz[c] = vz;
-  a.nxt.x[c] = ck[tid][0] + h * vx;
-  a.nxt.y[c] = ck[tid][1] + h * vy;
-  a.nxt.z[c] = ck[tid][2] + h * vz;
+  const double nxx = ck[tid][0] + h * vx, nxy = ck[tid][1] + h * vy, nxz = ck[tid][2] + h * vz;
+  a.nxt.x[c] = nxx;
+  a.nxt.y[c] = nxy;
+  a.nxt.z[c] = nxz;
+  if (a.drift_max > 0.0) {  // distributed: the ghost bands are only valid within drift_max
+    const double dx = nxx - a.xref[3 * c], dy = nxy - a.xref[3 * c + 1], dz = nxz - a.xref[3 * c + 2];
+    if (dx * dx + dy * dy + dz * dz > a.drift_max * a.drift_max) raise_error(a.ctl, -15, a.gid[c], 0);
+  }
   const double w0 = a.cur.wx[c], w1 = a.cur.wy[c], w2 = a.cur.wz[c];
   const double L0 = I0 * w0, L1 = I1 * w1, L2 = I2 * w2;
   const double g0 = w1 * L2 - w2 * L1, g1 = w2 * L0 - w0 * L2, g2 = w0 * L1 - w1 * L0;
@@ -281,21 +286,50 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
   a.nxt.qw[c] = rw / nrm; a.nxt.qx[c] = rx / nrm; a.nxt.qy[c] = ry / nrm; a.nxt.qz[c] = rz / nrm;
 }
 
-// wall entries of a row set (for dem_get_stats: canonical contacts = walls + pairs/2)
-__global__ void k_count_walls(Rows r, int ns, unsigned long long* out) {
+// canonical contacts held in a row set: entries whose own sphere key is the smaller one
+// (every wall entry, and one of the two directed copies of a sphere pair) — dem_get_stats
+__global__ void k_count_canonical(Rows r, const long long* __restrict__ s_key, int ns, unsigned long long* out) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
-  unsigned long long c = 0;
-  if (i < ns)
-    for (int e = r.row_ptr[i]; e < r.row_ptr[i + 1]; ++e) c += r.ent[e].key > (0x7fffffffffffffffLL - kMaxPlanes);
-  c = __reduce_add_sync(0xffffffffu, (unsigned)c);
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+  unsigned c = 0;
+  if (i < ns) {
+    const long long own = s_key[i];
+    for (int e = r.row_ptr[i]; e < r.row_ptr[i + 1]; ++e) c += r.ent[e].key > own;
+  }
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (unsigned long long)c);
 }
 
 void launch_force_integrate(const StepArgs& a, cudaStream_t s) {
   if (a.n_cta > 0) k_force_integrate<<<a.n_cta, kFT, 0, s>>>(a);
 }
-void launch_count_walls(const Rows& r, int ns, unsigned long long* out, cudaStream_t s) {
-  if (ns) k_count_walls<<<(ns + 255) / 256, 256, 0, s>>>(r, ns, out);
+void launch_count_canonical(const Rows& r, const long long* s_key, int ns, unsigned long long* out, cudaStream_t s) {
+  if (ns) k_count_canonical<<<(ns + 255) / 256, 256, 0, s>>>(r, s_key, ns, out);
 }
 
+}  // namespace dem
+
+namespace dem {
+// ghost halo pack / unpack (distributed): 13 fp64 per clump, SoA in the buffer
+__global__ void k_pack(State st, const int* __restrict__ idx, int n, double* __restrict__ buf) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int c = idx[k];
+  const double* f[13] = {st.x, st.y, st.z, st.qw, st.qx, st.qy, st.qz, st.vx, st.vy, st.vz, st.wx, st.wy, st.wz};
+#pragma unroll
+  for (int q = 0; q < 13; ++q) buf[(size_t)q * n + k] = f[q][c];
+}
+__global__ void k_unpack(State st, const int* __restrict__ idx, int n, const double* __restrict__ buf) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int c = idx[k];
+  double* f[13] = {st.x, st.y, st.z, st.qw, st.qx, st.qy, st.qz, st.vx, st.vy, st.vz, st.wx, st.wy, st.wz};
+#pragma unroll
+  for (int q = 0; q < 13; ++q) f[q][c] = buf[(size_t)q * n + k];
+}
+void launch_pack(const State& st, const int* idx, int n, double* buf, cudaStream_t s) {
+  if (n) k_pack<<<(n + 255) / 256, 256, 0, s>>>(st, idx, n, buf);
+}
+void launch_unpack(const State& st, const int* idx, int n, const double* buf, cudaStream_t s) {
+  if (n) k_unpack<<<(n + 255) / 256, 256, 0, s>>>(st, idx, n, buf);
+}
 }  // namespace dem

@@ -12,6 +12,8 @@
 #include <unordered_map>
 #include <vector>
 
+#include <nccl.h>
+
 #include "dem.h"
 #include "dem_device.cuh"
 
@@ -26,12 +28,15 @@ int force_cta_clumps();
 int force_cta_spheres();
 long long scan_tiles_needed(long long n);
 void launch_excl_scan(const int* in, int* out, long long n, int* tmp, const int* abort, cudaStream_t s);
-void launch_count_walls(const Rows& r, int ns, unsigned long long* out, cudaStream_t s);
+void launch_count_canonical(const Rows& r, const long long* s_key, int ns, unsigned long long* out, cudaStream_t s);
+void launch_pack(const State& st, const int* idx, int n, double* buf, cudaStream_t s);
+void launch_unpack(const State& st, const int* idx, int n, const double* buf, cudaStream_t s);
 }  // namespace dem
 
 using namespace dem;
 
-static constexpr int kStages = 8;
+static constexpr int kStages = 9;  // last: ghost halo pack + exchange + unpack (distributed)
+static constexpr int kKin13 = 13;  // doubles per ghost clump state
 static constexpr int kLaunchesPerStep = 12;  // 6 stage kernels + 2 x 3 scan kernels
 
 struct RowBuf {
@@ -99,6 +104,14 @@ struct dem_system {
   double stage_ms[kStages] = {0};
   int64_t prof_steps = 0;
   std::unordered_map<void*, size_t> allocs;
+  // slab decomposition: storage = owned clumps [0, n_own), then ghosts
+  bool dist = false;
+  ncclComm_t comm = nullptr;
+  int64_t n_own = 0, ns_own = 0;
+  int n_send[2] = {0, 0}, n_recv[2] = {0, 0};       // [0] left neighbour, [1] right neighbour
+  int *d_send_idx[2] = {nullptr, nullptr}, *d_recv_idx[2] = {nullptr, nullptr};
+  double *d_sendbuf[2] = {nullptr, nullptr}, *d_recvbuf[2] = {nullptr, nullptr};
+  double* d_xref = nullptr;                          // owned COM at dem_set_state (drift check)
 };
 
 // ------------------------------------------------------------------ helpers
@@ -214,6 +227,10 @@ static StepArgs make_args(dem_system* sys, int p) {
   (void)ns;
   a.cta_clump = sys->d_cta_clump;
   a.n_cta = sys->n_cta;
+  a.n_own = (int)sys->n_own;
+  a.ns_own = (int)sys->ns_own;
+  a.xref = sys->d_xref;
+  a.drift_max = sys->dist ? sys->P.drift_max : 0.0;
   a.cell_count = sys->d_cell_count;
   a.cell_start = sys->d_cell_start;
   a.items = sys->d_items;
@@ -228,8 +245,32 @@ static StepArgs make_args(dem_system* sys, int p) {
   return a;
 }
 
-// the step sequence; ev (optional) receives kStages+1 events around the stages
-static void enqueue_step(dem_system* sys, int p, cudaStream_t s, cudaEvent_t* ev) {
+// ghost halo (distributed): owners' new states -> the neighbours' ghost slots
+static void enqueue_pack(dem_system* sys, const StepArgs& a, cudaStream_t s) {
+  for (int side = 0; side < 2; ++side)
+    if (sys->n_send[side]) launch_pack(a.nxt, sys->d_send_idx[side], sys->n_send[side], sys->d_sendbuf[side], s);
+}
+static void enqueue_unpack(dem_system* sys, const StepArgs& a, cudaStream_t s) {
+  for (int side = 0; side < 2; ++side)
+    if (sys->n_recv[side]) launch_unpack(a.nxt, sys->d_recv_idx[side], sys->n_recv[side], sys->d_recvbuf[side], s);
+}
+static void enqueue_nccl_exchange(dem_system* sys, cudaStream_t s) {
+  const int r = sys->P.rank, P = sys->P.n_ranks;
+  ncclGroupStart();
+  if (r > 0) {
+    if (sys->n_send[0]) ncclSend(sys->d_sendbuf[0], (size_t)kKin13 * sys->n_send[0], ncclDouble, r - 1, sys->comm, s);
+    if (sys->n_recv[0]) ncclRecv(sys->d_recvbuf[0], (size_t)kKin13 * sys->n_recv[0], ncclDouble, r - 1, sys->comm, s);
+  }
+  if (r < P - 1) {
+    if (sys->n_send[1]) ncclSend(sys->d_sendbuf[1], (size_t)kKin13 * sys->n_send[1], ncclDouble, r + 1, sys->comm, s);
+    if (sys->n_recv[1]) ncclRecv(sys->d_recvbuf[1], (size_t)kKin13 * sys->n_recv[1], ncclDouble, r + 1, sys->comm, s);
+  }
+  ncclGroupEnd();
+}
+
+// the step sequence; ev (optional) receives kStages+1 events around the stages.  With
+// exchange = false (loopback groups) the halo is packed but moved by dem_step_group.
+static void enqueue_step(dem_system* sys, int p, cudaStream_t s, cudaEvent_t* ev, bool exchange = true) {
   StepArgs a = make_args(sys, p);
   const int* abort = &sys->d_ctl->abort;
   if (ev) cudaEventRecord(ev[0], s);
@@ -249,6 +290,14 @@ static void enqueue_step(dem_system* sys, int p, cudaStream_t s, cudaEvent_t* ev
   if (ev) cudaEventRecord(ev[7], s);
   launch_force_integrate(a, s);
   if (ev) cudaEventRecord(ev[8], s);
+  if (sys->dist) {
+    enqueue_pack(sys, a, s);
+    if (exchange && sys->P.transport == DEM_TRANSPORT_NCCL) {
+      enqueue_nccl_exchange(sys, s);
+      enqueue_unpack(sys, a, s);
+    }
+  }
+  if (ev) cudaEventRecord(ev[9], s);
 }
 
 static dem_status capture_graphs(dem_system* sys) {
@@ -302,6 +351,7 @@ extern "C" const char* dem_status_string(dem_status s) {
     case DEM_ERR_OUT_OF_DOMAIN: return "sphere out of domain";
     case DEM_ERR_NONFINITE: return "non-finite wrench";
     case DEM_ERR_DEGENERATE_CONTACT: return "degenerate contact (coincident centres)";
+    case DEM_ERR_REPARTITION: return "owned clump drifted beyond drift_max (repartition)";
     case DEM_ERR_CAPACITY: return "capacity";
   }
   return "unknown";
@@ -323,6 +373,11 @@ extern "C" dem_status dem_create(const dem_params* params, const dem_material* m
     return DEM_ERR_INVALID_ARG;
   for (int d = 0; d < 3; ++d)
     if (!(params->domain_hi[d] > params->domain_lo[d])) return DEM_ERR_INVALID_ARG;
+  if (params->n_ranks > 1 &&
+      (params->rank < 0 || params->rank >= params->n_ranks || !(params->slab_hi > params->slab_lo) ||
+       !(params->halo > 0) || !(params->drift_max >= 0) ||
+       (params->transport != DEM_TRANSPORT_NCCL && params->transport != DEM_TRANSPORT_LOOPBACK)))
+    return DEM_ERR_INVALID_ARG;
   for (int m = 0; m < n_mat; ++m)
     if (!material_ok(materials[m])) return DEM_ERR_BAD_MATERIAL;
   for (int p = 0; p < n_planes; ++p) {
@@ -414,13 +469,36 @@ extern "C" dem_status dem_create(const dem_params* params, const dem_material* m
     dem_destroy(sys);
     return DEM_ERR_CUDA;
   }
+  if (params->n_ranks > 1) {
+    sys->dist = true;
+    if (params->transport == DEM_TRANSPORT_NCCL) {
+      ncclUniqueId id;
+      static_assert(sizeof(id.internal) == 128, "ncclUniqueId size");
+      std::memcpy(id.internal, params->nccl_id, 128);
+      ncclResult_t r = ncclCommInitRank(&sys->comm, params->n_ranks, id, params->rank);
+      if (r != ncclSuccess) {
+        sys->err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+        dem_destroy(sys);
+        return DEM_ERR_NCCL;
+      }
+    }
+  }
   *out = sys;
+  return DEM_OK;
+}
+
+extern "C" dem_status dem_nccl_unique_id(unsigned char out[128]) {
+  if (!out) return DEM_ERR_INVALID_ARG;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return DEM_ERR_NCCL;
+  std::memcpy(out, id.internal, 128);
   return DEM_OK;
 }
 
 extern "C" void dem_destroy(dem_system* sys) {
   if (!sys) return;
   cudaStreamSynchronize(sys->stream);
+  if (sys->comm) ncclCommDestroy(sys->comm);
   free_graphs(sys);
   std::vector<void*> ptrs;
   for (auto& kv : sys->allocs) ptrs.push_back(kv.first);
@@ -492,31 +570,52 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
       t[c] = tid[c];
     }
   }
-  int64_t ns = 0;
-  for (int64_t c = 0; c < n; ++c) {
+  for (int64_t c = 0; c < n; ++c)
     if (t[c] < 0 || t[c] >= sys->n_tmpl || g[c] < 0 || g[c] >= (1LL << 56)) {
       sys->err = "clump " + std::to_string(c) + ": bad template id or gid";
       return DEM_ERR_INVALID_ARG;
     }
+  // distributed: the held subset (owned + ghosts) of the global input
+  std::vector<int8_t> role(n, 1), sendf(n, 0);
+  if (sys->dist) {
+    const dem_params& P = sys->P;
+    TRY(dem_partition_plan(n, src[0], P.slab_lo, P.slab_hi, P.halo, P.rank > 0, P.rank < P.n_ranks - 1,
+                           role.data(), sendf.data()));
+  }
+  free_graphs(sys);
+  // grid: cell edge (auto: 4 x mean sphere radius + margin, at least 2 r_min + margin)
+  int64_t ns = 0, n_hold = 0;
+  double rsum = 0;
+  for (int64_t c = 0; c < n; ++c) {
+    if (!role[c]) continue;
+    ++n_hold;
     ns += sys->tpl_ncomp[t[c]];
+    for (int j = 0; j < sys->tpl_ncomp[t[c]]; ++j) rsum += sys->tc_rad[sys->tpl_coff[t[c]] + j];
   }
   if (ns >= (1LL << 29)) {  // the per-bin pair kernel packs sphere indices into 29 bits
     sys->err = "more than 2^29 spheres per system";
     return DEM_ERR_INVALID_ARG;
   }
-  free_graphs(sys);
-  // grid: cell edge (auto: 4 x mean sphere radius + margin, at least 2 r_min + margin)
-  double rsum = 0;
-  for (int64_t c = 0; c < n; ++c)
-    for (int j = 0; j < sys->tpl_ncomp[t[c]]; ++j) rsum += sys->tc_rad[sys->tpl_coff[t[c]] + j];
   double rmean = ns ? rsum / ns : sys->rmax;
   double cell = sys->P.cell_size > 0 ? sys->P.cell_size : std::max(4.0 * rmean, 2.0 * sys->rmin) + sys->P.margin;
+  // bin region: the domain (distributed: restricted in x to the slab and its halo; spheres that
+  // stray outside the bin region are clamped into its edge bins, which stays exact)
+  double blo[3], bhi[3];
+  for (int d = 0; d < 3; ++d) {
+    blo[d] = sys->P.domain_lo[d];
+    bhi[d] = sys->P.domain_hi[d];
+  }
+  if (sys->dist) {
+    blo[0] = std::max(blo[0], sys->P.slab_lo - sys->P.halo);
+    bhi[0] = std::min(bhi[0], sys->P.slab_hi + sys->P.halo);
+    if (!(bhi[0] > blo[0])) bhi[0] = blo[0] + cell;
+  }
   // the bin edge only changes speed, never results: coarsen it while a sparse domain would
   // need more than max(4M, 16 ns) bins
   const long long max_cells = std::max<long long>(4LL << 20, 16 * ns);
   auto cells_for = [&](double c) {
     long long m = 1;
-    for (int d = 0; d < 3; ++d) m *= (long long)std::ceil((sys->P.domain_hi[d] - sys->P.domain_lo[d]) / c) + 1;
+    for (int d = 0; d < 3; ++d) m *= (long long)std::ceil((bhi[d] - blo[d]) / c) + 1;
     return m;
   };
   if (sys->P.cell_size <= 0)
@@ -527,11 +626,10 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
   G.pad = 0.5 * sys->P.margin + 1e-9;
   long long ncell = 1;
   for (int d = 0; d < 3; ++d) {
-    G.lo[d] = sys->P.domain_lo[d];
+    G.lo[d] = blo[d];
     G.dom_lo[d] = sys->P.domain_lo[d];
     G.dom_hi[d] = sys->P.domain_hi[d];
-    double ext = sys->P.domain_hi[d] - sys->P.domain_lo[d];
-    long long nd = (long long)std::ceil(ext / cell) + 1;
+    long long nd = (long long)std::ceil((bhi[d] - blo[d]) / cell) + 1;
     if (nd > (1LL << 20)) {
       sys->err = "grid too fine for the domain";
       return DEM_ERR_INVALID_ARG;
@@ -558,8 +656,10 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
       s *= G.n[ord[k]];
     }
   }
-  // storage order: clumps sorted by the bin of their COM (spatial locality for every gather);
-  // results do not depend on it (keys, canonical sums).  h_perm maps storage -> caller order.
+  // storage order: owned clumps, then ghosts, each sorted by the bin of the COM (spatial
+  // locality for every gather); results do not depend on it (keys, canonical sums).
+  // h_perm maps storage -> caller index.
+  int64_t n_own = 0;
   {
     std::vector<long long> ckey(n);
     for (int64_t c = 0; c < n; ++c) {
@@ -571,21 +671,42 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
       }
       ckey[c] = id[0] * G.st[0] + id[1] * G.st[1] + id[2] * G.st[2];
     }
-    sys->h_perm.resize(n);
-    for (int64_t c = 0; c < n; ++c) sys->h_perm[c] = c;
-    std::stable_sort(sys->h_perm.begin(), sys->h_perm.end(),
-                     [&](int64_t x, int64_t y) { return ckey[x] < ckey[y]; });
-    std::vector<long long> g2(n);
-    std::vector<int> t2(n);
-    for (int64_t c = 0; c < n; ++c) {
+    sys->h_perm.clear();
+    for (int64_t c = 0; c < n; ++c)
+      if (role[c] == 1) sys->h_perm.push_back(c);
+    n_own = (int64_t)sys->h_perm.size();
+    for (int64_t c = 0; c < n; ++c)
+      if (role[c] >= 2) sys->h_perm.push_back(c);
+    auto by_bin = [&](int64_t x, int64_t y) { return ckey[x] < ckey[y]; };
+    std::stable_sort(sys->h_perm.begin(), sys->h_perm.begin() + n_own, by_bin);
+    std::stable_sort(sys->h_perm.begin() + n_own, sys->h_perm.end(), by_bin);
+    std::vector<long long> g2(n_hold);
+    std::vector<int> t2(n_hold);
+    for (int64_t c = 0; c < n_hold; ++c) {
       g2[c] = g[sys->h_perm[c]];
       t2[c] = t[sys->h_perm[c]];
     }
     g.swap(g2);
     t.swap(t2);
   }
+  // halo lists (ascending gid on both sides of every exchange)
+  std::vector<int> lists[4];  // send left, send right, recv left, recv right (storage indices)
+  if (sys->dist) {
+    for (int64_t i = 0; i < n_hold; ++i) {
+      const int64_t c = sys->h_perm[i];
+      if (i < n_own) {
+        if (sendf[c] & 1) lists[0].push_back((int)i);
+        if (sendf[c] & 2) lists[1].push_back((int)i);
+      } else {
+        lists[role[c] == 2 ? 2 : 3].push_back((int)i);
+      }
+    }
+    for (auto& L : lists) std::sort(L.begin(), L.end(), [&](int x, int y) { return g[x] < g[y]; });
+  }
+  n = n_hold;
   sys->n = n;
   sys->ns = ns;
+  sys->n_own = n_own;
   sys->h_gid = g;
   sys->h_tid = t;
   sys->h_sph_off.assign(n + 1, 0);
@@ -602,6 +723,7 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
     }
   }
   sys->h_sph_off[n] = (int)k;
+  sys->ns_own = sys->h_sph_off[n_own];
   // SoA state on the host, one upload
   std::vector<double> st((size_t)13 * n);
   for (int64_t i = 0; i < n; ++i) {
@@ -638,10 +760,11 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
   TRY(alloc_arr(sys, &sys->d_pairs, sys->cap_pairs));
   // CTA partition of the fused force/integrate kernel: consecutive whole clumps, at most
   // force_cta_clumps() clumps and force_cta_spheres() spheres per CTA
+  // (owned clumps only: ghosts are integrated by their owners)
   std::vector<int> cta{0};
   {
     int nc = 0, nsph = 0;
-    for (int64_t c = 0; c < n; ++c) {
+    for (int64_t c = 0; c < n_own; ++c) {
       const int m = sys->tpl_ncomp[t[c]];
       if (nc == force_cta_clumps() || nsph + m > force_cta_spheres()) {
         cta.push_back((int)c);
@@ -651,7 +774,7 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
       ++nc;
       nsph += m;
     }
-    if (n > 0) cta.push_back((int)n);
+    if (n_own > 0) cta.push_back((int)n_own);
   }
   sys->n_cta = (int)cta.size() - 1;
   TRY(alloc_arr(sys, &sys->d_cta_clump, cta.size()));
@@ -661,7 +784,21 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
   TRY(alloc_arr(sys, &sys->d_row_cnt, ns + 1));
   TRY(alloc_arr(sys, &sys->d_scan_tmp, std::max(scan_tiles_needed(ncell), scan_tiles_needed(ns)) + 1));
   for (int p = 0; p < 2; ++p) TRY(alloc_arr(sys, &sys->rows[p].row_ptr, ns + 1));
-  long long cap = std::max<long long>(1024, 8 * ns);
+  // halo buffers and the partition-time COMs of owned clumps (drift check)
+  std::vector<double> xref((size_t)3 * n_own);
+  for (int64_t i = 0; i < n_own; ++i)
+    for (int d = 0; d < 3; ++d) xref[3 * i + d] = src[0][3 * sys->h_perm[i] + d];
+  TRY(alloc_arr(sys, &sys->d_xref, xref.size() + 1));
+  for (int side = 0; side < 2; ++side) {
+    sys->n_send[side] = (int)lists[side].size();
+    sys->n_recv[side] = (int)lists[2 + side].size();
+    TRY(alloc_arr(sys, &sys->d_send_idx[side], lists[side].size() + 1));
+    TRY(alloc_arr(sys, &sys->d_recv_idx[side], lists[2 + side].size() + 1));
+    TRY(alloc_arr(sys, &sys->d_sendbuf[side], (size_t)kKin13 * lists[side].size() + 1));
+    TRY(alloc_arr(sys, &sys->d_recvbuf[side], (size_t)kKin13 * lists[2 + side].size() + 1));
+  }
+  const double eps = sys->P.entries_per_sphere > 0 ? sys->P.entries_per_sphere : 8.0;
+  long long cap = std::max<long long>(1024, (long long)(eps * ns));
   sys->cap_entries = 0;
   for (int p = 0; p < 2; ++p) {
     dfree(sys, sys->rows[p].ent); sys->rows[p].ent = nullptr;
@@ -670,6 +807,15 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
   TRY(alloc_rows(sys, cap));
   cudaStream_t s = sys->stream;
   CK(cudaMemcpyAsync(sys->d_cta_clump, cta.data(), sizeof(int) * cta.size(), cudaMemcpyHostToDevice, s));
+  if (n_own) CK(cudaMemcpyAsync(sys->d_xref, xref.data(), sizeof(double) * xref.size(), cudaMemcpyHostToDevice, s));
+  for (int side = 0; side < 2; ++side) {
+    if (!lists[side].empty())
+      CK(cudaMemcpyAsync(sys->d_send_idx[side], lists[side].data(), sizeof(int) * lists[side].size(),
+                         cudaMemcpyHostToDevice, s));
+    if (!lists[2 + side].empty())
+      CK(cudaMemcpyAsync(sys->d_recv_idx[side], lists[2 + side].data(), sizeof(int) * lists[2 + side].size(),
+                         cudaMemcpyHostToDevice, s));
+  }
   CK(cudaMemcpyAsync(sys->d_gid, g.data(), sizeof(long long) * n, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(sys->d_tid, t.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(sys->d_sph_off, sys->h_sph_off.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice, s));
@@ -694,7 +840,7 @@ extern "C" dem_status dem_set_contact_history(dem_system* sys, int64_t n, const 
   if (!sys || n < 0 || (n && (!key_a || !key_b || !u_t))) return DEM_ERR_INVALID_ARG;
   std::unordered_map<long long, int> idx;
   idx.reserve((size_t)sys->ns * 2);
-  for (int64_t s = 0; s < sys->ns; ++s) idx[sys->h_s_key[s]] = (int)s;
+  for (int64_t s = 0; s < sys->ns_own; ++s) idx[sys->h_s_key[s]] = (int)s;  // owned spheres only
   struct E {
     long long key;
     double u[3];
@@ -759,6 +905,10 @@ static dem_status device_error(dem_system* sys) {
       std::snprintf(buf, sizeof buf, "coincident centres of spheres %lld and %lld at step %lld", c.err_key,
                     c.err_key2, c.err_step);
       break;
+    case DEM_ERR_REPARTITION:
+      std::snprintf(buf, sizeof buf, "owned clump gid %lld drifted beyond drift_max at step %lld: repartition",
+                    c.err_key, c.err_step);
+      break;
     default:
       std::snprintf(buf, sizeof buf, "device error %d at step %lld", c.err_code, c.err_step);
   }
@@ -813,6 +963,10 @@ extern "C" dem_status dem_step(dem_system* sys, int64_t n_steps) {
     if (sys->h_ctl->err_code) return device_error(sys);
     remaining -= done;
     if (!sys->h_ctl->abort) break;
+    if (sys->dist) {  // a local regrow would desynchronise the ranks' halo exchanges
+      sys->err = "capacity overflow on a distributed system (raise params.entries_per_sphere)";
+      return DEM_ERR_CAPACITY;
+    }
     // capacity abort: regrow and re-run the steps that did not complete
     if (++guard > 8) {
       sys->err = "capacity regrow did not converge";
@@ -857,13 +1011,22 @@ extern "C" dem_status dem_synchronize(dem_system* sys) {
 extern "C" dem_status dem_get_state(dem_system* sys, int64_t cap, int64_t* n, int64_t* gid, int32_t* tid,
                                     double* pos, double* quat, double* vel, double* omega, int32_t on_device) {
   if (!sys) return DEM_ERR_INVALID_ARG;
-  if (n) *n = sys->n;
-  if (cap < sys->n) return (pos || quat || vel || omega || gid || tid) ? DEM_ERR_INVALID_ARG : DEM_OK;
+  const int64_t NO = sys->n_own;  // owned clumps (all of them on a single system)
+  if (n) *n = NO;
+  if (cap < NO) return (pos || quat || vel || omega || gid || tid) ? DEM_ERR_INVALID_ARG : DEM_OK;
   CK(cudaStreamSynchronize(sys->stream));
   const int64_t N = sys->n;
   std::vector<double> st((size_t)13 * N);
   if (N)
     CK(cudaMemcpy(st.data(), sys->d_state[sys->launched & 1], sizeof(double) * 13 * N, cudaMemcpyDeviceToHost));
+  // output row of each owned storage index: rank of its caller index among the owned ones
+  std::vector<int64_t> outpos(NO);
+  {
+    std::vector<int64_t> ord(NO);
+    for (int64_t i = 0; i < NO; ++i) ord[i] = i;
+    std::sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) { return sys->h_perm[x] < sys->h_perm[y]; });
+    for (int64_t r = 0; r < NO; ++r) outpos[ord[r]] = r;
+  }
   std::vector<double> out[4];
   double* dst[4] = {pos, quat, vel, omega};
   const int width[4] = {3, 4, 3, 3}, first[4] = {0, 3, 7, 10};
@@ -871,32 +1034,102 @@ extern "C" dem_status dem_get_state(dem_system* sys, int64_t cap, int64_t* n, in
     if (!dst[k]) continue;
     double* o = dst[k];
     if (on_device) {
-      out[k].resize((size_t)width[k] * N);
+      out[k].resize((size_t)width[k] * NO);
       o = out[k].data();
     }
-    for (int64_t i = 0; i < N; ++i) {
-      const int64_t c = sys->h_perm[i];
+    for (int64_t i = 0; i < NO; ++i) {
+      const int64_t c = outpos[i];
       for (int d = 0; d < width[k]; ++d) o[width[k] * c + d] = st[(first[k] + d) * N + i];
     }
-    if (on_device && N) CK(cudaMemcpy(dst[k], o, sizeof(double) * width[k] * N, cudaMemcpyHostToDevice));
+    if (on_device && NO) CK(cudaMemcpy(dst[k], o, sizeof(double) * width[k] * NO, cudaMemcpyHostToDevice));
   }
-  std::vector<long long> go(N);
-  std::vector<int> to(N);
-  for (int64_t i = 0; i < N; ++i) {
-    go[sys->h_perm[i]] = sys->h_gid[i];
-    to[sys->h_perm[i]] = sys->h_tid[i];
+  std::vector<long long> go(NO);
+  std::vector<int> to(NO);
+  for (int64_t i = 0; i < NO; ++i) {
+    go[outpos[i]] = sys->h_gid[i];
+    to[outpos[i]] = sys->h_tid[i];
   }
   if (gid) {
     if (on_device)
-      CK(cudaMemcpy(gid, go.data(), sizeof(long long) * N, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(gid, go.data(), sizeof(long long) * NO, cudaMemcpyHostToDevice));
     else
-      std::memcpy(gid, go.data(), sizeof(long long) * N);
+      std::memcpy(gid, go.data(), sizeof(long long) * NO);
   }
   if (tid) {
     if (on_device)
-      CK(cudaMemcpy(tid, to.data(), sizeof(int) * N, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(tid, to.data(), sizeof(int) * NO, cudaMemcpyHostToDevice));
     else
-      std::memcpy(tid, to.data(), sizeof(int) * N);
+      std::memcpy(tid, to.data(), sizeof(int) * NO);
+  }
+  return DEM_OK;
+}
+
+extern "C" dem_status dem_partition_plan(int64_t n, const double* pos, double slab_lo, double slab_hi, double halo,
+                                         int32_t has_left, int32_t has_right, int8_t* role, int8_t* send) {
+  if (n < 0 || (n && (!pos || !role || !send)) || !(slab_hi > slab_lo) || !(halo >= 0)) return DEM_ERR_INVALID_ARG;
+  for (int64_t c = 0; c < n; ++c) {
+    const double x = pos[3 * c];
+    int8_t r = 0, f = 0;
+    if (x >= slab_lo && x < slab_hi) {
+      r = 1;
+      if (has_left && x < slab_lo + halo) f |= 1;
+      if (has_right && x >= slab_hi - halo) f |= 2;
+    } else if (has_left && x < slab_lo && x >= slab_lo - halo) {
+      r = 2;
+    } else if (has_right && x >= slab_hi && x < slab_hi + halo) {
+      r = 3;
+    }
+    role[c] = r;
+    send[c] = f;
+  }
+  return DEM_OK;
+}
+
+extern "C" dem_status dem_step_group(dem_system* const* systems, int32_t n, int64_t n_steps) {
+  if (!systems || n < 1 || n_steps < 0) return DEM_ERR_INVALID_ARG;
+  cudaStream_t s = systems[0]->stream;
+  for (int r = 0; r < n; ++r) {
+    dem_system* sys = systems[r];
+    if (!sys || sys->stream != s || (n > 1 && (!sys->dist || sys->P.transport != DEM_TRANSPORT_LOOPBACK ||
+                                               sys->P.rank != r || sys->P.n_ranks != n)))
+      return DEM_ERR_INVALID_ARG;
+    if (sys->h_ctl->err_code) return (dem_status)sys->h_ctl->err_code;
+  }
+  for (int64_t k = 0; k < n_steps; ++k) {
+    for (int r = 0; r < n; ++r) {
+      dem_system* sys = systems[r];
+      enqueue_step(sys, (int)(sys->launched & 1), s, nullptr, /*exchange=*/false);
+    }
+    // ghost halo: rank r's left-side ghosts are rank r-1's right-side sends, and vice versa
+    for (int r = 0; r < n; ++r) {
+      dem_system* sys = systems[r];
+      if (r > 0 && sys->n_recv[0]) {
+        if (systems[r - 1]->n_send[1] != sys->n_recv[0]) return DEM_ERR_INVALID_ARG;
+        CK(cudaMemcpyAsync(sys->d_recvbuf[0], systems[r - 1]->d_sendbuf[1], sizeof(double) * kKin13 * sys->n_recv[0],
+                           cudaMemcpyDeviceToDevice, s));
+      }
+      if (r < n - 1 && sys->n_recv[1]) {
+        if (systems[r + 1]->n_send[0] != sys->n_recv[1]) return DEM_ERR_INVALID_ARG;
+        CK(cudaMemcpyAsync(sys->d_recvbuf[1], systems[r + 1]->d_sendbuf[0], sizeof(double) * kKin13 * sys->n_recv[1],
+                           cudaMemcpyDeviceToDevice, s));
+      }
+    }
+    for (int r = 0; r < n; ++r) {
+      dem_system* sys = systems[r];
+      StepArgs a = make_args(sys, (int)(sys->launched & 1));
+      enqueue_unpack(sys, a, s);
+      sys->launched++;
+    }
+  }
+  for (int r = 0; r < n; ++r) {
+    dem_system* sys = systems[r];
+    TRY(read_ctl(sys));
+    sys->steps_done = sys->h_ctl->step;
+    if (sys->h_ctl->err_code) return device_error(sys);
+    if (sys->h_ctl->abort) {
+      sys->err = "capacity overflow in a loopback group (size entries_per_sphere generously)";
+      return DEM_ERR_CAPACITY;
+    }
   }
   return DEM_OK;
 }
@@ -966,23 +1199,27 @@ extern "C" dem_status dem_get_stats(dem_system* sys, dem_stats* out) {
   out->steps = sys->steps_done;
   out->n_clumps = sys->n;
   out->n_spheres = sys->ns;
+  out->n_owned_clumps = sys->n_own;
+  out->n_owned_spheres = sys->ns_own;
+  out->n_ghost_clumps = sys->n - sys->n_own;
   out->n_cells = sys->ncell;
   out->cell_size = sys->grid.cell;
   out->regrows = sys->regrows;
-  out->kernel_launches_per_step = kLaunchesPerStep;
+  out->kernel_launches_per_step = kLaunchesPerStep + (sys->dist ? 4 : 0);
   if (sys->launched > 0 && sys->ns > 0) {
     const RowBuf& R = sys->rows[(sys->launched - 1) & 1];
     int tot = 0, ins = 0;
     CK(cudaMemcpyAsync(&tot, R.row_ptr + sys->ns, sizeof(int), cudaMemcpyDeviceToHost, sys->stream));
     CK(cudaMemcpyAsync(&ins, sys->d_cell_start + sys->ncell, sizeof(int), cudaMemcpyDeviceToHost, sys->stream));
     CK(cudaMemsetAsync(sys->d_counter, 0, sizeof(unsigned long long), sys->stream));
-    launch_count_walls(Rows{R.row_ptr, R.ent, R.ut}, (int)sys->ns, sys->d_counter, sys->stream);
-    unsigned long long walls = 0;
-    CK(cudaMemcpyAsync(&walls, sys->d_counter, sizeof(walls), cudaMemcpyDeviceToHost, sys->stream));
+    // canonical contacts held here: entries whose own key is the smaller (walls included)
+    launch_count_canonical(Rows{R.row_ptr, R.ent, R.ut}, sys->d_s_key, (int)sys->ns_own, sys->d_counter, sys->stream);
+    unsigned long long canon = 0;
+    CK(cudaMemcpyAsync(&canon, sys->d_counter, sizeof(canon), cudaMemcpyDeviceToHost, sys->stream));
     CK(cudaStreamSynchronize(sys->stream));
     out->n_entries = tot;
     out->n_inserts = ins;
-    out->n_contacts = (int64_t)walls + ((int64_t)tot - (int64_t)walls) / 2;
+    out->n_contacts = (int64_t)canon;
   }
   return DEM_OK;
 }

@@ -1,0 +1,89 @@
+"""Slab decomposition on one GPU (loopback transport): P = 2, 3 ranks vs one system, bitwise.
+
+Mirror-exact directed rows and canonical sums make every owned clump's state independent of
+the decomposition, provided the ghost states are bitwise copies — so the gathered states and
+contact lists of a P-rank run must equal the single-system run exactly.
+"""
+import numpy as np
+import pytest
+
+from workloads import beds
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dem():
+    import torch
+
+    assert torch.cuda.is_available()
+    import paper_2307_03445_b200 as pkg
+
+    return pkg
+
+
+def _strip(seed=0):
+    bed = beds.c5_bed()
+    c = 0.5 * (bed.domain_lo + bed.domain_hi)
+    s = beds.crop(bed, [c[0] - 0.07, c[1] - 0.025, -1], [c[0] + 0.07, c[1] + 0.025, 10])
+    rng = np.random.default_rng(seed)
+    s.vel = s.vel + rng.uniform(-0.05, 0.05, size=s.vel.shape)  # keep it moving
+    return s
+
+
+def _group(dem, scene, P, drift_max=1e-3, record=True):
+    halo = dem.halo_width(scene, drift_max)
+    b = dem.slab_bounds(scene.pos[:, 0], P, scene.domain_lo[0], scene.domain_hi[0])
+    systems = []
+    for r in range(P):
+        d = dict(rank=r, n_ranks=P, slab_lo=b[r], slab_hi=b[r + 1], halo=halo, drift_max=drift_max,
+                 transport=dem.TRANSPORT_LOOPBACK)
+        systems.append(dem.system_from_scene(scene, record_contacts=record, dist=d, entries_per_sphere=12))
+    return systems
+
+
+def _gather(systems):
+    st = [s.dem_get_state() for s in systems]
+    out = {k: np.concatenate([x[k] for x in st]) for k in st[0]}
+    order = np.argsort(out["gid"])
+    return {k: v[order] for k, v in out.items()}
+
+
+def _contacts(systems):
+    cs = [s.dem_get_contacts() for s in systems]
+    out = {k: np.concatenate([x[k] for x in cs]) for k in cs[0]}
+    order = np.lexsort((out["key_b"], out["key_a"]))
+    return {k: v[order] for k, v in out.items()}
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_loopback_decomposition_is_bitwise_identical(dem, P):
+    scene = _strip()
+    assert scene.n_clumps > 10_000
+    ref = dem.system_from_scene(scene, record_contacts=True)
+    ref.dem_step(30)
+    sr = ref.dem_get_state()
+    order = np.argsort(sr["gid"])
+    sr = {k: v[order] for k, v in sr.items()}
+    systems = _group(dem, scene, P)
+    stats = [s.dem_get_stats() for s in systems]
+    assert sum(st["n_owned_clumps"] for st in stats) == scene.n_clumps
+    assert all(st["n_ghost_clumps"] > 0 for st in stats)
+    dem.step_group(systems, 30)
+    sg = _gather(systems)
+    assert np.array_equal(sg["gid"], sr["gid"])
+    for k in ("pos", "quat", "vel", "omega"):
+        assert np.array_equal(sg[k], sr[k]), k
+    cr, cg = ref.dem_get_contacts(), _contacts(systems)
+    for k in cr:
+        assert np.array_equal(cg[k], cr[k]), k
+    assert sum(s.dem_get_stats()["n_contacts"] for s in systems) == ref.dem_get_stats()["n_contacts"]
+
+
+def test_drift_beyond_halo_guard_is_reported(dem):
+    scene = _strip()
+    scene.vel[:, 0] += 2.0  # 2 m/s: 0.1 mm drift in 50 steps exceeds a 20 um allowance
+    systems = _group(dem, scene, 2, drift_max=20e-6, record=False)
+    with pytest.raises(dem.DemError) as e:
+        dem.step_group(systems, 50)
+    assert e.value.status == -15
