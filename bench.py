@@ -177,17 +177,30 @@ def run_ours(a):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    if world > 1:
-        if rank == 0:
-            print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world,
-                              "error": "multi-GPU slab decomposition is not built yet (round 1: single GPU)"}))
-        return
+    local = int(os.environ.get("LOCAL_RANK", "0"))
     import paper_2307_03445_b200 as dem
 
-    torch.cuda.set_device(0)
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as td
+
+        td.init_process_group("nccl", device_id=torch.device("cuda", local))
+        obj = [dem.nccl_unique_id() if rank == 0 else None]
+        td.broadcast_object_list(obj, src=0)
+        dist = td
     t_setup = time.perf_counter()
     scene = make_scene(a.config)
-    sys_ = dem.system_from_scene(scene, record_contacts=False, cell_size=a.cell_size)
+    dparams = None
+    if world > 1:
+        # spatial slab decomposition along x, equal clump counts; fixed bed = strong scaling
+        drift = 1e-3
+        b = dem.slab_bounds(scene.pos[:, 0], world, scene.domain_lo[0], scene.domain_hi[0])
+        dparams = dict(rank=rank, n_ranks=world, slab_lo=b[rank], slab_hi=b[rank + 1],
+                       halo=dem.halo_width(scene, drift), drift_max=drift, transport=dem.TRANSPORT_NCCL,
+                       nccl_id=obj[0])
+    sys_ = dem.system_from_scene(scene, record_contacts=False, cell_size=a.cell_size, dist=dparams,
+                                 entries_per_sphere=12 if world > 1 else 0)
     stream = sys_.stream
     sys_.dem_step(a.warmup)
     torch.cuda.synchronize()
@@ -195,26 +208,39 @@ def run_ours(a):
 
     # ---------------- timed region: K steps, stage events on the system stream
     sys_.dem_set_profiling(True)
-    clk = Clocks(0)
+    clk = Clocks(local)
+    if dist:
+        dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     sys_.dem_step(a.steps)
     ev1.record(stream)
     torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1)
+    if dist:
+        dist.barrier()
+    ms_local = ev0.elapsed_time(ev1)
     clocks = clk.stop()
     stages = sys_.dem_get_stage_times()
     sys_.dem_set_profiling(False)
     st = sys_.dem_get_stats()
-    ns = st["n_spheres"]
-    value = ns * a.steps / (ms * 1e-3)
+    ns_own = st["n_owned_spheres"]
+    ms, ns_total, n_contacts = ms_local, ns_own, st["n_contacts"]
+    if dist:
+        t = torch.tensor([ms_local], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        t = torch.tensor([ns_own, st["n_contacts"]], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        ns_total, n_contacts = int(t[0].item()), int(t[1].item())
+    value = ns_total * a.steps / (ms * 1e-3)
 
-    # ---------------- roofline of the dominant kernel
+    # ---------------- roofline of the dominant kernel (this rank's launches)
     peak, peak_kind = peaks()
     sb = stage_bytes(st)
-    dom = max(stages, key=stages.get)
-    achieved = sb[dom] / (stages[dom] * 1e-3) / 1e9
+    stages_k = {k: v for k, v in stages.items() if k in sb}
+    dom = max(stages_k, key=stages_k.get)
+    achieved = sb[dom] / (stages_k[dom] * 1e-3) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
@@ -222,8 +248,8 @@ def run_ours(a):
             traffic = json.load(open(prof)).get(a.config, {}).get(dom)
         except Exception:
             traffic = None
-    c = st["n_contacts"] / max(ns, 1)
-    step_bytes = survey_bytes_per_sphere_step(c) * ns
+    c = n_contacts / max(ns_total, 1)
+    step_bytes = survey_bytes_per_sphere_step(c) * ns_total
 
     # ---------------- e2e through the C-ABI with host buffers (pinned)
     e2e = None
@@ -231,6 +257,8 @@ def run_ours(a):
         pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()  # noqa: E731
         hs = {k: pin(getattr(scene, k)) for k in ("gid", "tid", "pos", "quat", "vel", "omega")}
         h2d = sum(v.nbytes for v in hs.values())
+        if dist:
+            dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         sys_.dem_set_state(hs["gid"], hs["tid"], hs["pos"], hs["quat"], hs["vel"], hs["omega"])
@@ -238,14 +266,19 @@ def run_ours(a):
         out = sys_.dem_get_state()
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
         d2h = sum(v.nbytes for v in out.values())
-        e2e = {"value": ns * a.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d / a.steps,
+        e2e = {"value": ns_total * a.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d / a.steps,
                "d2h_bytes_per_step": d2h / a.steps,
-               "note": "dem_set_state(host) + dem_step(K) + dem_get_state(host), wall clock, per-step bytes = total/K"}
+               "note": "dem_set_state(host) + dem_step(K) + dem_get_state(host), wall clock (max over ranks), "
+                       "per-step bytes = total/K per rank"}
 
-    # ---------------- CPU oracle baseline on a bounded sample of the same bed
+    # ---------------- CPU oracle baseline on a bounded sample of the same bed (rank 0, N = 1 only)
     cpu = None
-    if not a.no_cpu_baseline:
+    if not a.no_cpu_baseline and world == 1:
         crop = sample_crop(scene) if a.config in ("c5", "c4", "c3") else scene
         v_cpu, steps_cpu, dt_cpu = oracle_rate(crop, budget_s=a.cpu_budget)
         cpu = {"value": v_cpu, "unit": UNIT, "cores": 1, "kind": "oracle",
@@ -253,27 +286,33 @@ def run_ours(a):
                          f"({crop.n_clumps} clumps / {crop.n_spheres} spheres) of the same bed"}
 
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": a.steps, "warmup": a.warmup,
-        "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": scene.name, "clumps": st["n_clumps"], "spheres": ns,
+        "config": {"workload": scene.name, "clumps": scene.n_clumps, "spheres": ns_total,
                    "contacts_per_sphere": c, "directed_entries": st["n_entries"], "bin_inserts": st["n_inserts"],
                    "cell_size_m": st["cell_size"], "rebuild_every": 1, "h": scene.h,
                    "l2": "inputs larger than L2 (state + rows > 10 GB); no flush",
-                   "parallelism": "single-gpu", "setup_s": round(setup_s, 1)},
+                   "parallelism": f"slab{world}" if world > 1 else "single-gpu",
+                   "ghost_clumps_rank0": st["n_ghost_clumps"], "setup_s": round(setup_s, 1)},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "alg_bytes_per_launch": sb[dom], "avg_launch_ms": stages[dom]},
+                     "alg_bytes_per_launch": sb[dom], "avg_launch_ms": stages_k[dom]},
         "step_roofline": {"bytes_per_sphere_step": survey_bytes_per_sphere_step(c),
                           "achieved_gbs": step_bytes / (ms / a.steps * 1e-3) / 1e9,
-                          "frac": step_bytes / (ms / a.steps * 1e-3) / 1e9 / peak},
+                          "frac": step_bytes / (ms / a.steps * 1e-3) / 1e9 / (peak * world)},
         "stage_ms": stages,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": int(st["kernel_launches_per_step"]) * a.steps,
         "clocks": clocks,
     }
-    print(json.dumps(line), flush=True)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        sys_.close()
+        dist.destroy_process_group()
 
 
 def main():
