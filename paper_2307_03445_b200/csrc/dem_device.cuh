@@ -64,6 +64,8 @@ struct Grid {
   double dom_lo[3], dom_hi[3];
   int n[3];
   long long st[3];  // linear bin id = sum_d idx[d] * st[d]; shortest axis fastest (locality)
+  int ax[3];        // axes from fastest to slowest
+  double inv_n_ax[2];  // 1 / n[ax[0]], 1 / n[ax[1]] for the fast bin-id decode
   double pad;  // r + pad is the half-extent of a sphere's bin AABB (margin/2 + eps)
 };
 
@@ -171,6 +173,32 @@ __device__ __forceinline__ void cell_range(const Grid& g, int d, double c, doubl
   double e = r + g.pad;
   lo = clampi(__double2int_rd((c - e - g.lo[d]) * g.inv_cell), 0, g.n[d] - 1);
   hi = clampi(__double2int_rd((c + e - g.lo[d]) * g.inv_cell), 0, g.n[d] - 1);
+}
+
+// q = quot * d + rem for 0 <= q < 2^31 (bin ids), via an fp64 reciprocal and a one-step fix-up
+// (the 64-bit integer division it replaces is a ~60-instruction software routine)
+__device__ __forceinline__ int divmod_fast(int q, int d, double inv_d, int& rem) {
+  int quot = __double2int_rz((double)q * inv_d);
+  int r = q - quot * d;
+  if (r < 0) {
+    --quot;
+    r += d;
+  } else if (r >= d) {
+    ++quot;
+    r -= d;
+  }
+  rem = r;
+  return quot;
+}
+
+// linear bin id -> bin coordinates (inverse of sum_d idx[d] * st[d])
+__device__ __forceinline__ void decode_bin(const Grid& g, long long cid, int& cx, int& cy, int& cz) {
+  int c[3];
+  int q = divmod_fast((int)cid, g.n[g.ax[0]], g.inv_n_ax[0], c[g.ax[0]]);
+  c[g.ax[2]] = divmod_fast(q, g.n[g.ax[1]], g.inv_n_ax[1], c[g.ax[1]]);
+  cx = c[0];
+  cy = c[1];
+  cz = c[2];
 }
 
 __device__ __forceinline__ int cell_lo(const Grid& g, int d, double c, double r) {

@@ -226,40 +226,42 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
     const int k0 = a.cell_start[cid];
     const int m = a.cell_start[cid + 1] - k0;
     if (m < 2) continue;
-    const int cx = (int)((cid / g.st[0]) % g.n[0]);
-    const int cy = (int)((cid / g.st[1]) % g.n[1]);
-    const int cz = (int)((cid / g.st[2]) % g.n[2]);
+    int cx, cy, cz;
+    decode_bin(g, cid, cx, cy, cz);
     if (m <= 32) {
-      // Common case: lane l holds member l in registers.  Rotation schedule: in round k
-      // (1 <= k <= m/2) lane l tests the pair (l, l + k mod m), partner data by shuffle;
-      // for even m the last round keeps lanes l < m/2 only.  Every unordered pair of the
-      // bin is tested exactly once, with all m lanes busy and no index decoding.
+      // Common case: lane l holds member l in registers and publishes it to the warp's shared
+      // slot.  Rotation schedule: in round k (1 <= k <= m/2) lane l tests the pair
+      // (l, l + k mod m), reading the partner from shared memory (the integer tests first,
+      // the coordinates only if they pass); for even m the last round keeps lanes l < m/2
+      // only.  Every unordered pair of the bin is tested exactly once, with all m lanes busy.
       double4 u = make_double4(0.0, 0.0, 0.0, 0.0);
       int2 mu = make_int2(-1, 0);
+      __syncwarp();
       if (lane < m) {
         const int idx = a.items[k0 + lane];
         u = a.spos[idx];
         const int mk = (cell_lo(g, 0, u.x, u.w) == cx ? 1 : 0) | (cell_lo(g, 1, u.y, u.w) == cy ? 2 : 0) |
                        (cell_lo(g, 2, u.z, u.w) == cz ? 4 : 0);
         mu = make_int2(a.s_clump[idx], idx | (mk << 29));
+        A.p[lane] = u;
+        A.meta[lane] = mu;
       }
+      __syncwarp();
+      const bool in = lane < m;
+      const int n_own = a.n_own;
+      const double margin = a.margin;
+      int src = lane < m ? lane : 0;
       for (int k = 1; 2 * k <= m; ++k) {
-        int src = lane + k;
-        if (src >= m) src -= m;
-        if (lane >= m) src = lane;
-        const int vcl = __shfl_sync(0xffffffffu, mu.x, src);
-        const int vmeta = __shfl_sync(0xffffffffu, mu.y, src);
-        const double vx = __shfl_sync(0xffffffffu, u.x, src);
-        const double vy = __shfl_sync(0xffffffffu, u.y, src);
-        const double vz = __shfl_sync(0xffffffffu, u.z, src);
-        const double vw = __shfl_sync(0xffffffffu, u.w, src);
-        const bool active = lane < m && !(2 * k == m && lane >= k);
+        src = (src + 1 == m) ? 0 : src + 1;  // (lane + k) mod m
+        const int2 mv = A.meta[src];
+        const bool active = in && (2 * k != m || lane < k);
         bool hit = false;
         // different clumps, at least one owned (ghost-ghost pairs belong to other ranks), dedupe bin
-        if (active && mu.x != vcl && min(mu.x, vcl) < a.n_own && (((unsigned)(mu.y | vmeta) >> 29) == 7u)) {
-          const double dx = sub(vx, u.x), dy = sub(vy, u.y), dz = sub(vz, u.z);
+        if (active && mu.x != mv.x && min(mu.x, mv.x) < n_own && (((unsigned)(mu.y | mv.y) >> 29) == 7u)) {
+          const double4 v = A.p[src];
+          const double dx = sub(v.x, u.x), dy = sub(v.y, u.y), dz = sub(v.z, u.z);
           const double d2 = add(add(mul(dx, dx), mul(dy, dy)), mul(dz, dz));
-          const double s = add(add(u.w, vw), a.margin);
+          const double s = add(add(u.w, v.w), margin);
           hit = d2 <= mul(s, s);
         }
         const unsigned mask = __ballot_sync(0xffffffffu, hit);
@@ -270,8 +272,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
             nbuf = 0;
           }
           if (hit)
-            bf[nbuf + __popc(mask & ((1u << lane) - 1u))] =
-                pair_record(a, mu.y & 0x1fffffff, vmeta & 0x1fffffff);
+            bf[nbuf + __popc(mask & ((1u << lane) - 1u))] = pair_record(a, mu.y & 0x1fffffff, mv.y & 0x1fffffff);
           nbuf += cnt;
         }
       }

@@ -654,7 +654,10 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
     for (int k = 0; k < 3; ++k) {
       G.st[ord[k]] = s;
       s *= G.n[ord[k]];
+      G.ax[k] = ord[k];
     }
+    G.inv_n_ax[0] = 1.0 / G.n[ord[0]];
+    G.inv_n_ax[1] = 1.0 / G.n[ord[1]];
   }
   // storage order: owned clumps, then ghosts, each sorted by the bin of the COM (spatial
   // locality for every gather); results do not depend on it (keys, canonical sums).
