@@ -46,6 +46,7 @@ def lib():
         L.orc_get_state.argtypes = [P, P, P, P, P]
         L.orc_set_history.argtypes = [P, I64, P, P, P]
         L.orc_step.argtypes = [P, I64]
+        L.orc_set_cd_every.argtypes = [P, C.c_int]
         L.orc_num_contacts.restype = I64
         L.orc_num_contacts.argtypes = [P]
         L.orc_steps_done.restype = I64
@@ -76,7 +77,7 @@ class OracleError(RuntimeError):
 class Oracle:
     """One oracle system built from a `workloads.Scene`."""
 
-    def __init__(self, scene, detect: int = -1, margin: float | None = None):
+    def __init__(self, scene, detect: int = -1, margin: float | None = None, cd_every: int = 1):
         L = lib()
         ncomp, offs, rad, mat, mass, inertia = scene.template_arrays()
         pts, nrm, pmat = scene.plane_arrays()
@@ -92,6 +93,8 @@ class Oracle:
                                 _p(k[10]), _p(k[11]), _p(k[12]), detect)
         self.n = 0
         self.set_state(scene.gid, scene.tid, scene.pos, scene.quat, scene.vel, scene.omega)
+        if cd_every != 1:
+            self._check(L.orc_set_cd_every(self.sys, int(cd_every)))
 
     def __del__(self):
         if getattr(self, "sys", None):

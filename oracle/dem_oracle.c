@@ -46,6 +46,7 @@ struct orc_sys {
   double *ppt, *pn;
   int32_t* pmat;
   int detect;
+  int cd_every, since_rebuild; /* contact-set rebuild cadence */
   /* clump state */
   int64_t n;
   int64_t* gid;
@@ -236,6 +237,8 @@ orc_sys* orc_create(double h, const double gravity[3], double margin, const doub
     memcpy(s->pmat, plane_mat, sizeof(int32_t) * n_planes);
   }
   s->detect = detect;
+  s->cd_every = 1;
+  s->since_rebuild = 0;
   return s;
 }
 
@@ -303,6 +306,16 @@ int orc_set_state(orc_sys* s, int64_t n, const int64_t* gid, const int32_t* tid,
   }
   s->nh = 0;
   s->nc = 0;
+  s->since_rebuild = 0;
+  return ORC_OK;
+}
+
+/* contact-set rebuild cadence: the set is rebuilt every k steps, counted from the
+ * next step */
+int orc_set_cd_every(orc_sys* s, int k) {
+  if (k < 1) return ORC_ERR_ARG;
+  s->cd_every = k;
+  s->since_rebuild = 0;
   return ORC_OK;
 }
 
@@ -337,6 +350,7 @@ int orc_set_history(orc_sys* s, int64_t n, const int64_t* ka, const int64_t* kb,
   }
   qsort(s->hist, n, sizeof(hist_rec), cmp_hist);
   s->nh = n;
+  s->since_rebuild = 0; /* a new history is read by a rebuild */
   return ORC_OK;
 }
 
@@ -509,15 +523,20 @@ static int one_step(orc_sys* s) {
       }
     }
   }
-  /* (2) active contact set, rebuilt this step ("traditional way") */
-  s->nc = 0;
-  int brute = s->detect == 0 || (s->detect < 0 && s->ns <= 10000);
-  if (brute)
-    detect_brute(s);
-  else
-    detect_grid(s);
-  detect_planes(s);
-  qsort(s->con, s->nc, sizeof(contact), cmp_contact);
+  /* (2) active contact set: rebuilt every cd_every steps from the margin-enlarged geometry
+   * (P:142); cd_every = 1 is the "traditional way".  In between, the same set is
+   * used and every member is re-evaluated at each step. */
+  if (s->since_rebuild == 0) {
+    s->nc = 0;
+    int brute = s->detect == 0 || (s->detect < 0 && s->ns <= 10000);
+    if (brute)
+      detect_brute(s);
+    else
+      detect_grid(s);
+    detect_planes(s);
+    qsort(s->con, s->nc, sizeof(contact), cmp_contact);
+  }
+  s->since_rebuild = (s->since_rebuild + 1) % s->cd_every;
   /* (3) history carried for surviving keys, zero at birth */
   for (k = 0; k < s->nc; ++k) {
     hist_rec key, *hit;
