@@ -54,6 +54,8 @@ typedef enum {
   DEM_ERR_OUT_OF_DOMAIN = -10,    /* a sphere centre left [domain_lo, domain_hi]       */
   DEM_ERR_NONFINITE = -11,        /* non-finite wrench/state                          */
   DEM_ERR_DEGENERATE_CONTACT = -12, /* coincident sphere centres in a contact         */
+  DEM_ERR_VMAX = -13,             /* cd_every > 1: a sphere moved more than margin/2 since the last
+                                     contact-set rebuild; raise margin or lower cd_every */
   DEM_ERR_CAPACITY = -14,         /* a buffer could not be grown (device memory exhausted)   */
   DEM_ERR_REPARTITION = -15       /* distributed: an owned clump drifted beyond drift_max    */
 } dem_status;
@@ -90,7 +92,10 @@ typedef struct {
   double h;                  /* time step [s] */
   double gravity[3];         /* [m/s^2]; tilt it for inclines */
   double margin;             /* total contact-detection enlargement [m]; 0 for per-step rebuild */
-  int32_t cd_every;          /* steps per contact-set rebuild; must be 1 in this version */
+  int32_t cd_every;          /* steps per contact-set rebuild; >= 1.  With cd_every > 1 the set is
+                                built from spheres enlarged by margin/2 each and re-evaluated every step
+                                (members with delta <= 0 get zero force); margin must cover the
+                                relative motion over the window, e.g. 2 v_max h cd_every */
   double domain_lo[3], domain_hi[3]; /* every sphere centre must stay inside */
   double cell_size;          /* bin edge [m]; 0 = automatic */
   int32_t record_contacts;   /* 1: keep per-contact force/point/normal/delta for dem_get_contacts */

@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("DEM_LIB_PATH") or os.path.join(_HERE, "libdem_b200.so
 
 DEM_STATUS = {0: "ok", -1: "invalid argument", -2: "CUDA error", -3: "out of device memory", -4: "NCCL error",
               -5: "bad material", -6: "bad template", -10: "sphere out of domain", -11: "non-finite wrench",
-              -12: "degenerate contact", -14: "capacity", -15: "repartition needed"}
+              -12: "degenerate contact", -13: "v_max / margin exceeded", -14: "capacity", -15: "repartition needed"}
 
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
 FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
@@ -122,7 +122,7 @@ class System:
 
     def __init__(self, materials, templates, planes=(), *, h, gravity=(0.0, 0.0, -9.81), domain_lo, domain_hi,
                  margin=0.0, cell_size=0.0, record_contacts=False, use_torch_allocator=True, stream=None,
-                 entries_per_sphere=0.0, dist=None):
+                 entries_per_sphere=0.0, dist=None, cd_every=1):
         """dist (optional): dict(rank, n_ranks, slab_lo, slab_hi, halo, drift_max, transport, nccl_id) —
         the slab decomposition of dem_params (include/dem.h); nccl_id from nccl_unique_id() on rank 0."""
         import torch  # plumbing only: device memory and streams
@@ -155,7 +155,7 @@ class System:
         p.h = h
         p.gravity[:] = [float(x) for x in gravity]
         p.margin = margin
-        p.cd_every = 1
+        p.cd_every = int(cd_every)
         p.domain_lo[:] = [float(x) for x in domain_lo]
         p.domain_hi[:] = [float(x) for x in domain_hi]
         p.cell_size = cell_size

@@ -111,6 +111,9 @@ struct StepArgs {
   double* kin;               // per clump [kKin]: X(3), V(3), omega_world(3), mass
   const int* cta_clump;      // [n_cta + 1] clump ranges of the fused force/integrate CTAs
   int n_cta;
+  int rebuild;               // 1: this step rebuilds the contact set; 0: re-evaluates rows
+  double4* spos_ref;         // sphere centres at the last rebuild
+  double half_margin;        // > 0 (cd_every > 1): displacement allowed since the last rebuild
   int n_own, ns_own;         // owned clumps / spheres come first; the rest are ghosts (§8e)
   const double* xref;        // [3 n_own] owned COMs at dem_set_state (distributed drift check)
   double drift_max;          // 0: no check

@@ -27,7 +27,7 @@ namespace dem {
 __global__ void __launch_bounds__(256) k_pose_count(StepArgs a) {
   if (a.ctl->abort) return;
   int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i == 0) *a.pair_cursor = 0ull;
+  if (i == 0 && a.rebuild) *a.pair_cursor = 0ull;
   if (i >= a.ns) return;
   const int c = a.s_clump[i];
   const int tc = a.s_tc[i];
@@ -57,6 +57,15 @@ __global__ void __launch_bounds__(256) k_pose_count(StepArgs a) {
     raise_error(a.ctl, -10, a.s_key[i], a.gid[c]);
     return;
   }
+  if (!a.rebuild) {
+    // the deferred set stays complete while no sphere has moved more than margin/2 since it
+    // was built ("v_max violated"): otherwise report it instead of missing contacts
+    const double4 q = a.spos_ref[i];
+    const double dx = cx - q.x, dy = cy - q.y, dz = cz - q.z;
+    if (dx * dx + dy * dy + dz * dz > a.half_margin * a.half_margin) raise_error(a.ctl, -13, a.s_key[i], a.gid[c]);
+    return;
+  }
+  if (a.half_margin > 0.0) a.spos_ref[i] = make_double4(cx, cy, cz, r);
   // sphere-plane candidates: (r + margin) - (c - p_w).n_w >= 0
   int walls = 0;
   for (int p = 0; p < a.tab.n_planes; ++p) {

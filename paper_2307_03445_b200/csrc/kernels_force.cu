@@ -97,11 +97,13 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
       const int t = ent.partner;
       // (a4) history remap: the slot of this key in the previous rows was found by the
       // row merge in k_rows_finish (-1: contact born this step, u_t = 0)
+      // (between rebuilds the set is unchanged: the entry's own slot of the previous u_t)
       double ux = 0.0, uy = 0.0, uz = 0.0;
-      if (ent.prev >= 0) {
-        ux = a.prev.ut[3 * ent.prev];
-        uy = a.prev.ut[3 * ent.prev + 1];
-        uz = a.prev.ut[3 * ent.prev + 2];
+      const int pidx = a.rebuild ? ent.prev : e;
+      if (pidx >= 0) {
+        ux = a.prev.ut[3 * pidx];
+        uy = a.prev.ut[3 * pidx + 1];
+        uz = a.prev.ut[3 * pidx + 2];
       }
       // (a5) geometry: n from i (own) to j (partner)
       double nx, ny, nz, px, py, pz, delta, rbar, mbar;

@@ -84,17 +84,22 @@ struct dem_system {
   long long ncell = 0, cap_inserts = 0;
   int *d_cell_count = nullptr, *d_cell_start = nullptr, *d_items = nullptr;
   int *d_row_cnt = nullptr, *d_scan_tmp = nullptr;
-  // rows
+  // rows: the entry sets (row_ptr, ent) of rows[ep] are the latest contact set and ping-pong
+  // at every rebuild; the u_t arrays of rows[up] hold the latest tangential history and
+  // ping-pong at every step; the state ping-pongs every step (sp)
   RowBuf rows[2];
+  int sp = 0, up = 0, ep = 0;
+  int since_rebuild = 0;                 // steps since the last contact-set rebuild
+  double4* d_spos_ref = nullptr;         // sphere centres at the last rebuild (displacement check)
   long long cap_entries = 0;
   Record rec{};
   Ctl* d_ctl = nullptr;
   Ctl* h_ctl = nullptr;
   unsigned long long* d_counter = nullptr;
-  // graphs
-  cudaGraphExec_t graph[2] = {nullptr, nullptr};
+  // graphs, one per (sp, up, ep, rebuild)
+  cudaGraphExec_t graph[16] = {};
   bool graphs_valid = false;
-  int64_t launched = 0;  // steps launched since dem_set_state (selects the parity)
+  int64_t launched = 0;  // steps launched since dem_set_state
   int64_t steps_done = 0;
   int64_t regrows = 0;
   long long last_entries = 0, last_inserts = 0;
@@ -165,15 +170,19 @@ static dem_status alloc_arr(dem_system* sys, T** out, size_t count) {
   } while (0)
 
 static void free_graphs(dem_system* sys) {
-  for (int p = 0; p < 2; ++p)
-    if (sys->graph[p]) {
-      cudaGraphExecDestroy(sys->graph[p]);
-      sys->graph[p] = nullptr;
+  for (auto& g : sys->graph)
+    if (g) {
+      cudaGraphExecDestroy(g);
+      g = nullptr;
     }
   sys->graphs_valid = false;
 }
 
-static StepArgs make_args(dem_system* sys, int p) {
+// Arguments of the next step from the host parities: state sp -> sp^1, u_t up -> up^1; a
+// rebuild step writes a new entry set rows[ep^1] (rows[ep] = the previous set, for the
+// history merge), other steps re-evaluate the current set rows[ep].
+static StepArgs make_args(dem_system* sys, bool rebuild) {
+  const int p = sys->sp;
   StepArgs a{};
   a.n = (int)sys->n;
   a.ns = (int)sys->ns;
@@ -235,10 +244,13 @@ static StepArgs make_args(dem_system* sys, int p) {
   a.cell_start = sys->d_cell_start;
   a.items = sys->d_items;
   a.row_cnt = sys->d_row_cnt;
-  const RowBuf& R = sys->rows[p];
-  const RowBuf& Q = sys->rows[p ^ 1];
-  a.rows = Rows{R.row_ptr, R.ent, R.ut};
-  a.prev = Rows{Q.row_ptr, Q.ent, Q.ut};
+  const RowBuf& E = sys->rows[rebuild ? sys->ep ^ 1 : sys->ep];
+  const RowBuf& Q = sys->rows[sys->ep];
+  a.rows = Rows{E.row_ptr, E.ent, sys->rows[sys->up ^ 1].ut};
+  a.prev = Rows{Q.row_ptr, Q.ent, sys->rows[sys->up].ut};
+  a.rebuild = rebuild ? 1 : 0;
+  a.spos_ref = sys->d_spos_ref;
+  a.half_margin = sys->P.cd_every > 1 ? 0.5 * sys->P.margin : 0.0;
   a.rec = sys->rec;
   a.record = sys->P.record_contacts ? 1 : 0;
   a.ctl = sys->d_ctl;
@@ -270,23 +282,23 @@ static void enqueue_nccl_exchange(dem_system* sys, cudaStream_t s) {
 
 // the step sequence; ev (optional) receives kStages+1 events around the stages.  With
 // exchange = false (loopback groups) the halo is packed but moved by dem_step_group.
-static void enqueue_step(dem_system* sys, int p, cudaStream_t s, cudaEvent_t* ev, bool exchange = true) {
-  StepArgs a = make_args(sys, p);
+static void enqueue_step(dem_system* sys, bool rebuild, cudaStream_t s, cudaEvent_t* ev, bool exchange = true) {
+  StepArgs a = make_args(sys, rebuild);
   const int* abort = &sys->d_ctl->abort;
   if (ev) cudaEventRecord(ev[0], s);
   launch_pose_count(a, s);
   if (ev) cudaEventRecord(ev[1], s);
-  launch_excl_scan(sys->d_cell_count, sys->d_cell_start, sys->ncell, sys->d_scan_tmp, abort, s);
+  if (rebuild) launch_excl_scan(sys->d_cell_count, sys->d_cell_start, sys->ncell, sys->d_scan_tmp, abort, s);
   if (ev) cudaEventRecord(ev[2], s);
-  launch_bin_scatter(a, s);
+  if (rebuild) launch_bin_scatter(a, s);
   if (ev) cudaEventRecord(ev[3], s);
-  launch_pairs(a, s, sys->n_sm);
+  if (rebuild) launch_pairs(a, s, sys->n_sm);
   if (ev) cudaEventRecord(ev[4], s);
-  launch_excl_scan(sys->d_row_cnt, sys->rows[p].row_ptr, sys->ns, sys->d_scan_tmp, abort, s);
+  if (rebuild) launch_excl_scan(sys->d_row_cnt, a.rows.row_ptr, sys->ns, sys->d_scan_tmp, abort, s);
   if (ev) cudaEventRecord(ev[5], s);
-  launch_rows_scatter(a, s, sys->n_sm);
+  if (rebuild) launch_rows_scatter(a, s, sys->n_sm);
   if (ev) cudaEventRecord(ev[6], s);
-  launch_rows_finish(a, s);
+  if (rebuild) launch_rows_finish(a, s);
   if (ev) cudaEventRecord(ev[7], s);
   launch_force_integrate(a, s);
   if (ev) cudaEventRecord(ev[8], s);
@@ -300,14 +312,19 @@ static void enqueue_step(dem_system* sys, int p, cudaStream_t s, cudaEvent_t* ev
   if (ev) cudaEventRecord(ev[9], s);
 }
 
-static dem_status capture_graphs(dem_system* sys) {
-  free_graphs(sys);
-  for (int p = 0; p < 2; ++p) {
+static int graph_key(const dem_system* sys, bool rebuild) {
+  return sys->sp | (sys->up << 1) | (sys->ep << 2) | ((rebuild ? 1 : 0) << 3);
+}
+
+// the step graph for the current parities, captured on first use
+static dem_status step_graph(dem_system* sys, bool rebuild, cudaGraphExec_t* out) {
+  const int key = graph_key(sys, rebuild);
+  if (!sys->graph[key]) {
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(sys->cap_stream, cudaStreamCaptureModeThreadLocal));
-    enqueue_step(sys, p, sys->cap_stream, nullptr);
+    enqueue_step(sys, rebuild, sys->cap_stream, nullptr);
     CK(cudaStreamEndCapture(sys->cap_stream, &g));
-    cudaError_t e = cudaGraphInstantiate(&sys->graph[p], g, 0);
+    cudaError_t e = cudaGraphInstantiate(&sys->graph[key], g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) {
       sys->err = std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e);
@@ -315,6 +332,7 @@ static dem_status capture_graphs(dem_system* sys) {
     }
   }
   sys->graphs_valid = true;
+  *out = sys->graph[key];
   return DEM_OK;
 }
 
@@ -352,6 +370,7 @@ extern "C" const char* dem_status_string(dem_status s) {
     case DEM_ERR_NONFINITE: return "non-finite wrench";
     case DEM_ERR_DEGENERATE_CONTACT: return "degenerate contact (coincident centres)";
     case DEM_ERR_REPARTITION: return "owned clump drifted beyond drift_max (repartition)";
+    case DEM_ERR_VMAX: return "sphere moved more than margin/2 since the last contact-set rebuild";
     case DEM_ERR_CAPACITY: return "capacity";
   }
   return "unknown";
@@ -369,7 +388,8 @@ extern "C" dem_status dem_create(const dem_params* params, const dem_material* m
   if (!params || !out || n_mat <= 0 || n_tmpl <= 0 || n_planes < 0 || n_planes > kMaxPlanes || !materials ||
       !templates || (n_planes && !planes))
     return DEM_ERR_INVALID_ARG;
-  if (!(params->h > 0) || params->margin < 0 || params->cd_every != 1 || params->cell_size < 0)
+  if (!(params->h > 0) || params->margin < 0 || params->cd_every < 1 || params->cell_size < 0 ||
+      (params->cd_every > 1 && !(params->margin > 0)))
     return DEM_ERR_INVALID_ARG;
   for (int d = 0; d < 3; ++d)
     if (!(params->domain_hi[d] > params->domain_lo[d])) return DEM_ERR_INVALID_ARG;
@@ -759,6 +779,7 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
   TRY(alloc_arr(sys, &sys->d_s_tc, ns));
   TRY(alloc_arr(sys, &sys->d_s_key, ns));
   TRY(alloc_arr(sys, &sys->d_spos, ns));
+  TRY(alloc_arr(sys, &sys->d_spos_ref, ns));
   sys->cap_pairs = std::max<long long>(1024, 4 * ns);
   TRY(alloc_arr(sys, &sys->d_pairs, sys->cap_pairs));
   // CTA partition of the fused force/integrate kernel: consecutive whole clumps, at most
@@ -833,6 +854,8 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
   CK(cudaStreamSynchronize(s));
   sys->launched = 0;
   sys->steps_done = 0;
+  sys->sp = sys->up = sys->ep = 0;
+  sys->since_rebuild = 0;
   sys->last_entries = 0;
   sys->err.clear();
   return DEM_OK;
@@ -874,15 +897,16 @@ extern "C" dem_status dem_set_contact_history(dem_system* sys, int64_t n, const 
   }
   long long m = (long long)ents.size();
   if (m > sys->cap_entries) TRY(alloc_rows(sys, m + m / 4 + 1024));
-  int prev = (int)((sys->launched & 1) ^ 1);
+  // the imported history is the "previous" set of the next step, which is forced to be a rebuild
   cudaStream_t s = sys->stream;
-  RowBuf& R = sys->rows[prev];
+  RowBuf& R = sys->rows[sys->ep];
   CK(cudaMemcpyAsync(R.row_ptr, rp.data(), sizeof(int) * (sys->ns + 1), cudaMemcpyHostToDevice, s));
   if (m) {
     CK(cudaMemcpyAsync(R.ent, ents.data(), sizeof(Entry) * m, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(R.ut, ut.data(), sizeof(double) * 3 * m, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(sys->rows[sys->up].ut, ut.data(), sizeof(double) * 3 * m, cudaMemcpyHostToDevice, s));
   }
   CK(cudaStreamSynchronize(s));
+  sys->since_rebuild = 0;
   return DEM_OK;
 }
 
@@ -908,6 +932,10 @@ static dem_status device_error(dem_system* sys) {
       std::snprintf(buf, sizeof buf, "coincident centres of spheres %lld and %lld at step %lld", c.err_key,
                     c.err_key2, c.err_step);
       break;
+    case DEM_ERR_VMAX:
+      std::snprintf(buf, sizeof buf, "sphere %lld of clump gid %lld moved more than margin/2 since the last "
+                    "contact-set rebuild at step %lld", c.err_key, c.err_key2, c.err_step);
+      break;
     case DEM_ERR_REPARTITION:
       std::snprintf(buf, sizeof buf, "owned clump gid %lld drifted beyond drift_max at step %lld: repartition",
                     c.err_key, c.err_step);
@@ -929,26 +957,39 @@ static dem_status ensure_events(dem_system* sys, int64_t steps) {
   return DEM_OK;
 }
 
+// advance the host parities after a launched step
+static void advance_parities(dem_system* sys, bool rebuild) {
+  sys->sp ^= 1;
+  sys->up ^= 1;
+  if (rebuild) sys->ep ^= 1;
+  sys->since_rebuild = (sys->since_rebuild + 1) % std::max(1, sys->P.cd_every);
+  sys->launched++;
+}
+
 extern "C" dem_status dem_step(dem_system* sys, int64_t n_steps) {
   if (!sys || n_steps < 0) return DEM_ERR_INVALID_ARG;
   if (sys->h_ctl->err_code) return (dem_status)sys->h_ctl->err_code;
   int64_t remaining = n_steps;
   int guard = 0;
+  struct Sched {
+    int up, ep, since;
+  };
+  std::vector<Sched> sched;
   while (remaining > 0) {
-    if (!sys->profiling && !sys->graphs_valid) TRY(capture_graphs(sys));
-    const int64_t launched_before = sys->launched;
     const int64_t done_before = sys->h_ctl->step;
-    if (sys->profiling) {
-      TRY(ensure_events(sys, remaining));
-      for (int64_t k = 0; k < remaining; ++k) {
-        enqueue_step(sys, (int)(sys->launched & 1), sys->stream, &sys->ev[(size_t)k * (kStages + 1)]);
-        sys->launched++;
+    sched.clear();
+    if (sys->profiling) TRY(ensure_events(sys, remaining));
+    for (int64_t k = 0; k < remaining; ++k) {
+      const bool rebuild = sys->since_rebuild == 0;
+      sched.push_back(Sched{sys->up, sys->ep, sys->since_rebuild});
+      if (sys->profiling) {
+        enqueue_step(sys, rebuild, sys->stream, &sys->ev[(size_t)k * (kStages + 1)]);
+      } else {
+        cudaGraphExec_t g;
+        TRY(step_graph(sys, rebuild, &g));
+        CK(cudaGraphLaunch(g, sys->stream));
       }
-    } else {
-      for (int64_t k = 0; k < remaining; ++k) {
-        CK(cudaGraphLaunch(sys->graph[sys->launched & 1], sys->stream));
-        sys->launched++;
-      }
+      advance_parities(sys, rebuild);
     }
     TRY(read_ctl(sys));
     const int64_t done = sys->h_ctl->step - done_before;
@@ -970,16 +1011,17 @@ extern "C" dem_status dem_step(dem_system* sys, int64_t n_steps) {
       sys->err = "capacity overflow on a distributed system (raise params.entries_per_sphere)";
       return DEM_ERR_CAPACITY;
     }
-    // capacity abort: regrow and re-run the steps that did not complete
+    // capacity abort in step `done` (always a rebuild step): the state was carried forward
+    // through the aborted steps (sp is already right); the latest valid u_t and entry set are
+    // those that step read.  Regrow and re-run from there.
     if (++guard > 8) {
       sys->err = "capacity regrow did not converge";
       return DEM_ERR_CAPACITY;
     }
     sys->regrows++;
-    // rows of the last successful step must become the next step's "prev" side
-    const int valid = (int)((launched_before + done - 1) & 1);
-    const int want_prev = (int)((sys->launched & 1) ^ 1);
-    if (valid != want_prev) std::swap(sys->rows[0], sys->rows[1]);
+    sys->up = sched[(size_t)done].up;
+    sys->ep = sched[(size_t)done].ep;
+    sys->since_rebuild = sched[(size_t)done].since;
     if (sys->h_ctl->need_entries > sys->cap_entries) {
       long long need = sys->h_ctl->need_entries;
       TRY(alloc_rows(sys, need + need / 4 + 1024));
@@ -1021,7 +1063,7 @@ extern "C" dem_status dem_get_state(dem_system* sys, int64_t cap, int64_t* n, in
   const int64_t N = sys->n;
   std::vector<double> st((size_t)13 * N);
   if (N)
-    CK(cudaMemcpy(st.data(), sys->d_state[sys->launched & 1], sizeof(double) * 13 * N, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(st.data(), sys->d_state[sys->sp], sizeof(double) * 13 * N, cudaMemcpyDeviceToHost));
   // output row of each owned storage index: rank of its caller index among the owned ones
   std::vector<int64_t> outpos(NO);
   {
@@ -1101,7 +1143,7 @@ extern "C" dem_status dem_step_group(dem_system* const* systems, int32_t n, int6
   for (int64_t k = 0; k < n_steps; ++k) {
     for (int r = 0; r < n; ++r) {
       dem_system* sys = systems[r];
-      enqueue_step(sys, (int)(sys->launched & 1), s, nullptr, /*exchange=*/false);
+      enqueue_step(sys, sys->since_rebuild == 0, s, nullptr, /*exchange=*/false);
     }
     // ghost halo: rank r's left-side ghosts are rank r-1's right-side sends, and vice versa
     for (int r = 0; r < n; ++r) {
@@ -1119,9 +1161,9 @@ extern "C" dem_status dem_step_group(dem_system* const* systems, int32_t n, int6
     }
     for (int r = 0; r < n; ++r) {
       dem_system* sys = systems[r];
-      StepArgs a = make_args(sys, (int)(sys->launched & 1));
+      StepArgs a = make_args(sys, sys->since_rebuild == 0);
       enqueue_unpack(sys, a, s);
-      sys->launched++;
+      advance_parities(sys, sys->since_rebuild == 0);
     }
   }
   for (int r = 0; r < n; ++r) {
@@ -1150,7 +1192,7 @@ extern "C" dem_status dem_get_contacts(dem_system* sys, int64_t cap, int64_t* n,
     *n = 0;
     return DEM_OK;
   }
-  const RowBuf& R = sys->rows[(sys->launched - 1) & 1];
+  const RowBuf& R = sys->rows[sys->ep];  // the last step's set; its u_t is rows[up].ut
   const int64_t ns = sys->ns;
   std::vector<int> rp(ns + 1);
   CK(cudaMemcpy(rp.data(), R.row_ptr, sizeof(int) * (ns + 1), cudaMemcpyDeviceToHost));
@@ -1184,7 +1226,7 @@ extern "C" dem_status dem_get_contacts(dem_system* sys, int64_t cap, int64_t* n,
     if (key_a) key_a[k] = sys->h_s_key[sel[k].first];
     if (key_b) key_b[k] = keys[sel[k].second];
   }
-  TRY(fetch3(R.ut, u_t));
+  TRY(fetch3(sys->rows[sys->up].ut, u_t));
   TRY(fetch3(sys->rec.F, force_on_b));
   TRY(fetch3(sys->rec.p, point));
   TRY(fetch3(sys->rec.n, normal));
@@ -1210,7 +1252,7 @@ extern "C" dem_status dem_get_stats(dem_system* sys, dem_stats* out) {
   out->regrows = sys->regrows;
   out->kernel_launches_per_step = kLaunchesPerStep + (sys->dist ? 4 : 0);
   if (sys->launched > 0 && sys->ns > 0) {
-    const RowBuf& R = sys->rows[(sys->launched - 1) & 1];
+    const RowBuf& R = sys->rows[sys->ep];
     int tot = 0, ins = 0;
     CK(cudaMemcpyAsync(&tot, R.row_ptr + sys->ns, sizeof(int), cudaMemcpyDeviceToHost, sys->stream));
     CK(cudaMemcpyAsync(&ins, sys->d_cell_start + sys->ncell, sizeof(int), cudaMemcpyDeviceToHost, sys->stream));
