@@ -199,8 +199,10 @@ def run_ours(a):
         dparams = dict(rank=rank, n_ranks=world, slab_lo=b[rank], slab_hi=b[rank + 1],
                        halo=dem.halo_width(scene, drift), drift_max=drift, transport=dem.TRANSPORT_NCCL,
                        nccl_id=obj[0])
+    # deferred rebuild (NEXT-1): margin = 2 v_max h k; k = 1 is the headline
+    margin = 2.0 * a.vmax * scene.h * a.cd_every if a.cd_every > 1 else 0.0
     sys_ = dem.system_from_scene(scene, record_contacts=False, cell_size=a.cell_size, dist=dparams,
-                                 entries_per_sphere=12 if world > 1 else 0)
+                                 entries_per_sphere=12 if world > 1 else 0, margin=margin, cd_every=a.cd_every)
     stream = sys_.stream
     sys_.dem_step(a.warmup)
     torch.cuda.synchronize()
@@ -238,8 +240,11 @@ def run_ours(a):
     # ---------------- roofline of the dominant kernel (this rank's launches)
     peak, peak_kind = peaks()
     sb = stage_bytes(st)
-    stages_k = {k: v for k, v in stages.items() if k in sb}
-    dom = max(stages_k, key=stages_k.get)
+    # per-launch durations: the detection stages run once per rebuild (every cd_every steps)
+    per_step = {k: v for k, v in stages.items() if k in sb}
+    stages_k = {k: (v * a.cd_every if k not in ("pose+bin_count", "force+integrate") else v)
+                for k, v in per_step.items()}
+    dom = max(per_step, key=per_step.get)
     achieved = sb[dom] / (stages_k[dom] * 1e-3) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -249,7 +254,7 @@ def run_ours(a):
         except Exception:
             traffic = None
     c = n_contacts / max(ns_total, 1)
-    step_bytes = survey_bytes_per_sphere_step(c) * ns_total
+    step_bytes = survey_bytes_per_sphere_step(c, a.cd_every) * ns_total
 
     # ---------------- e2e through the C-ABI with host buffers (pinned)
     e2e = None
@@ -291,14 +296,14 @@ def run_ours(a):
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": scene.name, "clumps": scene.n_clumps, "spheres": ns_total,
                    "contacts_per_sphere": c, "directed_entries": st["n_entries"], "bin_inserts": st["n_inserts"],
-                   "cell_size_m": st["cell_size"], "rebuild_every": 1, "h": scene.h,
+                   "cell_size_m": st["cell_size"], "rebuild_every": a.cd_every, "margin_m": margin, "h": scene.h,
                    "l2": "inputs larger than L2 (state + rows > 10 GB); no flush",
                    "parallelism": f"slab{world}" if world > 1 else "single-gpu",
                    "ghost_clumps_rank0": st["n_ghost_clumps"], "setup_s": round(setup_s, 1)},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "alg_bytes_per_launch": sb[dom], "avg_launch_ms": stages_k[dom]},
-        "step_roofline": {"bytes_per_sphere_step": survey_bytes_per_sphere_step(c),
+        "step_roofline": {"bytes_per_sphere_step": survey_bytes_per_sphere_step(c, a.cd_every),
                           "achieved_gbs": step_bytes / (ms / a.steps * 1e-3) / 1e9,
                           "frac": step_bytes / (ms / a.steps * 1e-3) / 1e9 / (peak * world)},
         "stage_ms": stages,
@@ -323,6 +328,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="c5", choices=["c5", "c4", "c3", "c1"])
     ap.add_argument("--cell-size", type=float, default=0.0)
+    ap.add_argument("--cd-every", type=int, default=1, help="contact-set rebuild period k (1 = headline)")
+    ap.add_argument("--vmax", type=float, default=1.0, help="speed bound for the k > 1 margin [m/s]")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer end-to-end pass (A/B runs)")
