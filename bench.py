@@ -92,10 +92,9 @@ def stage_bytes(st):
         "pose+bin_count": n * 188 + ns * 44 + nc * 8,
         "bin_scan": nc * 8,
         "bin_scatter": ns * 32 + nc * 12 + ins * 4,
-        "pairs": nc * 4 + ins * 40 + pairs * (16 + 16),
+        "pairs": nc * 4 + ins * 40 + pairs * 8,
         "row_scan": ns * 8,
-        "rows_scatter": pairs * 72,
-        "rows_finish": ns * 40 + ent * 32,
+        "rows_finish": ns * 40 + ent * 32 + pairs * 2 * 12,
         "force+integrate": ns * (32 + 8 + 8) + n * (80 + 56 + 4 + 104) + ent * 72,
     }
 

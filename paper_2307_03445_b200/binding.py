@@ -113,7 +113,7 @@ def _f64(a, shape=None):
     return a if shape is None else a.reshape(shape)
 
 
-STAGES = ["pose+bin_count", "bin_scan", "bin_scatter", "pairs", "row_scan", "rows_scatter", "rows_finish",
+STAGES = ["pose+bin_count", "bin_scan", "bin_scatter", "pairs", "row_scan", "rows_finish",
           "force+integrate", "halo"]
 
 

@@ -11,7 +11,7 @@
 //   sphere        clump (i32), template-component (i32), key (i64), (x,y,z,r) (double4 AoS),
 //                 partial force/torque (3+3 fp64 SoA)
 //   bins          cell_count (i32, ncell), cell_start (i32, ncell+1), items (i32, n_inserts)
-//   pairs         unordered candidate pairs of the step (int2), built by the per-bin warps
+//   slots         fixed-width candidate partner lists per owned sphere (i32), filled by the per-bin warps
 //   rows (x2)     CSR by own sphere: row_ptr (i32, ns+1), partner (i32), key (i64), u_t (3 fp64 AoS)
 #pragma once
 #include <cstdint>
@@ -33,7 +33,7 @@ struct Ctl {
   long long step;     // steps completed since dem_set_state
   long long need_inserts;
   long long need_entries;
-  long long need_pairs;
+  long long need_width;  // row-slot width a rebuild needed (fixed-width candidate rows)
 };
 
 constexpr int kKin = 10;  // doubles per clump in the packed kinematics record
@@ -121,9 +121,8 @@ struct StepArgs {
   int* cell_start;
   int* items;
   int* row_cnt;              // walls + sphere partners per sphere (built by atomics each step)
-  int4* pairs;               // candidate pairs of the step: (a, b, slot in row a, slot in row b)
-  unsigned long long* pair_cursor;
-  long long cap_pairs;
+  int* slots;                // [ns_own * row_width] candidate partners of each owned sphere (k_pairs)
+  int row_width;             // slots per sphere (walls included: slot w is the w-th entry of the row)
   Rows rows, prev;
   Record rec;
   int record;

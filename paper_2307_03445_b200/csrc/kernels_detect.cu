@@ -15,10 +15,12 @@
 //                   pair of the bin tested once by one lane, kept only in the bin of the
 //                   minimum corner of the two AABBs' bin-range intersection (so each pair
 //                   is found exactly once grid-wide); hits compacted with warp ballots
-//                   into a per-warp shared buffer, flushed with one atomic per 128 pairs
-//   scan            row offsets
-//   k_rows_scatter  per pair: both directed entries placed into their rows
-//   k_rows_finish   per sphere: wall entries + row sorted by partner key
+//                   into a per-warp shared buffer; at a flush every pair takes a slot in both
+//                   spheres' rows (counting atomics) and is written into the fixed-width
+//                   candidate lists (slots) of both
+//   scan            row offsets (CSR)
+//   k_rows_finish   per sphere: wall entries + its candidate list, sorted by partner key,
+//                   written to its CSR row, merged with its previous row (history index)
 #include "dem_device.cuh"
 
 namespace dem {
@@ -27,7 +29,6 @@ namespace dem {
 __global__ void __launch_bounds__(256) k_pose_count(StepArgs a) {
   if (a.ctl->abort) return;
   int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i == 0 && a.rebuild) *a.pair_cursor = 0ull;
   if (i >= a.ns) return;
   const int c = a.s_clump[i];
   const int tc = a.s_tc[i];
@@ -113,15 +114,12 @@ __global__ void __launch_bounds__(256) k_bin_scatter(StepArgs a) {
 
 // ---------------------------------------------------------------- (a3) per-bin pair tests
 // tuning knobs (build-time; see build.py -D): buffered pairs per warp, min CTAs/SM for the
-// register budget, and whether the row-slot atomics are deferred to the buffer flush
+// register budget, bins per CTA run
 #ifndef DEM_PAIRS_BUF
 #define DEM_PAIRS_BUF 64
 #endif
 #ifndef DEM_PAIRS_MINB
 #define DEM_PAIRS_MINB 5
-#endif
-#ifndef DEM_PAIRS_DEFER
-#define DEM_PAIRS_DEFER 1
 #endif
 #ifndef DEM_PAIRS_CONTIG
 #define DEM_PAIRS_CONTIG 64  // bins per run (0: plain grid-stride over bins)
@@ -157,19 +155,26 @@ __device__ __forceinline__ void decode_tri(int p, int& i, int& j) {
   i = p - jj * (jj - 1) / 2;
 }
 
-// Flush a warp's buffered pairs: one cursor atomic per warp, then the per-row counting
-// atomics that hand out each entry's slot in its row (walls come first).  The row atomics
-// are issued here, 2 x kPairBuf/32 independent ones per lane, so their latency overlaps
-// instead of stalling the pair loop on every hit.
-__device__ __forceinline__ void flush_pairs(const StepArgs& a, int4* bf, int n, int lane) {
+// one directed candidate: partner t in slot `slot` of own's row (slot -1: own is a ghost,
+// evaluated by its owner); a slot beyond the row width asks the host for wider rows
+__device__ __forceinline__ void put_slot(const StepArgs& a, int own, int slot, int t) {
+  if (slot < 0) return;
+  if (slot < a.row_width) {
+    a.slots[(size_t)own * a.row_width + slot] = t;
+  } else {
+    atomicMax(&a.ctl->need_width, (long long)slot + 1);
+    atomicExch(&a.ctl->abort, 1);
+  }
+}
+
+// Flush a warp's buffered pairs: the per-row counting atomics that hand out each entry's
+// slot in its row (walls come first), 2 x kPairBuf/32 independent ones per lane so their
+// latency overlaps, then both directed candidates written into the spheres' slot lists.
+__device__ __forceinline__ void flush_pairs(const StepArgs& a, const int2* bf, int n, int lane) {
   __syncwarp();
   if (n == 0) return;
-  unsigned long long off = 0;
-  if (lane == 0) off = atomicAdd(a.pair_cursor, (unsigned long long)n);
-  off = __shfl_sync(0xffffffffu, off, 0);
-#if DEM_PAIRS_DEFER
   constexpr int kPer = kPairBuf / 32;
-  int4 v[kPer];
+  int2 v[kPer];
   int sa[kPer], sb[kPer];
 #pragma unroll
   for (int j = 0; j < kPer; ++j) {
@@ -182,31 +187,18 @@ __device__ __forceinline__ void flush_pairs(const StepArgs& a, int4* bf, int n, 
   }
 #pragma unroll
   for (int j = 0; j < kPer; ++j) {
-    const int k = lane + 32 * j;
-    if (k < n && (long long)(off + k) < a.cap_pairs) a.pairs[off + k] = make_int4(v[j].x, v[j].y, sa[j], sb[j]);
+    if (lane + 32 * j < n) {
+      put_slot(a, v[j].x, sa[j], v[j].y);
+      put_slot(a, v[j].y, sb[j], v[j].x);
+    }
   }
-#else
-  for (int k = lane; k < n; k += 32)
-    if ((long long)(off + k) < a.cap_pairs) a.pairs[off + k] = bf[k];
-#endif
   __syncwarp();
-}
-
-// a hit of the pair loop: buffered; with DEM_PAIRS_DEFER = 0 the slots are taken right here
-__device__ __forceinline__ int4 pair_record(const StepArgs& a, int ia, int ib) {
-#if DEM_PAIRS_DEFER
-  return make_int4(ia, ib, 0, 0);
-#else
-  const int sa = ia < a.ns_own ? atomicAdd(&a.row_cnt[ia], 1) : -1;
-  const int sb = ib < a.ns_own ? atomicAdd(&a.row_cnt[ib], 1) : -1;
-  return make_int4(ia, ib, sa, sb);
-#endif
 }
 
 __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepArgs a) {
   __shared__ Members smA[kPairWarps];
   __shared__ Members smB[kPairWarps];
-  __shared__ int4 sbuf[kPairWarps][kPairBuf];
+  __shared__ int2 sbuf[kPairWarps][kPairBuf];
   if (a.ctl->abort) return;
   if ((long long)a.cell_start[a.ncell] > a.cap_inserts) {
     a.ctl->need_inserts = a.cell_start[a.ncell];
@@ -216,10 +208,9 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   Members& A = smA[w];
   Members& B = smB[w];
-  int4* bf = sbuf[w];
+  int2* bf = sbuf[w];
   int nbuf = 0;  // warp-uniform
   const Grid& g = a.grid;
-  const long long nw = (long long)gridDim.x * kPairWarps;
 #if DEM_PAIRS_CONTIG
   // CTAs take spans of kPairWarps x DEM_PAIRS_CONTIG consecutive bins round-robin and their
   // warps interleave inside the span: concurrent warps work on adjacent bins (shared L1
@@ -230,6 +221,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
        cid < a.ncell;
        (cid += kPairWarps) >= stop ? (cid += (long long)(gridDim.x - 1) * kSpan, stop = min(a.ncell, stop + (long long)gridDim.x * kSpan)) : 0) {
 #else
+  const long long nw = (long long)gridDim.x * kPairWarps;
   for (long long cid = (long long)blockIdx.x * kPairWarps + w; cid < a.ncell; cid += nw) {
 #endif
     const int k0 = a.cell_start[cid];
@@ -281,7 +273,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
             nbuf = 0;
           }
           if (hit)
-            bf[nbuf + __popc(mask & ((1u << lane) - 1u))] = pair_record(a, mu.y & 0x1fffffff, mv.y & 0x1fffffff);
+            bf[nbuf + __popc(mask & ((1u << lane) - 1u))] = make_int2(mu.y & 0x1fffffff, mv.y & 0x1fffffff);
           nbuf += cnt;
         }
       }
@@ -334,7 +326,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
               flush_pairs(a, bf, nbuf, lane);
               nbuf = 0;
             }
-            if (hit) bf[nbuf + __popc(mask & ((1u << lane) - 1u))] = pair_record(a, ia, ibx);
+            if (hit) bf[nbuf + __popc(mask & ((1u << lane) - 1u))] = make_int2(ia, ibx);
             nbuf += cnt;
           }
         }
@@ -345,40 +337,18 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
 }
 
 // ---------------------------------------------------------------- rows
-// per pair: both directed entries at the slots handed out in k_pairs (walls stay in front)
-__global__ void __launch_bounds__(256) k_rows_scatter(StepArgs a) {
-  if (a.ctl->abort) return;
-  const unsigned long long np = *a.pair_cursor;
-  const int total = a.rows.row_ptr[a.ns];
-  if ((long long)np > a.cap_pairs || (long long)total > a.cap_entries) {
-    if ((long long)np > a.cap_pairs) a.ctl->need_pairs = (long long)np;
-    if ((long long)total > a.cap_entries) a.ctl->need_entries = total;
-    atomicExch(&a.ctl->abort, 1);
-    return;
-  }
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < (long long)np; t += stride) {
-    const int4 pr = a.pairs[t];
-    if (pr.z >= 0) {  // slot -1: ghost sphere, evaluated by its owner
-      Entry ta;
-      ta.key = a.s_key[pr.y];
-      ta.partner = pr.y;
-      ta.prev = -1;
-      a.rows.ent[a.rows.row_ptr[pr.x] + pr.z] = ta;
-    }
-    if (pr.w >= 0) {
-      Entry tb;
-      tb.key = a.s_key[pr.x];
-      tb.partner = pr.x;
-      tb.prev = -1;
-      a.rows.ent[a.rows.row_ptr[pr.y] + pr.w] = tb;
-    }
-  }
-}
-
-// per sphere: wall entries in front, then the whole row sorted by partner key
+// per sphere: wall entries in front, then its candidate partners (keys gathered), the whole
+// row sorted by partner key in place
 __global__ void __launch_bounds__(256) k_rows_finish(StepArgs a) {
   if (a.ctl->abort) return;
+  const int total = a.rows.row_ptr[a.ns];
+  if ((long long)total > a.cap_entries) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+      a.ctl->need_entries = total;
+      atomicExch(&a.ctl->abort, 1);
+    }
+    return;
+  }
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.ns_own) return;
   const int beg = a.rows.row_ptr[i];
@@ -397,6 +367,17 @@ __global__ void __launch_bounds__(256) k_rows_finish(StepArgs a) {
       e.prev = -1;
       R[w++] = e;
     }
+  }
+  // slots [w, m) of the candidate list were handed out by k_pairs after k_pose_count
+  // counted the same w walls (same exactly rounded predicate)
+  const int* S = a.slots + (size_t)i * a.row_width;
+  for (int u = w; u < m; ++u) {
+    const int t = S[u];
+    Entry e;
+    e.key = a.s_key[t];
+    e.partner = t;
+    e.prev = -1;
+    R[u] = e;
   }
   for (int u = 1; u < m; ++u) {
     const Entry x = R[u];
@@ -432,9 +413,6 @@ void launch_pairs(const StepArgs& a, cudaStream_t s, int n_sm) {
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   k_pairs<<<(unsigned)blocks, kPairWarps * 32, 0, s>>>(a);
-}
-void launch_rows_scatter(const StepArgs& a, cudaStream_t s, int n_sm) {
-  k_rows_scatter<<<n_sm * 16, 256, 0, s>>>(a);
 }
 void launch_rows_finish(const StepArgs& a, cudaStream_t s) {
   if (a.ns) k_rows_finish<<<(a.ns + 255) / 256, 256, 0, s>>>(a);

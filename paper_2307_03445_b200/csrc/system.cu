@@ -21,7 +21,6 @@ namespace dem {
 void launch_pose_count(const StepArgs&, cudaStream_t);
 void launch_bin_scatter(const StepArgs&, cudaStream_t);
 void launch_pairs(const StepArgs&, cudaStream_t, int n_sm);
-void launch_rows_scatter(const StepArgs&, cudaStream_t, int n_sm);
 void launch_rows_finish(const StepArgs&, cudaStream_t);
 void launch_force_integrate(const StepArgs&, cudaStream_t);
 int force_cta_clumps();
@@ -35,9 +34,10 @@ void launch_unpack(const State& st, const int* idx, int n, const double* buf, cu
 
 using namespace dem;
 
-static constexpr int kStages = 9;  // last: ghost halo pack + exchange + unpack (distributed)
+static constexpr int kStages = 8;  // last: ghost halo pack + exchange + unpack (distributed)
 static constexpr int kKin13 = 13;  // doubles per ghost clump state
-static constexpr int kLaunchesPerStep = 12;  // 6 stage kernels + 2 x 3 scan kernels
+static constexpr int kRowWidth = 32;  // initial candidate slots per owned sphere
+static constexpr int kLaunchesPerStep = 11;  // 5 stage kernels + 2 x 3 scan kernels
 
 struct RowBuf {
   int* row_ptr = nullptr;
@@ -75,9 +75,8 @@ struct dem_system {
   double4* d_spos = nullptr;
   int* d_cta_clump = nullptr;
   int n_cta = 0;
-  int4* d_pairs = nullptr;
-  unsigned long long* d_pair_cursor = nullptr;
-  long long cap_pairs = 0;
+  int* d_slots = nullptr;  // fixed-width candidate partner lists of the owned spheres
+  int row_width = 0;
   int n_sm = 148;
   // bins
   Grid grid{};
@@ -228,12 +227,9 @@ static StepArgs make_args(dem_system* sys, bool rebuild) {
   a.s_clump = sys->d_s_clump;
   a.s_tc = sys->d_s_tc;
   a.s_key = sys->d_s_key;
-  size_t ns = (size_t)sys->ns;
   a.spos = sys->d_spos;
-  a.pairs = sys->d_pairs;
-  a.pair_cursor = sys->d_pair_cursor;
-  a.cap_pairs = sys->cap_pairs;
-  (void)ns;
+  a.slots = sys->d_slots;
+  a.row_width = sys->row_width;
   a.cta_clump = sys->d_cta_clump;
   a.n_cta = sys->n_cta;
   a.n_own = (int)sys->n_own;
@@ -296,12 +292,10 @@ static void enqueue_step(dem_system* sys, bool rebuild, cudaStream_t s, cudaEven
   if (ev) cudaEventRecord(ev[4], s);
   if (rebuild) launch_excl_scan(sys->d_row_cnt, a.rows.row_ptr, sys->ns, sys->d_scan_tmp, abort, s);
   if (ev) cudaEventRecord(ev[5], s);
-  if (rebuild) launch_rows_scatter(a, s, sys->n_sm);
-  if (ev) cudaEventRecord(ev[6], s);
   if (rebuild) launch_rows_finish(a, s);
-  if (ev) cudaEventRecord(ev[7], s);
+  if (ev) cudaEventRecord(ev[6], s);
   launch_force_integrate(a, s);
-  if (ev) cudaEventRecord(ev[8], s);
+  if (ev) cudaEventRecord(ev[7], s);
   if (sys->dist) {
     enqueue_pack(sys, a, s);
     if (exchange && sys->P.transport == DEM_TRANSPORT_NCCL) {
@@ -309,7 +303,7 @@ static void enqueue_step(dem_system* sys, bool rebuild, cudaStream_t s, cudaEven
       enqueue_unpack(sys, a, s);
     }
   }
-  if (ev) cudaEventRecord(ev[9], s);
+  if (ev) cudaEventRecord(ev[8], s);
 }
 
 static int graph_key(const dem_system* sys, bool rebuild) {
@@ -468,8 +462,7 @@ extern "C" dem_status dem_create(const dem_params* params, const dem_material* m
     dem_destroy(sys);
     return st;
   }
-  if ((st = alloc_arr(sys, &sys->d_ctl, 1)) || (st = alloc_arr(sys, &sys->d_counter, 1)) ||
-      (st = alloc_arr(sys, &sys->d_pair_cursor, 1))) {
+  if ((st = alloc_arr(sys, &sys->d_ctl, 1)) || (st = alloc_arr(sys, &sys->d_counter, 1))) {
     dem_destroy(sys);
     return st;
   }
@@ -780,8 +773,10 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
   TRY(alloc_arr(sys, &sys->d_s_key, ns));
   TRY(alloc_arr(sys, &sys->d_spos, ns));
   TRY(alloc_arr(sys, &sys->d_spos_ref, ns));
-  sys->cap_pairs = std::max<long long>(1024, 4 * ns);
-  TRY(alloc_arr(sys, &sys->d_pairs, sys->cap_pairs));
+  // candidate lists: kRowWidth slots per owned sphere to start with (walls included), widened
+  // on overflow (the rows of a settled bed hold a few entries)
+  sys->row_width = kRowWidth;
+  TRY(alloc_arr(sys, &sys->d_slots, (size_t)sys->ns_own * sys->row_width + 1));
   // CTA partition of the fused force/integrate kernel: consecutive whole clumps, at most
   // force_cta_clumps() clumps and force_cta_spheres() spheres per CTA
   // (owned clumps only: ghosts are integrated by their owners)
@@ -1031,16 +1026,15 @@ extern "C" dem_status dem_step(dem_system* sys, int64_t n_steps) {
       sys->cap_inserts = need + need / 4 + 1024;
       TRY(alloc_arr(sys, &sys->d_items, sys->cap_inserts));
     }
-    if (sys->h_ctl->need_pairs > sys->cap_pairs) {
-      long long need = sys->h_ctl->need_pairs;
-      sys->cap_pairs = need + need / 4 + 1024;
-      TRY(alloc_arr(sys, &sys->d_pairs, sys->cap_pairs));
+    if (sys->h_ctl->need_width > sys->row_width) {
+      sys->row_width = (int)std::min<long long>(sys->h_ctl->need_width + 8, 1 << 16);
+      TRY(alloc_arr(sys, &sys->d_slots, (size_t)sys->ns_own * sys->row_width + 1));
     }
     free_graphs(sys);
     sys->h_ctl->abort = 0;
     sys->h_ctl->need_entries = 0;
     sys->h_ctl->need_inserts = 0;
-    sys->h_ctl->need_pairs = 0;
+    sys->h_ctl->need_width = 0;
     CK(cudaMemcpyAsync(sys->d_ctl, sys->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, sys->stream));
   }
   return DEM_OK;

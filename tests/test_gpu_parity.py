@@ -235,6 +235,24 @@ def test_capacity_regrow_keeps_parity(dem):
     assert_forces_close(cg, co, scene)
 
 
+def test_row_width_regrow_keeps_parity(dem):
+    """A margin of several radii gives some spheres more candidates than the initial 32
+    slots of their candidate lists: the library widens them and re-runs the step; the
+    contact set and forces still match the oracle."""
+    scene = w.random_clumps(52, 300, box=0.02)
+    g = dem.system_from_scene(scene, record_contacts=True, margin=4e-3)
+    o = oracle.Oracle(scene, margin=4e-3)
+    g.dem_step(1)
+    o.step(1)
+    co = o.contacts()
+    keys, cnt = np.unique(np.concatenate([co["key_a"], co["key_b"][co["key_b"] < 2**62]]), return_counts=True)
+    assert cnt.max() > 32
+    assert g.dem_get_stats()["regrows"] >= 1
+    cg = g.dem_get_contacts()
+    assert_same_contact_set(cg, co)
+    assert_forces_close(cg, co, scene)
+
+
 @pytest.mark.parametrize("cell", [0.0, 1.5e-3, 8e-3])
 def test_contact_set_independent_of_cell_size(dem, cell):
     scene = w.random_clumps(50, 400, box=0.03)
