@@ -121,7 +121,7 @@ struct StepArgs {
   int* cell_start;
   int* items;
   int* row_cnt;              // walls + sphere partners per sphere (built by atomics each step)
-  int* slots;                // [ns_own * row_width] candidate partners of each owned sphere (k_pairs)
+  int* slots;                // [row_width][ns_own] candidate partners of the owned spheres (k_pairs)
   int row_width;             // slots per sphere (walls included: slot w is the w-th entry of the row)
   Rows rows, prev;
   Record rec;

@@ -160,7 +160,7 @@ __device__ __forceinline__ void decode_tri(int p, int& i, int& j) {
 __device__ __forceinline__ void put_slot(const StepArgs& a, int own, int slot, int t) {
   if (slot < 0) return;
   if (slot < a.row_width) {
-    a.slots[(size_t)own * a.row_width + slot] = t;
+    a.slots[(size_t)slot * a.ns_own + own] = t;  // slot-major: k_rows_finish reads coalesced
   } else {
     atomicMax(&a.ctl->need_width, (long long)slot + 1);
     atomicExch(&a.ctl->abort, 1);
@@ -337,8 +337,19 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
 }
 
 // ---------------------------------------------------------------- rows
-// per sphere: wall entries in front, then its candidate partners (keys gathered), the whole
-// row sorted by partner key in place
+// Per owned sphere: its candidate partners (keys gathered) sorted by partner key, then its
+// wall entries (keys INT64_MAX - p sort last, larger p first), written to its CSR row, and
+// each entry's history index found in the sphere's previous row ("persist between
+// timesteps"; -1 for a contact born this step).  Rows of up to kRegRow candidates — nearly
+// all of them — are sorted and matched in registers; longer ones in place in memory.
+constexpr int kRegRow = 8;
+
+__device__ __forceinline__ int prev_index(const Rows& prev, int pb, int pe, long long key) {
+  for (int v = pb; v < pe; ++v)
+    if (prev.ent[v].key == key) return v;
+  return -1;
+}
+
 __global__ void __launch_bounds__(256) k_rows_finish(StepArgs a) {
   if (a.ctl->abort) return;
   const int total = a.rows.row_ptr[a.ns];
@@ -353,50 +364,90 @@ __global__ void __launch_bounds__(256) k_rows_finish(StepArgs a) {
   if (i >= a.ns_own) return;
   const int beg = a.rows.row_ptr[i];
   const int m = a.rows.row_ptr[i + 1] - beg;
+  const int pb = a.prev.row_ptr[i], pe = a.prev.row_ptr[i + 1];
   Entry* R = a.rows.ent + beg;
   const double4 s = a.spos[i];
-  int w = 0;
+  unsigned wmask = 0;  // walls, same exactly rounded predicate as k_pose_count's count
   for (int p = 0; p < a.tab.n_planes; ++p) {
     const double* pp = a.tab.plane_pt[p];
     const double* nw = a.tab.plane_n[p];
     const double dd = add(add(mul(sub(s.x, pp[0]), nw[0]), mul(sub(s.y, pp[1]), nw[1])), mul(sub(s.z, pp[2]), nw[2]));
-    if (sub(add(s.w, a.margin), dd) >= 0.0) {
+    if (sub(add(s.w, a.margin), dd) >= 0.0) wmask |= 1u << p;
+  }
+  const int w = __popc(wmask);
+  const int nc = m - w;  // k_pairs handed out slots [w, m) of the candidate list
+  const int* S = a.slots + (size_t)w * a.ns_own + i;  // S[q * ns_own]: candidate q
+  if (nc <= kRegRow) {
+    int tt[kRegRow], hh[kRegRow];
+    long long kk[kRegRow];
+#pragma unroll
+    for (int q = 0; q < kRegRow; ++q) tt[q] = q < nc ? S[(size_t)q * a.ns_own] : 0;
+#pragma unroll
+    for (int q = 0; q < kRegRow; ++q) {
+      kk[q] = q < nc ? a.s_key[tt[q]] : 0x7fffffffffffffffLL;
+      hh[q] = -1;
+    }
+    // odd-even transposition sort (keys of the candidates are distinct; padding sorts last)
+#pragma unroll
+    for (int r = 0; r < kRegRow; ++r)
+#pragma unroll
+      for (int q = r & 1; q + 1 < kRegRow; q += 2)
+        if (kk[q] > kk[q + 1]) {
+          const long long tk = kk[q];
+          kk[q] = kk[q + 1];
+          kk[q + 1] = tk;
+          const int t = tt[q];
+          tt[q] = tt[q + 1];
+          tt[q + 1] = t;
+        }
+#pragma unroll 4
+    for (int v = pb; v < pe; ++v) {
+      const long long pk = a.prev.ent[v].key;
+#pragma unroll
+      for (int q = 0; q < kRegRow; ++q)
+        if (kk[q] == pk) hh[q] = v;
+    }
+#pragma unroll
+    for (int q = 0; q < kRegRow; ++q)
+      if (q < nc) {
+        Entry e;
+        e.key = kk[q];
+        e.partner = tt[q];
+        e.prev = hh[q];
+        R[q] = e;
+      }
+  } else {
+    for (int u = 0; u < nc; ++u) {
+      const int t = S[(size_t)u * a.ns_own];
+      Entry e;
+      e.key = a.s_key[t];
+      e.partner = t;
+      R[u] = e;
+    }
+    for (int u = 1; u < nc; ++u) {
+      const Entry x = R[u];
+      int v = u - 1;
+      while (v >= 0 && R[v].key > x.key) {
+        R[v + 1] = R[v];
+        --v;
+      }
+      R[v + 1] = x;
+    }
+    int pj = pb;  // merge with the previous row (both sorted by key)
+    for (int u = 0; u < nc; ++u) {
+      const long long k = R[u].key;
+      while (pj < pe && a.prev.ent[pj].key < k) ++pj;
+      R[u].prev = (pj < pe && a.prev.ent[pj].key == k) ? pj : -1;
+    }
+  }
+  for (int u = nc, p = a.tab.n_planes - 1; p >= 0; --p)
+    if (wmask >> p & 1u) {
       Entry e;
       e.key = (long long)(0x7fffffffffffffffLL - p);
       e.partner = -1 - p;
-      e.prev = -1;
-      R[w++] = e;
+      e.prev = prev_index(a.prev, pb, pe, e.key);
+      R[u++] = e;
     }
-  }
-  // slots [w, m) of the candidate list were handed out by k_pairs after k_pose_count
-  // counted the same w walls (same exactly rounded predicate)
-  const int* S = a.slots + (size_t)i * a.row_width;
-  for (int u = w; u < m; ++u) {
-    const int t = S[u];
-    Entry e;
-    e.key = a.s_key[t];
-    e.partner = t;
-    e.prev = -1;
-    R[u] = e;
-  }
-  for (int u = 1; u < m; ++u) {
-    const Entry x = R[u];
-    int v = u - 1;
-    while (v >= 0 && R[v].key > x.key) {
-      R[v + 1] = R[v];
-      --v;
-    }
-    R[v + 1] = x;
-  }
-  // (a4) history remap: merge with the sphere's previous row (both sorted by key) and keep
-  // the index of each surviving key's u_t, or -1 for a contact born this step
-  int pj = a.prev.row_ptr[i];
-  const int pend = a.prev.row_ptr[i + 1];
-  for (int u = 0; u < m; ++u) {
-    const long long k = R[u].key;
-    while (pj < pend && a.prev.ent[pj].key < k) ++pj;
-    R[u].prev = (pj < pend && a.prev.ent[pj].key == k) ? pj : -1;
-  }
 }
 
 // host launchers
