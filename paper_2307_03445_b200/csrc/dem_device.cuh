@@ -45,7 +45,7 @@ struct Tables {
   const int* tpl_coff;    // [n_tmpl]
   const double* tpl_mass;
   const double* tpl_inertia;  // [3 * n_tmpl]
-  const double* pair;     // [n_mat * n_mat * 4]: E*, G*, beta, mu (symmetric)
+  const double* pair;     // [n_mat * n_mat * 8]: 2E*, 8G*, 2 sqrt(5/6) beta, mu, sqrt(4G*/E*) (symmetric)
   int n_mat;
   int n_planes;
   double plane_pt[kMaxPlanes][3];
@@ -109,7 +109,7 @@ struct StepArgs {
   const long long* s_key;
   double4* spos;             // sphere (x, y, z, r), written by the pose kernel each step
   double* kin;               // per clump [kKin]: X(3), V(3), omega_world(3), mass
-  const int* cta_clump;      // [n_cta + 1] clump ranges of the fused force/integrate CTAs
+  const int2* cta_clump;     // [n_cta + 1] (first clump, first sphere) of the fused force/integrate CTAs
   int n_cta;
   int rebuild;               // 1: this step rebuilds the contact set; 0: re-evaluates rows
   double4* spos_ref;         // sphere centres at the last rebuild

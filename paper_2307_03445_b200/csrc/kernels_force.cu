@@ -25,6 +25,7 @@
 
 namespace dem {
 
+constexpr int kPairStride = 8;  // doubles per material pair in Tables::pair
 constexpr int kFC = 32;     // max clumps per CTA (host partition, see system.cu)
 constexpr int kMaxS = 160;  // max spheres per CTA
 constexpr int kFT = 128;    // threads per CTA (= entries per chunk)
@@ -45,7 +46,8 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
   __shared__ double part[6][kFT];
   __shared__ double acc[6][kMaxS];
   const int tid = threadIdx.x;
-  const int c0 = a.cta_clump[blockIdx.x], c1 = a.cta_clump[blockIdx.x + 1];
+  const int2 b0 = a.cta_clump[blockIdx.x], b1 = a.cta_clump[blockIdx.x + 1];
+  const int c0 = b0.x, c1 = b1.x;
   const int ncl = c1 - c0;
   if (a.ctl->abort) {
     // capacity abort / error: carry the state forward unchanged so the ping-pong stays valid
@@ -59,8 +61,8 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
     return;
   }
   if (blockIdx.x == 0 && tid == 0) a.ctl->step += 1;  // no other thread of this launch reads it
-  const int s0 = a.sph_off[c0];
-  const int nsph = a.sph_off[c1] - s0;
+  const int s0 = b0.y;
+  const int nsph = b1.y - s0;
   for (int k = tid; k <= nsph; k += kFT) {
     rp[k] = a.rows.row_ptr[s0 + k];
   }
@@ -75,7 +77,6 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
   for (int k = tid; k < ncl * kKin; k += kFT) ck[k / kKin][k % kKin] = a.kin[(size_t)kKin * c0 + k];
   __syncthreads();
   const double h = a.h;
-  const double k56 = 2.0 * sqrt(5.0 / 6.0);
   const int E0 = rp[0], E1 = rp[nsph];
   for (int c0e = E0; c0e < E1; c0e += kFT) {
     const int e = c0e + tid;
@@ -120,9 +121,10 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
         const double dist = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
         degenerate = dist == 0.0;
         delta = (ri + rj) - dist;
-        nx = dx / dist;
-        ny = dy / dist;
-        nz = dz / dist;
+        const double inv = 1.0 / dist;  // sign-symmetric: the mirror entry gets exactly -n
+        nx = dx * inv;
+        ny = dy * inv;
+        nz = dz * inv;
         const double hr = 0.5 * (ri - rj);
         px = __fma_rn(hr, nx, 0.5 * (cx + pj.x));
         py = __fma_rn(hr, ny, 0.5 * (cy + pj.y));
@@ -162,13 +164,14 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
         point_velocity(ki[3], ki[4], ki[5], ki[6], ki[7], ki[8], rix, riy, riz, vix, viy, viz);
         if (!wall) point_velocity(Vjx, Vjy, Vjz, Wjx, Wjy, Wjz, px - Xjx, py - Xjy, pz - Xjz, vjx, vjy, vjz);
         const double vrx = vjx - vix, vry = vjy - viy, vrz = vjz - viz;
-        const double* pr = a.tab.pair + 4 * (own_mat[ls] * a.tab.n_mat + mj);
-        const double estar = pr[0], gstar = pr[1], beta = pr[2], mu = pr[3];
+        // pair table (system.cu): 2E*, 8G*, 2 sqrt(5/6) beta, mu, sqrt(k_t / S_n) = sqrt(4G*/E*)
+        const double* pr = a.tab.pair + kPairStride * (own_mat[ls] * a.tab.n_mat + mj);
+        const double e2 = pr[0], g8 = pr[1], kb = pr[2], mu = pr[3], rt = pr[4];
         // (a6) normal force, Eq. 1a
         const double sq = sqrt(rbar * delta);
-        const double Sn = 2.0 * estar * sq;
+        const double Sn = e2 * sq;
         const double kn = (2.0 / 3.0) * Sn;
-        const double cn = k56 * beta * sqrt(Sn * mbar);
+        const double cn = kb * sqrt(Sn * mbar);
         const double vn = vrx * nx + vry * ny + vrz * nz;
         const double fns = kn * delta - cn * vn;
         const double fnx = fns * nx, fny = fns * ny, fnz = fns * nz;
@@ -179,18 +182,19 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
           const double upx = ux + h * vtx, upy = uy + h * vty, upz = uz + h * vtz;
           const double upn = upx * nx + upy * ny + upz * nz;
           const double utx = upx - upn * nx, uty = upy - upn * ny, utz = upz - upn * nz;
-          const double kt = 8.0 * gstar * sq;
-          const double ct = k56 * beta * sqrt(kt * mbar);
+          const double kt = g8 * sq;
+          const double ct = cn * rt;  // 2 sqrt(5/6) beta sqrt(k_t m) = c_n sqrt(k_t / S_n)
           const double trx = -kt * utx - ct * vtx, try_ = -kt * uty - ct * vty, trz = -kt * utz - ct * vtz;
-          const double cap = mu * sqrt(fnx * fnx + fny * fny + fnz * fnz);
-          const double tmag = sqrt(trx * trx + try_ * try_ + trz * trz);
-          if (tmag <= cap) {
+          const double cap = mu * fabs(fns);  // mu |F_n| (n is a unit vector)
+          // |F_t trial| <= mu |F_n|, compared squared
+          if (trx * trx + try_ * try_ + trz * trz <= cap * cap) {
             ftx = trx; fty = try_; ftz = trz;
             nux = utx; nuy = uty; nuz = utz;
           } else {
             const double um = sqrt(utx * utx + uty * uty + utz * utz);
             if (um > 0.0) {
-              const double dxu = utx / um, dyu = uty / um, dzu = utz / um;
+              const double iu = 1.0 / um;
+              const double dxu = utx * iu, dyu = uty * iu, dzu = utz * iu;
               const double s = cap / kt;
               nux = s * dxu; nuy = s * dyu; nuz = s * dzu;
               ftx = -cap * dxu; fty = -cap * dyu; ftz = -cap * dzu;

@@ -73,7 +73,7 @@ struct dem_system {
   int *d_s_clump = nullptr, *d_s_tc = nullptr;
   long long* d_s_key = nullptr;
   double4* d_spos = nullptr;
-  int* d_cta_clump = nullptr;
+  int2* d_cta_clump = nullptr;  // per CTA boundary: (first clump, first sphere)
   int n_cta = 0;
   int* d_slots = nullptr;  // fixed-width candidate partner lists of the owned spheres
   int row_width = 0;
@@ -431,14 +431,17 @@ extern "C" dem_status dem_create(const dem_params* params, const dem_material* m
       sys->rmax = std::max(sys->rmax, T.radius[k]);
     }
   }
-  sys->pair.assign((size_t)n_mat * n_mat * 4, 0.0);
+  // per material pair, the factors of the force law (kernels_force.cu): 2E*, 8G*,
+  // 2 sqrt(5/6) beta, mu, sqrt(4 G*/E*) (so c_t = c_n sqrt(k_t / S_n) without a second sqrt)
+  sys->pair.assign((size_t)n_mat * n_mat * 8, 0.0);
   for (int i = 0; i < n_mat; ++i)
     for (int j = i; j < n_mat; ++j) {
       double o[4];
       pair_params(materials[i], materials[j], o);
-      for (int q = 0; q < 4; ++q) {
-        sys->pair[4 * (i * n_mat + j) + q] = o[q];
-        sys->pair[4 * (j * n_mat + i) + q] = o[q];
+      const double f[5] = {2.0 * o[0], 8.0 * o[1], 2.0 * std::sqrt(5.0 / 6.0) * o[2], o[3], std::sqrt(4.0 * o[1] / o[0])};
+      for (int q = 0; q < 5; ++q) {
+        sys->pair[8 * (i * n_mat + j) + q] = f[q];
+        sys->pair[8 * (j * n_mat + i) + q] = f[q];
       }
     }
   cudaError_t e = cudaStreamCreateWithFlags(&sys->cap_stream, cudaStreamNonBlocking);
@@ -825,7 +828,11 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
   }
   TRY(alloc_rows(sys, cap));
   cudaStream_t s = sys->stream;
-  CK(cudaMemcpyAsync(sys->d_cta_clump, cta.data(), sizeof(int) * cta.size(), cudaMemcpyHostToDevice, s));
+  {
+    std::vector<int2> bnd(cta.size());  // (first clump, first sphere) of every CTA
+    for (size_t k = 0; k < cta.size(); ++k) bnd[k] = make_int2(cta[k], (int)sys->h_sph_off[cta[k]]);
+    CK(cudaMemcpyAsync(sys->d_cta_clump, bnd.data(), sizeof(int2) * bnd.size(), cudaMemcpyHostToDevice, s));
+  }
   if (n_own) CK(cudaMemcpyAsync(sys->d_xref, xref.data(), sizeof(double) * xref.size(), cudaMemcpyHostToDevice, s));
   for (int side = 0; side < 2; ++side) {
     if (!lists[side].empty())
