@@ -36,6 +36,7 @@ struct Ctl {
   long long need_width;  // row-slot width a rebuild needed (fixed-width candidate rows)
 };
 
+constexpr int kUt = 4;    // doubles per entry of the tangential history (padded)
 constexpr int kKin = 10;  // doubles per clump in the packed kinematics record
 
 struct Tables {
@@ -78,7 +79,7 @@ struct __align__(16) Entry {
 struct Rows {
   int* row_ptr;     // [ns + 1]
   Entry* ent;       // [cap]
-  double* ut;       // [3 * cap] AoS, oriented own -> partner
+  double* ut;       // [kUt * cap] AoS (x, y, z, 0): one 32-byte sector per entry, oriented own -> partner
 };
 
 struct Record {

@@ -102,9 +102,10 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
       double ux = 0.0, uy = 0.0, uz = 0.0;
       const int pidx = a.rebuild ? ent.prev : e;
       if (pidx >= 0) {
-        ux = a.prev.ut[3 * pidx];
-        uy = a.prev.ut[3 * pidx + 1];
-        uz = a.prev.ut[3 * pidx + 2];
+        const double2 u01 = *reinterpret_cast<const double2*>(a.prev.ut + kUt * pidx);
+        ux = u01.x;
+        uy = u01.y;
+        uz = a.prev.ut[kUt * pidx + 2];
       }
       // (a5) geometry: n from i (own) to j (partner)
       double nx, ny, nz, px, py, pz, delta, rbar, mbar;
@@ -114,7 +115,7 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
       bool degenerate = false;
       if (!wall) {
         const double4 pj = a.spos[t];
-        const double* kj = a.kin + (size_t)kKin * a.s_clump[t];
+        const double2* kj = reinterpret_cast<const double2*>(a.kin + (size_t)kKin * a.s_clump[t]);
         mj = a.tab.tc_mat[a.s_tc[t]];
         const double rj = pj.w;
         const double dx = pj.x - cx, dy = pj.y - cy, dz = pj.z - cz;
@@ -130,11 +131,12 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
         py = __fma_rn(hr, ny, 0.5 * (cy + pj.y));
         pz = __fma_rn(hr, nz, 0.5 * (cz + pj.z));
         rbar = (ri * rj) / (ri + rj);
-        const double Mj = kj[9];
+        const double2 k01 = kj[0], k23 = kj[1], k45 = kj[2], k67 = kj[3], k89 = kj[4];
+        const double Mj = k89.y;
         mbar = (Mi * Mj) / (Mi + Mj);
-        Xjx = kj[0]; Xjy = kj[1]; Xjz = kj[2];
-        Vjx = kj[3]; Vjy = kj[4]; Vjz = kj[5];
-        Wjx = kj[6]; Wjy = kj[7]; Wjz = kj[8];
+        Xjx = k01.x; Xjy = k01.y; Xjz = k23.x;
+        Vjx = k23.y; Vjy = k45.x; Vjz = k45.y;
+        Wjx = k67.x; Wjy = k67.y; Wjz = k89.x;
       } else {
         const int pl = -1 - t;
         const double* pp = a.tab.plane_pt[pl];
@@ -205,9 +207,8 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
         Fy = fny + fty;
         Fz = fnz + ftz;
       }
-      a.rows.ut[3 * e] = nux;
-      a.rows.ut[3 * e + 1] = nuy;
-      a.rows.ut[3 * e + 2] = nuz;
+      *reinterpret_cast<double2*>(a.rows.ut + kUt * e) = make_double2(nux, nuy);
+      *reinterpret_cast<double2*>(a.rows.ut + kUt * e + 2) = make_double2(nuz, 0.0);
       if (a.record) {
         a.rec.F[3 * e] = Fx; a.rec.F[3 * e + 1] = Fy; a.rec.F[3 * e + 2] = Fz;
         a.rec.p[3 * e] = px; a.rec.p[3 * e + 1] = py; a.rec.p[3 * e + 2] = pz;

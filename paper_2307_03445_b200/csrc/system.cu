@@ -533,7 +533,7 @@ static dem_status alloc_rows(dem_system* sys, long long cap) {
     RowBuf nb;
     nb.row_ptr = sys->rows[p].row_ptr;
     nb.ent = (Entry*)dalloc(sys, sizeof(Entry) * cap);
-    nb.ut = (double*)dalloc(sys, sizeof(double) * 3 * cap);
+    nb.ut = (double*)dalloc(sys, sizeof(double) * kUt * cap);
     if (!nb.ent || !nb.ut) {
       sys->err = "row buffer allocation failed";
       return DEM_ERR_OOM;
@@ -541,7 +541,7 @@ static dem_status alloc_rows(dem_system* sys, long long cap) {
     if (sys->rows[p].ent && sys->cap_entries) {
       size_t m = (size_t)std::min(cap, sys->cap_entries);
       cudaMemcpyAsync(nb.ent, sys->rows[p].ent, sizeof(Entry) * m, cudaMemcpyDeviceToDevice, sys->stream);
-      cudaMemcpyAsync(nb.ut, sys->rows[p].ut, sizeof(double) * 3 * m, cudaMemcpyDeviceToDevice, sys->stream);
+      cudaMemcpyAsync(nb.ut, sys->rows[p].ut, sizeof(double) * kUt * m, cudaMemcpyDeviceToDevice, sys->stream);
     }
     dfree(sys, sys->rows[p].ent);
     dfree(sys, sys->rows[p].ut);
@@ -893,7 +893,7 @@ extern "C" dem_status dem_set_contact_history(dem_system* sys, int64_t n, const 
       en.partner = -1;  // only the key and u_t of the previous rows are read
       en.prev = -1;
       ents.push_back(en);
-      for (int d = 0; d < 3; ++d) ut.push_back(e.u[d]);
+      for (int d = 0; d < kUt; ++d) ut.push_back(d < 3 ? e.u[d] : 0.0);
     }
     rp[s + 1] = (int)ents.size();
   }
@@ -905,7 +905,7 @@ extern "C" dem_status dem_set_contact_history(dem_system* sys, int64_t n, const 
   CK(cudaMemcpyAsync(R.row_ptr, rp.data(), sizeof(int) * (sys->ns + 1), cudaMemcpyHostToDevice, s));
   if (m) {
     CK(cudaMemcpyAsync(R.ent, ents.data(), sizeof(Entry) * m, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(sys->rows[sys->up].ut, ut.data(), sizeof(double) * 3 * m, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(sys->rows[sys->up].ut, ut.data(), sizeof(double) * kUt * m, cudaMemcpyHostToDevice, s));
   }
   CK(cudaStreamSynchronize(s));
   sys->since_rebuild = 0;
@@ -1215,19 +1215,19 @@ extern "C" dem_status dem_get_contacts(dem_system* sys, int64_t cap, int64_t* n,
   *n = (int64_t)sel.size();
   if (cap == 0) return DEM_OK;
   if (cap < (int64_t)sel.size()) return DEM_ERR_INVALID_ARG;
-  auto fetch3 = [&](const double* dev, double* out) -> dem_status {
+  auto fetch3 = [&](const double* dev, double* out, int stride = 3) -> dem_status {
     if (!out) return DEM_OK;
-    std::vector<double> buf((size_t)3 * m);
-    if (m) CK(cudaMemcpy(buf.data(), dev, sizeof(double) * 3 * m, cudaMemcpyDeviceToHost));
+    std::vector<double> buf((size_t)stride * m);
+    if (m) CK(cudaMemcpy(buf.data(), dev, sizeof(double) * stride * m, cudaMemcpyDeviceToHost));
     for (size_t k = 0; k < sel.size(); ++k)
-      for (int d = 0; d < 3; ++d) out[3 * k + d] = buf[3 * sel[k].second + d];
+      for (int d = 0; d < 3; ++d) out[3 * k + d] = buf[stride * sel[k].second + d];
     return DEM_OK;
   };
   for (size_t k = 0; k < sel.size(); ++k) {
     if (key_a) key_a[k] = sys->h_s_key[sel[k].first];
     if (key_b) key_b[k] = keys[sel[k].second];
   }
-  TRY(fetch3(sys->rows[sys->up].ut, u_t));
+  TRY(fetch3(sys->rows[sys->up].ut, u_t, kUt));
   TRY(fetch3(sys->rec.F, force_on_b));
   TRY(fetch3(sys->rec.p, point));
   TRY(fetch3(sys->rec.n, normal));
