@@ -120,7 +120,7 @@ struct StepArgs {
   double drift_max;          // 0: no check
   int* cell_count;
   int* cell_start;
-  int* items;
+  int* items;                // [cap_inserts] bin items: sphere index | lowest-bin mask << 29
   int* row_cnt;              // walls + sphere partners per sphere (built by atomics each step)
   int* slots;                // [row_width][ns_own] candidate partners of the owned spheres (k_pairs)
   int row_width;             // slots per sphere (walls included: slot w is the w-th entry of the row)

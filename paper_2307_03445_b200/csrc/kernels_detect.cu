@@ -11,10 +11,10 @@
 //                   bin counts; component 0 packs the clump kinematics record
 //   scan            bin offsets
 //   k_bin_scatter   per sphere: bin item lists (slots by decrementing the counts)
-//   k_pairs         one warp per bin: members staged in shared memory, every unordered
-//                   pair of the bin tested once by one lane, kept only in the bin of the
-//                   minimum corner of the two AABBs' bin-range intersection (so each pair
-//                   is found exactly once grid-wide); hits compacted with warp ballots
+//   k_pairs         one warp per bin: members staged in shared memory ordered by which of
+//                   the bin's faces are their lowest; only the pairs whose lowest common bin
+//                   is this one (so each pair is found exactly once grid-wide) enumerated
+//                   flat over the lanes and tested; hits compacted with warp ballots
 //                   into a per-warp shared buffer; at a flush every pair takes a slot in both
 //                   spheres' rows (counting atomics) and is written into the fixed-width
 //                   candidate lists (slots) of both
@@ -107,7 +107,8 @@ __global__ void __launch_bounds__(256) k_bin_scatter(StepArgs a) {
       for (int x = lx; x <= hx; ++x) {
         const long long cid = base + x * g.st[0];
         const int slot = atomicSub(&a.cell_count[cid], 1) - 1;
-        if (fits) a.items[a.cell_start[cid] + slot] = i;
+        // the item carries the sphere's lowest-bin mask for k_pairs (ns < 2^29, checked)
+        if (fits) a.items[a.cell_start[cid] + slot] = i | (((x == lx ? 1 : 0) | (y == ly ? 2 : 0) | (z == lz ? 4 : 0)) << 29);
       }
     }
 }
@@ -119,32 +120,49 @@ __global__ void __launch_bounds__(256) k_bin_scatter(StepArgs a) {
 #define DEM_PAIRS_BUF 64
 #endif
 #ifndef DEM_PAIRS_MINB
-#define DEM_PAIRS_MINB 5
+#define DEM_PAIRS_MINB 4
 #endif
 #ifndef DEM_PAIRS_CONTIG
-#define DEM_PAIRS_CONTIG 64  // bins per run (0: plain grid-stride over bins)
+#define DEM_PAIRS_CONTIG 64  // bins per warp in a CTA span
 #endif
 constexpr int kPairWarps = 8;
 constexpr int kPairBuf = DEM_PAIRS_BUF;
 
-// Shared-memory member of a bin.  Both spheres of a pair overlap the bin C, so their
-// lowest bins satisfy lo <= C on every axis and max(lo_a, lo_b) == C  <=>  on every axis
-// lo_a == C or lo_b == C.  Each member therefore carries a 3-bit mask "C is my lowest bin
-// along axis d" (bits 29..31 of meta.y, the sphere index in bits 0..28), and the pair is
-// kept iff (mask_a | mask_b) == 7.
+// Members of a bin, staged in the warp's shared memory.  Both spheres of a pair overlap the
+// bin C, so their lowest bins satisfy lo <= C on every axis, and max(lo_a, lo_b) == C  <=>
+// on every axis lo_a == C or lo_b == C.  With g = the 3-bit mask "C is my lowest bin along
+// axis d", the pair belongs to C iff (g_a | g_b) == 7: that is how each pair is found in
+// exactly one bin.
+constexpr int kFlatMax = 64;  // bins up to this size: member groups + flat pair enumeration
 struct Members {
-  double4 p[32];  // x, y, z, r
-  int2 meta[32];  // (clump, idx | mask << 29)
+  double4 p[kFlatMax];  // x, y, z, r
+  int2 meta[kFlatMax];  // (clump, sphere index [| g << 29 on the large-bin path])
 };
 
-__device__ __forceinline__ void load_member(const StepArgs& a, Members& M, int slot, int idx, int cx, int cy,
-                                            int cz) {
-  const double4 p = a.spos[idx];
-  M.p[slot] = p;
-  const int mask = (cell_lo(a.grid, 0, p.x, p.w) == cx ? 1 : 0) | (cell_lo(a.grid, 1, p.y, p.w) == cy ? 2 : 0) |
-                   (cell_lo(a.grid, 2, p.z, p.w) == cz ? 4 : 0);
-  M.meta[slot] = make_int2(a.s_clump[idx], idx | (mask << 29));
+__device__ __forceinline__ void load_member(const StepArgs& a, Members& M, int slot, int item) {
+  const int it = a.items[item];
+  const int idx = it & 0x1fffffff;
+  M.p[slot] = a.spos[idx];
+  M.meta[slot] = make_int2(a.s_clump[idx], it);
 }
+
+// Member order of the flat path: groups by g in the order 7, 6, 1, 5, 3, 2, 4, 0 (nibble g of
+// kGroupPos is the position of group g).  The pairs with (g_a | g_b) == 7 are then the five
+// blocks  T: group 7 with itself;  R0: group 7 x every later member;  R1: group 6 x groups
+// {1, 5, 3};  R2: group 5 x groups {3, 2};  R3: group 3 x group 4 — each a triangle or a
+// rectangle of the member order, enumerated without testing any other pair.
+constexpr unsigned kGroupPos = 0x01364527u;
+
+__device__ __forceinline__ unsigned long long warp_incl_scan64(unsigned long long x, int lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned long long t = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= d) x += t;
+  }
+  return x;
+}
+
+__device__ __forceinline__ int byte_of(unsigned long long v, int k) { return (int)((v >> (8 * k)) & 0xffu); }
 
 // p -> (i, j), 0 <= i < j, p = j (j - 1) / 2 + i
 __device__ __forceinline__ void decode_tri(int p, int& i, int& j) {
@@ -195,10 +213,49 @@ __device__ __forceinline__ void flush_pairs(const StepArgs& a, const int2* bf, i
   __syncwarp();
 }
 
+// a warp's hits of one pass: compacted with a ballot into the warp's buffer (flushed when full)
+__device__ __forceinline__ void push_hits(const StepArgs& a, int2* bf, int& nbuf, bool hit, int ia, int ib,
+                                          int lane) {
+  const unsigned mask = __ballot_sync(0xffffffffu, hit);
+  if (mask) {
+    const int cnt = __popc(mask);
+    if (nbuf + cnt > kPairBuf) {
+      flush_pairs(a, bf, nbuf, lane);
+      nbuf = 0;
+    }
+    if (hit) bf[nbuf + __popc(mask & ((1u << lane) - 1u))] = make_int2(ia, ib);
+    nbuf += cnt;
+  }
+}
+
+// candidate predicate (R14): different clumps, at least one owned (ghost-ghost
+// pairs belong to other ranks), |d|^2 <= (r_a + r_b + margin)^2 with explicit roundings
+__device__ __forceinline__ bool candidate(const StepArgs& a, const int2& mi, const int2& mj, const double4& pi,
+                                          const double4& pj) {
+  const double dx = sub(pj.x, pi.x), dy = sub(pj.y, pi.y), dz = sub(pj.z, pi.z);
+  const double d2 = add(add(mul(dx, dx), mul(dy, dy)), mul(dz, dz));
+  const double s = add(add(pi.w, pj.w), a.margin);
+  return mi.x != mj.x && min(mi.x, mj.x) < a.n_own && d2 <= mul(s, s);
+}
+
+constexpr int kTri = kFlatMax * (kFlatMax - 1) / 2;
+// 1/W for the block widths W <= kFlatMax, correctly rounded (constant-folded divisions)
+#define DEM_R8(n) 1.0f / (n), 1.0f / (n + 1), 1.0f / (n + 2), 1.0f / (n + 3), 1.0f / (n + 4), 1.0f / (n + 5), \
+                  1.0f / (n + 6), 1.0f / (n + 7)
+__constant__ float c_rcp[kFlatMax + 8] = {1.0f,      DEM_R8(1),  DEM_R8(9),  DEM_R8(17), DEM_R8(25),
+                                          DEM_R8(33), DEM_R8(41), DEM_R8(49), DEM_R8(57)};
+#undef DEM_R8
+
 __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepArgs a) {
   __shared__ Members smA[kPairWarps];
-  __shared__ Members smB[kPairWarps];
   __shared__ int2 sbuf[kPairWarps][kPairBuf];
+  __shared__ unsigned short tri_ij[kTri];  // p -> i | j << 8 for p = j (j - 1) / 2 + i, i < j
+  for (int p = threadIdx.x; p < kTri; p += blockDim.x) {
+    int i, j;
+    decode_tri(p, i, j);
+    tri_ij[p] = (unsigned short)(i | (j << 8));
+  }
+  __syncthreads();
   if (a.ctl->abort) return;
   if ((long long)a.cell_start[a.ncell] > a.cap_inserts) {
     a.ctl->need_inserts = a.cell_start[a.ncell];
@@ -207,127 +264,152 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
   }
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   Members& A = smA[w];
-  Members& B = smB[w];
   int2* bf = sbuf[w];
   int nbuf = 0;  // warp-uniform
-  const Grid& g = a.grid;
-#if DEM_PAIRS_CONTIG
-  // CTAs take spans of kPairWarps x DEM_PAIRS_CONTIG consecutive bins round-robin and their
-  // warps interleave inside the span: concurrent warps work on adjacent bins (shared L1
-  // lines of multiply-inserted spheres), and a warp's buffered pairs — so the pair list and
-  // the row scatter that follows — stay spatially local
+  // Bin iterator: CTAs take spans of kPairWarps x DEM_PAIRS_CONTIG consecutive bins
+  // round-robin and their warps interleave inside the span, so concurrent warps work on
+  // adjacent bins (shared L1 lines of multiply-inserted spheres) and a warp's buffered pairs
+  // — so the slot writes that follow — stay spatially local.
   constexpr long long kSpan = (long long)kPairWarps * DEM_PAIRS_CONTIG;
-  for (long long cid = (long long)blockIdx.x * kSpan + w, stop = min(a.ncell, (long long)blockIdx.x * kSpan + kSpan);
-       cid < a.ncell;
-       (cid += kPairWarps) >= stop ? (cid += (long long)(gridDim.x - 1) * kSpan, stop = min(a.ncell, stop + (long long)gridDim.x * kSpan)) : 0) {
-#else
-  const long long nw = (long long)gridDim.x * kPairWarps;
-  for (long long cid = (long long)blockIdx.x * kPairWarps + w; cid < a.ncell; cid += nw) {
-#endif
+  const long long ncell = a.ncell;
+  long long it = (long long)blockIdx.x * kSpan + w, it_stop = min(ncell, (long long)blockIdx.x * kSpan + kSpan);
+  auto advance = [&]() {
+    if ((it += kPairWarps) >= it_stop) {
+      it += (long long)(gridDim.x - 1) * kSpan;
+      it_stop = min(ncell, it_stop + (long long)gridDim.x * kSpan);
+    }
+  };
+  for (long long cid = it; cid < ncell; advance(), cid = it) {
     const int k0 = a.cell_start[cid];
     const int m = a.cell_start[cid + 1] - k0;
-    if (m < 2) continue;
-    int cx, cy, cz;
-    decode_bin(g, cid, cx, cy, cz);
-    if (m <= 32) {
-      // Common case: lane l holds member l in registers and publishes it to the warp's shared
-      // slot.  Rotation schedule: in round k (1 <= k <= m/2) lane l tests the pair
-      // (l, l + k mod m), reading the partner from shared memory (the integer tests first,
-      // the coordinates only if they pass); for even m the last round keeps lanes l < m/2
-      // only.  Every unordered pair of the bin is tested exactly once, with all m lanes busy.
-      double4 u = make_double4(0.0, 0.0, 0.0, 0.0);
-      int2 mu = make_int2(-1, 0);
-      __syncwarp();
-      if (lane < m) {
-        const int idx = a.items[k0 + lane];
-        u = a.spos[idx];
-        const int mk = (cell_lo(g, 0, u.x, u.w) == cx ? 1 : 0) | (cell_lo(g, 1, u.y, u.w) == cy ? 2 : 0) |
-                       (cell_lo(g, 2, u.z, u.w) == cz ? 4 : 0);
-        mu = make_int2(a.s_clump[idx], idx | (mk << 29));
-        A.p[lane] = u;
-        A.meta[lane] = mu;
-      }
-      __syncwarp();
-      const bool in = lane < m;
-      const int n_own = a.n_own;
-      const double margin = a.margin;
-      int src = lane < m ? lane : 0;
-      for (int k = 1; 2 * k <= m; ++k) {
-        src = (src + 1 == m) ? 0 : src + 1;  // (lane + k) mod m
-        const int2 mv = A.meta[src];
-        const bool active = in && (2 * k != m || lane < k);
-        bool hit = false;
-        // different clumps, at least one owned (ghost-ghost pairs belong to other ranks), dedupe bin
-        if (active && mu.x != mv.x && min(mu.x, mv.x) < n_own && (((unsigned)(mu.y | mv.y) >> 29) == 7u)) {
-          const double4 v = A.p[src];
-          const double dx = sub(v.x, u.x), dy = sub(v.y, u.y), dz = sub(v.z, u.z);
-          const double d2 = add(add(mul(dx, dx), mul(dy, dy)), mul(dz, dz));
-          const double s = add(add(u.w, v.w), margin);
-          hit = d2 <= mul(s, s);
+    if (m >= 2) {
+      if (m <= kFlatMax) {
+        // Lane l loads members l and l + 32 and stores them at their place in the group order
+        // (a 64-bit warp scan of one-hot byte counters gives every member its rank in its group
+        // and every group its start); then the warp enumerates the pair blocks flat, 32 pairs
+        // per pass, so no lane tests a pair that belongs to another bin.
+        double4 u0 = make_double4(0.0, 0.0, 0.0, 0.0), u1 = u0;
+        int2 mt0 = make_int2(0, 0), mt1 = mt0;
+        int pos0 = 0, pos1 = 0;
+        unsigned long long v0 = 0, v1 = 0;
+        if (lane < m) {
+          const int it = a.items[k0 + lane];
+          const int idx = it & 0x1fffffff;
+          u0 = a.spos[idx];
+          mt0 = make_int2(a.s_clump[idx], idx);
+          pos0 = (kGroupPos >> (4 * ((unsigned)it >> 29))) & 7;
+          v0 = 1ull << (8 * pos0);
         }
-        const unsigned mask = __ballot_sync(0xffffffffu, hit);
-        if (mask) {
-          const int cnt = __popc(mask);
-          if (nbuf + cnt > kPairBuf) {
-            flush_pairs(a, bf, nbuf, lane);
-            nbuf = 0;
-          }
-          if (hit)
-            bf[nbuf + __popc(mask & ((1u << lane) - 1u))] = make_int2(mu.y & 0x1fffffff, mv.y & 0x1fffffff);
-          nbuf += cnt;
+        if (lane + 32 < m) {
+          const int it = a.items[k0 + 32 + lane];
+          const int idx = it & 0x1fffffff;
+          u1 = a.spos[idx];
+          mt1 = make_int2(a.s_clump[idx], idx);
+          pos1 = (kGroupPos >> (4 * ((unsigned)it >> 29))) & 7;
+          v1 = 1ull << (8 * pos1);
         }
-      }
-      continue;
-    }
-    // Large bins (m > 32): blocks of 32 members staged in shared memory, pairs by index decode.
-    for (int ib = 0; ib < m; ib += 32) {
-      const int mi = min(32, m - ib);
-      __syncwarp();
-      if (lane < mi) load_member(a, A, lane, a.items[k0 + ib + lane], cx, cy, cz);
-      for (int jb = ib; jb < m; jb += 32) {
-        const int mj = min(32, m - jb);
-        const bool same = jb == ib;
-        const Members& Bp = same ? A : B;
-        if (!same) {
-          __syncwarp();
-          if (lane < mj) load_member(a, B, lane, a.items[k0 + jb + lane], cx, cy, cz);
+        const unsigned long long x0 = warp_incl_scan64(v0, lane);
+        const unsigned long long t0 = __shfl_sync(0xffffffffu, x0, 31);
+        unsigned long long x1 = 0, t1 = 0;
+        if (m > 32) {  // warp-uniform
+          x1 = warp_incl_scan64(v1, lane);
+          t1 = __shfl_sync(0xffffffffu, x1, 31);
+        }
+        const unsigned long long tot = t0 + t1;                          // byte k: size of group at position k
+        const unsigned long long st = (tot << 8) * 0x0101010101010101ull;  // byte k: start of position k
+        __syncwarp();
+        if (lane < m) {
+          const int q = byte_of(st, pos0) + byte_of(x0 - v0, pos0);
+          A.p[q] = u0;
+          A.meta[q] = mt0;
+        }
+        if (lane + 32 < m) {
+          const int q = byte_of(st, pos1) + byte_of(t0, pos1) + byte_of(x1 - v1, pos1);
+          A.p[q] = u1;
+          A.meta[q] = mt1;
         }
         __syncwarp();
-        const int np = same ? mi * (mi - 1) / 2 : mi * mj;
-        for (int base = 0; base < np; base += 32) {
+        const int n7 = byte_of(tot, 0), n6 = byte_of(tot, 1), n5 = byte_of(tot, 3), n3 = byte_of(tot, 4),
+                  n4 = byte_of(tot, 6);
+        const int s6 = byte_of(st, 1), s1 = byte_of(st, 2), s5 = byte_of(st, 3), s3 = byte_of(st, 4),
+                  s2 = byte_of(st, 5), s4 = byte_of(st, 6);
+        // blocks after T: pair = (A0 + q % W, B0 + q / W)
+        const int tri = n7 * (n7 - 1) / 2;
+        const int W1 = s2 - s1, W2 = s4 - s3;
+        const int e0 = tri + n7 * (m - n7);
+        const int e1 = e0 + n6 * W1;
+        const int e2 = e1 + n5 * W2;
+        const int total = e2 + n3 * n4;
+        // correctly rounded reciprocals of the block widths: q < 64 * 64, so (q + 1/2) / W,
+        // which is at least 1/(2W) away from an integer, truncates right
+        const float r0 = c_rcp[n7], r1 = c_rcp[W1], r2 = c_rcp[W2], r3 = c_rcp[n4];
+        for (int base = 0; base < total; base += 32) {
           const int p = base + lane;
           bool hit = false;
-          int ia = 0, ibx = 0;
-          if (p < np) {
+          int ia = 0, ib = 0;
+          if (p < total) {
             int i, j;
-            if (same) {
-              decode_tri(p, i, j);
+            if (p < tri) {
+              const int v = tri_ij[p];
+              i = v & 0xff;
+              j = v >> 8;
             } else {
-              i = p / mj;
-              j = p - i * mj;
+              const bool b1 = p >= e0, b2 = p >= e1, b3 = p >= e2;
+              const int q = p - (b3 ? e2 : b2 ? e1 : b1 ? e0 : tri);
+              const int W = b3 ? n4 : b2 ? W2 : b1 ? W1 : n7;
+              const float rw = b3 ? r3 : b2 ? r2 : b1 ? r1 : r0;
+              const int A0 = b3 ? s4 : b2 ? s3 : b1 ? s1 : 0;
+              const int B0 = b3 ? s3 : b2 ? s5 : b1 ? s6 : n7;
+              const int r = __float2int_rz(((float)q + 0.5f) * rw);
+              i = A0 + (q - r * W);
+              j = B0 + r;
             }
-            const int2 mu = A.meta[i];
-            const int2 mv = Bp.meta[j];
-            if (mu.x != mv.x && min(mu.x, mv.x) < a.n_own && (((unsigned)(mu.y | mv.y) >> 29) == 7u)) {
-              const double4 u = A.p[i];
-              const double4 v = Bp.p[j];
-              const double dx = sub(v.x, u.x), dy = sub(v.y, u.y), dz = sub(v.z, u.z);
-              const double d2 = add(add(mul(dx, dx), mul(dy, dy)), mul(dz, dz));
-              const double s = add(add(u.w, v.w), a.margin);
-              hit = d2 <= mul(s, s);
-              ia = mu.y & 0x1fffffff;
-              ibx = mv.y & 0x1fffffff;
-            }
+            const int2 mi = A.meta[i], mj = A.meta[j];
+            hit = candidate(a, mi, mj, A.p[i], A.p[j]);
+            ia = mi.y;
+            ib = mj.y;
           }
-          const unsigned mask = __ballot_sync(0xffffffffu, hit);
-          if (mask) {
-            const int cnt = __popc(mask);
-            if (nbuf + cnt > kPairBuf) {
-              flush_pairs(a, bf, nbuf, lane);
-              nbuf = 0;
+          push_hits(a, bf, nbuf, hit, ia, ib, lane);
+        }
+      } else {
+        // Large bins (m > kFlatMax): blocks of 32 members in the two halves of the shared slots,
+        // every pair of the bin tested (the group filter applied per pair).
+        for (int ib = 0; ib < m; ib += 32) {
+          const int mi = min(32, m - ib);
+          __syncwarp();
+          if (lane < mi) load_member(a, A, lane, k0 + ib + lane);
+          for (int jb = ib; jb < m; jb += 32) {
+            const int mj = min(32, m - jb);
+            const bool same = jb == ib;
+            const int ob = same ? 0 : 32;  // slots of the second block
+            if (!same) {
+              __syncwarp();
+              if (lane < mj) load_member(a, A, 32 + lane, k0 + jb + lane);
             }
-            if (hit) bf[nbuf + __popc(mask & ((1u << lane) - 1u))] = make_int2(ia, ibx);
-            nbuf += cnt;
+            __syncwarp();
+            const int np = same ? mi * (mi - 1) / 2 : mi * mj;
+            for (int base = 0; base < np; base += 32) {
+              const int p = base + lane;
+              bool hit = false;
+              int ia = 0, ibx = 0;
+              if (p < np) {
+                int i, j;
+                if (same) {
+                  decode_tri(p, i, j);
+                } else {
+                  i = p / mj;
+                  j = p - i * mj;
+                }
+                const int2 mu = A.meta[i];
+                const int2 mv = A.meta[ob + j];
+                if (((unsigned)(mu.y | mv.y) >> 29) == 7u) {
+                  hit = candidate(a, mu, mv, A.p[i], A.p[ob + j]);
+                  ia = mu.y & 0x1fffffff;
+                  ibx = mv.y & 0x1fffffff;
+                }
+              }
+              push_hits(a, bf, nbuf, hit, ia, ibx, lane);
+            }
           }
         }
       }

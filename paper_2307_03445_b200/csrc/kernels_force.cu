@@ -26,16 +26,19 @@
 namespace dem {
 
 constexpr int kPairStride = 8;  // doubles per material pair in Tables::pair
-constexpr int kFC = 32;     // max clumps per CTA (host partition, see system.cu)
-constexpr int kMaxS = 160;  // max spheres per CTA
-constexpr int kFT = 128;    // threads per CTA (= entries per chunk)
+#ifndef DEM_FORCE_FT
+#define DEM_FORCE_FT 128
+#endif
+constexpr int kFT = DEM_FORCE_FT;   // threads per CTA (= entries per chunk)
+constexpr int kFC = kFT / 4;        // max clumps per CTA (host partition, see system.cu)
+constexpr int kMaxS = kFT * 5 / 4;  // max spheres per CTA
 int force_cta_clumps() { return kFC; }
 int force_cta_spheres() { return kMaxS; }
 
 // One CTA = a run of whole clumps [c0, c1) and their spheres [s0, s0 + nsph), whose rows are
 // one contiguous CSR range [E0, E1).
 #ifndef DEM_FORCE_MINB
-#define DEM_FORCE_MINB 8
+#define DEM_FORCE_MINB (1024 / DEM_FORCE_FT)  // 64 registers
 #endif
 __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArgs a) {
   __shared__ int rp[kMaxS + 1];
