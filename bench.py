@@ -92,7 +92,9 @@ def stage_bytes(st):
         "pose+bin_count": n * 188 + ns * 44 + nc * 8,
         "bin_scan": nc * 8,
         "bin_scatter": ns * 32 + nc * 12 + ins * 4,
-        "pairs": nc * 4 + ins * 40 + pairs * 8,
+        # bin bounds, items, each member record (x, y, z, r, clump) once, 2 candidate slots +
+        # 2 row-count atomics (read + write) per pair
+        "pairs": nc * 4 + ins * 4 + ns * 36 + pairs * 24,
         "row_scan": ns * 8,
         "rows_finish": ns * 40 + ent * 32 + pairs * 2 * 12,
         "force+integrate": ns * (32 + 8 + 8) + n * (80 + 56 + 4 + 104) + ent * 72,
@@ -162,7 +164,7 @@ def run_reference(a):
     sample = f"{crop.n_clumps} clumps / {crop.n_spheres} spheres: 30x30 mm full-depth column of {scene.name}"
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
-        "warmup": a.warmup, "ms_per_step": dt / a.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "warmup": a.warmup, "ms_per_step": dt / a.steps * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": scene.name, "sample": sample, "parallelism": "cpu-1thread"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
