@@ -107,6 +107,7 @@ struct StepArgs {
   const int* sph_off;
   const int* s_clump;
   const int* s_tc;
+  const int* s_mat;          // material of each sphere (tc_mat[s_tc])
   const long long* s_key;
   double4* spos;             // sphere (x, y, z, r), written by the pose kernel each step
   double* kin;               // per clump [kKin]: X(3), V(3), omega_world(3), mass

@@ -29,9 +29,15 @@ constexpr int kPairStride = 8;  // doubles per material pair in Tables::pair
 #ifndef DEM_FORCE_FT
 #define DEM_FORCE_FT 128
 #endif
-constexpr int kFT = DEM_FORCE_FT;   // threads per CTA (= entries per chunk)
-constexpr int kFC = kFT / 4;        // max clumps per CTA (host partition, see system.cu)
-constexpr int kMaxS = kFT * 5 / 4;  // max spheres per CTA
+#ifndef DEM_FORCE_FC
+#define DEM_FORCE_FC (DEM_FORCE_FT / 4)
+#endif
+#ifndef DEM_FORCE_MAXS
+#define DEM_FORCE_MAXS (DEM_FORCE_FT * 5 / 4)
+#endif
+constexpr int kFT = DEM_FORCE_FT;      // threads per CTA (= entries per chunk)
+constexpr int kFC = DEM_FORCE_FC;      // max clumps per CTA (host partition, see system.cu)
+constexpr int kMaxS = DEM_FORCE_MAXS;  // max spheres per CTA
 int force_cta_clumps() { return kFC; }
 int force_cta_spheres() { return kMaxS; }
 
@@ -45,7 +51,7 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
   __shared__ double4 own_p[kMaxS];
   __shared__ int own_mat[kMaxS];
   __shared__ int own_lc[kMaxS];
-  __shared__ double ck[kFC][kKin];
+  __shared__ __align__(16) double ck[kFC * kKin];
   __shared__ double part[6][kFT];
   __shared__ double acc[6][kMaxS];
   const int tid = threadIdx.x;
@@ -72,12 +78,15 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
   for (int ls = tid; ls < nsph; ls += kFT) {
     const int i = s0 + ls;
     own_p[ls] = a.spos[i];
-    own_mat[ls] = a.tab.tc_mat[a.s_tc[i]];
+    own_mat[ls] = a.s_mat[i];
     own_lc[ls] = a.s_clump[i] - c0;
 #pragma unroll
     for (int q = 0; q < 6; ++q) acc[q][ls] = 0.0;
   }
-  for (int k = tid; k < ncl * kKin; k += kFT) ck[k / kKin][k % kKin] = a.kin[(size_t)kKin * c0 + k];
+  {
+    const double2* src = reinterpret_cast<const double2*>(a.kin + (size_t)kKin * c0);
+    for (int k = tid; k < ncl * (kKin / 2); k += kFT) reinterpret_cast<double2*>(ck)[k] = src[k];
+  }
   __syncthreads();
   const double h = a.h;
   const int E0 = rp[0], E1 = rp[nsph];
@@ -93,7 +102,7 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
       const int ls = lo;
       const double4 own = own_p[ls];
       const double cx = own.x, cy = own.y, cz = own.z, ri = own.w;
-      const double* ki = ck[own_lc[ls]];
+      const double* ki = ck + kKin * own_lc[ls];
       const double Xx = ki[0], Xy = ki[1], Xz = ki[2];
       const double Mi = ki[9];
       const Entry ent = a.rows.ent[e];
@@ -119,7 +128,7 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
       if (!wall) {
         const double4 pj = a.spos[t];
         const double2* kj = reinterpret_cast<const double2*>(a.kin + (size_t)kKin * a.s_clump[t]);
-        mj = a.tab.tc_mat[a.s_tc[t]];
+        mj = a.s_mat[t];
         const double rj = pj.w;
         const double dx = pj.x - cx, dy = pj.y - cy, dz = pj.z - cz;
         const double dist = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
@@ -244,7 +253,8 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
   // Omega += h I^-1 (tau - Omega x I Omega); q <- normalize(q (x) exp(h Omega)).
   const int c = c0 + tid;
   const int t = a.tid[c];
-  const double M = ck[tid][9];
+  const double* kc = ck + kKin * tid;  // this clump's X, V, omega_world, M
+  const double M = kc[9];
   const double I0 = a.tab.tpl_inertia[3 * t], I1 = a.tab.tpl_inertia[3 * t + 1], I2 = a.tab.tpl_inertia[3 * t + 2];
   double Fx = 0.0, Fy = 0.0, Fz = 0.0, Tx = 0.0, Ty = 0.0, Tz = 0.0;
   for (int s = a.sph_off[c] - s0, e = a.sph_off[c + 1] - s0; s < e; ++s) {
@@ -263,9 +273,9 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
   if (!isfinite(Fx) || !isfinite(Fy) || !isfinite(Fz) || !isfinite(tbx) || !isfinite(tby) || !isfinite(tbz)) {
     raise_error(a.ctl, -11, a.gid[c], 0);
   }
-  const double vx = ck[tid][3] + h * (Fx / M), vy = ck[tid][4] + h * (Fy / M), vz = ck[tid][5] + h * (Fz / M);
+  const double vx = kc[3] + h * (Fx / M), vy = kc[4] + h * (Fy / M), vz = kc[5] + h * (Fz / M);
   a.nxt.vx[c] = vx; a.nxt.vy[c] = vy; a.nxt.vz[c] = vz;
-  const double nxx = ck[tid][0] + h * vx, nxy = ck[tid][1] + h * vy, nxz = ck[tid][2] + h * vz;
+  const double nxx = kc[0] + h * vx, nxy = kc[1] + h * vy, nxz = kc[2] + h * vz;
   a.nxt.x[c] = nxx;
   a.nxt.y[c] = nxy;
   a.nxt.z[c] = nxz;

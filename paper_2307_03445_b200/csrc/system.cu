@@ -70,7 +70,7 @@ struct dem_system {
   int *d_tid = nullptr, *d_sph_off = nullptr;
   double* d_state[2] = {nullptr, nullptr};
   double* d_kin = nullptr;
-  int *d_s_clump = nullptr, *d_s_tc = nullptr;
+  int *d_s_clump = nullptr, *d_s_tc = nullptr, *d_s_mat = nullptr;
   long long* d_s_key = nullptr;
   double4* d_spos = nullptr;
   int2* d_cta_clump = nullptr;  // per CTA boundary: (first clump, first sphere)
@@ -226,6 +226,7 @@ static StepArgs make_args(dem_system* sys, bool rebuild) {
   a.kin = sys->d_kin;
   a.s_clump = sys->d_s_clump;
   a.s_tc = sys->d_s_tc;
+  a.s_mat = sys->d_s_mat;
   a.s_key = sys->d_s_key;
   a.spos = sys->d_spos;
   a.slots = sys->d_slots;
@@ -773,6 +774,7 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
   TRY(alloc_arr(sys, &sys->d_kin, (size_t)kKin * n));
   TRY(alloc_arr(sys, &sys->d_s_clump, ns));
   TRY(alloc_arr(sys, &sys->d_s_tc, ns));
+  TRY(alloc_arr(sys, &sys->d_s_mat, ns));
   TRY(alloc_arr(sys, &sys->d_s_key, ns));
   TRY(alloc_arr(sys, &sys->d_spos, ns));
   TRY(alloc_arr(sys, &sys->d_spos_ref, ns));
@@ -848,6 +850,9 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
   CK(cudaMemcpyAsync(sys->d_state[0], st.data(), sizeof(double) * 13 * n, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(sys->d_s_clump, s_clump.data(), sizeof(int) * ns, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(sys->d_s_tc, sys->h_s_tc.data(), sizeof(int) * ns, cudaMemcpyHostToDevice, s));
+  std::vector<int> s_mat(ns);
+  for (int64_t k = 0; k < ns; ++k) s_mat[k] = sys->tc_mat[sys->h_s_tc[k]];
+  CK(cudaMemcpyAsync(sys->d_s_mat, s_mat.data(), sizeof(int) * ns, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(sys->d_s_key, sys->h_s_key.data(), sizeof(long long) * ns, cudaMemcpyHostToDevice, s));
   CK(cudaMemsetAsync(sys->d_cell_count, 0, sizeof(int) * ncell, s));
   for (int p = 0; p < 2; ++p) CK(cudaMemsetAsync(sys->rows[p].row_ptr, 0, sizeof(int) * (ns + 1), s));
