@@ -47,6 +47,7 @@ def lib():
         L.orc_set_history.argtypes = [P, I64, P, P, P]
         L.orc_step.argtypes = [P, I64]
         L.orc_set_cd_every.argtypes = [P, C.c_int]
+        L.orc_set_overlap.argtypes = [P, C.c_int]
         L.orc_num_contacts.restype = I64
         L.orc_num_contacts.argtypes = [P]
         L.orc_steps_done.restype = I64
@@ -77,7 +78,8 @@ class OracleError(RuntimeError):
 class Oracle:
     """One oracle system built from a `workloads.Scene`."""
 
-    def __init__(self, scene, detect: int = -1, margin: float | None = None, cd_every: int = 1):
+    def __init__(self, scene, detect: int = -1, margin: float | None = None, cd_every: int = 1,
+                 overlap: bool = False):
         L = lib()
         ncomp, offs, rad, mat, mass, inertia = scene.template_arrays()
         pts, nrm, pmat = scene.plane_arrays()
@@ -95,6 +97,8 @@ class Oracle:
         self.set_state(scene.gid, scene.tid, scene.pos, scene.quat, scene.vel, scene.omega)
         if cd_every != 1:
             self._check(L.orc_set_cd_every(self.sys, int(cd_every)))
+        if overlap:  # next window's set detected one window ahead
+            self._check(L.orc_set_overlap(self.sys, 1))
 
     def __del__(self):
         if getattr(self, "sys", None):

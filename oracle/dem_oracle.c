@@ -47,6 +47,9 @@ struct orc_sys {
   int32_t* pmat;
   int detect;
   int cd_every, since_rebuild; /* contact-set rebuild cadence */
+  int overlap;                 /* detection one window ahead, "in the shadow" of the dynamics */
+  int64_t n_pend;              /* -1: no set pending; else the size of the set built for the next window */
+  contact* pend;
   /* clump state */
   int64_t n;
   int64_t* gid;
@@ -239,6 +242,7 @@ orc_sys* orc_create(double h, const double gravity[3], double margin, const doub
   s->detect = detect;
   s->cd_every = 1;
   s->since_rebuild = 0;
+  s->n_pend = -1;
   return s;
 }
 
@@ -256,7 +260,7 @@ void orc_destroy(orc_sys* s) {
   free_state(s);
   free(s->mat); free(s->ncomp); free(s->coff); free(s->offs); free(s->rad); free(s->cmat);
   free(s->mass); free(s->inertia); free(s->ppt); free(s->pn); free(s->pmat);
-  free(s->hist); free(s->con);
+  free(s->hist); free(s->con); free(s->pend);
   free(s);
 }
 
@@ -307,6 +311,7 @@ int orc_set_state(orc_sys* s, int64_t n, const int64_t* gid, const int32_t* tid,
   s->nh = 0;
   s->nc = 0;
   s->since_rebuild = 0;
+  s->n_pend = -1;
   return ORC_OK;
 }
 
@@ -316,6 +321,19 @@ int orc_set_cd_every(orc_sys* s, int k) {
   if (k < 1) return ORC_ERR_ARG;
   s->cd_every = k;
   s->since_rebuild = 0;
+  s->n_pend = -1;
+  return ORC_OK;
+}
+
+/* overlapped detection ("in the shadow"; NEXT-2): with k >= 2 the set for the next
+ * window is detected from the sphere positions of the second step of the current window and
+ * adopted at the next window start, so the detection can run concurrently with the k - 1
+ * force steps in between.  The margin must then cover 2k - 2 steps of motion. */
+int orc_set_overlap(orc_sys* s, int on) {
+  if (on && s->cd_every < 2) return ORC_ERR_ARG;
+  s->overlap = on ? 1 : 0;
+  s->since_rebuild = 0;
+  s->n_pend = -1;
   return ORC_OK;
 }
 
@@ -351,6 +369,7 @@ int orc_set_history(orc_sys* s, int64_t n, const int64_t* ka, const int64_t* kb,
   qsort(s->hist, n, sizeof(hist_rec), cmp_hist);
   s->nh = n;
   s->since_rebuild = 0; /* a new history is read by a rebuild */
+  s->n_pend = -1;
   return ORC_OK;
 }
 
@@ -501,6 +520,18 @@ static int cmp_entry(const void* A, const void* B) {
   return 0;
 }
 
+/* the candidate set of the current sphere positions, sorted by (key_a, key_b) */
+static void detect_set(orc_sys* s) {
+  s->nc = 0;
+  int brute = s->detect == 0 || (s->detect < 0 && s->ns <= 10000);
+  if (brute)
+    detect_brute(s);
+  else
+    detect_grid(s);
+  detect_planes(s);
+  qsort(s->con, s->nc, sizeof(contact), cmp_contact);
+}
+
 /* ------------------------------------------------------------------ the step */
 static int one_step(orc_sys* s) {
   int64_t a, c, k;
@@ -527,14 +558,29 @@ static int one_step(orc_sys* s) {
    * (P:142); cd_every = 1 is the "traditional way".  In between, the same set is
    * used and every member is re-evaluated at each step. */
   if (s->since_rebuild == 0) {
+    if (s->overlap && s->n_pend >= 0) { /* adopt the set detected during the last window */
+      free(s->con);
+      s->con = s->pend;
+      s->nc = s->cap = s->n_pend;
+      s->pend = NULL;
+      s->n_pend = -1;
+    } else {
+      detect_set(s);
+    }
+  } else if (s->overlap && s->since_rebuild == 1) {
+    /* detect the next window's set from this step's positions, keep the current one */
+    contact* cur = s->con;
+    int64_t nc = s->nc, cap = s->cap;
+    s->con = NULL;
     s->nc = 0;
-    int brute = s->detect == 0 || (s->detect < 0 && s->ns <= 10000);
-    if (brute)
-      detect_brute(s);
-    else
-      detect_grid(s);
-    detect_planes(s);
-    qsort(s->con, s->nc, sizeof(contact), cmp_contact);
+    s->cap = 0;
+    detect_set(s);
+    free(s->pend);
+    s->pend = s->con;
+    s->n_pend = s->nc;
+    s->con = cur;
+    s->nc = nc;
+    s->cap = cap;
   }
   s->since_rebuild = (s->since_rebuild + 1) % s->cd_every;
   /* (3) history carried for surviving keys, zero at birth */

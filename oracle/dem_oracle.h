@@ -46,6 +46,7 @@ int orc_set_history(orc_sys*, int64_t n, const int64_t* ka, const int64_t* kb, c
 int orc_step(orc_sys*, int64_t n_steps);
 /* rebuild the contact set every k steps (margin set at creation), counted from the next step */
 int orc_set_cd_every(orc_sys*, int k);
+int orc_set_overlap(orc_sys*, int on);
 int64_t orc_num_contacts(const orc_sys*);
 /* contacts of the last step (set built from the state at that step's start), sorted by (ka,kb):
  * force on b, contact point, normal a->b, tangential history after the step, penetration. */

@@ -57,3 +57,62 @@ def test_too_small_margin_misses_contacts():
     d = oracle.Oracle(s, detect=1, margin=0.0, cd_every=30)
     d.step(60)
     assert not np.array_equal(ref.state()["vel"], d.state()["vel"])
+
+
+# ---------------------------------------------------------------- NEXT-2: overlapped detection
+# The set of window w+1 is detected from the sphere positions of the second step of window w
+# (contact detection "in the shadow" of the dynamics), so it must stay complete over
+# 2k - 2 steps of motion instead of k.
+
+def _fast(scale=20.0):
+    s = _evolved()
+    s.vel *= scale  # relative motion large enough that the detection lag matters
+    return s, float(np.abs(s.vel).max() * np.sqrt(3.0))
+
+
+def test_overlap_equals_per_step_rebuild():
+    s, vmax = _fast()
+    k = 10
+    ref = oracle.Oracle(s, detect=1)
+    ref.step(60)
+    d = oracle.Oracle(s, detect=1, margin=2.0 * vmax * s.h * (2 * k - 2), cd_every=k, overlap=True)
+    d.step(60)
+    a, b = ref.state(), d.state()
+    for key in ("pos", "quat", "vel", "omega"):
+        assert np.array_equal(a[key], b[key]), key
+
+
+def test_overlap_lag_needs_the_larger_margin():
+    """The margin of the sequential cadence (k steps of motion) suffices without overlap but
+    not with it: the set adopted at a window start is k - 1 steps older."""
+    s, vmax = _fast()
+    k = 10
+    ref = oracle.Oracle(s, detect=1)
+    ref.step(60)
+    seq = oracle.Oracle(s, detect=1, margin=2.0 * vmax * s.h * k, cd_every=k)
+    seq.step(60)
+    ovl = oracle.Oracle(s, detect=1, margin=2.0 * vmax * s.h * k, cd_every=k, overlap=True)
+    ovl.step(60)
+    assert np.array_equal(ref.state()["vel"], seq.state()["vel"])
+    assert not np.array_equal(ref.state()["vel"], ovl.state()["vel"])
+
+
+def test_overlap_set_is_the_snapshot_set():
+    """Mid-window 1 the set in use is exactly the candidate set of the positions at the second
+    step of window 0 (independent numpy brute force on the state after one step)."""
+    from test_oracle_pins import _numpy_pairs
+
+    s, vmax = _fast(5.0)
+    k = 10
+    margin = 2.0 * vmax * s.h * (2 * k - 2)
+    d = oracle.Oracle(s, detect=1, margin=margin, cd_every=k, overlap=True)
+    d.step(k + 3)
+    c = d.contacts()
+    got = list(zip(c["key_a"].tolist(), c["key_b"].tolist()))
+    one = oracle.Oracle(s, detect=1)
+    one.step(1)  # the state at the start of step 1 = the snapshot
+    snap = s.copy()
+    st = one.state()
+    snap.pos, snap.quat = st["pos"], st["quat"]
+    want = [(int(a), int(b)) for a, b in _numpy_pairs(snap, margin)]
+    assert len(want) > 100 and got == want
