@@ -117,6 +117,15 @@ typedef struct {
   double slab_lo, slab_hi, halo, drift_max;
   int32_t transport;         /* DEM_TRANSPORT_NCCL or DEM_TRANSPORT_LOOPBACK */
   unsigned char nccl_id[128];/* ncclUniqueId from dem_nccl_unique_id on rank 0, broadcast by the caller */
+  /* Overlapped detection cadence (the active set is updated "in the shadow" of the
+   * dynamics; P:148 one GPU shares the two threads via CUDA streams).  With overlap = 1 and
+   * cd_every = k >= 2, the set used in window w+1 (steps (w+1)k .. (w+1)k + k-1) is detected from
+   * the sphere centres at step wk + 1, on a second stream, while the force steps of window w
+   * run; the first window detects in line.  The margin must cover 2k - 2 steps of motion
+   * (2 v_max h (2k - 2) x safety).  A sphere that moves more than margin/2 from the centres its
+   * set was detected from raises DEM_ERR_VMAX.  overlap = 0: detection in line at the window
+   * start.  Requires cd_every >= 2 (else DEM_ERR_INVALID_ARG). */
+  int32_t overlap;
 } dem_params;
 
 enum { DEM_TRANSPORT_NCCL = 0, DEM_TRANSPORT_LOOPBACK = 1 };

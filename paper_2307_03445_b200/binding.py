@@ -44,7 +44,7 @@ class dem_params(C.Structure):
                 ("record_contacts", C.c_int32), ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_ctx", C.c_void_p),
                 ("entries_per_sphere", C.c_double), ("rank", C.c_int32), ("n_ranks", C.c_int32),
                 ("slab_lo", C.c_double), ("slab_hi", C.c_double), ("halo", C.c_double), ("drift_max", C.c_double),
-                ("transport", C.c_int32), ("nccl_id", C.c_ubyte * 128)]
+                ("transport", C.c_int32), ("nccl_id", C.c_ubyte * 128), ("overlap", C.c_int32)]
 
 
 class dem_stats(C.Structure):
@@ -122,7 +122,7 @@ class System:
 
     def __init__(self, materials, templates, planes=(), *, h, gravity=(0.0, 0.0, -9.81), domain_lo, domain_hi,
                  margin=0.0, cell_size=0.0, record_contacts=False, use_torch_allocator=True, stream=None,
-                 entries_per_sphere=0.0, dist=None, cd_every=1):
+                 entries_per_sphere=0.0, dist=None, cd_every=1, overlap=False):
         """dist (optional): dict(rank, n_ranks, slab_lo, slab_hi, halo, drift_max, transport, nccl_id) —
         the slab decomposition of dem_params (include/dem.h); nccl_id from nccl_unique_id() on rank 0."""
         import torch  # plumbing only: device memory and streams
@@ -156,6 +156,7 @@ class System:
         p.gravity[:] = [float(x) for x in gravity]
         p.margin = margin
         p.cd_every = int(cd_every)
+        p.overlap = 1 if overlap else 0  # next window's set detected on a second stream
         p.domain_lo[:] = [float(x) for x in domain_lo]
         p.domain_hi[:] = [float(x) for x in domain_hi]
         p.cell_size = cell_size

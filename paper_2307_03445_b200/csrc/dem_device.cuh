@@ -34,6 +34,8 @@ struct Ctl {
   long long need_inserts;
   long long need_entries;
   long long need_width;  // row-slot width a rebuild needed (fixed-width candidate rows)
+  int det_abort;         // capacity overflow of a set detected ahead (overlapped cadence)
+  int pad_;
 };
 
 constexpr int kUt = 4;    // doubles per entry of the tangential history (padded)
@@ -113,8 +115,13 @@ struct StepArgs {
   double* kin;               // per clump [kKin]: X(3), V(3), omega_world(3), mass
   const int2* cta_clump;     // [n_cta + 1] (first clump, first sphere) of the fused force/integrate CTAs
   int n_cta;
-  int rebuild;               // 1: this step rebuilds the contact set; 0: re-evaluates rows
-  double4* spos_ref;         // sphere centres at the last rebuild
+  int count;                 // pose kernel: bin counts + wall row counts for a detection
+  int remap;                 // force kernel: a new set is adopted this step, u_t via Entry::prev
+  int adopt;                 // pose kernel: adopting a set detected ahead (turns det_abort into abort)
+  const double4* ref_in;     // sphere centres the set in use was detected from (displacement check) or null
+  double4* ref_out;          // where a counting pose kernel stores the centres it detects from, or null
+  const double4* dpos;       // sphere centres the detection kernels read (spos, or the ahead snapshot)
+  int* abort;                // abort word of the detection kernels (&ctl->abort, or &ctl->det_abort)
   double half_margin;        // > 0 (cd_every > 1): displacement allowed since the last rebuild
   int n_own, ns_own;         // owned clumps / spheres come first; the rest are ghosts (§8e)
   const double* xref;        // [3 n_own] owned COMs at dem_set_state (distributed drift check)

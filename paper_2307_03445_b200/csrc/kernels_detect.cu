@@ -27,6 +27,11 @@ namespace dem {
 
 // ---------------------------------------------------------------- (a1) + bin count
 __global__ void __launch_bounds__(256) k_pose_count(StepArgs a) {
+  if (a.adopt && blockIdx.x == 0 && threadIdx.x == 0 && a.ctl->det_abort) {
+    // the set detected ahead overflowed a capacity: abort this adoption step, the host regrows
+    // and rebuilds the set at this step instead (same trajectory: DESIGN.md §5.2)
+    atomicExch(&a.ctl->abort, 1);
+  }
   if (a.ctl->abort) return;
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.ns) return;
@@ -58,15 +63,15 @@ __global__ void __launch_bounds__(256) k_pose_count(StepArgs a) {
     raise_error(a.ctl, -10, a.s_key[i], a.gid[c]);
     return;
   }
-  if (!a.rebuild) {
+  if (a.ref_in) {
     // the deferred set stays complete while no sphere has moved more than margin/2 since it
     // was built ("v_max violated"): otherwise report it instead of missing contacts
-    const double4 q = a.spos_ref[i];
+    const double4 q = a.ref_in[i];
     const double dx = cx - q.x, dy = cy - q.y, dz = cz - q.z;
     if (dx * dx + dy * dy + dz * dz > a.half_margin * a.half_margin) raise_error(a.ctl, -13, a.s_key[i], a.gid[c]);
-    return;
   }
-  if (a.half_margin > 0.0) a.spos_ref[i] = make_double4(cx, cy, cz, r);
+  if (!a.count) return;
+  if (a.ref_out) a.ref_out[i] = make_double4(cx, cy, cz, r);
   // sphere-plane candidates: (r + margin) - (c - p_w).n_w >= 0
   int walls = 0;
   for (int p = 0; p < a.tab.n_planes; ++p) {
@@ -91,11 +96,11 @@ __global__ void __launch_bounds__(256) k_pose_count(StepArgs a) {
 // Slots are taken by decrementing the counts, which leaves cell_count all-zero for the
 // next step.  The order inside a bin is irrelevant: rows are sorted by partner key.
 __global__ void __launch_bounds__(256) k_bin_scatter(StepArgs a) {
-  if (a.ctl->abort) return;
+  if (*a.abort || a.ctl->abort) return;  // (an error in the steps running beside an ahead detection)
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.ns) return;
   const bool fits = (long long)a.cell_start[a.ncell] <= a.cap_inserts;
-  const double4 s = a.spos[i];
+  const double4 s = a.dpos[i];
   const Grid& g = a.grid;
   int lx, hx, ly, hy, lz, hz;
   cell_range(g, 0, s.x, s.w, lx, hx);
@@ -142,7 +147,7 @@ struct Members {
 __device__ __forceinline__ void load_member(const StepArgs& a, Members& M, int slot, int item) {
   const int it = a.items[item];
   const int idx = it & 0x1fffffff;
-  M.p[slot] = a.spos[idx];
+  M.p[slot] = a.dpos[idx];
   M.meta[slot] = make_int2(a.s_clump[idx], it);
 }
 
@@ -181,7 +186,7 @@ __device__ __forceinline__ void put_slot(const StepArgs& a, int own, int slot, i
     a.slots[(size_t)slot * a.ns_own + own] = t;  // slot-major: k_rows_finish reads coalesced
   } else {
     atomicMax(&a.ctl->need_width, (long long)slot + 1);
-    atomicExch(&a.ctl->abort, 1);
+    atomicExch(a.abort, 1);
   }
 }
 
@@ -256,10 +261,10 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
     tri_ij[p] = (unsigned short)(i | (j << 8));
   }
   __syncthreads();
-  if (a.ctl->abort) return;
+  if (*a.abort || a.ctl->abort) return;  // (an error in the steps running beside an ahead detection)
   if ((long long)a.cell_start[a.ncell] > a.cap_inserts) {
     a.ctl->need_inserts = a.cell_start[a.ncell];
-    atomicExch(&a.ctl->abort, 1);
+    atomicExch(a.abort, 1);
     return;
   }
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -295,7 +300,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
         if (lane < m) {
           const int it = a.items[k0 + lane];
           const int idx = it & 0x1fffffff;
-          u0 = a.spos[idx];
+          u0 = a.dpos[idx];
           mt0 = make_int2(a.s_clump[idx], idx);
           pos0 = (kGroupPos >> (4 * ((unsigned)it >> 29))) & 7;
           v0 = 1ull << (8 * pos0);
@@ -303,7 +308,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
         if (lane + 32 < m) {
           const int it = a.items[k0 + 32 + lane];
           const int idx = it & 0x1fffffff;
-          u1 = a.spos[idx];
+          u1 = a.dpos[idx];
           mt1 = make_int2(a.s_clump[idx], idx);
           pos1 = (kGroupPos >> (4 * ((unsigned)it >> 29))) & 7;
           v1 = 1ull << (8 * pos1);
@@ -433,12 +438,12 @@ __device__ __forceinline__ int prev_index(const Rows& prev, int pb, int pe, long
 }
 
 __global__ void __launch_bounds__(256) k_rows_finish(StepArgs a) {
-  if (a.ctl->abort) return;
+  if (*a.abort || a.ctl->abort) return;  // (an error in the steps running beside an ahead detection)
   const int total = a.rows.row_ptr[a.ns];
   if ((long long)total > a.cap_entries) {
     if (threadIdx.x == 0 && blockIdx.x == 0) {
       a.ctl->need_entries = total;
-      atomicExch(&a.ctl->abort, 1);
+      atomicExch(a.abort, 1);
     }
     return;
   }
@@ -448,7 +453,7 @@ __global__ void __launch_bounds__(256) k_rows_finish(StepArgs a) {
   const int m = a.rows.row_ptr[i + 1] - beg;
   const int pb = a.prev.row_ptr[i], pe = a.prev.row_ptr[i + 1];
   Entry* R = a.rows.ent + beg;
-  const double4 s = a.spos[i];
+  const double4 s = a.dpos[i];
   unsigned wmask = 0;  // walls, same exactly rounded predicate as k_pose_count's count
   for (int p = 0; p < a.tab.n_planes; ++p) {
     const double* pp = a.tab.plane_pt[p];

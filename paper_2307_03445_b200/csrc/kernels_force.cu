@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
       // row merge in k_rows_finish (-1: contact born this step, u_t = 0)
       // (between rebuilds the set is unchanged: the entry's own slot of the previous u_t)
       double ux = 0.0, uy = 0.0, uz = 0.0;
-      const int pidx = a.rebuild ? ent.prev : e;
+      const int pidx = a.remap ? ent.prev : e;
       if (pidx >= 0) {
         const double2 u01 = *reinterpret_cast<const double2*>(a.prev.ut + kUt * pidx);
         ux = u01.x;

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <unordered_map>
@@ -37,7 +38,8 @@ using namespace dem;
 static constexpr int kStages = 8;  // last: ghost halo pack + exchange + unpack (distributed)
 static constexpr int kKin13 = 13;  // doubles per ghost clump state
 static constexpr int kRowWidth = 32;  // initial candidate slots per owned sphere
-static constexpr int kLaunchesPerStep = 11;  // 5 stage kernels + 2 x 3 scan kernels
+static constexpr int kLaunchesPerStep = 11;
+static const int kOne = 1;  // 5 stage kernels + 2 x 3 scan kernels
 
 struct RowBuf {
   int* row_ptr = nullptr;
@@ -89,14 +91,20 @@ struct dem_system {
   RowBuf rows[2];
   int sp = 0, up = 0, ep = 0;
   int since_rebuild = 0;                 // steps since the last contact-set rebuild
-  double4* d_spos_ref = nullptr;         // sphere centres at the last rebuild (displacement check)
+  double4* d_spos_ref[2] = {nullptr, nullptr};  // sphere centres entry set e was detected from
+  // overlapped cadence ("in the shadow"): the next window's set is detected
+  // on det_stream from the positions of the window's second step, adopted at the next window start
+  bool pending = false;                  // rows[ep ^ 1] holds a set detected ahead, not yet adopted
+  cudaStream_t det_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_det = nullptr;
+  int fault_ahead = 0;  // test hook (env DEM_FAULT_AHEAD_OVERFLOW=n): the next n ahead detections report an overflow
   long long cap_entries = 0;
   Record rec{};
   Ctl* d_ctl = nullptr;
   Ctl* h_ctl = nullptr;
   unsigned long long* d_counter = nullptr;
   // graphs, one per (sp, up, ep, rebuild)
-  cudaGraphExec_t graph[16] = {};
+  std::unordered_map<int, cudaGraphExec_t> graph;  // key: graph_key()
   bool graphs_valid = false;
   int64_t launched = 0;  // steps launched since dem_set_state
   int64_t steps_done = 0;
@@ -170,17 +178,31 @@ static dem_status alloc_arr(dem_system* sys, T** out, size_t count) {
 
 static void free_graphs(dem_system* sys) {
   for (auto& g : sys->graph)
-    if (g) {
-      cudaGraphExecDestroy(g);
-      g = nullptr;
-    }
+    if (g.second) cudaGraphExecDestroy(g.second);
+  sys->graph.clear();
   sys->graphs_valid = false;
 }
 
-// Arguments of the next step from the host parities: state sp -> sp^1, u_t up -> up^1; a
-// rebuild step writes a new entry set rows[ep^1] (rows[ep] = the previous set, for the
-// history merge), other steps re-evaluate the current set rows[ep].
-static StepArgs make_args(dem_system* sys, bool rebuild) {
+// Step kinds.  FULL: detect the contact set from this step's positions and use it
+// (every step at cd_every = 1, the "traditional way").  CHECK: re-evaluate the set in use.
+// AHEAD (overlapped cadence, second step of a window): as CHECK, and detect the next window's
+// set from this step's positions into rows[ep ^ 1] (concurrently, on det_stream).  ADOPT
+// (window start with a set detected ahead): use it, history remapped by key.
+enum StepKind { K_FULL = 0, K_CHECK = 1, K_AHEAD = 2, K_ADOPT = 3 };
+
+static int step_kind(const dem_system* sys) {
+  if (sys->since_rebuild == 0) return sys->pending ? K_ADOPT : K_FULL;
+  if (sys->P.overlap && sys->since_rebuild == 1) return K_AHEAD;
+  return K_CHECK;
+}
+
+// Arguments of the next step from the host parities: state sp -> sp^1, u_t up -> up^1.  A
+// FULL/ADOPT step's force kernel reads the new entry set rows[ep^1] (rows[ep] = the previous
+// set, for the history remap), CHECK/AHEAD steps re-evaluate the current set rows[ep]
+// (P:142-144).  det = 1 gives the view of the detection kernels of an AHEAD step: they write
+// rows[ep^1] from the snapshot of this step's centres, with their own abort word.
+static StepArgs make_args(dem_system* sys, int kind, bool det = false) {
+  const bool rebuild = kind == K_FULL || kind == K_ADOPT || det;
   const int p = sys->sp;
   StepArgs a{};
   a.n = (int)sys->n;
@@ -245,9 +267,15 @@ static StepArgs make_args(dem_system* sys, bool rebuild) {
   const RowBuf& Q = sys->rows[sys->ep];
   a.rows = Rows{E.row_ptr, E.ent, sys->rows[sys->up ^ 1].ut};
   a.prev = Rows{Q.row_ptr, Q.ent, sys->rows[sys->up].ut};
-  a.rebuild = rebuild ? 1 : 0;
-  a.spos_ref = sys->d_spos_ref;
-  a.half_margin = sys->P.cd_every > 1 ? 0.5 * sys->P.margin : 0.0;
+  const bool deferred = sys->P.cd_every > 1;
+  a.count = (kind == K_FULL || kind == K_AHEAD) ? 1 : 0;
+  a.remap = rebuild ? 1 : 0;
+  a.adopt = kind == K_ADOPT ? 1 : 0;
+  a.ref_in = !deferred || kind == K_FULL ? nullptr : sys->d_spos_ref[kind == K_ADOPT ? sys->ep ^ 1 : sys->ep];
+  a.ref_out = deferred && a.count ? sys->d_spos_ref[sys->ep ^ 1] : nullptr;
+  a.dpos = det ? sys->d_spos_ref[sys->ep ^ 1] : sys->d_spos;
+  a.abort = det ? &sys->d_ctl->det_abort : &sys->d_ctl->abort;
+  a.half_margin = deferred ? 0.5 * sys->P.margin : 0.0;
   a.rec = sys->rec;
   a.record = sys->P.record_contacts ? 1 : 0;
   a.ctl = sys->d_ctl;
@@ -277,24 +305,37 @@ static void enqueue_nccl_exchange(dem_system* sys, cudaStream_t s) {
   ncclGroupEnd();
 }
 
-// the step sequence; ev (optional) receives kStages+1 events around the stages.  With
-// exchange = false (loopback groups) the halo is packed but moved by dem_step_group.
-static void enqueue_step(dem_system* sys, bool rebuild, cudaStream_t s, cudaEvent_t* ev, bool exchange = true) {
-  StepArgs a = make_args(sys, rebuild);
-  const int* abort = &sys->d_ctl->abort;
+// The step sequence, in three parts: pose (a1 + bin counts), detection (a2-a4: bin scan,
+// scatter, pairs, row scan, rows), force (a5-a10 + halo).  ev (optional) receives kStages+1
+// events around the stages.  With exchange = false (loopback groups) the halo is packed but
+// moved by dem_step_group.
+enum { PART_ALL = 0, PART_POSE = 1, PART_DET = 2, PART_FORCE = 3 };
+
+static void enqueue_pose(dem_system* sys, int kind, cudaStream_t s, cudaEvent_t* ev) {
+  StepArgs a = make_args(sys, kind);
   if (ev) cudaEventRecord(ev[0], s);
   launch_pose_count(a, s);
   if (ev) cudaEventRecord(ev[1], s);
-  if (rebuild) launch_excl_scan(sys->d_cell_count, sys->d_cell_start, sys->ncell, sys->d_scan_tmp, abort, s);
+}
+
+static void enqueue_detect(dem_system* sys, int kind, cudaStream_t s, cudaEvent_t* ev) {
+  const bool run = kind == K_FULL || kind == K_AHEAD;
+  StepArgs a = make_args(sys, kind, /*det=*/kind == K_AHEAD);
+  const int* abort = a.abort;
+  if (run) launch_excl_scan(sys->d_cell_count, sys->d_cell_start, sys->ncell, sys->d_scan_tmp, abort, s);
   if (ev) cudaEventRecord(ev[2], s);
-  if (rebuild) launch_bin_scatter(a, s);
+  if (run) launch_bin_scatter(a, s);
   if (ev) cudaEventRecord(ev[3], s);
-  if (rebuild) launch_pairs(a, s, sys->n_sm);
+  if (run) launch_pairs(a, s, sys->n_sm);
   if (ev) cudaEventRecord(ev[4], s);
-  if (rebuild) launch_excl_scan(sys->d_row_cnt, a.rows.row_ptr, sys->ns, sys->d_scan_tmp, abort, s);
+  if (run) launch_excl_scan(sys->d_row_cnt, a.rows.row_ptr, sys->ns, sys->d_scan_tmp, abort, s);
   if (ev) cudaEventRecord(ev[5], s);
-  if (rebuild) launch_rows_finish(a, s);
+  if (run) launch_rows_finish(a, s);
   if (ev) cudaEventRecord(ev[6], s);
+}
+
+static void enqueue_force(dem_system* sys, int kind, cudaStream_t s, cudaEvent_t* ev, bool exchange) {
+  StepArgs a = make_args(sys, kind);
   launch_force_integrate(a, s);
   if (ev) cudaEventRecord(ev[7], s);
   if (sys->dist) {
@@ -307,17 +348,32 @@ static void enqueue_step(dem_system* sys, bool rebuild, cudaStream_t s, cudaEven
   if (ev) cudaEventRecord(ev[8], s);
 }
 
-static int graph_key(const dem_system* sys, bool rebuild) {
-  return sys->sp | (sys->up << 1) | (sys->ep << 2) | ((rebuild ? 1 : 0) << 3);
+// the whole step on one stream (sequential; an AHEAD step's detection runs in line — the same
+// results as the concurrent launch, which only changes when the kernels run)
+static void enqueue_step(dem_system* sys, int kind, cudaStream_t s, cudaEvent_t* ev, bool exchange = true) {
+  enqueue_pose(sys, kind, s, ev);
+  enqueue_detect(sys, kind, s, ev);
+  enqueue_force(sys, kind, s, ev, exchange);
 }
 
-// the step graph for the current parities, captured on first use
-static dem_status step_graph(dem_system* sys, bool rebuild, cudaGraphExec_t* out) {
-  const int key = graph_key(sys, rebuild);
+static void enqueue_part(dem_system* sys, int kind, int part, cudaStream_t s) {
+  if (part == PART_ALL) enqueue_step(sys, kind, s, nullptr);
+  if (part == PART_POSE) enqueue_pose(sys, kind, s, nullptr);
+  if (part == PART_DET) enqueue_detect(sys, kind, s, nullptr);
+  if (part == PART_FORCE) enqueue_force(sys, kind, s, nullptr, true);
+}
+
+static int graph_key(const dem_system* sys, int kind, int part) {
+  return sys->sp | (sys->up << 1) | (sys->ep << 2) | (kind << 3) | (part << 5);
+}
+
+// the graph of one step (part) for the current parities, captured on first use
+static dem_status step_graph(dem_system* sys, int kind, int part, cudaGraphExec_t* out) {
+  const int key = graph_key(sys, kind, part);
   if (!sys->graph[key]) {
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(sys->cap_stream, cudaStreamCaptureModeThreadLocal));
-    enqueue_step(sys, rebuild, sys->cap_stream, nullptr);
+    enqueue_part(sys, kind, part, sys->cap_stream);
     CK(cudaStreamEndCapture(sys->cap_stream, &g));
     cudaError_t e = cudaGraphInstantiate(&sys->graph[key], g, 0);
     cudaGraphDestroy(g);
@@ -384,7 +440,7 @@ extern "C" dem_status dem_create(const dem_params* params, const dem_material* m
       !templates || (n_planes && !planes))
     return DEM_ERR_INVALID_ARG;
   if (!(params->h > 0) || params->margin < 0 || params->cd_every < 1 || params->cell_size < 0 ||
-      (params->cd_every > 1 && !(params->margin > 0)))
+      (params->cd_every > 1 && !(params->margin > 0)) || (params->overlap && params->cd_every < 2))
     return DEM_ERR_INVALID_ARG;
   for (int d = 0; d < 3; ++d)
     if (!(params->domain_hi[d] > params->domain_lo[d])) return DEM_ERR_INVALID_ARG;
@@ -411,6 +467,7 @@ extern "C" dem_status dem_create(const dem_params* params, const dem_material* m
   }
   dem_system* sys = new dem_system();
   sys->P = *params;
+  if (const char* fi = std::getenv("DEM_FAULT_AHEAD_OVERFLOW")) sys->fault_ahead = std::atoi(fi);
   sys->stream = (cudaStream_t)cuda_stream;
   sys->n_mat = n_mat;
   sys->n_tmpl = n_tmpl;
@@ -446,6 +503,9 @@ extern "C" dem_status dem_create(const dem_params* params, const dem_material* m
       }
     }
   cudaError_t e = cudaStreamCreateWithFlags(&sys->cap_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&sys->det_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sys->ev_fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sys->ev_det, cudaEventDisableTiming);
   if (e != cudaSuccess) {
     delete sys;
     return DEM_ERR_CUDA;
@@ -514,6 +574,7 @@ extern "C" dem_status dem_nccl_unique_id(unsigned char out[128]) {
 
 extern "C" void dem_destroy(dem_system* sys) {
   if (!sys) return;
+  if (sys->det_stream) cudaStreamSynchronize(sys->det_stream);
   cudaStreamSynchronize(sys->stream);
   if (sys->comm) ncclCommDestroy(sys->comm);
   free_graphs(sys);
@@ -524,6 +585,9 @@ extern "C" void dem_destroy(dem_system* sys) {
   if (sys->h_ctl) cudaFreeHost(sys->h_ctl);
   for (auto e : sys->ev) cudaEventDestroy(e);
   if (sys->cap_stream) cudaStreamDestroy(sys->cap_stream);
+  if (sys->det_stream) cudaStreamDestroy(sys->det_stream);
+  if (sys->ev_fork) cudaEventDestroy(sys->ev_fork);
+  if (sys->ev_det) cudaEventDestroy(sys->ev_det);
   delete sys;
 }
 
@@ -566,6 +630,7 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
   if (!sys || n < 0 || (n > 0 && (!gid || !tid || !pos || !quat || !vel || !omega))) return DEM_ERR_INVALID_ARG;
   if (n > (1LL << 30)) return DEM_ERR_INVALID_ARG;
   CK(cudaStreamSynchronize(sys->stream));
+  CK(cudaStreamSynchronize(sys->det_stream));
   std::vector<long long> g(n);
   std::vector<int> t(n);
   std::vector<double> in[4];
@@ -777,7 +842,7 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
   TRY(alloc_arr(sys, &sys->d_s_mat, ns));
   TRY(alloc_arr(sys, &sys->d_s_key, ns));
   TRY(alloc_arr(sys, &sys->d_spos, ns));
-  TRY(alloc_arr(sys, &sys->d_spos_ref, ns));
+  for (int e = 0; e < 2; ++e) TRY(alloc_arr(sys, &sys->d_spos_ref[e], sys->P.cd_every > 1 ? ns : 0));
   // candidate lists: kRowWidth slots per owned sphere to start with (walls included), widened
   // on overflow (the rows of a settled bed hold a few entries)
   sys->row_width = kRowWidth;
@@ -863,6 +928,7 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
   sys->steps_done = 0;
   sys->sp = sys->up = sys->ep = 0;
   sys->since_rebuild = 0;
+  sys->pending = false;
   sys->last_entries = 0;
   sys->err.clear();
   return DEM_OK;
@@ -871,6 +937,7 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
 extern "C" dem_status dem_set_contact_history(dem_system* sys, int64_t n, const int64_t* key_a,
                                               const int64_t* key_b, const double* u_t) {
   if (!sys || n < 0 || (n && (!key_a || !key_b || !u_t))) return DEM_ERR_INVALID_ARG;
+  CK(cudaStreamSynchronize(sys->det_stream));  // a set detected ahead is dropped
   std::unordered_map<long long, int> idx;
   idx.reserve((size_t)sys->ns * 2);
   for (int64_t s = 0; s < sys->ns_own; ++s) idx[sys->h_s_key[s]] = (int)s;  // owned spheres only
@@ -914,6 +981,7 @@ extern "C" dem_status dem_set_contact_history(dem_system* sys, int64_t n, const 
   }
   CK(cudaStreamSynchronize(s));
   sys->since_rebuild = 0;
+  sys->pending = false;
   return DEM_OK;
 }
 
@@ -965,10 +1033,12 @@ static dem_status ensure_events(dem_system* sys, int64_t steps) {
 }
 
 // advance the host parities after a launched step
-static void advance_parities(dem_system* sys, bool rebuild) {
+static void advance_parities(dem_system* sys, int kind) {
   sys->sp ^= 1;
   sys->up ^= 1;
-  if (rebuild) sys->ep ^= 1;
+  if (kind == K_FULL || kind == K_ADOPT) sys->ep ^= 1;
+  if (kind == K_AHEAD) sys->pending = true;
+  if (kind == K_ADOPT) sys->pending = false;
   sys->since_rebuild = (sys->since_rebuild + 1) % std::max(1, sys->P.cd_every);
   sys->launched++;
 }
@@ -980,6 +1050,7 @@ extern "C" dem_status dem_step(dem_system* sys, int64_t n_steps) {
   int guard = 0;
   struct Sched {
     int up, ep, since;
+    bool pending;
   };
   std::vector<Sched> sched;
   while (remaining > 0) {
@@ -987,16 +1058,35 @@ extern "C" dem_status dem_step(dem_system* sys, int64_t n_steps) {
     sched.clear();
     if (sys->profiling) TRY(ensure_events(sys, remaining));
     for (int64_t k = 0; k < remaining; ++k) {
-      const bool rebuild = sys->since_rebuild == 0;
-      sched.push_back(Sched{sys->up, sys->ep, sys->since_rebuild});
+      const int kind = step_kind(sys);
+      sched.push_back(Sched{sys->up, sys->ep, sys->since_rebuild, sys->pending});
       if (sys->profiling) {
-        enqueue_step(sys, rebuild, sys->stream, &sys->ev[(size_t)k * (kStages + 1)]);
+        // stage timing: every part in line on the system stream (same results)
+        enqueue_step(sys, kind, sys->stream, &sys->ev[(size_t)k * (kStages + 1)]);
+      } else if (kind == K_AHEAD) {
+        // the next window's detection forks off after this step's poses and runs on det_stream
+        // "in the shadow" of the force steps; the adopting step joins it
+        cudaGraphExec_t gp, gd, gf;
+        TRY(step_graph(sys, kind, PART_POSE, &gp));
+        TRY(step_graph(sys, kind, PART_DET, &gd));
+        TRY(step_graph(sys, kind, PART_FORCE, &gf));
+        CK(cudaGraphLaunch(gp, sys->stream));
+        CK(cudaEventRecord(sys->ev_fork, sys->stream));
+        CK(cudaStreamWaitEvent(sys->det_stream, sys->ev_fork, 0));
+        CK(cudaGraphLaunch(gd, sys->det_stream));
+        if (sys->fault_ahead > 0) {
+          --sys->fault_ahead;
+          CK(cudaMemcpyAsync(&sys->d_ctl->det_abort, &kOne, sizeof(int), cudaMemcpyHostToDevice, sys->det_stream));
+        }
+        CK(cudaEventRecord(sys->ev_det, sys->det_stream));
+        CK(cudaGraphLaunch(gf, sys->stream));
       } else {
+        if (kind == K_ADOPT) CK(cudaStreamWaitEvent(sys->stream, sys->ev_det, 0));
         cudaGraphExec_t g;
-        TRY(step_graph(sys, rebuild, &g));
+        TRY(step_graph(sys, kind, PART_ALL, &g));
         CK(cudaGraphLaunch(g, sys->stream));
       }
-      advance_parities(sys, rebuild);
+      advance_parities(sys, kind);
     }
     TRY(read_ctl(sys));
     const int64_t done = sys->h_ctl->step - done_before;
@@ -1018,17 +1108,22 @@ extern "C" dem_status dem_step(dem_system* sys, int64_t n_steps) {
       sys->err = "capacity overflow on a distributed system (raise params.entries_per_sphere)";
       return DEM_ERR_CAPACITY;
     }
-    // capacity abort in step `done` (always a rebuild step): the state was carried forward
-    // through the aborted steps (sp is already right); the latest valid u_t and entry set are
-    // those that step read.  Regrow and re-run from there.
+    // capacity abort in step `done` (a FULL step, or an ADOPT step whose set detected ahead
+    // overflowed): the state was carried forward through the aborted steps (sp is already
+    // right); the latest valid u_t and entry set are those that step read.  Regrow and re-run
+    // from there — an aborted adoption as a FULL rebuild at that step, which gives the same
+    // trajectory (every contact with delta > 0 is in both sets).
     if (++guard > 8) {
       sys->err = "capacity regrow did not converge";
       return DEM_ERR_CAPACITY;
     }
+    CK(cudaStreamSynchronize(sys->det_stream));
     sys->regrows++;
     sys->up = sched[(size_t)done].up;
     sys->ep = sched[(size_t)done].ep;
     sys->since_rebuild = sched[(size_t)done].since;
+    sys->pending = false;
+    sys->h_ctl->det_abort = 0;
     if (sys->h_ctl->need_entries > sys->cap_entries) {
       long long need = sys->h_ctl->need_entries;
       TRY(alloc_rows(sys, need + need / 4 + 1024));
@@ -1054,6 +1149,7 @@ extern "C" dem_status dem_step(dem_system* sys, int64_t n_steps) {
 
 extern "C" dem_status dem_synchronize(dem_system* sys) {
   if (!sys) return DEM_ERR_INVALID_ARG;
+  CK(cudaStreamSynchronize(sys->det_stream));
   TRY(read_ctl(sys));
   if (sys->h_ctl->err_code) return device_error(sys);
   return DEM_OK;
@@ -1149,7 +1245,7 @@ extern "C" dem_status dem_step_group(dem_system* const* systems, int32_t n, int6
   for (int64_t k = 0; k < n_steps; ++k) {
     for (int r = 0; r < n; ++r) {
       dem_system* sys = systems[r];
-      enqueue_step(sys, sys->since_rebuild == 0, s, nullptr, /*exchange=*/false);
+      enqueue_step(sys, step_kind(sys), s, nullptr, /*exchange=*/false);
     }
     // ghost halo: rank r's left-side ghosts are rank r-1's right-side sends, and vice versa
     for (int r = 0; r < n; ++r) {
@@ -1167,9 +1263,10 @@ extern "C" dem_status dem_step_group(dem_system* const* systems, int32_t n, int6
     }
     for (int r = 0; r < n; ++r) {
       dem_system* sys = systems[r];
-      StepArgs a = make_args(sys, sys->since_rebuild == 0);
+      const int kind = step_kind(sys);
+      StepArgs a = make_args(sys, kind);
       enqueue_unpack(sys, a, s);
-      advance_parities(sys, sys->since_rebuild == 0);
+      advance_parities(sys, kind);
     }
   }
   for (int r = 0; r < n; ++r) {
