@@ -209,6 +209,8 @@ def run_ours(a):
                                  overlap=a.overlap)
     stream = sys_.stream
     sys_.dem_step(a.warmup)
+    if world > 1:
+        sys_.dem_migrate(threshold=0.5 * drift)  # collective drift check; a settling bed stays put
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t_setup
 

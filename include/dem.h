@@ -213,6 +213,22 @@ dem_status dem_partition_plan(int64_t n, const double* pos, double slab_lo, doub
  * between neighbours.  Lets one GPU run a P-rank decomposition (tests, scaling studies). */
 dem_status dem_step_group(dem_system* const* systems, int32_t n, int64_t n_steps);
 
+/* Clump migration between slabs.  Collective over the n_ranks systems of an
+ * NCCL decomposition (every rank calls it at the same point, between dem_step calls).  The
+ * largest displacement of an owned COM since the last dem_set_state is reduced over the ranks
+ * (device reduction + ncclAllReduce MAX); if it exceeds `threshold` [m] (use a fraction of
+ * drift_max, e.g. drift_max / 2; 0 forces a migration), every rank's owned states and canonical
+ * contact histories (keys + u_t) are all-gathered over NCCL (counts, then payloads) and every
+ * rank re-partitions the gathered global state by COM x (dem_set_state semantics) and imports
+ * the gathered history (dem_set_contact_history), so clumps that crossed a face move to their new
+ * owner with their tangential history and the ghost bands are rebuilt around the new positions.
+ * The trajectory is unchanged: owned states are bitwise independent of the decomposition.
+ * *moved (optional) receives 1 if a migration happened.  Non-distributed systems: no-op. */
+dem_status dem_migrate(dem_system* sys, double threshold, int32_t* moved);
+
+/* dem_migrate for a LOOPBACK group (ranks 0..n-1 in order, as dem_step_group); host gather. */
+dem_status dem_migrate_group(dem_system* const* systems, int32_t n, double threshold, int32_t* moved);
+
 const char* dem_status_string(dem_status s);
 dem_status dem_last_error(const dem_system* sys, char* buf, size_t len);
 void dem_destroy(dem_system* sys);

@@ -59,7 +59,7 @@ TRANSPORT_NCCL, TRANSPORT_LOOPBACK = 0, 1
 EXPORTS = ["dem_create", "dem_set_state", "dem_set_contact_history", "dem_step", "dem_synchronize",
            "dem_get_state", "dem_get_contacts", "dem_get_stats", "dem_set_profiling", "dem_get_stage_times",
            "dem_status_string", "dem_last_error", "dem_destroy", "dem_nccl_unique_id", "dem_partition_plan",
-           "dem_step_group"]
+           "dem_step_group", "dem_migrate", "dem_migrate_group"]
 
 _lib = None
 
@@ -91,6 +91,8 @@ def load_library(path: str = LIB_PATH):
     L.dem_nccl_unique_id.argtypes = [P]
     L.dem_partition_plan.argtypes = [I64, P, C.c_double, C.c_double, C.c_double, I32, I32, P, P]
     L.dem_step_group.argtypes = [P, I32, I64]
+    L.dem_migrate.argtypes = [P, C.c_double, C.POINTER(I32)]
+    L.dem_migrate_group.argtypes = [P, I32, C.c_double, C.POINTER(I32)]
     for f in EXPORTS:
         if f not in ("dem_destroy", "dem_status_string"):
             getattr(L, f).restype = C.c_int
@@ -235,6 +237,13 @@ class System:
     def dem_synchronize(self):
         self._check(load_library().dem_synchronize(self.sys), "dem_synchronize")
 
+    def dem_migrate(self, threshold=0.0) -> bool:
+        """Collective (NCCL ranks): migrate clumps between slabs if an owned COM moved more than
+        `threshold` [m] since the last partition (0 forces it).  True if a migration happened."""
+        moved = C.c_int32(0)
+        self._check(load_library().dem_migrate(self.sys, float(threshold), C.byref(moved)), "dem_migrate")
+        return bool(moved.value)
+
     def dem_get_state(self):
         cnt = C.c_int64()
         self._check(load_library().dem_get_state(self.sys, 0, C.byref(cnt), None, None, None, None, None, None, 0),
@@ -347,3 +356,19 @@ def halo_width(scene, drift_max):
     """Ghost band: 2 x the largest bounding radius + margin + 2 drift_max (include/dem.h)."""
     rb = max(float(np.max(np.linalg.norm(t.offsets, axis=1) + t.radius)) for t in scene.templates)
     return 2.0 * rb + float(scene.margin) + 2.0 * drift_max
+
+
+def migrate_group(systems, threshold=0.0) -> bool:
+    """dem_migrate_group: re-partition a loopback group if an owned COM moved more than
+    `threshold` since the last partition (0 forces it).  Returns True if clumps were migrated."""
+    arr = (C.c_void_p * len(systems))(*[s.sys for s in systems])
+    moved = C.c_int32(0)
+    rc = load_library().dem_migrate_group(arr, len(systems), float(threshold), C.byref(moved))
+    if rc:
+        buf = C.create_string_buffer(512)
+        for s in systems:
+            load_library().dem_last_error(s.sys, buf, 512)
+            if buf.value:
+                break
+        raise DemError(rc, f"dem_migrate_group: {buf.value.decode()}")
+    return bool(moved.value)

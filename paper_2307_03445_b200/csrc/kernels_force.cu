@@ -353,3 +353,26 @@ void launch_unpack(const State& st, const int* idx, int n, const double* buf, cu
   if (n) k_unpack<<<(n + 255) / 256, 256, 0, s>>>(st, idx, n, buf);
 }
 }  // namespace dem
+
+namespace dem {
+// largest squared displacement of an owned COM from its dem_set_state position, as the bits
+// of a non-negative double (ordered like unsigned integers) — dem_migrate
+__global__ void k_max_drift(State st, const double* __restrict__ xref, int n, unsigned long long* out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  double d2 = 0.0;
+  if (c < n) {
+    const double dx = st.x[c] - xref[3 * c], dy = st.y[c] - xref[3 * c + 1], dz = st.z[c] - xref[3 * c + 2];
+    d2 = dx * dx + dy * dy + dz * dz;
+  }
+  unsigned long long b = (unsigned long long)__double_as_longlong(d2);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long v = __shfl_xor_sync(0xffffffffu, b, o);
+    b = v > b ? v : b;
+  }
+  if ((threadIdx.x & 31) == 0 && b) atomicMax(out, b);
+}
+void launch_max_drift(const State& st, const double* xref, int n, unsigned long long* out, cudaStream_t s) {
+  if (n) k_max_drift<<<(n + 255) / 256, 256, 0, s>>>(st, xref, n, out);
+}
+}  // namespace dem

@@ -31,6 +31,7 @@ void launch_excl_scan(const int* in, int* out, long long n, int* tmp, const int*
 void launch_count_canonical(const Rows& r, const long long* s_key, int ns, unsigned long long* out, cudaStream_t s);
 void launch_pack(const State& st, const int* idx, int n, double* buf, cudaStream_t s);
 void launch_unpack(const State& st, const int* idx, int n, const double* buf, cudaStream_t s);
+void launch_max_drift(const State& st, const double* xref, int n, unsigned long long* out, cudaStream_t s);
 }  // namespace dem
 
 using namespace dem;
@@ -1383,5 +1384,165 @@ extern "C" dem_status dem_set_profiling(dem_system* sys, int32_t enable) {
 extern "C" dem_status dem_get_stage_times(dem_system* sys, int32_t n_stages, double* ms) {
   if (!sys || !ms) return DEM_ERR_INVALID_ARG;
   for (int s = 0; s < n_stages && s < kStages; ++s) ms[s] = sys->prof_steps ? sys->stage_ms[s] / sys->prof_steps : 0.0;
+  return DEM_OK;
+}
+
+// ------------------------------------------------------------------ migration
+// Largest owned-COM displacement since dem_set_state on this system (squared, device reduction).
+static dem_status local_max_drift2(dem_system* sys, double* out) {
+  CK(cudaMemsetAsync(sys->d_counter, 0, sizeof(unsigned long long), sys->stream));
+  StepArgs a = make_args(sys, K_CHECK);
+  launch_max_drift(a.cur, sys->d_xref, (int)sys->n_own, sys->d_counter, sys->stream);
+  return DEM_OK;
+}
+
+// owned states and canonical contact histories of one system, packed as doubles:
+// per clump [gid bits, tid, pos 3, quat 4, vel 3, omega 3], per contact [key_a bits, key_b bits, u_t 3]
+static constexpr int kMigClump = 15, kMigContact = 5;
+static dem_status pack_owned(dem_system* sys, std::vector<double>& buf, int64_t& nc, int64_t& nk) {
+  int64_t n = 0, m = 0;
+  TRY(dem_get_state(sys, 0, &n, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0));
+  std::vector<int64_t> gid(n);
+  std::vector<int32_t> tid(n);
+  std::vector<double> pos(3 * n), quat(4 * n), vel(3 * n), om(3 * n);
+  TRY(dem_get_state(sys, n, &n, gid.data(), tid.data(), pos.data(), quat.data(), vel.data(), om.data(), 0));
+  TRY(dem_get_contacts(sys, 0, &m, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr));
+  std::vector<int64_t> ka(m), kb(m);
+  std::vector<double> ut(3 * m);
+  if (m) TRY(dem_get_contacts(sys, m, &m, ka.data(), kb.data(), nullptr, nullptr, nullptr, ut.data(), nullptr));
+  buf.assign((size_t)kMigClump * n + (size_t)kMigContact * m, 0.0);
+  double* o = buf.data();
+  for (int64_t c = 0; c < n; ++c, o += kMigClump) {
+    std::memcpy(&o[0], &gid[c], 8);
+    o[1] = (double)tid[c];
+    for (int d = 0; d < 3; ++d) o[2 + d] = pos[3 * c + d];
+    for (int d = 0; d < 4; ++d) o[5 + d] = quat[4 * c + d];
+    for (int d = 0; d < 3; ++d) o[9 + d] = vel[3 * c + d];
+    for (int d = 0; d < 3; ++d) o[12 + d] = om[3 * c + d];
+  }
+  for (int64_t k = 0; k < m; ++k, o += kMigContact) {
+    std::memcpy(&o[0], &ka[k], 8);
+    std::memcpy(&o[1], &kb[k], 8);
+    for (int d = 0; d < 3; ++d) o[2 + d] = ut[3 * k + d];
+  }
+  nc = n;
+  nk = m;
+  return DEM_OK;
+}
+
+// the gathered global state + history (rank order) -> this system's new partition
+struct Global {
+  std::vector<int64_t> gid, ka, kb;
+  std::vector<int32_t> tid;
+  std::vector<double> pos, quat, vel, om, ut;
+  void add(const double* b, int64_t nc, int64_t nk) {
+    for (int64_t c = 0; c < nc; ++c, b += kMigClump) {
+      int64_t g;
+      std::memcpy(&g, &b[0], 8);
+      gid.push_back(g);
+      tid.push_back((int32_t)b[1]);
+      pos.insert(pos.end(), b + 2, b + 5);
+      quat.insert(quat.end(), b + 5, b + 9);
+      vel.insert(vel.end(), b + 9, b + 12);
+      om.insert(om.end(), b + 12, b + 15);
+    }
+    for (int64_t k = 0; k < nk; ++k, b += kMigContact) {
+      int64_t x, y;
+      std::memcpy(&x, &b[0], 8);
+      std::memcpy(&y, &b[1], 8);
+      ka.push_back(x);
+      kb.push_back(y);
+      ut.insert(ut.end(), b + 2, b + 5);
+    }
+  }
+  dem_status apply(dem_system* sys) const {
+    const int64_t n = (int64_t)gid.size(), m = (int64_t)ka.size();
+    TRY(dem_set_state(sys, n, gid.data(), tid.data(), pos.data(), quat.data(), vel.data(), om.data(), 0));
+    return dem_set_contact_history(sys, m, ka.data(), kb.data(), ut.data());
+  }
+};
+
+extern "C" dem_status dem_migrate(dem_system* sys, double threshold, int32_t* moved) {
+  if (!sys || !(threshold >= 0)) return DEM_ERR_INVALID_ARG;
+  if (moved) *moved = 0;
+  if (!sys->dist || sys->launched == 0) return DEM_OK;  // nothing moved since the last partition
+  if (sys->P.transport != DEM_TRANSPORT_NCCL) {
+    sys->err = "dem_migrate needs the NCCL transport (loopback groups: dem_migrate_group)";
+    return DEM_ERR_INVALID_ARG;
+  }
+  TRY(dem_synchronize(sys));
+  cudaStream_t s = sys->stream;
+  const int P = sys->P.n_ranks;
+  TRY(local_max_drift2(sys, nullptr));
+  if (ncclAllReduce(sys->d_counter, sys->d_counter, 1, ncclDouble, ncclMax, sys->comm, s) != ncclSuccess)
+    return DEM_ERR_NCCL;
+  double d2 = 0;
+  CK(cudaMemcpyAsync(&d2, sys->d_counter, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (threshold > 0 && std::sqrt(d2) <= threshold) return DEM_OK;
+  std::vector<double> mine;
+  int64_t nc = 0, nk = 0;
+  TRY(pack_owned(sys, mine, nc, nk));
+  // two-phase all-gather: counts, then payloads padded to the largest rank's
+  int64_t* d_cnt = (int64_t*)dalloc(sys, sizeof(int64_t) * 2 * (P + 1));
+  if (!d_cnt) return DEM_ERR_OOM;
+  const int64_t cnt[2] = {nc, nk};
+  std::vector<int64_t> all((size_t)2 * P);
+  CK(cudaMemcpyAsync(d_cnt, cnt, sizeof(cnt), cudaMemcpyHostToDevice, s));
+  if (ncclAllGather(d_cnt, d_cnt + 2, 2, ncclInt64, sys->comm, s) != ncclSuccess) return DEM_ERR_NCCL;
+  CK(cudaMemcpyAsync(all.data(), d_cnt + 2, sizeof(int64_t) * 2 * P, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  dfree(sys, d_cnt);
+  size_t len = 1;
+  for (int r = 0; r < P; ++r) len = std::max(len, (size_t)(kMigClump * all[2 * r] + kMigContact * all[2 * r + 1]));
+  double* d_send = (double*)dalloc(sys, sizeof(double) * len);
+  double* d_all = (double*)dalloc(sys, sizeof(double) * len * P);
+  if (!d_send || !d_all) return DEM_ERR_OOM;
+  if (!mine.empty()) CK(cudaMemcpyAsync(d_send, mine.data(), sizeof(double) * mine.size(), cudaMemcpyHostToDevice, s));
+  if (ncclAllGather(d_send, d_all, len, ncclDouble, sys->comm, s) != ncclSuccess) return DEM_ERR_NCCL;
+  std::vector<double> host(len * P);
+  CK(cudaMemcpyAsync(host.data(), d_all, sizeof(double) * len * P, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  dfree(sys, d_send);
+  dfree(sys, d_all);
+  Global G;
+  for (int r = 0; r < P; ++r) G.add(host.data() + len * r, all[2 * r], all[2 * r + 1]);
+  TRY(G.apply(sys));
+  if (moved) *moved = 1;
+  return DEM_OK;
+}
+
+extern "C" dem_status dem_migrate_group(dem_system* const* systems, int32_t n, double threshold, int32_t* moved) {
+  if (!systems || n < 1 || !(threshold >= 0)) return DEM_ERR_INVALID_ARG;
+  if (moved) *moved = 0;
+  for (int r = 0; r < n; ++r) {
+    dem_system* sys = systems[r];
+    if (!sys || (n > 1 && (!sys->dist || sys->P.transport != DEM_TRANSPORT_LOOPBACK || sys->P.rank != r ||
+                           sys->P.n_ranks != n)))
+      return DEM_ERR_INVALID_ARG;
+  }
+  if (n == 1 && !systems[0]->dist) return DEM_OK;
+  if (systems[0]->launched == 0) return DEM_OK;  // nothing moved since the last partition
+  double d2 = 0;
+  for (int r = 0; r < n; ++r) {
+    dem_system* sys = systems[r];
+    TRY(dem_synchronize(sys));
+    TRY(local_max_drift2(sys, nullptr));
+    double v = 0;
+    if (cudaMemcpyAsync(&v, sys->d_counter, sizeof(double), cudaMemcpyDeviceToHost, sys->stream) != cudaSuccess ||
+        cudaStreamSynchronize(sys->stream) != cudaSuccess)
+      return DEM_ERR_CUDA;
+    d2 = std::max(d2, v);
+  }
+  if (threshold > 0 && std::sqrt(d2) <= threshold) return DEM_OK;
+  Global G;
+  for (int r = 0; r < n; ++r) {
+    std::vector<double> buf;
+    int64_t nc = 0, nk = 0;
+    TRY(pack_owned(systems[r], buf, nc, nk));
+    G.add(buf.data(), nc, nk);
+  }
+  for (int r = 0; r < n; ++r) TRY(G.apply(systems[r]));
+  if (moved) *moved = 1;
   return DEM_OK;
 }

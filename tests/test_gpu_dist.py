@@ -87,3 +87,44 @@ def test_drift_beyond_halo_guard_is_reported(dem):
     with pytest.raises(dem.DemError) as e:
         dem.step_group(systems, 50)
     assert e.value.status == -15
+
+
+def test_migration_keeps_the_trajectory_bitwise(dem):
+    """Clumps streaming across the slab face are migrated to their new owner with their
+    tangential history (dem_migrate_group); the gathered P = 2 trajectory stays
+    bitwise equal to the single-system run and no drift guard fires."""
+    scene = _strip(seed=3)
+    scene.vel[:, 0] += 1.5  # 1.5 m/s along x: ~0.15 mm per 100 steps, across the face
+    ref = dem.system_from_scene(scene, record_contacts=True)
+    drift = 0.1e-3
+    systems = _group(dem, scene, 2, drift_max=drift)
+    owned0 = [s.dem_get_stats()["n_owned_clumps"] for s in systems]
+    moves = 0
+    for _ in range(8):
+        ref.dem_step(40)
+        dem.step_group(systems, 40)
+        moves += dem.migrate_group(systems, threshold=0.5 * drift)
+    ref.dem_step(5)  # the contact lists of a step after the last migration
+    dem.step_group(systems, 5)
+    assert moves >= 3
+    owned1 = [s.dem_get_stats()["n_owned_clumps"] for s in systems]
+    assert owned1 != owned0 and sum(owned1) == scene.n_clumps
+    sr = ref.dem_get_state()
+    order = np.argsort(sr["gid"])
+    sr = {k: v[order] for k, v in sr.items()}
+    sg = _gather(systems)
+    assert np.array_equal(sg["gid"], sr["gid"])
+    for k in ("pos", "quat", "vel", "omega"):
+        assert np.array_equal(sg[k], sr[k]), k
+    cr, cg = ref.dem_get_contacts(), _contacts(systems)
+    for k in ("key_a", "key_b", "u_t", "force_b"):
+        assert np.array_equal(cg[k], cr[k]), k
+
+
+def test_migration_below_threshold_is_a_no_op(dem):
+    scene = _strip()
+    systems = _group(dem, scene, 2, record=False)
+    dem.step_group(systems, 5)
+    owned = [s.dem_get_stats()["n_owned_clumps"] for s in systems]
+    assert not dem.migrate_group(systems, threshold=1.0)
+    assert [s.dem_get_stats()["n_owned_clumps"] for s in systems] == owned
