@@ -58,6 +58,10 @@ def lib():
         L.orc_last_error.argtypes = [P]
         L.orc_pair_params.argtypes = [P, P, P]
         L.orc_contact_force.argtypes = [D, D, D, D, D, D, D, D, P, P, P, P, P, P]
+        L.orc_add_mesh.argtypes = [P, I64, P, C.c_int, P, P, P, P]
+        L.orc_set_mesh_motion.argtypes = [P, C.c_int, P, P, P, P]
+        L.orc_get_mesh.argtypes = [P, C.c_int, P, P, P, P]
+        L.orc_closest_on_triangle.argtypes = [P, P, P, P, P]
         _lib = L
     return _lib
 
@@ -99,6 +103,13 @@ class Oracle:
             self._check(L.orc_set_cd_every(self.sys, int(cd_every)))
         if overlap:  # next window's set detected one window ahead
             self._check(L.orc_set_overlap(self.sys, 1))
+        for m in getattr(scene, "meshes", []):  # kinematic triangle meshes (NEXT-3)
+            v = _f64(m.verts).reshape(-1)
+            arr = [_f64(m.pos), _f64(m.quat), _f64(m.vel), _f64(m.omega)]
+            self._keep += [v] + arr
+            rc = L.orc_add_mesh(self.sys, v.shape[0] // 9, _p(v), int(m.material), *[_p(a) for a in arr])
+            if rc < 0:
+                self._check(rc)
 
     def __del__(self):
         if getattr(self, "sys", None):
@@ -145,6 +156,17 @@ class Oracle:
                                                ("key_a", "key_b", "force_b", "point", "normal", "u_t", "delta")])
         return out
 
+    def set_mesh_motion(self, m, pos, quat, vel, omega):
+        arr = [_f64(pos), _f64(quat), _f64(vel), _f64(omega)]
+        self._check(lib().orc_set_mesh_motion(self.sys, int(m), *[_p(a) for a in arr]))
+
+    def mesh(self, m=0):
+        """Pose after the last step; force on the mesh and torque about its reference point from the
+        last step's contacts."""
+        X, q, f, t = np.zeros(3), np.zeros(4), np.zeros(3), np.zeros(3)
+        self._check(lib().orc_get_mesh(self.sys, int(m), _p(X), _p(q), _p(f), _p(t)))
+        return dict(pos=X, quat=q, force=f, torque=t)
+
     def wrench(self):
         f, t = np.zeros((self.n, 3)), np.zeros((self.n, 3))
         lib().orc_get_wrench(self.sys, _p(f), _p(t))
@@ -163,3 +185,10 @@ def contact_force(e_star, g_star, beta, mu, r_bar, m_bar, h, delta, n, v_rel, ut
     lib().orc_contact_force(e_star, g_star, beta, mu, r_bar, m_bar, h, delta, _p(n), _p(v), _p(u), _p(fn),
                             _p(ft), _p(un))
     return fn, ft, un
+
+
+def closest_on_triangle(p, a, b, c):
+    """(closest point, region): region 0 face, 1-3 edge ab/ac/bc, 4-6 vertex a/b/c."""
+    p, a, b, c, o = _f64(p), _f64(a), _f64(b), _f64(c), np.zeros(3)
+    reg = lib().orc_closest_on_triangle(_p(p), _p(a), _p(b), _p(c), _p(o))
+    return o, reg

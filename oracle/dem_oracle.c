@@ -11,6 +11,10 @@
  *   contact set        pinned  (independent numpy brute force, grid == brute)
  *   accumulate/integr. pinned  (free fall closed form, tumbling invariants,
  *                               momentum conservation, incline closed forms)
+ *   meshes (NEXT-3)    pinned  (closest point vs an independent projection; sphere on a
+ *                               mesh square == sphere on the analytic plane; head-on
+ *                               restitution against a moving mesh wall; resting-weight
+ *                               wrench; exact rotation of a spinning mesh)
  */
 #include "dem_oracle.h"
 
@@ -21,6 +25,7 @@
 
 #define KEY_STRIDE 64
 #define WALL_KEY(p) (INT64_MAX - (int64_t)(p))
+#define MAX_PLANES 16 /* triangle t has key INT64_MAX - MAX_PLANES - t and partner code -1 - MAX_PLANES - t */
 
 typedef struct {
   int64_t ka, kb;
@@ -69,6 +74,15 @@ struct orc_sys {
   int64_t nc, cap;
   contact* con;
   int64_t steps;
+  /* kinematic triangle meshes (NEXT-3; P:277 cone, P:307 funnel, P:344 wheel):
+   * prescribed pose X, q (body -> world), velocity v and angular velocity w (world), advanced
+   * after every step by X += h v, q <- normalize(qs (x) q) with qs the rotation by h|w| */
+  int n_mesh;
+  int64_t n_tri;
+  double *mX, *mQ, *mV, *mW, *mQs, *mF, *mT; /* per mesh: 3, 4, 3, 3, 4, 3 (force), 3 (torque about X) */
+  int32_t *mmat, *tri_mesh;
+  int64_t* tri_vid;             /* 3 per triangle: vertex ids (bitwise-equal body vertices of a mesh share one) */
+  double *tri_body, *tri_world; /* 9 per triangle (a, b, c) */
   char err[256];
 };
 
@@ -192,6 +206,230 @@ void orc_contact_force(double e_star, double g_star, double beta, double mu, dou
   }
 }
 
+/* ------------------------------------------------------------------ triangles (NEXT-3)
+ * Closest point of triangle (a, b, c) to p by its Voronoi regions (vertex, edge, face), the
+ * textbook construction ("closest point on the triangle (face, edge, or vertex
+ * region)"), in the fixed operation order of DESIGN.md R25: dot products (x x' + y y') + z z',
+ * no fused multiply-add (the library is compiled with -ffp-contract=off). */
+static double dot3(const double* u, const double* v) { return (u[0] * v[0] + u[1] * v[1]) + u[2] * v[2]; }
+
+/* returns the region of the closest point: TRI_FACE, TRI_EDGE_AB/AC/BC, TRI_VERT_A/B/C */
+enum { TRI_FACE = 0, TRI_EDGE_AB = 1, TRI_EDGE_AC = 2, TRI_EDGE_BC = 3, TRI_VERT_A = 4, TRI_VERT_B = 5, TRI_VERT_C = 6 };
+int orc_closest_on_triangle(const double p[3], const double a[3], const double b[3], const double c[3],
+                            double out[3]) {
+  double ab[3], ac[3], ap[3], bp[3], cp[3];
+  int d;
+  for (d = 0; d < 3; ++d) {
+    ab[d] = b[d] - a[d];
+    ac[d] = c[d] - a[d];
+    ap[d] = p[d] - a[d];
+  }
+  double d1 = dot3(ab, ap), d2 = dot3(ac, ap);
+  if (d1 <= 0.0 && d2 <= 0.0) { /* vertex a */
+    for (d = 0; d < 3; ++d) out[d] = a[d];
+    return TRI_VERT_A;
+  }
+  for (d = 0; d < 3; ++d) bp[d] = p[d] - b[d];
+  double d3 = dot3(ab, bp), d4 = dot3(ac, bp);
+  if (d3 >= 0.0 && d4 <= d3) { /* vertex b */
+    for (d = 0; d < 3; ++d) out[d] = b[d];
+    return TRI_VERT_B;
+  }
+  double vc = d1 * d4 - d3 * d2;
+  if (vc <= 0.0 && d1 >= 0.0 && d3 <= 0.0) { /* edge ab */
+    double v = d1 / (d1 - d3);
+    for (d = 0; d < 3; ++d) out[d] = a[d] + v * ab[d];
+    return TRI_EDGE_AB;
+  }
+  for (d = 0; d < 3; ++d) cp[d] = p[d] - c[d];
+  double d5 = dot3(ab, cp), d6 = dot3(ac, cp);
+  if (d6 >= 0.0 && d5 <= d6) { /* vertex c */
+    for (d = 0; d < 3; ++d) out[d] = c[d];
+    return TRI_VERT_C;
+  }
+  double vb = d5 * d2 - d1 * d6;
+  if (vb <= 0.0 && d2 >= 0.0 && d6 <= 0.0) { /* edge ac */
+    double w = d2 / (d2 - d6);
+    for (d = 0; d < 3; ++d) out[d] = a[d] + w * ac[d];
+    return TRI_EDGE_AC;
+  }
+  double va = d3 * d6 - d5 * d4;
+  double e43 = d4 - d3, e56 = d5 - d6;
+  if (va <= 0.0 && e43 >= 0.0 && e56 >= 0.0) { /* edge bc */
+    double w = e43 / (e43 + e56);
+    for (d = 0; d < 3; ++d) out[d] = b[d] + w * (c[d] - b[d]);
+    return TRI_EDGE_BC;
+  }
+  double denom = 1.0 / ((va + vb) + vc); /* face */
+  double v = vb * denom, w = vc * denom;
+  for (d = 0; d < 3; ++d) out[d] = (a[d] + ab[d] * v) + ac[d] * w;
+  return TRI_FACE;
+}
+
+/* world vertices of every triangle: x = X + R(q) x_body (the sphere-centre arithmetic, R22) */
+static void mesh_world(orc_sys* s) {
+  int64_t t;
+  int k;
+  for (t = 0; t < s->n_tri; ++t) {
+    int m = s->tri_mesh[t];
+    double R[9], v[3];
+    quat_to_R(s->mQ + 4 * m, R);
+    for (k = 0; k < 3; ++k) {
+      mat_vec(R, s->tri_body + 9 * t + 3 * k, v);
+      s->tri_world[9 * t + 3 * k] = s->mX[3 * m] + v[0];
+      s->tri_world[9 * t + 3 * k + 1] = s->mX[3 * m + 1] + v[1];
+      s->tri_world[9 * t + 3 * k + 2] = s->mX[3 * m + 2] + v[2];
+    }
+  }
+}
+
+/* the rotation of one step, h |w| about w/|w| (the exponential map of the clump update, R12) */
+static void mesh_step_quat(double h, const double* w, double* qs) {
+  double wn = sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
+  qs[0] = 1.0;
+  qs[1] = qs[2] = qs[3] = 0.0;
+  if (wn > 0.0) {
+    double half = 0.5 * (h * wn);
+    double sn = sin(half) / wn;
+    qs[0] = cos(half);
+    qs[1] = w[0] * sn;
+    qs[2] = w[1] * sn;
+    qs[3] = w[2] * sn;
+  }
+}
+
+static void mesh_advance(orc_sys* s) {
+  int m, d;
+  for (m = 0; m < s->n_mesh; ++m) {
+    double* X = s->mX + 3 * m;
+    double* q = s->mQ + 4 * m;
+    const double* a = s->mQs + 4 * m;
+    for (d = 0; d < 3; ++d) X[d] = X[d] + s->h * s->mV[3 * m + d];
+    double w1 = a[0], x1 = a[1], y1 = a[2], z1 = a[3];
+    double w2 = q[0], x2 = q[1], y2 = q[2], z2 = q[3];
+    double nq[4];
+    nq[0] = w1 * w2 - x1 * x2 - y1 * y2 - z1 * z2;
+    nq[1] = w1 * x2 + x1 * w2 + y1 * z2 - z1 * y2;
+    nq[2] = w1 * y2 - x1 * z2 + y1 * w2 + z1 * x2;
+    nq[3] = w1 * z2 + x1 * y2 - y1 * x2 + z1 * w2;
+    double nrm = sqrt(nq[0] * nq[0] + nq[1] * nq[1] + nq[2] * nq[2] + nq[3] * nq[3]);
+    for (d = 0; d < 4; ++d) q[d] = nq[d] / nrm;
+  }
+}
+
+/* One contact per surface feature (R26): the closest point of a sphere to a triangle
+ * lies on its face, one of its edges or one of its vertices.  A face contact always counts; an
+ * edge contact counts unless the sphere's set holds a face contact on a triangle of the same mesh
+ * containing that edge, or the same edge reached from a lower-index triangle; a vertex contact
+ * counts unless there is a face or edge contact (same mesh) containing that vertex, or the same
+ * vertex from a lower-index triangle.  So a sphere on a flat mesh is pushed once, however the
+ * mesh is triangulated.  Contacts that do not count get F = 0 and u_t = 0 (as delta <= 0). */
+static int tri_has(const orc_sys* s, int64_t t, int64_t v) {
+  return s->tri_vid[3 * t] == v || s->tri_vid[3 * t + 1] == v || s->tri_vid[3 * t + 2] == v;
+}
+
+static void tri_feature(const orc_sys* s, int64_t t, int region, int* kind, int64_t* u, int64_t* v) {
+  const int64_t* id = s->tri_vid + 3 * t;
+  static const int ea[4] = {0, 0, 0, 1}, eb[4] = {0, 1, 2, 2};
+  if (region == TRI_FACE) {
+    *kind = 2;
+    *u = *v = t;
+  } else if (region <= TRI_EDGE_BC) {
+    int64_t x = id[ea[region]], y = id[eb[region]];
+    *kind = 1;
+    *u = x < y ? x : y;
+    *v = x < y ? y : x;
+  } else {
+    *kind = 0;
+    *u = *v = id[region - TRI_VERT_A];
+  }
+}
+
+static int mesh_contact_active(const orc_sys* s, int64_t k, const int* region) {
+  const contact* C = s->con;
+  int64_t lo = k, hi = k, j;
+  while (lo > 0 && C[lo - 1].ka == C[k].ka) --lo;
+  while (hi + 1 < s->nc && C[hi + 1].ka == C[k].ka) ++hi;
+  int64_t t = -1 - MAX_PLANES - C[k].sb;
+  int kind, kj;
+  int64_t u, v, uj, vj;
+  tri_feature(s, t, region[k], &kind, &u, &v);
+  if (kind == 2) return 1;
+  for (j = lo; j <= hi; ++j) {
+    if (j == k || C[j].sb > -1 - MAX_PLANES) continue;
+    int64_t tj = -1 - MAX_PLANES - C[j].sb;
+    if (s->tri_mesh[tj] != s->tri_mesh[t]) continue;
+    tri_feature(s, tj, region[j], &kj, &uj, &vj);
+    if (kind == 1) {
+      if (kj == 2 && tri_has(s, tj, u) && tri_has(s, tj, v)) return 0;
+      if (kj == 1 && uj == u && vj == v && tj < t) return 0;
+    } else {
+      if (kj == 2 && tri_has(s, tj, u)) return 0;
+      if (kj == 1 && (uj == u || vj == u)) return 0;
+      if (kj == 0 && uj == u && tj < t) return 0;
+    }
+  }
+  return 1;
+}
+
+int orc_add_mesh(orc_sys* s, int64_t n_tri, const double* verts, int material, const double X[3],
+                 const double q[4], const double v[3], const double w[3]) {
+  if (n_tri < 1 || material < 0 || material >= s->n_mat) return ORC_ERR_ARG;
+  int m = s->n_mesh++;
+  int64_t t0 = s->n_tri, t;
+  s->n_tri += n_tri;
+  s->mX = (double*)realloc(s->mX, sizeof(double) * 3 * s->n_mesh);
+  s->mQ = (double*)realloc(s->mQ, sizeof(double) * 4 * s->n_mesh);
+  s->mV = (double*)realloc(s->mV, sizeof(double) * 3 * s->n_mesh);
+  s->mW = (double*)realloc(s->mW, sizeof(double) * 3 * s->n_mesh);
+  s->mQs = (double*)realloc(s->mQs, sizeof(double) * 4 * s->n_mesh);
+  s->mF = (double*)realloc(s->mF, sizeof(double) * 3 * s->n_mesh);
+  s->mT = (double*)realloc(s->mT, sizeof(double) * 3 * s->n_mesh);
+  s->mmat = (int32_t*)realloc(s->mmat, sizeof(int32_t) * s->n_mesh);
+  s->tri_mesh = (int32_t*)realloc(s->tri_mesh, sizeof(int32_t) * s->n_tri);
+  s->tri_body = (double*)realloc(s->tri_body, sizeof(double) * 9 * s->n_tri);
+  s->tri_world = (double*)realloc(s->tri_world, sizeof(double) * 9 * s->n_tri);
+  s->tri_vid = (int64_t*)realloc(s->tri_vid, sizeof(int64_t) * 3 * s->n_tri);
+  if (!s->mX || !s->mQ || !s->mV || !s->mW || !s->mQs || !s->mF || !s->mT || !s->mmat || !s->tri_mesh ||
+      !s->tri_body || !s->tri_world || !s->tri_vid)
+    abort();
+  s->mmat[m] = material;
+  for (t = 0; t < n_tri; ++t) s->tri_mesh[t0 + t] = m;
+  memcpy(s->tri_body + 9 * t0, verts, sizeof(double) * 9 * n_tri);
+  /* topology: a vertex id is the first (triangle, corner) of the mesh with bitwise-equal body
+   * coordinates (plain O(n^2) scan) */
+  for (t = 0; t < 3 * n_tri; ++t) {
+    const double* v = verts + 3 * t;
+    int64_t u;
+    for (u = 0; u <= t; ++u)
+      if (memcmp(verts + 3 * u, v, sizeof(double) * 3) == 0) break;
+    s->tri_vid[3 * t0 + t] = 3 * t0 + u;
+  }
+  memset(s->mF + 3 * m, 0, sizeof(double) * 3);
+  memset(s->mT + 3 * m, 0, sizeof(double) * 3);
+  return orc_set_mesh_motion(s, m, X, q, v, w) == ORC_OK ? m : ORC_ERR_ARG;
+}
+
+int orc_set_mesh_motion(orc_sys* s, int m, const double X[3], const double q[4], const double v[3],
+                        const double w[3]) {
+  if (m < 0 || m >= s->n_mesh) return ORC_ERR_ARG;
+  memcpy(s->mX + 3 * m, X, sizeof(double) * 3);
+  memcpy(s->mQ + 4 * m, q, sizeof(double) * 4);
+  memcpy(s->mV + 3 * m, v, sizeof(double) * 3);
+  memcpy(s->mW + 3 * m, w, sizeof(double) * 3);
+  mesh_step_quat(s->h, w, s->mQs + 4 * m);
+  return ORC_OK;
+}
+
+int orc_get_mesh(const orc_sys* s, int m, double X[3], double q[4], double force[3], double torque[3]) {
+  if (m < 0 || m >= s->n_mesh) return ORC_ERR_ARG;
+  if (X) memcpy(X, s->mX + 3 * m, sizeof(double) * 3);
+  if (q) memcpy(q, s->mQ + 4 * m, sizeof(double) * 4);
+  if (force) memcpy(force, s->mF + 3 * m, sizeof(double) * 3);
+  if (torque) memcpy(torque, s->mT + 3 * m, sizeof(double) * 3);
+  return ORC_OK;
+}
+
 /* ------------------------------------------------------------------ lifecycle */
 orc_sys* orc_create(double h, const double gravity[3], double margin, const double dom_lo[3],
                     const double dom_hi[3], int n_mat, const double* mat4, int n_tmpl, const int32_t* ncomp,
@@ -261,6 +499,8 @@ void orc_destroy(orc_sys* s) {
   free(s->mat); free(s->ncomp); free(s->coff); free(s->offs); free(s->rad); free(s->cmat);
   free(s->mass); free(s->inertia); free(s->ppt); free(s->pn); free(s->pmat);
   free(s->hist); free(s->con); free(s->pend);
+  free(s->mX); free(s->mQ); free(s->mV); free(s->mW); free(s->mQs); free(s->mF); free(s->mT);
+  free(s->mmat); free(s->tri_mesh); free(s->tri_body); free(s->tri_world); free(s->tri_vid);
   free(s);
 }
 
@@ -484,6 +724,23 @@ static void detect_grid(orc_sys* s) {
   free(cstart); free(cidx); free(items); free(cc); free(fill);
 }
 
+/* sphere-triangle candidates: |c - closest(c, T)|^2 <= (r + margin)^2 (R25) */
+static void detect_meshes(orc_sys* s) {
+  int64_t a, t;
+  for (a = 0; a < s->ns; ++a) {
+    const double* c = s->s_pos + 3 * a;
+    double r = sphere_radius(s, a);
+    for (t = 0; t < s->n_tri; ++t) {
+      const double* T = s->tri_world + 9 * t;
+      double q[3];
+      orc_closest_on_triangle(c, T, T + 3, T + 6, q);
+      double dx = c[0] - q[0], dy = c[1] - q[1], dz = c[2] - q[2];
+      double sr = r + s->margin;
+      if ((dx * dx + dy * dy) + dz * dz <= sr * sr) push_contact(s, a, -1 - MAX_PLANES - t);
+    }
+  }
+}
+
 static void detect_planes(orc_sys* s) {
   int64_t a;
   int p;
@@ -528,6 +785,7 @@ static void detect_set(orc_sys* s) {
     detect_brute(s);
   else
     detect_grid(s);
+  detect_meshes(s);
   detect_planes(s);
   qsort(s->con, s->nc, sizeof(contact), cmp_contact);
 }
@@ -554,6 +812,8 @@ static int one_step(orc_sys* s) {
       }
     }
   }
+  /* (1b) mesh triangles at this step's mesh poses (NEXT-3) */
+  mesh_world(s);
   /* (2) active contact set: rebuilt every cd_every steps from the margin-enlarged geometry
    * (P:142); cd_every = 1 is the "traditional way".  In between, the same set is
    * used and every member is re-evaluated at each step. */
@@ -592,6 +852,22 @@ static int one_step(orc_sys* s) {
     for (d = 0; d < 3; ++d) s->con[k].ut[d] = hit ? hit->ut[d] : 0.0;
   }
   /* (4) per-contact kinematics (Eq. 2) and forces (Eqs. 1, 3) */
+  int* mreg = NULL;
+  char* mact = NULL;
+  if (s->n_mesh) {
+    memset(s->mF, 0, sizeof(double) * 3 * s->n_mesh);
+    memset(s->mT, 0, sizeof(double) * 3 * s->n_mesh);
+    mreg = (int*)xcalloc(s->nc, sizeof(int));
+    mact = (char*)xcalloc(s->nc, 1);
+    for (k = 0; k < s->nc; ++k)
+      if (s->con[k].sb <= -1 - MAX_PLANES) {
+        const double* T = s->tri_world + 9 * (-1 - MAX_PLANES - s->con[k].sb);
+        double q[3];
+        mreg[k] = orc_closest_on_triangle(s->s_pos + 3 * s->con[k].sa, T, T + 3, T + 6, q);
+      }
+    for (k = 0; k < s->nc; ++k)
+      if (s->con[k].sb <= -1 - MAX_PLANES) mact[k] = (char)mesh_contact_active(s, k, mreg);
+  }
   int64_t* n_ent = (int64_t*)xcalloc(s->ns + 1, sizeof(int64_t));
   for (k = 0; k < s->nc; ++k) {
     n_ent[s->con[k].sa]++;
@@ -612,7 +888,32 @@ static int one_step(orc_sys* s) {
     double n[3], p[3], delta, r_bar, m_bar;
     double Mi = s->mass[s->tid[i]];
     int64_t j = -1;
-    if (sb >= 0) {
+    int mesh = -1;
+    if (sb <= -1 - MAX_PLANES) {
+      /* sphere (a) on a mesh triangle (b): n from the sphere to its closest point on the
+       * triangle, delta = r - |c - q|, R_bar = r and m_bar = M (the flat-wall limit),
+       * contact point at the middle of the overlap as for walls (O6); the triangle moves with
+       * its mesh: v_b = v_m + w_m x (p - X_m) */
+      int64_t t = -1 - MAX_PLANES - sb;
+      const double* T = s->tri_world + 9 * t;
+      double q[3], dv[3];
+      mesh = s->tri_mesh[t];
+      orc_closest_on_triangle(ca, T, T + 3, T + 6, q);
+      for (d = 0; d < 3; ++d) dv[d] = ca[d] - q[d];
+      double dist = sqrt((dv[0] * dv[0] + dv[1] * dv[1]) + dv[2] * dv[2]);
+      if (dist == 0.0) {
+        snprintf(s->err, sizeof s->err, "sphere centre %lld on triangle %lld at step %lld", (long long)C->ka,
+                 (long long)t, (long long)s->steps);
+        free(n_ent); free(e_off); free(ent); free(mreg); free(mact);
+        return ORC_ERR_DEGENERATE;
+      }
+      delta = ra - dist;
+      for (d = 0; d < 3; ++d) n[d] = -(dv[d] / dist);
+      for (d = 0; d < 3; ++d) p[d] = ca[d] + (ra - 0.5 * delta) * n[d];
+      r_bar = ra;
+      m_bar = Mi;
+      mat_b = s->mat + 4 * s->mmat[mesh];
+    } else if (sb >= 0) {
       j = s->s_clump[sb];
       const double* cb = s->s_pos + 3 * sb;
       double rb = sphere_radius(s, sb);
@@ -622,7 +923,7 @@ static int one_step(orc_sys* s) {
       if (dist == 0.0) {
         snprintf(s->err, sizeof s->err, "coincident sphere centres %lld/%lld at step %lld",
                  (long long)C->ka, (long long)C->kb, (long long)s->steps);
-        free(n_ent); free(e_off); free(ent);
+        free(n_ent); free(e_off); free(ent); free(mreg); free(mact);
         return ORC_ERR_DEGENERATE;
       }
       delta = (ra + rb) - dist;
@@ -659,12 +960,18 @@ static int one_step(orc_sys* s) {
       for (d = 0; d < 3; ++d) rj[d] = p[d] - s->X[3 * j + d];
       cross(wj, rj, tmp);
       for (d = 0; d < 3; ++d) vj[d] = s->V[3 * j + d] + tmp[d];
+    } else if (mesh >= 0) {
+      for (d = 0; d < 3; ++d) rj[d] = p[d] - s->mX[3 * mesh + d];
+      cross(s->mW + 3 * mesh, rj, tmp);
+      for (d = 0; d < 3; ++d) vj[d] = s->mV[3 * mesh + d] + tmp[d];
     }
     double vrel[3];
     for (d = 0; d < 3; ++d) vrel[d] = vj[d] - vi[d];
     double pp4[4], fn[3], ft[3], un[3];
     orc_pair_params(mat_a, mat_b, pp4);
     orc_contact_force(pp4[0], pp4[1], pp4[2], pp4[3], r_bar, m_bar, h, delta, n, vrel, C->ut, fn, ft, un);
+    if (mesh >= 0 && !mact[k])
+      for (d = 0; d < 3; ++d) fn[d] = ft[d] = un[d] = 0.0; /* not this feature's contact (R26) */
     for (d = 0; d < 3; ++d) {
       C->F[d] = fn[d] + ft[d];
       C->p[d] = p[d];
@@ -672,6 +979,13 @@ static int one_step(orc_sys* s) {
       C->ut[d] = un[d];
     }
     C->delta = delta;
+    if (mesh >= 0) { /* reaction on the mesh, torque about its reference point */
+      cross(rj, C->F, tmp);
+      for (d = 0; d < 3; ++d) {
+        s->mF[3 * mesh + d] += C->F[d];
+        s->mT[3 * mesh + d] += tmp[d];
+      }
+    }
     /* entries: -F on a at r_i, +F on b at r_j (Eq. 4, reading O1/O11) */
     entry* ea = &ent[e_off[sa] + n_ent[sa]++];
     ea->partner = C->kb;
@@ -709,7 +1023,7 @@ static int one_step(orc_sys* s) {
       s->Tc[3 * cl + d] += ts[d];
     }
   }
-  free(n_ent); free(e_off); free(ent);
+  free(n_ent); free(e_off); free(ent); free(mreg); free(mact);
   /* (6) integrate (Eq. 4a-4b; reading O11/O12): semi-implicit Euler */
   for (c = 0; c < s->n; ++c) {
     int32_t t = s->tid[c];
@@ -759,6 +1073,8 @@ static int one_step(orc_sys* s) {
     double nrm = sqrt(nq[0] * nq[0] + nq[1] * nq[1] + nq[2] * nq[2] + nq[3] * nq[3]);
     for (d = 0; d < 4; ++d) q[d] = nq[d] / nrm;
   }
+  /* (6b) prescribed mesh motion */
+  mesh_advance(s);
   /* (7) this step's set and u_t become the history of the next */
   free(s->hist);
   s->hist = (hist_rec*)xcalloc(s->nc, sizeof(hist_rec));

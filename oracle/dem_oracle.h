@@ -56,6 +56,16 @@ int orc_get_contacts(const orc_sys*, int64_t* ka, int64_t* kb, double* force_b, 
 int orc_get_wrench(const orc_sys*, double* force, double* torque_body);
 const char* orc_last_error(const orc_sys*);
 int64_t orc_steps_done(const orc_sys*);
+/* kinematic triangle meshes (NEXT-3): verts [9 n_tri] body frame; pose X, q (body -> world),
+ * velocity v and angular velocity w (world, about X); returns the mesh index or < 0 */
+int orc_add_mesh(orc_sys*, int64_t n_tri, const double* verts, int material, const double X[3], const double q[4],
+                 const double v[3], const double w[3]);
+int orc_set_mesh_motion(orc_sys*, int m, const double X[3], const double q[4], const double v[3], const double w[3]);
+/* pose after the last step; force on the mesh and torque about X from the last step's contacts */
+int orc_get_mesh(const orc_sys*, int m, double X[3], double q[4], double force[3], double torque[3]);
+/* closest point of triangle (a, b, c) to p; returns its region: 0 face, 1-3 edge ab/ac/bc, 4-6 vertex a/b/c */
+int orc_closest_on_triangle(const double p[3], const double a[3], const double b[3], const double c[3],
+                            double out[3]);
 
 /* single-contact building blocks, exposed for unit pins */
 void orc_pair_params(const double* mat_a4, const double* mat_b4, double out4[4] /* E*, G*, beta, mu */);

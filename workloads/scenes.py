@@ -32,6 +32,17 @@ GID_STRIDE = 64  # sphere gid = clump_gid * 64 + component
 
 
 @dataclass
+class Mesh:
+    """A kinematic triangle mesh (NEXT-3): triangles in the body frame, prescribed motion."""
+    verts: np.ndarray  # (n_tri, 3, 3) body-frame vertices (a, b, c)
+    material: int = 0
+    pos: tuple = (0.0, 0.0, 0.0)  # reference point X (world)
+    quat: tuple = (1.0, 0.0, 0.0, 0.0)  # body -> world
+    vel: tuple = (0.0, 0.0, 0.0)  # world
+    omega: tuple = (0.0, 0.0, 0.0)  # world, about X
+
+
+@dataclass
 class Plane:
     point: tuple
     normal: tuple  # unit, pointing into the domain
@@ -57,6 +68,7 @@ class Scene:
     vel: np.ndarray = None  # (n,3) world
     omega: np.ndarray = None  # (n,3) body frame
     name: str = ""
+    meshes: list = field(default_factory=list)  # kinematic triangle meshes (NEXT-3)
 
     @property
     def n_clumps(self) -> int:
@@ -88,7 +100,7 @@ class Scene:
     def copy(self) -> "Scene":
         return replace(self, gid=self.gid.copy(), tid=self.tid.copy(), pos=self.pos.copy(),
                        quat=self.quat.copy(), vel=self.vel.copy(), omega=self.omega.copy(),
-                       planes=list(self.planes), templates=list(self.templates))
+                       planes=list(self.planes), templates=list(self.templates), meshes=list(self.meshes))
 
     def subset(self, idx) -> "Scene":
         s = self.copy()
@@ -449,3 +461,50 @@ def load_scene(path: str) -> Scene:
                  gravity=z["gravity"], domain_lo=z["domain_lo"], domain_hi=z["domain_hi"],
                  margin=float(z["margin"]), cell_size=float(z["cell_size"]), gid=z["gid"], tid=z["tid"],
                  pos=z["pos"], quat=z["quat"], vel=z["vel"], omega=z["omega"], name=str(z["name"]))
+
+
+# ------------------------------------------------------------------ triangle meshes (NEXT-3)
+def mesh_rect(lx: float, ly: float, nx: int = 1, ny: int = 1) -> np.ndarray:
+    """A flat rectangle [-lx/2, lx/2] x [-ly/2, ly/2] in the body x-y plane, normal +z (counter-
+    clockwise from above), split into nx x ny cells of two triangles each."""
+    xs, ys = np.linspace(-lx / 2, lx / 2, nx + 1), np.linspace(-ly / 2, ly / 2, ny + 1)
+    tris = []
+    for i in range(nx):
+        for j in range(ny):
+            a, b = (xs[i], ys[j], 0.0), (xs[i + 1], ys[j], 0.0)
+            c, d = (xs[i + 1], ys[j + 1], 0.0), (xs[i], ys[j + 1], 0.0)
+            tris += [(a, b, c), (a, c, d)]
+    return np.array(tris, dtype=np.float64)
+
+
+def mesh_cone(radius: float, height: float, n: int = 24) -> np.ndarray:
+    """The lateral surface of a cone with its apex at the body origin pointing down (-z) and a
+    base circle of `radius` at z = height (the penetrometer tip of P:277: 60 deg opening for
+    radius = height tan 30 deg), n facets, outward normals."""
+    th = np.linspace(0.0, 2 * np.pi, n + 1)
+    tris = []
+    for k in range(n):
+        p0 = (radius * np.cos(th[k]), radius * np.sin(th[k]), height)
+        p1 = (radius * np.cos(th[k + 1]), radius * np.sin(th[k + 1]), height)
+        tris.append(((0.0, 0.0, 0.0), p1, p0))
+    return np.array(tris, dtype=np.float64)
+
+
+def sphere_on_mesh(material_sphere=0, material_mesh=0, r: float = 1e-3, drop: float = 0.0, v0=(0.0, 0.0, 0.0),
+                   mesh_vel=(0.0, 0.0, 0.0), mesh_omega=(0.0, 0.0, 0.0), g=(0.0, 0.0, -9.81), h: float = 1e-6,
+                   with_plane: bool = False, materials=None, at=(0.3e-3, -0.2e-3)) -> Scene:
+    """One sphere clump (rho 2600) above a 10 x 10 mm mesh square at z = 0 (or, with_plane,
+    above the analytic plane z = 0 instead): gap `drop`, velocity v0."""
+    mats = np.array(materials if materials is not None else [M0])
+    t = sphere_template(r, material_sphere)
+    gid, tid, pos, quat, vel, om = _mk_state(1)
+    pos[0] = (at[0], at[1], r + drop)
+    vel[0] = v0
+    s = Scene(materials=mats, templates=[t], planes=[], h=h, gravity=np.array(g, float),
+              domain_lo=np.array([-0.02, -0.02, -0.01]), domain_hi=np.array([0.02, 0.02, 0.03]), gid=gid, tid=tid,
+              pos=pos, quat=quat, vel=vel, omega=om, name="sphere-on-mesh")
+    if with_plane:
+        s.planes = [Plane((0.0, 0.0, 0.0), (0.0, 0.0, 1.0), material_mesh)]
+    else:
+        s.meshes = [Mesh(mesh_rect(0.01, 0.01, 2, 2), material_mesh, vel=tuple(mesh_vel), omega=tuple(mesh_omega))]
+    return s
