@@ -213,6 +213,37 @@ dem_status dem_partition_plan(int64_t n, const double* pos, double slab_lo, doub
  * between neighbours.  Lets one GPU run a P-rank decomposition (tests, scaling studies). */
 dem_status dem_step_group(dem_system* const* systems, int32_t n, int64_t n_steps);
 
+/* ---- kinematic triangle meshes (P:277 cone, P:307 funnel, P:344 wheel;
+ * S:241-262).  A mesh is a set of triangles in its body frame with a prescribed motion: reference
+ * point X and orientation q (body -> world), velocity v and angular velocity w (world, about X);
+ * every step advances X += h v and q <- normalize(q_step (x) q), q_step the rotation by h|w|
+ * about w (R27).  A sphere contacts triangle t if |c - closest(c, t)| <= r + margin
+ * (closest point by Voronoi regions, R25); the contact key is (sphere key, INT64_MAX - 16 - t)
+ * with t counted over all meshes in the order added.  The force is the flat-wall limit
+ * (R_bar = r, m_bar = clump mass) with the normal from the sphere to its closest point,
+ * the boundary point velocity v + w x (p - X), and one contact per surface feature: a
+ * sphere touching a shared edge or vertex is pushed once (R26).  At most 8 meshes, 2^24
+ * triangles; not on distributed systems (DEM_ERR_INVALID_ARG). */
+typedef struct {
+  int64_t n_tri;
+  const double* verts;       /* [9 n_tri] body-frame vertices a, b, c of each triangle (copied) */
+  int32_t material;
+  double pos[3], quat[4], vel[3], omega[3];
+} dem_mesh;
+
+/* Add a mesh (host arrays, copied); *mesh_id receives its index.  Call between dem_step calls. */
+dem_status dem_add_mesh(dem_system* sys, const dem_mesh* mesh, int32_t* mesh_id);
+
+/* Replace a mesh's pose and motion before the next step (co-simulation: the caller's multibody
+ * solver sets the pose each step). */
+dem_status dem_set_mesh_motion(dem_system* sys, int32_t mesh, const double pos[3], const double quat[4],
+                               const double vel[3], const double omega[3]);
+
+/* The mesh pose after the last step, and the wrench the granular material exerted on it during
+ * that step: force and torque about X (the sum over its contacts in a fixed order). */
+dem_status dem_get_mesh(dem_system* sys, int32_t mesh, double pos[3], double quat[4], double force[3],
+                        double torque[3]);
+
 /* Clump migration between slabs.  Collective over the n_ranks systems of an
  * NCCL decomposition (every rank calls it at the same point, between dem_step calls).  The
  * largest displacement of an owned COM since the last dem_set_state is reduced over the ranks

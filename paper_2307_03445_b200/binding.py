@@ -47,6 +47,11 @@ class dem_params(C.Structure):
                 ("transport", C.c_int32), ("nccl_id", C.c_ubyte * 128), ("overlap", C.c_int32)]
 
 
+class dem_mesh(C.Structure):
+    _fields_ = [("n_tri", C.c_int64), ("verts", C.POINTER(C.c_double)), ("material", C.c_int32),
+                ("pos", C.c_double * 3), ("quat", C.c_double * 4), ("vel", C.c_double * 3), ("omega", C.c_double * 3)]
+
+
 class dem_stats(C.Structure):
     _fields_ = [("steps", C.c_int64), ("n_clumps", C.c_int64), ("n_spheres", C.c_int64),
                 ("n_owned_clumps", C.c_int64), ("n_owned_spheres", C.c_int64), ("n_ghost_clumps", C.c_int64),
@@ -59,7 +64,8 @@ TRANSPORT_NCCL, TRANSPORT_LOOPBACK = 0, 1
 EXPORTS = ["dem_create", "dem_set_state", "dem_set_contact_history", "dem_step", "dem_synchronize",
            "dem_get_state", "dem_get_contacts", "dem_get_stats", "dem_set_profiling", "dem_get_stage_times",
            "dem_status_string", "dem_last_error", "dem_destroy", "dem_nccl_unique_id", "dem_partition_plan",
-           "dem_step_group", "dem_migrate", "dem_migrate_group"]
+           "dem_step_group", "dem_migrate", "dem_migrate_group", "dem_add_mesh", "dem_set_mesh_motion",
+           "dem_get_mesh"]
 
 _lib = None
 
@@ -93,6 +99,9 @@ def load_library(path: str = LIB_PATH):
     L.dem_step_group.argtypes = [P, I32, I64]
     L.dem_migrate.argtypes = [P, C.c_double, C.POINTER(I32)]
     L.dem_migrate_group.argtypes = [P, I32, C.c_double, C.POINTER(I32)]
+    L.dem_add_mesh.argtypes = [P, C.POINTER(dem_mesh), C.POINTER(I32)]
+    L.dem_set_mesh_motion.argtypes = [P, I32, P, P, P, P]
+    L.dem_get_mesh.argtypes = [P, I32, P, P, P, P]
     for f in EXPORTS:
         if f not in ("dem_destroy", "dem_status_string"):
             getattr(L, f).restype = C.c_int
@@ -237,6 +246,31 @@ class System:
     def dem_synchronize(self):
         self._check(load_library().dem_synchronize(self.sys), "dem_synchronize")
 
+    def dem_add_mesh(self, verts, material=0, pos=(0.0, 0.0, 0.0), quat=(1.0, 0.0, 0.0, 0.0), vel=(0.0, 0.0, 0.0),
+                     omega=(0.0, 0.0, 0.0)) -> int:
+        """Add a kinematic triangle mesh (verts (n_tri, 3, 3) body frame); returns its index."""
+        v = _f64(verts).reshape(-1)
+        m = dem_mesh()
+        m.n_tri = v.shape[0] // 9
+        m.verts = v.ctypes.data_as(C.POINTER(C.c_double))
+        m.material = int(material)
+        m.pos[:], m.quat[:], m.vel[:], m.omega[:] = [[float(x) for x in a] for a in (pos, quat, vel, omega)]
+        out = C.c_int32(-1)
+        self._check(load_library().dem_add_mesh(self.sys, C.byref(m), C.byref(out)), "dem_add_mesh")
+        return out.value
+
+    def dem_set_mesh_motion(self, mesh, pos, quat, vel, omega):
+        arr = [_f64(x) for x in (pos, quat, vel, omega)]
+        self._check(load_library().dem_set_mesh_motion(self.sys, int(mesh), *[_ptr(x) for x in arr]),
+                    "dem_set_mesh_motion")
+
+    def dem_get_mesh(self, mesh=0):
+        """Pose after the last step and the wrench on the mesh from that step's contacts."""
+        X, q, f, t = np.zeros(3), np.zeros(4), np.zeros(3), np.zeros(3)
+        self._check(load_library().dem_get_mesh(self.sys, int(mesh), *[_ptr(x) for x in (X, q, f, t)]),
+                    "dem_get_mesh")
+        return dict(pos=X, quat=q, force=f, torque=t)
+
     def dem_migrate(self, threshold=0.0) -> bool:
         """Collective (NCCL ranks): migrate clumps between slabs if an owned COM moved more than
         `threshold` [m] since the last partition (0 forces it).  True if a migration happened."""
@@ -303,6 +337,8 @@ def system_from_scene(scene, record_contacts=False, cell_size=None, margin=None,
     s = System(scene.materials, templates, planes, h=scene.h, gravity=scene.gravity, domain_lo=scene.domain_lo,
                domain_hi=scene.domain_hi, margin=scene.margin if margin is None else margin,
                cell_size=scene.cell_size if cell_size is None else cell_size, record_contacts=record_contacts, **kw)
+    for m in getattr(scene, "meshes", []):  # kinematic triangle meshes (NEXT-3)
+        s.dem_add_mesh(m.verts, m.material, m.pos, m.quat, m.vel, m.omega)
     s.dem_set_state(scene.gid, scene.tid, scene.pos, scene.quat, scene.vel, scene.omega)
     return s
 

@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdem_b200.so")
-SOURCES = ["system.cu", "kernels_detect.cu", "kernels_force.cu", "kernels_scan.cu"]
+SOURCES = ["system.cu", "kernels_detect.cu", "kernels_force.cu", "kernels_scan.cu", "kernels_mesh.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-Xcompiler", "-fPIC",
          "-shared", "-Xptxas", "-v", "--expt-relaxed-constexpr"]

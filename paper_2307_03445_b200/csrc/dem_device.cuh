@@ -21,6 +21,8 @@ namespace dem {
 
 constexpr int kKeyStride = 64;
 constexpr int kMaxPlanes = 16;
+constexpr int kMaxMeshes = 8;
+constexpr int kMeshRec = 17;  // per mesh: X(3), q(4), v(3), w(3), q_step(4) — DESIGN.md R27
 constexpr int kMaxRowSort = 64;  // rows longer than this are sorted in place in global memory
 
 // device status word (host reads it after each dem_step)
@@ -122,6 +124,20 @@ struct StepArgs {
   double4* ref_out;          // where a counting pose kernel stores the centres it detects from, or null
   const double4* dpos;       // sphere centres the detection kernels read (spos, or the ahead snapshot)
   int* abort;                // abort word of the detection kernels (&ctl->abort, or &ctl->det_abort)
+  // kinematic triangle meshes (NEXT-3): partner code of triangle t = -1 - kMaxPlanes - t,
+  // key INT64_MAX - kMaxPlanes - t
+  int n_tri, n_mesh;
+  const double* tri_body;    // [9 n_tri] body-frame vertices
+  const int* tri_vid;        // [3 n_tri] vertex ids (topology for one contact per feature, R26)
+  const int* tri_mesh;       // [n_tri]
+  double* tri_world;         // [9 n_tri] world vertices of this step (k_mesh_pose)
+  double* tri_snap;          // [9 n_tri] copy for an ahead detection, or null
+  const double* tri_dpos;    // the vertices the detection kernels read (tri_world or tri_snap)
+  double* mesh;              // [kMeshRec n_mesh] pose + motion (advanced by k_mesh_finish)
+  const int* mesh_mat;       // [n_mesh]
+  double* mesh_part;         // [6 n_mesh n_cta] per-CTA wrench partials (force on mesh, torque about X)
+  int* mesh_flag;            // [n_cta] 1 if the CTA wrote a partial this step
+  double* mesh_wrench;       // [6 n_mesh] the last step's wrench
   double half_margin;        // > 0 (cd_every > 1): displacement allowed since the last rebuild
   int n_own, ns_own;         // owned clumps / spheres come first; the rest are ghosts (§8e)
   const double* xref;        // [3 n_own] owned COMs at dem_set_state (distributed drift check)
@@ -225,6 +241,82 @@ __device__ __forceinline__ void point_velocity(double Vx, double Vy, double Vz, 
   ox = __dadd_rn(Vx, __fma_rn(wy, rz, -__dmul_rn(wz, ry)));
   oy = __dadd_rn(Vy, __fma_rn(wz, rx, -__dmul_rn(wx, rz)));
   oz = __dadd_rn(Vz, __fma_rn(wx, ry, -__dmul_rn(wy, rx)));
+}
+
+// ---------------------------------------------------------------- triangles (NEXT-3)
+// Closest point of triangle (a, b, c) to p by Voronoi regions, R25: the operation
+// order of the oracle's plain-C construction, every operation rounded separately, so the
+// sphere-triangle candidate set is a function of the fp64 inputs.  Returns the region: 0 face,
+// 1/2/3 edge ab/ac/bc, 4/5/6 vertex a/b/c.
+__device__ __forceinline__ double dot3r(double ux, double uy, double uz, double vx, double vy, double vz) {
+  return add(add(mul(ux, vx), mul(uy, vy)), mul(uz, vz));
+}
+
+__device__ __forceinline__ int closest_on_triangle(const double* T, double px, double py, double pz, double& qx,
+                                                   double& qy, double& qz) {
+  const double ax = T[0], ay = T[1], az = T[2], bx = T[3], by = T[4], bz = T[5], cx = T[6], cy = T[7], cz = T[8];
+  const double abx = sub(bx, ax), aby = sub(by, ay), abz = sub(bz, az);
+  const double acx = sub(cx, ax), acy = sub(cy, ay), acz = sub(cz, az);
+  const double apx = sub(px, ax), apy = sub(py, ay), apz = sub(pz, az);
+  const double d1 = dot3r(abx, aby, abz, apx, apy, apz), d2 = dot3r(acx, acy, acz, apx, apy, apz);
+  if (d1 <= 0.0 && d2 <= 0.0) {
+    qx = ax; qy = ay; qz = az;
+    return 4;
+  }
+  const double bpx = sub(px, bx), bpy = sub(py, by), bpz = sub(pz, bz);
+  const double d3 = dot3r(abx, aby, abz, bpx, bpy, bpz), d4 = dot3r(acx, acy, acz, bpx, bpy, bpz);
+  if (d3 >= 0.0 && d4 <= d3) {
+    qx = bx; qy = by; qz = bz;
+    return 5;
+  }
+  const double vc = sub(mul(d1, d4), mul(d3, d2));
+  if (vc <= 0.0 && d1 >= 0.0 && d3 <= 0.0) {
+    const double v = __ddiv_rn(d1, sub(d1, d3));
+    qx = add(ax, mul(v, abx)); qy = add(ay, mul(v, aby)); qz = add(az, mul(v, abz));
+    return 1;
+  }
+  const double cpx = sub(px, cx), cpy = sub(py, cy), cpz = sub(pz, cz);
+  const double d5 = dot3r(abx, aby, abz, cpx, cpy, cpz), d6 = dot3r(acx, acy, acz, cpx, cpy, cpz);
+  if (d6 >= 0.0 && d5 <= d6) {
+    qx = cx; qy = cy; qz = cz;
+    return 6;
+  }
+  const double vb = sub(mul(d5, d2), mul(d1, d6));
+  if (vb <= 0.0 && d2 >= 0.0 && d6 <= 0.0) {
+    const double w = __ddiv_rn(d2, sub(d2, d6));
+    qx = add(ax, mul(w, acx)); qy = add(ay, mul(w, acy)); qz = add(az, mul(w, acz));
+    return 2;
+  }
+  const double va = sub(mul(d3, d6), mul(d5, d4));
+  const double e43 = sub(d4, d3), e56 = sub(d5, d6);
+  if (va <= 0.0 && e43 >= 0.0 && e56 >= 0.0) {
+    const double w = __ddiv_rn(e43, add(e43, e56));
+    qx = add(bx, mul(w, sub(cx, bx))); qy = add(by, mul(w, sub(cy, by))); qz = add(bz, mul(w, sub(cz, bz)));
+    return 3;
+  }
+  const double denom = __drcp_rn(add(add(va, vb), vc));
+  const double v = mul(vb, denom), w = mul(vc, denom);
+  qx = add(add(ax, mul(abx, v)), mul(acx, w));
+  qy = add(add(ay, mul(aby, v)), mul(acy, w));
+  qz = add(add(az, mul(abz, v)), mul(acz, w));
+  return 0;
+}
+
+// feature of (triangle, region) for one contact per feature (R26): kind 2 face (u = t),
+// 1 edge (u < v vertex ids), 0 vertex (u)
+__device__ __forceinline__ void tri_feature(const int* vid, int t, int region, int& kind, int& u, int& v) {
+  if (region == 0) {
+    kind = 2; u = v = t;
+  } else if (region <= 3) {
+    const int x = vid[3 * t + (region == 3 ? 1 : 0)], y = vid[3 * t + (region == 1 ? 1 : 2)];
+    kind = 1; u = min(x, y); v = max(x, y);
+  } else {
+    kind = 0; u = v = vid[3 * t + region - 4];
+  }
+}
+
+__device__ __forceinline__ bool tri_has(const int* vid, int t, int x) {
+  return vid[3 * t] == x || vid[3 * t + 1] == x || vid[3 * t + 2] == x;
 }
 
 }  // namespace dem

@@ -431,6 +431,12 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
 // all of them — are sorted and matched in registers; longer ones in place in memory.
 constexpr int kRegRow = 8;
 
+// key of a candidate partner: a sphere's key, or INT64_MAX - kMaxPlanes - t for triangle t
+// (partner code -1 - kMaxPlanes - t, written by k_mesh_pairs): sorts after every sphere
+__device__ __forceinline__ long long partner_key(const StepArgs& a, int code) {
+  return code >= 0 ? a.s_key[code] : 0x7fffffffffffffffLL - (long long)(-1 - code);
+}
+
 __device__ __forceinline__ int prev_index(const Rows& prev, int pb, int pe, long long key) {
   for (int v = pb; v < pe; ++v)
     if (prev.ent[v].key == key) return v;
@@ -471,7 +477,7 @@ __global__ void __launch_bounds__(256) k_rows_finish(StepArgs a) {
     for (int q = 0; q < kRegRow; ++q) tt[q] = q < nc ? S[(size_t)q * a.ns_own] : 0;
 #pragma unroll
     for (int q = 0; q < kRegRow; ++q) {
-      kk[q] = q < nc ? a.s_key[tt[q]] : 0x7fffffffffffffffLL;
+      kk[q] = q < nc ? partner_key(a, tt[q]) : 0x7fffffffffffffffLL;
       hh[q] = -1;
     }
     // odd-even transposition sort (keys of the candidates are distinct; padding sorts last)
@@ -507,7 +513,7 @@ __global__ void __launch_bounds__(256) k_rows_finish(StepArgs a) {
     for (int u = 0; u < nc; ++u) {
       const int t = S[(size_t)u * a.ns_own];
       Entry e;
-      e.key = a.s_key[t];
+      e.key = partner_key(a, t);
       e.partner = t;
       R[u] = e;
     }

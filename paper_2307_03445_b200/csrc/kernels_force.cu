@@ -46,6 +46,61 @@ int force_cta_spheres() { return kMaxS; }
 #ifndef DEM_FORCE_MINB
 #define DEM_FORCE_MINB (1024 / DEM_FORCE_FT)  // 64 registers
 #endif
+// A mesh entry (NEXT-3): the sphere's closest point on the triangle (R25), counted only if it is
+// its feature's contact among the sphere's entries on the same mesh (R26).  Outputs the contact
+// frame as for a wall (n from the sphere to the surface, the middle of the overlap), the mesh's
+// reference point, velocity and angular velocity (the point velocity of the boundary).
+__device__ __noinline__ bool mesh_entry(const StepArgs& a, int tri, int row_beg, int row_end, double cx,
+                                        double cy, double cz, double ri, double& nx, double& ny, double& nz,
+                                        double& px, double& py, double& pz, double& delta, int& mj, double* Xvw,
+                                        int& mesh, bool& degenerate) {
+  const double* T = a.tri_world + 9 * tri;
+  double qx, qy, qz;
+  const int reg = closest_on_triangle(T, cx, cy, cz, qx, qy, qz);
+  const double dx = sub(cx, qx), dy = sub(cy, qy), dz = sub(cz, qz);
+  const double dist = sqrt(add(add(mul(dx, dx), mul(dy, dy)), mul(dz, dz)));
+  degenerate = dist == 0.0;
+  delta = ri - dist;
+  const double inv = 1.0 / dist;
+  nx = -(dx * inv);
+  ny = -(dy * inv);
+  nz = -(dz * inv);
+  const double arm = ri - 0.5 * delta;
+  px = cx + arm * nx;
+  py = cy + arm * ny;
+  pz = cz + arm * nz;
+  mesh = a.tri_mesh[tri];
+  mj = a.mesh_mat[mesh];
+  const double* M = a.mesh + kMeshRec * mesh;
+  Xvw[0] = M[0]; Xvw[1] = M[1]; Xvw[2] = M[2];
+  Xvw[3] = M[7]; Xvw[4] = M[8]; Xvw[5] = M[9];
+  Xvw[6] = M[10]; Xvw[7] = M[11]; Xvw[8] = M[12];
+  // one contact per feature: face > edge > vertex, ties to the lower triangle index
+  int kind, u, v;
+  tri_feature(a.tri_vid, tri, reg, kind, u, v);
+  if (kind == 2) return true;
+  for (int e = row_beg; e < row_end; ++e) {
+    const int code = a.rows.ent[e].partner;
+    if (code > -1 - kMaxPlanes) continue;
+    const int tj = -1 - kMaxPlanes - code;
+    if (tj == tri || a.tri_mesh[tj] != mesh) continue;
+    double ox, oy, oz;
+    const int rj = closest_on_triangle(a.tri_world + 9 * tj, cx, cy, cz, ox, oy, oz);
+    int kj, uj, vj;
+    tri_feature(a.tri_vid, tj, rj, kj, uj, vj);
+    if (kind == 1) {
+      if (kj == 2 && tri_has(a.tri_vid, tj, u) && tri_has(a.tri_vid, tj, v)) return false;
+      if (kj == 1 && uj == u && vj == v && tj < tri) return false;
+    } else {
+      if (kj == 2 && tri_has(a.tri_vid, tj, u)) return false;
+      if (kj == 1 && (uj == u || vj == u)) return false;
+      if (kj == 0 && uj == u && tj < tri) return false;
+    }
+  }
+  return true;
+}
+
+template <bool kMesh>
 __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArgs a) {
   __shared__ int rp[kMaxS + 1];
   __shared__ double4 own_p[kMaxS];
@@ -54,6 +109,11 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
   __shared__ __align__(16) double ck[kFC * kKin];
   __shared__ double part[6][kFT];
   __shared__ double acc[6][kMaxS];
+  // mesh wrench (kMesh): per entry the mesh id (-1: not a mesh entry) and torque about its X
+  __shared__ int emesh[kMesh ? kFT : 1];
+  __shared__ double mtq[3][kMesh ? kFT : 1];
+  __shared__ double cw[kMesh ? kMaxMeshes : 1][6];
+  bool cta_mesh = false;
   const int tid = threadIdx.x;
   const int2 b0 = a.cta_clump[blockIdx.x], b1 = a.cta_clump[blockIdx.x + 1];
   const int c0 = b0.x, c1 = b1.x;
@@ -87,11 +147,13 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
     const double2* src = reinterpret_cast<const double2*>(a.kin + (size_t)kKin * c0);
     for (int k = tid; k < ncl * (kKin / 2); k += kFT) reinterpret_cast<double2*>(ck)[k] = src[k];
   }
+  if (kMesh && tid < kMaxMeshes * 6) cw[tid / 6][tid % 6] = 0.0;
   __syncthreads();
   const double h = a.h;
   const int E0 = rp[0], E1 = rp[nsph];
   for (int c0e = E0; c0e < E1; c0e += kFT) {
     const int e = c0e + tid;
+    if (kMesh) emesh[tid] = -1;
     if (e < E1) {
       // owner: last ls with rp[ls] <= e
       int lo = 0, hi = nsph - 1;
@@ -125,7 +187,18 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
       int mj;
       const bool wall = t < 0;
       bool degenerate = false;
-      if (!wall) {
+      bool active = true;
+      int mesh = -1;
+      if (kMesh && t <= -1 - kMaxPlanes) {
+        double Xvw[9];
+        active = mesh_entry(a, -1 - kMaxPlanes - t, rp[ls], rp[ls + 1], cx, cy, cz, ri, nx, ny, nz, px, py, pz,
+                            delta, mj, Xvw, mesh, degenerate);
+        rbar = ri;
+        mbar = Mi;
+        Xjx = Xvw[0]; Xjy = Xvw[1]; Xjz = Xvw[2];
+        Vjx = Xvw[3]; Vjy = Xvw[4]; Vjz = Xvw[5];
+        Wjx = Xvw[6]; Wjy = Xvw[7]; Wjz = Xvw[8];
+      } else if (!wall) {
         const double4 pj = a.spos[t];
         const double2* kj = reinterpret_cast<const double2*>(a.kin + (size_t)kKin * a.s_clump[t]);
         mj = a.s_mat[t];
@@ -172,11 +245,12 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
       }
       double Fx = 0.0, Fy = 0.0, Fz = 0.0, nux = 0.0, nuy = 0.0, nuz = 0.0;
       const double rix = px - Xx, riy = py - Xy, riz = pz - Xz;
-      if (delta > 0.0) {
-        // contact-point velocities (Eq. 2a)
+      if (delta > 0.0 && active) {
+        // contact-point velocities (Eq. 2a); a mesh point moves with its mesh
         double vix, viy, viz, vjx = 0.0, vjy = 0.0, vjz = 0.0;
         point_velocity(ki[3], ki[4], ki[5], ki[6], ki[7], ki[8], rix, riy, riz, vix, viy, viz);
-        if (!wall) point_velocity(Vjx, Vjy, Vjz, Wjx, Wjy, Wjz, px - Xjx, py - Xjy, pz - Xjz, vjx, vjy, vjz);
+        if (!wall || mesh >= 0)
+          point_velocity(Vjx, Vjy, Vjz, Wjx, Wjy, Wjz, px - Xjx, py - Xjy, pz - Xjz, vjx, vjy, vjz);
         const double vrx = vjx - vix, vry = vjy - viy, vrz = vjz - viz;
         // pair table (system.cu): 2E*, 8G*, 2 sqrt(5/6) beta, mu, sqrt(k_t / S_n) = sqrt(4G*/E*)
         const double* pr = a.tab.pair + kPairStride * (own_mat[ls] * a.tab.n_mat + mj);
@@ -235,6 +309,27 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
       part[3][tid] = __fma_rn(riy, fz, -__dmul_rn(riz, fy));
       part[4][tid] = __fma_rn(riz, fx, -__dmul_rn(rix, fz));
       part[5][tid] = __fma_rn(rix, fy, -__dmul_rn(riy, fx));
+      if (kMesh && mesh >= 0) {
+        // reaction on the mesh: +F at p, torque (p - X_m) x F
+        const double mx = px - Xjx, my = py - Xjy, mz = pz - Xjz;
+        emesh[tid] = mesh;
+        mtq[0][tid] = my * Fz - mz * Fy;
+        mtq[1][tid] = mz * Fx - mx * Fz;
+        mtq[2][tid] = mx * Fy - my * Fx;
+      }
+    }
+    if (kMesh) {
+      // the CTA's mesh wrench, entries in row order (deterministic)
+      if (__syncthreads_or(emesh[tid] >= 0)) {
+        cta_mesh = true;
+        if (tid == 0)
+          for (int q = 0; q < kFT; ++q) {
+            const int m = emesh[q];
+            if (m < 0) continue;
+            cw[m][0] -= part[0][q]; cw[m][1] -= part[1][q]; cw[m][2] -= part[2][q];
+            cw[m][3] += mtq[0][q]; cw[m][4] += mtq[1][q]; cw[m][5] += mtq[2][q];
+          }
+      }
     }
     __syncthreads();
     // (a9, first level) canonical per-sphere sums: entries in row (partner-key) order
@@ -246,6 +341,11 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
       }
     }
     __syncthreads();
+  }
+  if (kMesh) {
+    if (cta_mesh && tid < a.n_mesh * 6)
+      a.mesh_part[((size_t)blockIdx.x * a.n_mesh + tid / 6) * 6 + tid % 6] = cw[tid / 6][tid % 6];
+    if (tid == 0) a.mesh_flag[blockIdx.x] = cta_mesh ? 1 : 0;
   }
   if (tid >= ncl) return;
   // (a9, second level) + (a10): per clump, spheres in component order.
@@ -320,7 +420,11 @@ __global__ void k_count_canonical(Rows r, const long long* __restrict__ s_key, i
 }
 
 void launch_force_integrate(const StepArgs& a, cudaStream_t s) {
-  if (a.n_cta > 0) k_force_integrate<<<a.n_cta, kFT, 0, s>>>(a);
+  if (a.n_cta <= 0) return;
+  if (a.n_tri)
+    k_force_integrate<true><<<a.n_cta, kFT, 0, s>>>(a);
+  else
+    k_force_integrate<false><<<a.n_cta, kFT, 0, s>>>(a);
 }
 void launch_count_canonical(const Rows& r, const long long* s_key, int ns, unsigned long long* out, cudaStream_t s) {
   if (ns) k_count_canonical<<<(ns + 255) / 256, 256, 0, s>>>(r, s_key, ns, out);

@@ -45,8 +45,8 @@ __device__ __forceinline__ int block_excl_scan(int v, int* total) {
 
 __global__ void __launch_bounds__(kScanThreads) k_scan_tiles(const int* __restrict__ in, int* __restrict__ out,
                                                              int* __restrict__ tile_sums, long long n,
-                                                             const int* abort) {
-  if (abort && *abort) return;
+                                                             const int* abort, const int* abort2) {
+  if ((abort && *abort) || (abort2 && *abort2)) return;
   const long long base = (long long)blockIdx.x * kScanTile + (long long)threadIdx.x * kScanItems;
   int v[kScanItems];
   int s = 0;
@@ -66,8 +66,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_tiles(const int* __restri
 }
 
 __global__ void __launch_bounds__(kScanThreads) k_scan_sums(int* tile_sums, int n_tiles, int* out_total,
-                                                            const int* abort) {
-  if (abort && *abort) return;
+                                                            const int* abort, const int* abort2) {
+  if ((abort && *abort) || (abort2 && *abort2)) return;
   int carry = 0;
   for (int b = 0; b < n_tiles; b += kScanThreads) {
     int i = b + threadIdx.x;
@@ -81,8 +81,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_sums(int* tile_sums, int 
 }
 
 __global__ void __launch_bounds__(kScanThreads) k_scan_add(int* out, const int* tile_sums, long long n,
-                                                           const int* abort) {
-  if (abort && *abort) return;
+                                                           const int* abort, const int* abort2) {
+  if ((abort && *abort) || (abort2 && *abort2)) return;
   const int add = tile_sums[blockIdx.x];
   if (add == 0) return;
   const long long base = (long long)blockIdx.x * kScanTile;
@@ -93,15 +93,16 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_add(int* out, const int* 
 long long scan_tiles_needed(long long n) { return (n + kScanTile - 1) / kScanTile; }
 
 // out must hold n + 1 ints; tmp must hold scan_tiles_needed(n) ints
-void launch_excl_scan(const int* in, int* out, long long n, int* tmp, const int* abort, cudaStream_t s) {
+void launch_excl_scan(const int* in, int* out, long long n, int* tmp, const int* abort, cudaStream_t s,
+                      const int* abort2) {
   long long tiles = scan_tiles_needed(n);
   if (tiles == 0) {
     cudaMemsetAsync(out, 0, sizeof(int), s);
     return;
   }
-  k_scan_tiles<<<(unsigned)tiles, kScanThreads, 0, s>>>(in, out, tmp, n, abort);
-  k_scan_sums<<<1, kScanThreads, 0, s>>>(tmp, (int)tiles, out + n, abort);
-  k_scan_add<<<(unsigned)tiles, kScanThreads, 0, s>>>(out, tmp, n, abort);
+  k_scan_tiles<<<(unsigned)tiles, kScanThreads, 0, s>>>(in, out, tmp, n, abort, abort2);
+  k_scan_sums<<<1, kScanThreads, 0, s>>>(tmp, (int)tiles, out + n, abort, abort2);
+  k_scan_add<<<(unsigned)tiles, kScanThreads, 0, s>>>(out, tmp, n, abort, abort2);
 }
 
 }  // namespace dem

@@ -27,11 +27,15 @@ void launch_force_integrate(const StepArgs&, cudaStream_t);
 int force_cta_clumps();
 int force_cta_spheres();
 long long scan_tiles_needed(long long n);
-void launch_excl_scan(const int* in, int* out, long long n, int* tmp, const int* abort, cudaStream_t s);
+void launch_excl_scan(const int* in, int* out, long long n, int* tmp, const int* abort, cudaStream_t s,
+                      const int* abort2 = nullptr);
 void launch_count_canonical(const Rows& r, const long long* s_key, int ns, unsigned long long* out, cudaStream_t s);
 void launch_pack(const State& st, const int* idx, int n, double* buf, cudaStream_t s);
 void launch_unpack(const State& st, const int* idx, int n, const double* buf, cudaStream_t s);
 void launch_max_drift(const State& st, const double* xref, int n, unsigned long long* out, cudaStream_t s);
+void launch_mesh_pose(const StepArgs&, cudaStream_t);
+void launch_mesh_pairs(const StepArgs&, cudaStream_t);
+void launch_mesh_finish(const StepArgs&, cudaStream_t);
 }  // namespace dem
 
 using namespace dem;
@@ -98,7 +102,16 @@ struct dem_system {
   bool pending = false;                  // rows[ep ^ 1] holds a set detected ahead, not yet adopted
   cudaStream_t det_stream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_det = nullptr;
-  int fault_ahead = 0;  // test hook (env DEM_FAULT_AHEAD_OVERFLOW=n): the next n ahead detections report an overflow
+  int fault_ahead = 0;
+  bool debug_serial_det = false;  // debug (env DEM_DEBUG_SERIAL_DET=1): the force steps wait for the ahead detection
+  // kinematic triangle meshes (NEXT-3)
+  int n_mesh = 0, n_tri = 0;
+  std::vector<double> h_tri_body, h_mesh;  // host copies (9 per triangle; kMeshRec per mesh)
+  std::vector<int> h_tri_vid, h_tri_mesh, h_mesh_mat;
+  double *d_tri_body = nullptr, *d_tri_world = nullptr, *d_tri_snap = nullptr, *d_mesh = nullptr,
+         *d_mesh_part = nullptr, *d_mesh_wrench = nullptr;
+  int *d_tri_vid = nullptr, *d_tri_mesh = nullptr, *d_mesh_mat = nullptr, *d_mesh_flag = nullptr;
+  int mesh_part_ctas = 0;  // test hook (env DEM_FAULT_AHEAD_OVERFLOW=n): the next n ahead detections report an overflow
   long long cap_entries = 0;
   Record rec{};
   Ctl* d_ctl = nullptr;
@@ -277,6 +290,19 @@ static StepArgs make_args(dem_system* sys, int kind, bool det = false) {
   a.dpos = det ? sys->d_spos_ref[sys->ep ^ 1] : sys->d_spos;
   a.abort = det ? &sys->d_ctl->det_abort : &sys->d_ctl->abort;
   a.half_margin = deferred ? 0.5 * sys->P.margin : 0.0;
+  a.n_tri = sys->n_tri;
+  a.n_mesh = sys->n_mesh;
+  a.tri_body = sys->d_tri_body;
+  a.tri_vid = sys->d_tri_vid;
+  a.tri_mesh = sys->d_tri_mesh;
+  a.tri_world = sys->d_tri_world;
+  a.tri_snap = kind == K_AHEAD && !det ? sys->d_tri_snap : nullptr;
+  a.tri_dpos = det ? sys->d_tri_snap : sys->d_tri_world;
+  a.mesh = sys->d_mesh;
+  a.mesh_mat = sys->d_mesh_mat;
+  a.mesh_part = sys->d_mesh_part;
+  a.mesh_flag = sys->d_mesh_flag;
+  a.mesh_wrench = sys->d_mesh_wrench;
   a.rec = sys->rec;
   a.record = sys->P.record_contacts ? 1 : 0;
   a.ctl = sys->d_ctl;
@@ -315,6 +341,7 @@ enum { PART_ALL = 0, PART_POSE = 1, PART_DET = 2, PART_FORCE = 3 };
 static void enqueue_pose(dem_system* sys, int kind, cudaStream_t s, cudaEvent_t* ev) {
   StepArgs a = make_args(sys, kind);
   if (ev) cudaEventRecord(ev[0], s);
+  launch_mesh_pose(a, s);
   launch_pose_count(a, s);
   if (ev) cudaEventRecord(ev[1], s);
 }
@@ -322,14 +349,18 @@ static void enqueue_pose(dem_system* sys, int kind, cudaStream_t s, cudaEvent_t*
 static void enqueue_detect(dem_system* sys, int kind, cudaStream_t s, cudaEvent_t* ev) {
   const bool run = kind == K_FULL || kind == K_AHEAD;
   StepArgs a = make_args(sys, kind, /*det=*/kind == K_AHEAD);
+  // an ahead detection also stops on the main abort word (a capacity abort of an earlier step of
+  // the same launch batch: the re-run must find the entry sets as they were)
   const int* abort = a.abort;
-  if (run) launch_excl_scan(sys->d_cell_count, sys->d_cell_start, sys->ncell, sys->d_scan_tmp, abort, s);
+  const int* abort2 = &sys->d_ctl->abort;
+  if (run) launch_excl_scan(sys->d_cell_count, sys->d_cell_start, sys->ncell, sys->d_scan_tmp, abort, s, abort2);
   if (ev) cudaEventRecord(ev[2], s);
   if (run) launch_bin_scatter(a, s);
+  if (run) launch_mesh_pairs(a, s);
   if (ev) cudaEventRecord(ev[3], s);
   if (run) launch_pairs(a, s, sys->n_sm);
   if (ev) cudaEventRecord(ev[4], s);
-  if (run) launch_excl_scan(sys->d_row_cnt, a.rows.row_ptr, sys->ns, sys->d_scan_tmp, abort, s);
+  if (run) launch_excl_scan(sys->d_row_cnt, a.rows.row_ptr, sys->ns, sys->d_scan_tmp, abort, s, abort2);
   if (ev) cudaEventRecord(ev[5], s);
   if (run) launch_rows_finish(a, s);
   if (ev) cudaEventRecord(ev[6], s);
@@ -338,6 +369,7 @@ static void enqueue_detect(dem_system* sys, int kind, cudaStream_t s, cudaEvent_
 static void enqueue_force(dem_system* sys, int kind, cudaStream_t s, cudaEvent_t* ev, bool exchange) {
   StepArgs a = make_args(sys, kind);
   launch_force_integrate(a, s);
+  launch_mesh_finish(a, s);
   if (ev) cudaEventRecord(ev[7], s);
   if (sys->dist) {
     enqueue_pack(sys, a, s);
@@ -469,6 +501,7 @@ extern "C" dem_status dem_create(const dem_params* params, const dem_material* m
   dem_system* sys = new dem_system();
   sys->P = *params;
   if (const char* fi = std::getenv("DEM_FAULT_AHEAD_OVERFLOW")) sys->fault_ahead = std::atoi(fi);
+  if (const char* sd = std::getenv("DEM_DEBUG_SERIAL_DET")) sys->debug_serial_det = std::atoi(sd) != 0;
   sys->stream = (cudaStream_t)cuda_stream;
   sys->n_mat = n_mat;
   sys->n_tmpl = n_tmpl;
@@ -621,6 +654,126 @@ static dem_status alloc_rows(dem_system* sys, long long cap) {
   }
   sys->cap_entries = cap;
   free_graphs(sys);
+  return DEM_OK;
+}
+
+// ------------------------------------------------------------------ meshes (NEXT-3)
+// per-CTA wrench partials of the fused force kernel (sized by the CTA partition and the meshes)
+static dem_status ensure_mesh_buffers(dem_system* sys) {
+  if (!sys->n_mesh) return DEM_OK;
+  const int nc = std::max(1, sys->n_cta);
+  if (sys->mesh_part_ctas != nc || !sys->d_mesh_part) {
+    TRY(alloc_arr(sys, &sys->d_mesh_part, (size_t)nc * kMaxMeshes * 6));
+    TRY(alloc_arr(sys, &sys->d_mesh_flag, (size_t)nc));
+    CK(cudaMemsetAsync(sys->d_mesh_flag, 0, sizeof(int) * nc, sys->stream));
+    sys->mesh_part_ctas = nc;
+  }
+  return DEM_OK;
+}
+
+// one step's rotation of a mesh: h |w| about w/|w| (the exponential map of R12; the oracle's
+// formula, so both sides advance a spinning mesh through the same bits)
+static void mesh_step_quat(double h, const double* w, double* qs) {
+  const double wn = std::sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
+  qs[0] = 1.0;
+  qs[1] = qs[2] = qs[3] = 0.0;
+  if (wn > 0.0) {
+    const double half = 0.5 * (h * wn);
+    const double sn = std::sin(half) / wn;
+    qs[0] = std::cos(half);
+    qs[1] = w[0] * sn;
+    qs[2] = w[1] * sn;
+    qs[3] = w[2] * sn;
+  }
+}
+
+static void mesh_record(const dem_system* sys, const double* X, const double* q, const double* v, const double* w,
+                        double* rec) {
+  for (int d = 0; d < 3; ++d) rec[d] = X[d];
+  for (int d = 0; d < 4; ++d) rec[3 + d] = q[d];
+  for (int d = 0; d < 3; ++d) rec[7 + d] = v[d];
+  for (int d = 0; d < 3; ++d) rec[10 + d] = w[d];
+  mesh_step_quat(sys->P.h, w, rec + 13);
+}
+
+extern "C" dem_status dem_add_mesh(dem_system* sys, const dem_mesh* m, int32_t* mesh_id) {
+  if (!sys || !m || m->n_tri < 1 || !m->verts || m->material < 0 || m->material >= sys->n_mat) return DEM_ERR_INVALID_ARG;
+  if (sys->dist) {
+    sys->err = "meshes are not supported on a distributed system";
+    return DEM_ERR_INVALID_ARG;
+  }
+  if (sys->n_mesh >= kMaxMeshes || (int64_t)sys->n_tri + m->n_tri > (1 << 24)) {
+    sys->err = "too many meshes or triangles";
+    return DEM_ERR_INVALID_ARG;
+  }
+  const double qn = std::sqrt(m->quat[0] * m->quat[0] + m->quat[1] * m->quat[1] + m->quat[2] * m->quat[2] +
+                              m->quat[3] * m->quat[3]);
+  if (std::fabs(qn - 1.0) > 1e-9) return DEM_ERR_INVALID_ARG;
+  CK(cudaStreamSynchronize(sys->stream));
+  CK(cudaStreamSynchronize(sys->det_stream));
+  const int t0 = sys->n_tri, n = (int)m->n_tri;
+  sys->h_tri_body.insert(sys->h_tri_body.end(), m->verts, m->verts + 9 * (size_t)n);
+  // topology: a vertex id is the first corner of the mesh with bitwise-equal body coordinates
+  std::unordered_map<std::string, int> first;
+  for (int k = 0; k < 3 * n; ++k) {
+    std::string key((const char*)(m->verts + 3 * (size_t)k), 3 * sizeof(double));
+    auto it = first.emplace(key, 3 * t0 + k).first;
+    sys->h_tri_vid.push_back(it->second);
+  }
+  for (int k = 0; k < n; ++k) sys->h_tri_mesh.push_back(sys->n_mesh);
+  sys->h_mesh_mat.push_back(m->material);
+  sys->h_mesh.resize((size_t)kMeshRec * (sys->n_mesh + 1));
+  mesh_record(sys, m->pos, m->quat, m->vel, m->omega, sys->h_mesh.data() + (size_t)kMeshRec * sys->n_mesh);
+  // device copies: the mesh records are copied from the device first (poses advanced by steps)
+  if (sys->n_mesh && sys->d_mesh)
+    CK(cudaMemcpy(sys->h_mesh.data(), sys->d_mesh, sizeof(double) * kMeshRec * sys->n_mesh, cudaMemcpyDeviceToHost));
+  sys->n_mesh += 1;
+  sys->n_tri += n;
+  auto up = [&](auto** dst, const auto& vec) -> dem_status {
+    using T = std::remove_reference_t<decltype(**dst)>;
+    TRY(alloc_arr(sys, dst, vec.size()));
+    CK(cudaMemcpyAsync(*dst, vec.data(), sizeof(T) * vec.size(), cudaMemcpyHostToDevice, sys->stream));
+    return DEM_OK;
+  };
+  TRY(up(&sys->d_tri_body, sys->h_tri_body));
+  TRY(up(&sys->d_tri_vid, sys->h_tri_vid));
+  TRY(up(&sys->d_tri_mesh, sys->h_tri_mesh));
+  TRY(up(&sys->d_mesh_mat, sys->h_mesh_mat));
+  TRY(up(&sys->d_mesh, sys->h_mesh));
+  TRY(alloc_arr(sys, &sys->d_tri_world, (size_t)9 * sys->n_tri));
+  TRY(alloc_arr(sys, &sys->d_tri_snap, (size_t)9 * sys->n_tri));
+  TRY(alloc_arr(sys, &sys->d_mesh_wrench, (size_t)6 * kMaxMeshes));
+  CK(cudaMemsetAsync(sys->d_mesh_wrench, 0, sizeof(double) * 6 * kMaxMeshes, sys->stream));
+  sys->mesh_part_ctas = 0;
+  TRY(ensure_mesh_buffers(sys));
+  CK(cudaStreamSynchronize(sys->stream));
+  free_graphs(sys);
+  if (mesh_id) *mesh_id = sys->n_mesh - 1;
+  return DEM_OK;
+}
+
+extern "C" dem_status dem_set_mesh_motion(dem_system* sys, int32_t mesh, const double pos[3], const double quat[4],
+                                          const double vel[3], const double omega[3]) {
+  if (!sys || mesh < 0 || mesh >= sys->n_mesh || !pos || !quat || !vel || !omega) return DEM_ERR_INVALID_ARG;
+  double rec[kMeshRec];
+  mesh_record(sys, pos, quat, vel, omega, rec);
+  // ordered on the system stream after the steps already launched
+  CK(cudaMemcpyAsync(sys->d_mesh + (size_t)kMeshRec * mesh, rec, sizeof(rec), cudaMemcpyHostToDevice, sys->stream));
+  CK(cudaStreamSynchronize(sys->stream));
+  return DEM_OK;
+}
+
+extern "C" dem_status dem_get_mesh(dem_system* sys, int32_t mesh, double pos[3], double quat[4], double force[3],
+                                   double torque[3]) {
+  if (!sys || mesh < 0 || mesh >= sys->n_mesh) return DEM_ERR_INVALID_ARG;
+  CK(cudaStreamSynchronize(sys->stream));
+  double rec[kMeshRec], w[6];
+  CK(cudaMemcpy(rec, sys->d_mesh + (size_t)kMeshRec * mesh, sizeof(rec), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(w, sys->d_mesh_wrench + 6 * mesh, sizeof(w), cudaMemcpyDeviceToHost));
+  if (pos) std::memcpy(pos, rec, 3 * sizeof(double));
+  if (quat) std::memcpy(quat, rec + 3, 4 * sizeof(double));
+  if (force) std::memcpy(force, w, 3 * sizeof(double));
+  if (torque) std::memcpy(torque, w + 3, 3 * sizeof(double));
   return DEM_OK;
 }
 
@@ -867,6 +1020,7 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
     if (n_own > 0) cta.push_back((int)n_own);
   }
   sys->n_cta = (int)cta.size() - 1;
+  TRY(ensure_mesh_buffers(sys));
   TRY(alloc_arr(sys, &sys->d_cta_clump, cta.size()));
   TRY(alloc_arr(sys, &sys->d_cell_count, ncell));
   TRY(alloc_arr(sys, &sys->d_cell_start, ncell + 1));
@@ -1044,9 +1198,37 @@ static void advance_parities(dem_system* sys, int kind) {
   sys->launched++;
 }
 
+// Deferred sets and moving meshes: a sphere may move margin/2 from where its set was detected
+// (checked on the device), so a mesh point may move the other margin/2 over the steps a set is
+// used (k, or 2k - 2 with the overlapped cadence): (|v| + |w| R_max) h lag <= margin/2.
+static dem_status check_mesh_motion(dem_system* sys) {
+  if (sys->P.cd_every <= 1 || !sys->n_mesh) return DEM_OK;
+  const int lag = sys->P.overlap ? 2 * sys->P.cd_every - 2 : sys->P.cd_every;
+  std::vector<double> rec((size_t)kMeshRec * sys->n_mesh);
+  CK(cudaMemcpy(rec.data(), sys->d_mesh, sizeof(double) * rec.size(), cudaMemcpyDeviceToHost));
+  for (int m = 0; m < sys->n_mesh; ++m) {
+    const double* M = rec.data() + (size_t)kMeshRec * m;
+    double rmax = 0.0;
+    for (int t = 0; t < sys->n_tri; ++t)
+      if (sys->h_tri_mesh[t] == m)
+        for (int k = 0; k < 3; ++k) {
+          const double* v = sys->h_tri_body.data() + 9 * (size_t)t + 3 * k;
+          rmax = std::max(rmax, std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]));
+        }
+    const double sp = std::sqrt(M[7] * M[7] + M[8] * M[8] + M[9] * M[9]) +
+                      std::sqrt(M[10] * M[10] + M[11] * M[11] + M[12] * M[12]) * rmax;
+    if (sp * sys->P.h * lag > 0.5 * sys->P.margin) {
+      sys->err = "mesh " + std::to_string(m) + " moves more than margin/2 while a deferred contact set is in use";
+      return DEM_ERR_VMAX;
+    }
+  }
+  return DEM_OK;
+}
+
 extern "C" dem_status dem_step(dem_system* sys, int64_t n_steps) {
   if (!sys || n_steps < 0) return DEM_ERR_INVALID_ARG;
   if (sys->h_ctl->err_code) return (dem_status)sys->h_ctl->err_code;
+  TRY(check_mesh_motion(sys));
   int64_t remaining = n_steps;
   int guard = 0;
   struct Sched {
@@ -1080,6 +1262,7 @@ extern "C" dem_status dem_step(dem_system* sys, int64_t n_steps) {
           CK(cudaMemcpyAsync(&sys->d_ctl->det_abort, &kOne, sizeof(int), cudaMemcpyHostToDevice, sys->det_stream));
         }
         CK(cudaEventRecord(sys->ev_det, sys->det_stream));
+        if (sys->debug_serial_det) CK(cudaStreamWaitEvent(sys->stream, sys->ev_det, 0));
         CK(cudaGraphLaunch(gf, sys->stream));
       } else {
         if (kind == K_ADOPT) CK(cudaStreamWaitEvent(sys->stream, sys->ev_det, 0));
@@ -1119,6 +1302,11 @@ extern "C" dem_status dem_step(dem_system* sys, int64_t n_steps) {
       return DEM_ERR_CAPACITY;
     }
     CK(cudaStreamSynchronize(sys->det_stream));
+    if (std::getenv("DEM_DEBUG_LOG"))
+      std::fprintf(stderr, "dem: regrow at step %lld (kind %d, pending %d): need entries %lld inserts %lld width %lld det_abort %d\n",
+                   (long long)done, sched[(size_t)done].since == 0 ? (sched[(size_t)done].pending ? K_ADOPT : K_FULL) : -1,
+                   (int)sched[(size_t)done].pending, sys->h_ctl->need_entries, sys->h_ctl->need_inserts,
+                   sys->h_ctl->need_width, sys->h_ctl->det_abort);
     sys->regrows++;
     sys->up = sched[(size_t)done].up;
     sys->ep = sched[(size_t)done].ep;
@@ -1354,7 +1542,7 @@ extern "C" dem_status dem_get_stats(dem_system* sys, dem_stats* out) {
   out->n_cells = sys->ncell;
   out->cell_size = sys->grid.cell;
   out->regrows = sys->regrows;
-  out->kernel_launches_per_step = kLaunchesPerStep + (sys->dist ? 4 : 0);
+  out->kernel_launches_per_step = kLaunchesPerStep + (sys->dist ? 4 : 0) + (sys->n_mesh ? 3 : 0);
   if (sys->launched > 0 && sys->ns > 0) {
     const RowBuf& R = sys->rows[sys->ep];
     int tot = 0, ins = 0;

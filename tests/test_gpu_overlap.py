@@ -121,3 +121,20 @@ def test_overlap_needs_cd_every(dem):
     s, _ = _fast()
     with pytest.raises(dem.DemError):
         dem.system_from_scene(s, margin=1e-4, cd_every=1, overlap=True)
+
+
+def test_overlap_after_a_capacity_regrow_of_the_first_rebuild(dem):
+    """A wide margin overflows the initial candidate-row width in the first (in-line) rebuild; the
+    ahead detections already queued behind it in the same dem_step must not touch the entry sets
+    the re-run reads (regression: their row scan used to run on the stale counts)."""
+    from workloads import beds
+
+    s = beds.load_patch()
+    k = 4
+    margin = 2.0 * 12.0 * s.h * (2 * k - 2)
+    ref = dem.system_from_scene(s)
+    ref.dem_step(9)
+    d = dem.system_from_scene(s, margin=margin, cd_every=k, overlap=True)
+    d.dem_step(9)
+    assert d.dem_get_stats()["regrows"] >= 1
+    _same_state(ref.dem_get_state(), d.dem_get_state())

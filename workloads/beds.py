@@ -113,3 +113,29 @@ def crop(scene: Scene, lo, hi) -> Scene:
     lo, hi = np.asarray(lo), np.asarray(hi)
     sel = np.nonzero(np.all((scene.pos >= lo) & (scene.pos <= hi), axis=1))[0]
     return scene.subset(sel)
+
+
+def patch_mesh(cone_speed: float = 0.5, spin: float = 0.0, depth: float = 1.0e-3) -> Scene:
+    """Mesh parity bed (NEXT-3): the settled 30 mm patch with its floor plane replaced by an 18-
+    triangle mesh plate of another material, and a 24-facet 60-degree cone (base radius
+    6 mm) whose apex starts `depth` below the bed surface, pushed down at `cone_speed` and
+    optionally spun about its axis at `spin` rad/s."""
+    from .scenes import MAT_B, Mesh, mesh_cone, mesh_rect
+
+    s = load_patch()
+    floor = [p for p in s.planes if p.normal[2] > 0.5][0]
+    s.planes = [p for p in s.planes if not p.normal[2] > 0.5]
+    s.materials = np.array([M0, MAT_B])
+    side_x = max(pl.point[0] for pl in s.planes if pl.normal[0] < 0)
+    side_y = max(pl.point[1] for pl in s.planes if pl.normal[1] < 0)
+    cx, cy = 0.5 * side_x, 0.5 * side_y
+    s.meshes = [Mesh(mesh_rect(side_x + 2e-3, side_y + 2e-3, 3, 3), 1, pos=(cx, cy, float(floor.point[2])))]
+    rc = 6e-3
+    hc = rc / math.tan(math.radians(30.0))
+    near = np.hypot(s.pos[:, 0] - cx, s.pos[:, 1] - cy) < 5e-3
+    top = float(s.pos[near, 2].max())
+    s.meshes.append(Mesh(mesh_cone(rc, hc, 24), 0, pos=(cx + 0.37e-3, cy - 0.21e-3, top - depth),
+                         vel=(0.0, 0.0, -cone_speed), omega=(0.0, 0.0, spin)))
+    s.domain_hi = np.array(s.domain_hi, dtype=float) + np.array([0.0, 0.0, hc + 0.02])
+    s.name = "patch-mesh"
+    return s

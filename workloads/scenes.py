@@ -508,3 +508,25 @@ def sphere_on_mesh(material_sphere=0, material_mesh=0, r: float = 1e-3, drop: fl
     else:
         s.meshes = [Mesh(mesh_rect(0.01, 0.01, 2, 2), material_mesh, vel=tuple(mesh_vel), omega=tuple(mesh_omega))]
     return s
+
+
+def c1_mesh(seed: int = 1, cone_speed: float = 1.0, spin: float = 0.0) -> Scene:
+    """The C1 box with two kinematic meshes (NEXT-3): its floor replaced by a 3 x 3-cell mesh plate
+    (18 triangles, a different material) and a 24-facet 60-degree cone (the P:277 penetrometer
+    tip: base radius 4 mm, apex down) entering the top layer at `cone_speed`, optionally spinning
+    about its axis at `spin` rad/s (a wheel-like moving boundary)."""
+    s = c1_box(seed)
+    lo = np.array([p.point[2] for p in s.planes if p.normal[2] > 0.5])[0]
+    s.planes = [p for p in s.planes if not p.normal[2] > 0.5]
+    s.materials = np.array([M0, MAT_B])
+    side = float(s.domain_hi[0] - s.domain_lo[0])
+    c = 0.5 * (s.domain_lo + s.domain_hi)
+    s.meshes.append(Mesh(mesh_rect(side, side, 3, 3), 1, pos=(float(c[0]), float(c[1]), float(lo))))
+    top = float(s.pos[:, 2].max())
+    rc = 4e-3
+    hc = rc / math.tan(math.radians(30.0))
+    s.meshes.append(Mesh(mesh_cone(rc, hc, 24), 0, pos=(float(c[0]) + 0.4e-3, float(c[1]) - 0.3e-3, top - 0.5e-3),
+                         vel=(0.0, 0.0, -cone_speed), omega=(0.0, 0.0, spin)))
+    s.domain_hi = s.domain_hi + np.array([0.0, 0.0, hc + 2e-3])
+    s.name = "C1-mesh"
+    return s
