@@ -89,14 +89,16 @@ def stage_bytes(st):
     ins, ent = st["n_inserts"], st["n_entries"]
     pairs = ent - st["n_contacts"]  # entries = walls + 2 pairs, contacts = walls + pairs
     return {
-        "pose+bin_count": n * 188 + ns * 44 + nc * 8,
+        "pose+bin_count": n * 188 + ns * 46 + nc * 8,
         "bin_scan": nc * 8,
         "bin_scatter": ns * 32 + nc * 12 + ins * 4,
         # bin bounds, items, each member record (x, y, z, r, clump) once, 2 candidate slots +
         # 2 row-count atomics (read + write) per pair
         "pairs": nc * 4 + ins * 4 + ns * 36 + pairs * 24,
         "row_scan": ns * 8,
-        "rows_finish": ns * 40 + ent * 32 + pairs * 2 * 12,
+        # row bounds of the new and previous rows, the pose kernel's wall mask; entries written and
+        # the previous row's entries read once; per pair 2 candidate slots + 2 partner keys
+        "rows_finish": ns * 18 + ent * 32 + pairs * 2 * 12,
         "force+integrate": ns * (32 + 8 + 8) + n * (80 + 56 + 4 + 104) + ent * 72,
     }
 

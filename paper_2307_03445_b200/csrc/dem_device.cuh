@@ -146,6 +146,7 @@ struct StepArgs {
   int* cell_start;
   int* items;                // [cap_inserts] bin items: sphere index | lowest-bin mask << 29
   int* row_cnt;              // walls + sphere partners per sphere (built by atomics each step)
+  unsigned short* wall_mask; // [ns] sphere-plane candidates of the detection (bit p: plane p)
   int* slots;                // [row_width][ns_own] candidate partners of the owned spheres (k_pairs)
   int row_width;             // slots per sphere (walls included: slot w is the w-th entry of the row)
   Rows rows, prev;

@@ -73,14 +73,16 @@ __global__ void __launch_bounds__(256) k_pose_count(StepArgs a) {
   if (!a.count) return;
   if (a.ref_out) a.ref_out[i] = make_double4(cx, cy, cz, r);
   // sphere-plane candidates: (r + margin) - (c - p_w).n_w >= 0
-  int walls = 0;
+  unsigned wmask = 0;
   for (int p = 0; p < a.tab.n_planes; ++p) {
     const double* pp = a.tab.plane_pt[p];
     const double* nw = a.tab.plane_n[p];
     const double dd = add(add(mul(sub(cx, pp[0]), nw[0]), mul(sub(cy, pp[1]), nw[1])), mul(sub(cz, pp[2]), nw[2]));
-    walls += sub(add(r, a.margin), dd) >= 0.0;
+    if (sub(add(r, a.margin), dd) >= 0.0) wmask |= 1u << p;
   }
-  a.row_cnt[i] = i < a.ns_own ? walls : 0;  // ghosts get no rows (their owners evaluate them)
+  // ghosts get no rows (their owners evaluate them); the mask goes to k_rows_finish
+  a.row_cnt[i] = i < a.ns_own ? __popc(wmask) : 0;
+  a.wall_mask[i] = (unsigned short)wmask;
   int lx, hx, ly, hy, lz, hz;
   cell_range(g, 0, cx, r, lx, hx);
   cell_range(g, 1, cy, r, ly, hy);
@@ -180,13 +182,17 @@ __device__ __forceinline__ void decode_tri(int p, int& i, int& j) {
 
 // one directed candidate: partner t in slot `slot` of own's row (slot -1: own is a ghost,
 // evaluated by its owner); a slot beyond the row width asks the host for wider rows
+__device__ __noinline__ void slot_overflow(Ctl* ctl, int* abort, int slot) {
+  atomicMax(&ctl->need_width, (long long)slot + 1);
+  atomicExch(abort, 1);
+}
+
 __device__ __forceinline__ void put_slot(const StepArgs& a, int own, int slot, int t) {
   if (slot < 0) return;
   if (slot < a.row_width) {
     a.slots[(size_t)slot * a.ns_own + own] = t;  // slot-major: k_rows_finish reads coalesced
   } else {
-    atomicMax(&a.ctl->need_width, (long long)slot + 1);
-    atomicExch(a.abort, 1);
+    slot_overflow(a.ctl, a.abort, slot);  // cold path, kept out of the loop's registers
   }
 }
 
@@ -459,14 +465,7 @@ __global__ void __launch_bounds__(256) k_rows_finish(StepArgs a) {
   const int m = a.rows.row_ptr[i + 1] - beg;
   const int pb = a.prev.row_ptr[i], pe = a.prev.row_ptr[i + 1];
   Entry* R = a.rows.ent + beg;
-  const double4 s = a.dpos[i];
-  unsigned wmask = 0;  // walls, same exactly rounded predicate as k_pose_count's count
-  for (int p = 0; p < a.tab.n_planes; ++p) {
-    const double* pp = a.tab.plane_pt[p];
-    const double* nw = a.tab.plane_n[p];
-    const double dd = add(add(mul(sub(s.x, pp[0]), nw[0]), mul(sub(s.y, pp[1]), nw[1])), mul(sub(s.z, pp[2]), nw[2]));
-    if (sub(add(s.w, a.margin), dd) >= 0.0) wmask |= 1u << p;
-  }
+  const unsigned wmask = a.wall_mask[i];  // the pose kernel's sphere-plane candidates
   const int w = __popc(wmask);
   const int nc = m - w;  // k_pairs handed out slots [w, m) of the candidate list
   const int* S = a.slots + (size_t)w * a.ns_own + i;  // S[q * ns_own]: candidate q

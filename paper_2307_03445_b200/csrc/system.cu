@@ -90,6 +90,7 @@ struct dem_system {
   long long ncell = 0, cap_inserts = 0;
   int *d_cell_count = nullptr, *d_cell_start = nullptr, *d_items = nullptr;
   int *d_row_cnt = nullptr, *d_scan_tmp = nullptr;
+  unsigned short* d_wall_mask = nullptr;
   // rows: the entry sets (row_ptr, ent) of rows[ep] are the latest contact set and ping-pong
   // at every rebuild; the u_t arrays of rows[up] hold the latest tangential history and
   // ping-pong at every step; the state ping-pongs every step (sp)
@@ -277,6 +278,7 @@ static StepArgs make_args(dem_system* sys, int kind, bool det = false) {
   a.cell_start = sys->d_cell_start;
   a.items = sys->d_items;
   a.row_cnt = sys->d_row_cnt;
+  a.wall_mask = sys->d_wall_mask;
   const RowBuf& E = sys->rows[rebuild ? sys->ep ^ 1 : sys->ep];
   const RowBuf& Q = sys->rows[sys->ep];
   a.rows = Rows{E.row_ptr, E.ent, sys->rows[sys->up ^ 1].ut};
@@ -1026,6 +1028,7 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
   TRY(alloc_arr(sys, &sys->d_cell_start, ncell + 1));
   TRY(alloc_arr(sys, &sys->d_items, ins));
   TRY(alloc_arr(sys, &sys->d_row_cnt, ns + 1));
+  TRY(alloc_arr(sys, &sys->d_wall_mask, ns + 1));
   TRY(alloc_arr(sys, &sys->d_scan_tmp, std::max(scan_tiles_needed(ncell), scan_tiles_needed(ns)) + 1));
   for (int p = 0; p < 2; ++p) TRY(alloc_arr(sys, &sys->rows[p].row_ptr, ns + 1));
   // halo buffers and the partition-time COMs of owned clumps (drift check)
