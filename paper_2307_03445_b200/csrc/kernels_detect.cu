@@ -241,12 +241,15 @@ __device__ __forceinline__ void push_hits(const StepArgs& a, int2* bf, int& nbuf
 
 // candidate predicate (R14): different clumps, at least one owned (ghost-ghost
 // pairs belong to other ranks), |d|^2 <= (r_a + r_b + margin)^2 with explicit roundings
+template <bool kGhosts, bool kMargin>
 __device__ __forceinline__ bool candidate(const StepArgs& a, const int2& mi, const int2& mj, const double4& pi,
                                           const double4& pj) {
   const double dx = sub(pj.x, pi.x), dy = sub(pj.y, pi.y), dz = sub(pj.z, pi.z);
   const double d2 = add(add(mul(dx, dx), mul(dy, dy)), mul(dz, dz));
-  const double s = add(add(pi.w, pj.w), a.margin);
-  return mi.x != mj.x && min(mi.x, mj.x) < a.n_own && d2 <= mul(s, s);
+  // (r_a + r_b) + 0 is r_a + r_b exactly: the margin add is skipped when there is none
+  const double s = kMargin ? add(add(pi.w, pj.w), a.margin) : add(pi.w, pj.w);
+  // ghost-ghost pairs belong to other ranks (only a distributed system holds ghosts)
+  return mi.x != mj.x && (!kGhosts || min(mi.x, mj.x) < a.n_own) && d2 <= mul(s, s);
 }
 
 constexpr int kTri = kFlatMax * (kFlatMax - 1) / 2;
@@ -257,6 +260,7 @@ __constant__ float c_rcp[kFlatMax + 8] = {1.0f,      DEM_R8(1),  DEM_R8(9),  DEM
                                           DEM_R8(33), DEM_R8(41), DEM_R8(49), DEM_R8(57)};
 #undef DEM_R8
 
+template <bool kGhosts, bool kMargin>
 __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepArgs a) {
   __shared__ Members smA[kPairWarps];
   __shared__ int2 sbuf[kPairWarps][kPairBuf];
@@ -376,7 +380,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
               j = B0 + r;
             }
             const int2 mi = A.meta[i], mj = A.meta[j];
-            hit = candidate(a, mi, mj, A.p[i], A.p[j]);
+            hit = candidate<kGhosts, kMargin>(a, mi, mj, A.p[i], A.p[j]);
             ia = mi.y;
             ib = mj.y;
           }
@@ -414,7 +418,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
                 const int2 mu = A.meta[i];
                 const int2 mv = A.meta[ob + j];
                 if (((unsigned)(mu.y | mv.y) >> 29) == 7u) {
-                  hit = candidate(a, mu, mv, A.p[i], A.p[ob + j]);
+                  hit = candidate<kGhosts, kMargin>(a, mu, mv, A.p[i], A.p[ob + j]);
                   ia = mu.y & 0x1fffffff;
                   ibx = mv.y & 0x1fffffff;
                 }
@@ -555,7 +559,15 @@ void launch_pairs(const StepArgs& a, cudaStream_t s, int n_sm) {
   long long cap = (long long)n_sm * 8 * 16;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  k_pairs<<<(unsigned)blocks, kPairWarps * 32, 0, s>>>(a);
+  const bool ghosts = a.n_own < a.n, margin = a.margin != 0.0;
+  if (ghosts && margin)
+    k_pairs<true, true><<<(unsigned)blocks, kPairWarps * 32, 0, s>>>(a);
+  else if (ghosts)
+    k_pairs<true, false><<<(unsigned)blocks, kPairWarps * 32, 0, s>>>(a);
+  else if (margin)
+    k_pairs<false, true><<<(unsigned)blocks, kPairWarps * 32, 0, s>>>(a);
+  else
+    k_pairs<false, false><<<(unsigned)blocks, kPairWarps * 32, 0, s>>>(a);
 }
 void launch_rows_finish(const StepArgs& a, cudaStream_t s) {
   if (a.ns) k_rows_finish<<<(a.ns + 255) / 256, 256, 0, s>>>(a);
