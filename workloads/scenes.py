@@ -530,3 +530,17 @@ def c1_mesh(seed: int = 1, cone_speed: float = 1.0, spin: float = 0.0) -> Scene:
     s.domain_hi = s.domain_hi + np.array([0.0, 0.0, hc + 2e-3])
     s.name = "C1-mesh"
     return s
+
+
+def mesh_funnel(r_top: float, r_bottom: float, height: float, n: int = 32) -> np.ndarray:
+    """A conical hopper (frustum side wall, open at both ends): radius r_bottom at body z = 0 and
+    r_top at z = height, n facets of two triangles."""
+    th = np.linspace(0.0, 2 * np.pi, n + 1)
+    tris = []
+    for k in range(n):
+        a = (r_bottom * np.cos(th[k]), r_bottom * np.sin(th[k]), 0.0)
+        b = (r_bottom * np.cos(th[k + 1]), r_bottom * np.sin(th[k + 1]), 0.0)
+        c = (r_top * np.cos(th[k + 1]), r_top * np.sin(th[k + 1]), height)
+        d = (r_top * np.cos(th[k]), r_top * np.sin(th[k]), height)
+        tris += [(a, b, c), (a, c, d)]
+    return np.array(tris, dtype=np.float64)
