@@ -11,7 +11,10 @@ WANT = ["Duration", "DRAM Throughput", "Memory Throughput", "L1/TEX Cache Throug
         "Warp Cycles Per Issued Instruction", "Dynamic Shared Memory Per Block", "Static Shared Memory Per Block"]
 RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
        "l1tex__t_set_accesses_pipe_lsu_mem_global_op_atom.sum", "lts__t_sectors_op_atom.sum",
-       "lts__t_sectors_op_red.sum", "sm__inst_executed_pipe_fp64.sum", "lts__t_bytes.sum"]
+       "lts__t_sectors_op_red.sum", "sm__inst_executed_pipe_fp64.sum", "lts__t_bytes.sum",
+       "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+       "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
+       "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
 
 
 def summarise(rep):

@@ -14,4 +14,6 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 1500 ncu --set full --import-source on --clock-control none \
   -k regex:"k_pose_count|k_bin_scatter|k_pairs|k_rows_finish|k_force_integrate" --launch-skip 15 --launch-count 5 \
   -o "$OUT/full" python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-variants > "$OUT/full.log" 2>&1
+# measured FP64 FMA peak (SURVEY §8d FP64 check)
+nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o /tmp/fp64_peak tools/fp64_peak.cu && /tmp/fp64_peak > "$OUT/fp64_peak.json"
 tail -c 300 "$OUT/bench.json"

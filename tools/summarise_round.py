@@ -57,6 +57,9 @@ def main(rnd):
     ref = os.path.join(src, "bench_reference.json")
     if os.path.exists(ref):
         json.dump(last_json_line(ref), open(os.path.join(dst, "bench_reference_oracle.json"), "w"))
+    fp = os.path.join(src, "fp64_peak.json")
+    if os.path.exists(fp):
+        shutil.copy(fp, os.path.join(dst, "fp64_peak.json"))
     lc = os.path.join(src, "launches.csv")
     if os.path.exists(lc):
         shutil.copy(lc, os.path.join(dst, "ncu_launches_c5.csv"))
