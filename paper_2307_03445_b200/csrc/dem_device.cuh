@@ -74,21 +74,15 @@ struct Grid {
   double pad;  // r + pad is the half-extent of a sphere's bin AABB (margin/2 + eps)
 };
 
-// A directed contact-row entry as the force kernel reads it: everything it gathers about the
-// partner that does not change between rebuilds is resolved once by k_rows_finish, so the
-// partner's position and kinematics loads depend on this 16-byte record only.  The partner key
-// (the sort and history-match key) lives in the parallel array Rows::key.
 struct __align__(16) Entry {
-  int partner;      // partner local sphere index, or -1 - plane, or -1 - kMaxPlanes - triangle
+  long long key;    // partner key (sphere key, or INT64_MAX - plane)
+  int partner;      // partner local sphere index, or -1 - plane
   int prev;         // index of the same key in the previous step's rows (its u_t), or -1
-  int pclump;       // partner's clump (storage index); -1 for planes and triangles
-  int pmat;         // partner's material (a sphere's, a plane's or a mesh's)
 };
 
 struct Rows {
   int* row_ptr;     // [ns + 1]
   Entry* ent;       // [cap]
-  long long* key;   // [cap] partner key of each entry (sphere key, INT64_MAX - plane, INT64_MAX - 16 - t)
   double* ut;       // [kUt * cap] AoS (x, y, z, 0): one 32-byte sector per entry, oriented own -> partner
 };
 

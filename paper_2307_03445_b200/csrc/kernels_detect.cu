@@ -449,23 +449,8 @@ __device__ __forceinline__ long long partner_key(const StepArgs& a, int code) {
 
 __device__ __forceinline__ int prev_index(const Rows& prev, int pb, int pe, long long key) {
   for (int v = pb; v < pe; ++v)
-    if (prev.key[v] == key) return v;
+    if (prev.ent[v].key == key) return v;
   return -1;
-}
-
-// the force kernel's record of a candidate partner (code as in partner_key)
-__device__ __forceinline__ Entry make_entry(const StepArgs& a, int code, int prev) {
-  Entry e;
-  e.partner = code;
-  e.prev = prev;
-  if (code >= 0) {
-    e.pclump = a.s_clump[code];
-    e.pmat = a.s_mat[code];
-  } else {
-    e.pclump = -1;
-    e.pmat = a.mesh_mat[a.tri_mesh[-1 - kMaxPlanes - code]];
-  }
-  return e;
 }
 
 __global__ void __launch_bounds__(256) k_rows_finish(StepArgs a) {
@@ -484,7 +469,6 @@ __global__ void __launch_bounds__(256) k_rows_finish(StepArgs a) {
   const int m = a.rows.row_ptr[i + 1] - beg;
   const int pb = a.prev.row_ptr[i], pe = a.prev.row_ptr[i + 1];
   Entry* R = a.rows.ent + beg;
-  long long* K = a.rows.key + beg;
   const unsigned wmask = a.wall_mask[i];  // the pose kernel's sphere-plane candidates
   const int w = __popc(wmask);
   const int nc = m - w;  // k_pairs handed out slots [w, m) of the candidate list
@@ -514,7 +498,7 @@ __global__ void __launch_bounds__(256) k_rows_finish(StepArgs a) {
         }
 #pragma unroll 4
     for (int v = pb; v < pe; ++v) {
-      const long long pk = a.prev.key[v];
+      const long long pk = a.prev.ent[v].key;
 #pragma unroll
       for (int q = 0; q < kRegRow; ++q)
         if (kk[q] == pk) hh[q] = v;
@@ -522,45 +506,42 @@ __global__ void __launch_bounds__(256) k_rows_finish(StepArgs a) {
 #pragma unroll
     for (int q = 0; q < kRegRow; ++q)
       if (q < nc) {
-        K[q] = kk[q];
-        R[q] = make_entry(a, tt[q], hh[q]);
+        Entry e;
+        e.key = kk[q];
+        e.partner = tt[q];
+        e.prev = hh[q];
+        R[q] = e;
       }
   } else {
-    // long rows: keys and partner codes sorted in place in memory (insertion sort), then merged
-    // with the previous row (both sorted by key)
     for (int u = 0; u < nc; ++u) {
       const int t = S[(size_t)u * a.ns_own];
-      K[u] = partner_key(a, t);
-      R[u].partner = t;
+      Entry e;
+      e.key = partner_key(a, t);
+      e.partner = t;
+      R[u] = e;
     }
     for (int u = 1; u < nc; ++u) {
-      const long long xk = K[u];
-      const int xt = R[u].partner;
+      const Entry x = R[u];
       int v = u - 1;
-      while (v >= 0 && K[v] > xk) {
-        K[v + 1] = K[v];
-        R[v + 1].partner = R[v].partner;
+      while (v >= 0 && R[v].key > x.key) {
+        R[v + 1] = R[v];
         --v;
       }
-      K[v + 1] = xk;
-      R[v + 1].partner = xt;
+      R[v + 1] = x;
     }
-    int pj = pb;
+    int pj = pb;  // merge with the previous row (both sorted by key)
     for (int u = 0; u < nc; ++u) {
-      const long long k = K[u];
-      while (pj < pe && a.prev.key[pj] < k) ++pj;
-      R[u] = make_entry(a, R[u].partner, (pj < pe && a.prev.key[pj] == k) ? pj : -1);
+      const long long k = R[u].key;
+      while (pj < pe && a.prev.ent[pj].key < k) ++pj;
+      R[u].prev = (pj < pe && a.prev.ent[pj].key == k) ? pj : -1;
     }
   }
   for (int u = nc, p = a.tab.n_planes - 1; p >= 0; --p)
     if (wmask >> p & 1u) {
-      const long long key = (long long)(0x7fffffffffffffffLL - p);
       Entry e;
+      e.key = (long long)(0x7fffffffffffffffLL - p);
       e.partner = -1 - p;
-      e.prev = prev_index(a.prev, pb, pe, key);
-      e.pclump = -1;
-      e.pmat = a.tab.plane_mat[p];
-      K[u] = key;
+      e.prev = prev_index(a.prev, pb, pe, e.key);
       R[u++] = e;
     }
 }

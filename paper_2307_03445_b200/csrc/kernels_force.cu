@@ -168,6 +168,7 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
       const double Xx = ki[0], Xy = ki[1], Xz = ki[2];
       const double Mi = ki[9];
       const Entry ent = a.rows.ent[e];
+      const long long key = ent.key;
       const int t = ent.partner;
       // (a4) history remap: the slot of this key in the previous rows was found by the
       // row merge in k_rows_finish (-1: contact born this step, u_t = 0)
@@ -198,11 +199,9 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
         Vjx = Xvw[3]; Vjy = Xvw[4]; Vjz = Xvw[5];
         Wjx = Xvw[6]; Wjy = Xvw[7]; Wjz = Xvw[8];
       } else if (!wall) {
-        // the partner's clump and material come with the entry (k_rows_finish): both gathers
-        // below depend on the entry load only
         const double4 pj = a.spos[t];
-        const double2* kj = reinterpret_cast<const double2*>(a.kin + (size_t)kKin * ent.pclump);
-        mj = ent.pmat;
+        const double2* kj = reinterpret_cast<const double2*>(a.kin + (size_t)kKin * a.s_clump[t]);
+        mj = a.s_mat[t];
         const double rj = pj.w;
         const double dx = pj.x - cx, dy = pj.y - cy, dz = pj.z - cz;
         const double dist = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
@@ -241,7 +240,7 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
         mj = a.tab.plane_mat[pl];
       }
       if (degenerate) {
-        raise_error(a.ctl, -12, a.s_key[s0 + ls], a.rows.key[e]);
+        raise_error(a.ctl, -12, a.s_key[s0 + ls], key);
         delta = 0.0;
       }
       double Fx = 0.0, Fy = 0.0, Fz = 0.0, nux = 0.0, nuy = 0.0, nuz = 0.0;
@@ -414,7 +413,7 @@ __global__ void k_count_canonical(Rows r, const long long* __restrict__ s_key, i
   unsigned c = 0;
   if (i < ns) {
     const long long own = s_key[i];
-    for (int e = r.row_ptr[i]; e < r.row_ptr[i + 1]; ++e) c += r.key[e] > own;
+    for (int e = r.row_ptr[i]; e < r.row_ptr[i + 1]; ++e) c += r.ent[e].key > own;
   }
   c = __reduce_add_sync(0xffffffffu, c);
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (unsigned long long)c);
