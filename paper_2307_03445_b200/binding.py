@@ -278,13 +278,16 @@ class System:
         self._check(load_library().dem_migrate(self.sys, float(threshold), C.byref(moved)), "dem_migrate")
         return bool(moved.value)
 
-    def dem_get_state(self):
+    def dem_get_state(self, out=None):
+        """Host numpy arrays in the caller's order.  `out` (optional): preallocated arrays (e.g. in
+        pinned memory) with keys gid, tid, pos, quat, vel, omega, filled in place."""
         cnt = C.c_int64()
         self._check(load_library().dem_get_state(self.sys, 0, C.byref(cnt), None, None, None, None, None, None, 0),
                     "dem_get_state")
         n = cnt.value  # owned clumps (all of them on a single system)
-        out = dict(gid=np.zeros(n, np.int64), tid=np.zeros(n, np.int32), pos=np.zeros((n, 3)), quat=np.zeros((n, 4)),
-                   vel=np.zeros((n, 3)), omega=np.zeros((n, 3)))
+        if out is None:
+            out = dict(gid=np.zeros(n, np.int64), tid=np.zeros(n, np.int32), pos=np.zeros((n, 3)),
+                       quat=np.zeros((n, 4)), vel=np.zeros((n, 3)), omega=np.zeros((n, 3)))
         nn = C.c_int64()
         self._check(load_library().dem_get_state(self.sys, n, C.byref(nn), *[_ptr(out[k]) for k in
                                                                             ("gid", "tid", "pos", "quat", "vel",

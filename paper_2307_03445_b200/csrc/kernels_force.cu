@@ -480,3 +480,44 @@ void launch_max_drift(const State& st, const double* xref, int n, unsigned long 
   if (n) k_max_drift<<<(n + 255) / 256, 256, 0, s>>>(st, xref, n, out);
 }
 }  // namespace dem
+
+namespace dem {
+// State I/O in the caller's order (dem_set_state fast path, dem_get_state): the permutation to
+// and from the bin-sorted storage order runs on the device, so the host only moves the caller's
+// arrays (AoS rows: pos 3, quat 4, vel 3, omega 3 per clump).
+__global__ void k_state_in(State st, const int* __restrict__ perm, int n, const double* __restrict__ pos,
+                           const double* __restrict__ quat, const double* __restrict__ vel,
+                           const double* __restrict__ om, int* bad) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int c = perm[i];
+  const double x = pos[3 * c], y = pos[3 * c + 1], z = pos[3 * c + 2];
+  const double vx = vel[3 * c], vy = vel[3 * c + 1], vz = vel[3 * c + 2];
+  const double wx = om[3 * c], wy = om[3 * c + 1], wz = om[3 * c + 2];
+  if (!isfinite(x) || !isfinite(y) || !isfinite(z) || !isfinite(vx) || !isfinite(vy) || !isfinite(vz) ||
+      !isfinite(wx) || !isfinite(wy) || !isfinite(wz))
+    atomicExch(bad, 1);
+  st.x[i] = x; st.y[i] = y; st.z[i] = z;
+  st.qw[i] = quat[4 * c]; st.qx[i] = quat[4 * c + 1]; st.qy[i] = quat[4 * c + 2]; st.qz[i] = quat[4 * c + 3];
+  st.vx[i] = vx; st.vy[i] = vy; st.vz[i] = vz;
+  st.wx[i] = wx; st.wy[i] = wy; st.wz[i] = wz;
+}
+__global__ void k_state_out(State st, const int* __restrict__ outpos, int n_own, double* __restrict__ pos,
+                            double* __restrict__ quat, double* __restrict__ vel, double* __restrict__ om) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_own) return;
+  const int r = outpos[i];
+  if (pos) { pos[3 * r] = st.x[i]; pos[3 * r + 1] = st.y[i]; pos[3 * r + 2] = st.z[i]; }
+  if (quat) { quat[4 * r] = st.qw[i]; quat[4 * r + 1] = st.qx[i]; quat[4 * r + 2] = st.qy[i]; quat[4 * r + 3] = st.qz[i]; }
+  if (vel) { vel[3 * r] = st.vx[i]; vel[3 * r + 1] = st.vy[i]; vel[3 * r + 2] = st.vz[i]; }
+  if (om) { om[3 * r] = st.wx[i]; om[3 * r + 1] = st.wy[i]; om[3 * r + 2] = st.wz[i]; }
+}
+void launch_state_in(const State& st, const int* perm, int n, const double* pos, const double* quat,
+                     const double* vel, const double* om, int* bad, cudaStream_t s) {
+  if (n) k_state_in<<<(n + 255) / 256, 256, 0, s>>>(st, perm, n, pos, quat, vel, om, bad);
+}
+void launch_state_out(const State& st, const int* outpos, int n_own, double* pos, double* quat, double* vel,
+                      double* om, cudaStream_t s) {
+  if (n_own) k_state_out<<<(n_own + 255) / 256, 256, 0, s>>>(st, outpos, n_own, pos, quat, vel, om);
+}
+}  // namespace dem

@@ -34,6 +34,10 @@ void launch_pack(const State& st, const int* idx, int n, double* buf, cudaStream
 void launch_unpack(const State& st, const int* idx, int n, const double* buf, cudaStream_t s);
 void launch_max_drift(const State& st, const double* xref, int n, unsigned long long* out, cudaStream_t s);
 void launch_mesh_pose(const StepArgs&, cudaStream_t);
+void launch_state_in(const State& st, const int* perm, int n, const double* pos, const double* quat,
+                     const double* vel, const double* om, int* bad, cudaStream_t s);
+void launch_state_out(const State& st, const int* outpos, int n_own, double* pos, double* quat, double* vel,
+                      double* om, cudaStream_t s);
 void launch_mesh_pairs(const StepArgs&, cudaStream_t);
 void launch_mesh_finish(const StepArgs&, cudaStream_t);
 }  // namespace dem
@@ -73,6 +77,13 @@ struct dem_system {
   std::vector<int> h_tid, h_sph_off, h_s_tc;
   std::vector<long long> h_s_key;
   std::vector<int64_t> h_perm;  // storage index -> caller index
+  // the last dem_set_state input's gids/tids (caller order): a later call with the same clumps
+  // takes the fast path (no re-layout); device permutations for state I/O in caller order
+  std::vector<long long> h_in_gid;
+  std::vector<int> h_in_tid;
+  std::vector<int> h_outpos;        // owned storage index -> output row of dem_get_state
+  int *d_perm = nullptr, *d_outpos = nullptr, *d_io_bad = nullptr;
+  double* d_io = nullptr;           // 13 n doubles of staging (caller-order AoS rows)
   long long* d_gid = nullptr;
   int *d_tid = nullptr, *d_sph_off = nullptr;
   double* d_state[2] = {nullptr, nullptr};
@@ -797,17 +808,56 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
       CK(cudaMemcpy(g.data(), gid, sizeof(long long) * n, cudaMemcpyDeviceToHost));
       CK(cudaMemcpy(t.data(), tid, sizeof(int) * n, cudaMemcpyDeviceToHost));
     }
-    for (int k = 0; k < 4; ++k) {
-      in[k].resize((size_t)width[k] * n);
-      if (n) CK(cudaMemcpy(in[k].data(), src[k], sizeof(double) * width[k] * n, cudaMemcpyDeviceToHost));
-      src[k] = in[k].data();
-    }
   } else {
     for (int64_t c = 0; c < n; ++c) {
       g[c] = gid[c];
       t[c] = tid[c];
     }
   }
+  // fast path: the same clumps as the last call (a state reset or restore): the state is
+  // permuted into the existing storage order on the device, nothing is re-laid out
+  if (!sys->dist && n > 0 && sys->n == n && (int64_t)sys->h_in_gid.size() == n && sys->d_perm &&
+      std::equal(g.begin(), g.end(), sys->h_in_gid.begin()) && std::equal(t.begin(), t.end(), sys->h_in_tid.begin())) {
+    cudaStream_t s = sys->stream;
+    const double* dsrc[4] = {pos, quat, vel, omega};
+    if (!on_device) {
+      size_t off = 0;
+      for (int k = 0; k < 4; ++k) {
+        CK(cudaMemcpyAsync(sys->d_io + off, src[k], sizeof(double) * width[k] * n, cudaMemcpyHostToDevice, s));
+        dsrc[k] = sys->d_io + off;
+        off += (size_t)width[k] * n;
+      }
+    }
+    CK(cudaMemsetAsync(sys->d_io_bad, 0, sizeof(int), s));
+    sys->sp = 0;
+    const StepArgs a = make_args(sys, K_FULL);
+    launch_state_in(a.cur, sys->d_perm, (int)n, dsrc[0], dsrc[1], dsrc[2], dsrc[3], sys->d_io_bad, s);
+    CK(cudaMemsetAsync(sys->d_cell_count, 0, sizeof(int) * sys->ncell, s));
+    for (int p = 0; p < 2; ++p) CK(cudaMemsetAsync(sys->rows[p].row_ptr, 0, sizeof(int) * (sys->ns + 1), s));
+    std::memset(sys->h_ctl, 0, sizeof(Ctl));
+    CK(cudaMemcpyAsync(sys->d_ctl, sys->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, s));
+    int bad = 0;
+    CK(cudaMemcpyAsync(&bad, sys->d_io_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (bad) return DEM_ERR_NONFINITE;
+    sys->launched = 0;
+    sys->steps_done = 0;
+    sys->up = sys->ep = 0;
+    sys->since_rebuild = 0;
+    sys->pending = false;
+    sys->last_entries = 0;
+    sys->err.clear();
+    return DEM_OK;
+  }
+  if (on_device) {
+    for (int k = 0; k < 4; ++k) {
+      in[k].resize((size_t)width[k] * n);
+      if (n) CK(cudaMemcpy(in[k].data(), src[k], sizeof(double) * width[k] * n, cudaMemcpyDeviceToHost));
+      src[k] = in[k].data();
+    }
+  }
+  std::vector<long long> g_in(g);
+  std::vector<int> t_in(t);
   for (int64_t c = 0; c < n; ++c)
     if (t[c] < 0 || t[c] >= sys->n_tmpl || g[c] < 0 || g[c] >= (1LL << 56)) {
       sys->err = "clump " + std::to_string(c) + ": bad template id or gid";
@@ -1081,7 +1131,28 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
   for (int p = 0; p < 2; ++p) CK(cudaMemsetAsync(sys->rows[p].row_ptr, 0, sizeof(int) * (ns + 1), s));
   std::memset(sys->h_ctl, 0, sizeof(Ctl));
   CK(cudaMemcpyAsync(sys->d_ctl, sys->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, s));
-  CK(cudaStreamSynchronize(s));
+  // caller-order I/O: storage -> caller index, owned storage -> output row of dem_get_state
+  // (the rank of its caller index among the owned ones), staging for the fast paths
+  sys->h_in_gid.swap(g_in);
+  sys->h_in_tid.swap(t_in);
+  {
+    std::vector<int> perm(n);
+    for (int64_t i = 0; i < n; ++i) perm[i] = (int)sys->h_perm[i];
+    sys->h_outpos.assign(n_own, 0);
+    std::vector<int64_t> ord(n_own);
+    for (int64_t i = 0; i < n_own; ++i) ord[i] = i;
+    if (sys->dist)
+      std::sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) { return sys->h_perm[x] < sys->h_perm[y]; });
+    for (int64_t r = 0; r < n_own; ++r) sys->h_outpos[sys->dist ? ord[r] : r] = sys->dist ? (int)r : perm[r];
+    TRY(alloc_arr(sys, &sys->d_perm, (size_t)n + 1));
+    TRY(alloc_arr(sys, &sys->d_outpos, (size_t)n_own + 1));
+    TRY(alloc_arr(sys, &sys->d_io, (size_t)13 * n + 1));
+    TRY(alloc_arr(sys, &sys->d_io_bad, 1));
+    if (n) CK(cudaMemcpyAsync(sys->d_perm, perm.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
+    if (n_own)
+      CK(cudaMemcpyAsync(sys->d_outpos, sys->h_outpos.data(), sizeof(int) * n_own, cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+  }
   sys->launched = 0;
   sys->steps_done = 0;
   sys->sp = sys->up = sys->ep = 0;
@@ -1354,52 +1425,49 @@ extern "C" dem_status dem_get_state(dem_system* sys, int64_t cap, int64_t* n, in
   if (n) *n = NO;
   if (cap < NO) return (pos || quat || vel || omega || gid || tid) ? DEM_ERR_INVALID_ARG : DEM_OK;
   CK(cudaStreamSynchronize(sys->stream));
-  const int64_t N = sys->n;
-  std::vector<double> st((size_t)13 * N);
-  if (N)
-    CK(cudaMemcpy(st.data(), sys->d_state[sys->sp], sizeof(double) * 13 * N, cudaMemcpyDeviceToHost));
-  // output row of each owned storage index: rank of its caller index among the owned ones
-  std::vector<int64_t> outpos(NO);
-  {
-    std::vector<int64_t> ord(NO);
-    for (int64_t i = 0; i < NO; ++i) ord[i] = i;
-    std::sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) { return sys->h_perm[x] < sys->h_perm[y]; });
-    for (int64_t r = 0; r < NO; ++r) outpos[ord[r]] = r;
-  }
-  std::vector<double> out[4];
+  cudaStream_t s = sys->stream;
+  // device gather from the storage order into caller-order rows, then one copy per array
   double* dst[4] = {pos, quat, vel, omega};
-  const int width[4] = {3, 4, 3, 3}, first[4] = {0, 3, 7, 10};
+  const int width[4] = {3, 4, 3, 3};
+  double* dev[4] = {nullptr, nullptr, nullptr, nullptr};
+  size_t off = 0;
   for (int k = 0; k < 4; ++k) {
-    if (!dst[k]) continue;
-    double* o = dst[k];
-    if (on_device) {
-      out[k].resize((size_t)width[k] * NO);
-      o = out[k].data();
-    }
+    if (dst[k]) dev[k] = on_device ? dst[k] : sys->d_io + off;
+    off += (size_t)width[k] * NO;
+  }
+  const StepArgs a = make_args(sys, K_CHECK);
+  if (NO) launch_state_out(a.cur, sys->d_outpos, (int)NO, dev[0], dev[1], dev[2], dev[3], s);
+  if (!on_device)
+    for (int k = 0; k < 4; ++k)
+      if (dst[k] && NO) CK(cudaMemcpyAsync(dst[k], dev[k], sizeof(double) * width[k] * NO, cudaMemcpyDeviceToHost, s));
+  // gids and template ids from the host copies
+  std::vector<long long> go;
+  std::vector<int> to;
+  const long long* gsrc = sys->h_in_gid.data();
+  const int* tsrc = sys->h_in_tid.data();
+  if (sys->dist && (gid || tid)) {
+    go.resize(NO);
+    to.resize(NO);
     for (int64_t i = 0; i < NO; ++i) {
-      const int64_t c = outpos[i];
-      for (int d = 0; d < width[k]; ++d) o[width[k] * c + d] = st[(first[k] + d) * N + i];
+      go[sys->h_outpos[i]] = sys->h_gid[i];
+      to[sys->h_outpos[i]] = sys->h_tid[i];
     }
-    if (on_device && NO) CK(cudaMemcpy(dst[k], o, sizeof(double) * width[k] * NO, cudaMemcpyHostToDevice));
+    gsrc = go.data();
+    tsrc = to.data();
   }
-  std::vector<long long> go(NO);
-  std::vector<int> to(NO);
-  for (int64_t i = 0; i < NO; ++i) {
-    go[outpos[i]] = sys->h_gid[i];
-    to[outpos[i]] = sys->h_tid[i];
-  }
-  if (gid) {
+  if (gid && NO) {
     if (on_device)
-      CK(cudaMemcpy(gid, go.data(), sizeof(long long) * NO, cudaMemcpyHostToDevice));
+      CK(cudaMemcpyAsync(gid, gsrc, sizeof(long long) * NO, cudaMemcpyHostToDevice, s));
     else
-      std::memcpy(gid, go.data(), sizeof(long long) * NO);
+      std::memcpy(gid, gsrc, sizeof(long long) * NO);
   }
-  if (tid) {
+  if (tid && NO) {
     if (on_device)
-      CK(cudaMemcpy(tid, to.data(), sizeof(int) * NO, cudaMemcpyHostToDevice));
+      CK(cudaMemcpyAsync(tid, tsrc, sizeof(int) * NO, cudaMemcpyHostToDevice, s));
     else
-      std::memcpy(tid, to.data(), sizeof(int) * NO);
+      std::memcpy(tid, tsrc, sizeof(int) * NO);
   }
+  CK(cudaStreamSynchronize(s));
   return DEM_OK;
 }
 
