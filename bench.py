@@ -348,7 +348,8 @@ def run_ours(a):
                    "overlap": bool(a.overlap),
                    "l2": "inputs larger than L2 (state + rows > 10 GB); no flush",
                    "parallelism": f"slab{world}" if world > 1 else "single-gpu",
-                   "ghost_clumps_rank0": st["n_ghost_clumps"], "setup_s": round(setup_s, 1)},
+                   "ghost_clumps_rank0": st["n_ghost_clumps"], "setup_s": round(setup_s, 1),
+                   "capacity_regrows": st["regrows"]},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "alg_bytes_per_launch": sb[dom], "avg_launch_ms": stages_k[dom]},

@@ -1051,7 +1051,9 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
   for (int e = 0; e < 2; ++e) TRY(alloc_arr(sys, &sys->d_spos_ref[e], sys->P.cd_every > 1 ? ns : 0));
   // candidate lists: kRowWidth slots per owned sphere to start with (walls included), widened
   // on overflow (the rows of a settled bed hold a few entries)
-  sys->row_width = kRowWidth;
+  // (a distributed system cannot regrow mid-run without desynchronising its neighbours: it starts
+  // with twice the width)
+  sys->row_width = sys->dist ? 2 * kRowWidth : kRowWidth;
   TRY(alloc_arr(sys, &sys->d_slots, (size_t)sys->ns_own * sys->row_width + 1));
   // CTA partition of the fused force/integrate kernel: consecutive whole clumps, at most
   // force_cta_clumps() clumps and force_cta_spheres() spheres per CTA
