@@ -50,7 +50,18 @@ int force_cta_spheres() { return kMaxS; }
 // its feature's contact among the sphere's entries on the same mesh (R26).  Outputs the contact
 // frame as for a wall (n from the sphere to the surface, the middle of the overlap), the mesh's
 // reference point, velocity and angular velocity (the point velocity of the boundary).
-__device__ __noinline__ bool mesh_entry(const StepArgs& a, int tri, int row_beg, int row_end, double cx,
+// (the pointers it needs, by value: a reference to the kernel's StepArgs would make every thread
+// copy the whole parameter block to its stack)
+struct MeshView {
+  const double* tri_world;
+  const int* tri_mesh;
+  const int* tri_vid;
+  const double* mesh;
+  const int* mesh_mat;
+  const Entry* ent;
+};
+
+__device__ __noinline__ bool mesh_entry(const MeshView a, int tri, int row_beg, int row_end, double cx,
                                         double cy, double cz, double ri, double& nx, double& ny, double& nz,
                                         double& px, double& py, double& pz, double& delta, int& mj, double* Xvw,
                                         int& mesh, bool& degenerate) {
@@ -80,7 +91,7 @@ __device__ __noinline__ bool mesh_entry(const StepArgs& a, int tri, int row_beg,
   tri_feature(a.tri_vid, tri, reg, kind, u, v);
   if (kind == 2) return true;
   for (int e = row_beg; e < row_end; ++e) {
-    const int code = a.rows.ent[e].partner;
+    const int code = a.ent[e].partner;
     if (code > -1 - kMaxPlanes) continue;
     const int tj = -1 - kMaxPlanes - code;
     if (tj == tri || a.tri_mesh[tj] != mesh) continue;
@@ -191,7 +202,8 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
       int mesh = -1;
       if (kMesh && t <= -1 - kMaxPlanes) {
         double Xvw[9];
-        active = mesh_entry(a, -1 - kMaxPlanes - t, rp[ls], rp[ls + 1], cx, cy, cz, ri, nx, ny, nz, px, py, pz,
+        const MeshView mv{a.tri_world, a.tri_mesh, a.tri_vid, a.mesh, a.mesh_mat, a.rows.ent};
+        active = mesh_entry(mv, -1 - kMaxPlanes - t, rp[ls], rp[ls + 1], cx, cy, cz, ri, nx, ny, nz, px, py, pz,
                             delta, mj, Xvw, mesh, degenerate);
         rbar = ri;
         mbar = Mi;

@@ -46,7 +46,7 @@ __device__ __forceinline__ void span_bins(const Grid& g, int d, double lo, doubl
   bhi = clampi(__double2int_rd((hi - g.lo[d]) * g.inv_cell), 0, g.n[d] - 1);
 }
 
-// one warp per (triangle, bin) sweep: blockIdx.x = triangle, warps stride over its bins
+// blockIdx.x = triangle; the warps of kMeshPairSplit CTAs (blockIdx.y) stride over its bins
 __global__ void __launch_bounds__(256) k_mesh_pairs(StepArgs a) {
   if (*a.abort || a.ctl->abort) return;
   const int t = blockIdx.x;
@@ -61,7 +61,8 @@ __global__ void __launch_bounds__(256) k_mesh_pairs(StepArgs a) {
   }
   const int nx = thi[0] - tlo[0] + 1, ny = thi[1] - tlo[1] + 1, nz = thi[2] - tlo[2] + 1;
   const long long nb = (long long)nx * ny * nz;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, nw = (blockDim.x >> 5) * gridDim.y;
+  const int warp = blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int code = -1 - kMaxPlanes - t;
   for (long long b = warp; b < nb; b += nw) {
     const int bx = tlo[0] + (int)(b % nx), by = tlo[1] + (int)((b / nx) % ny), bz = tlo[2] + (int)(b / ((long long)nx * ny));
@@ -147,8 +148,9 @@ __global__ void __launch_bounds__(1024) k_mesh_finish(StepArgs a) {
 void launch_mesh_pose(const StepArgs& a, cudaStream_t s) {
   if (a.n_tri) k_mesh_pose<<<(a.n_tri + 255) / 256, 256, 0, s>>>(a);
 }
+constexpr int kMeshPairSplit = 16;  // CTAs per triangle (large facets span thousands of bins)
 void launch_mesh_pairs(const StepArgs& a, cudaStream_t s) {
-  if (a.n_tri) k_mesh_pairs<<<a.n_tri, 256, 0, s>>>(a);
+  if (a.n_tri) k_mesh_pairs<<<dim3(a.n_tri, kMeshPairSplit), 256, 0, s>>>(a);
 }
 void launch_mesh_finish(const StepArgs& a, cudaStream_t s) {
   if (a.n_mesh) k_mesh_finish<<<1, 1024, 0, s>>>(a);

@@ -38,7 +38,7 @@ def launch_summary(csv_path):
     for r in rows:
         if r["Metric Name"] != "gpu__time_duration.sum":
             continue
-        k = r["Kernel Name"].split("(")[0]
+        k = r["Kernel Name"].split("(")[0].replace("void ", "")
         per.setdefault(k, []).append(float(r["Metric Value"]) * (1e-6 if r["Metric Unit"] == "ns" else 1e-3))
     total = sum(sum(v) for v in per.values())
     lines = ["ncu --metrics gpu__time_duration.sum --clock-control none, python bench.py --steps 2 --warmup 3 "
@@ -75,7 +75,7 @@ def main(rnd):
                     f.write(f"   {m:45s} {x}\n")
         traffic = {}
         for k, v in s.items():
-            name = k.split("#")[0].split("::")[-1]
+            name = k.split("#")[0].split("::")[-1].replace("void ", "").split("<")[0].strip()
             if name in STAGE_OF and "dram__bytes_read.sum" in v:
                 def gb(x):
                     val, unit = x.split()
