@@ -113,9 +113,10 @@ __global__ void __launch_bounds__(256) k_bin_scatter(StepArgs a) {
       const long long base = z * g.st[2] + y * g.st[1];
       for (int x = lx; x <= hx; ++x) {
         const long long cid = base + x * g.st[0];
+        const int start = a.cell_start[cid];  // issued before the atomic: the two are independent
         const int slot = atomicSub(&a.cell_count[cid], 1) - 1;
         // the item carries the sphere's lowest-bin mask for k_pairs (ns < 2^29, checked)
-        if (fits) a.items[a.cell_start[cid] + slot] = i | (((x == lx ? 1 : 0) | (y == ly ? 2 : 0) | (z == lz ? 4 : 0)) << 29);
+        if (fits) a.items[start + slot] = i | (((x == lx ? 1 : 0) | (y == ly ? 2 : 0) | (z == lz ? 4 : 0)) << 29);
       }
     }
 }
