@@ -200,7 +200,8 @@ def run_ours(a):
         drift = 1e-3
         b = dem.slab_bounds(scene.pos[:, 0], world, scene.domain_lo[0], scene.domain_hi[0])
         dparams = dict(rank=rank, n_ranks=world, slab_lo=b[rank], slab_hi=b[rank + 1],
-                       halo=dem.halo_width(scene, drift), drift_max=drift, transport=dem.TRANSPORT_NCCL,
+                       halo=dem.halo_width(scene, drift), drift_max=drift,
+                       transport=dem.TRANSPORT_PEER if a.transport == "peer" else dem.TRANSPORT_NCCL,
                        nccl_id=obj[0])
     # deferred rebuild (NEXT-1): margin = 2 v_max h k; k = 1 is the headline.
     # Overlapped cadence (NEXT-2): the set is used 2k - 2 steps after its detection.
@@ -210,6 +211,8 @@ def run_ours(a):
                                  entries_per_sphere=12 if world > 1 else 0, margin=margin, cd_every=a.cd_every,
                                  overlap=a.overlap)
     stream = sys_.stream
+    if world > 1 and a.transport == "peer":
+        sys_.dem_peer_link(rank, world)  # fused halo: neighbours' arrays mapped over NVLink
     sys_.dem_step(a.warmup)
     if world > 1:
         sys_.dem_migrate(threshold=0.5 * drift)  # collective drift check; a settling bed stays put
@@ -348,6 +351,7 @@ def run_ours(a):
                    "overlap": bool(a.overlap),
                    "l2": "inputs larger than L2 (state + rows > 10 GB); no flush",
                    "parallelism": f"slab{world}" if world > 1 else "single-gpu",
+                   "halo_transport": (a.transport if world > 1 else None),
                    "ghost_clumps_rank0": st["n_ghost_clumps"], "setup_s": round(setup_s, 1),
                    "capacity_regrows": st["regrows"]},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -387,6 +391,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer end-to-end pass (A/B runs)")
     ap.add_argument("--no-variants", action="store_true", help="skip the deferred-cadence variants (k = 10)")
+    ap.add_argument("--transport", choices=["peer", "nccl"], default="peer",
+                    help="N > 1 ghost halo: fused peer stores from the force kernel (default) or NCCL send/recv")
     a = ap.parse_args()
     if a.warmup < 3:
         a.warmup = 3

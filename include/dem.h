@@ -115,7 +115,7 @@ typedef struct {
    * DEM_ERR_REPARTITION (re-call dem_set_state with the gathered global state to migrate). */
   int32_t rank, n_ranks;
   double slab_lo, slab_hi, halo, drift_max;
-  int32_t transport;         /* DEM_TRANSPORT_NCCL or DEM_TRANSPORT_LOOPBACK */
+  int32_t transport;         /* DEM_TRANSPORT_NCCL, _PEER, _LOOPBACK or _LOOPBACK_PEER (below) */
   unsigned char nccl_id[128];/* ncclUniqueId from dem_nccl_unique_id on rank 0, broadcast by the caller */
   /* Overlapped detection cadence (the active set is updated "in the shadow" of the
    * dynamics; P:148 one GPU shares the two threads via CUDA streams).  With overlap = 1 and
@@ -128,7 +128,14 @@ typedef struct {
   int32_t overlap;
 } dem_params;
 
-enum { DEM_TRANSPORT_NCCL = 0, DEM_TRANSPORT_LOOPBACK = 1 };
+/* Ghost-halo transports.  NCCL: the owners' new ghost states are packed and sent with grouped
+ * ncclSend/ncclRecv after the force kernel.  PEER: the fused halo — the force/integrate kernel
+ * writes each ghosted clump's new state straight into the neighbour's next-state array over
+ * NVLink (CUDA IPC mappings exchanged inside dem_set_state over the NCCL communicator), and a
+ * one-thread flag handshake per step (release/acquire, system scope) keeps neighbours within one
+ * step of each other; no pack, collective or unpack kernels.  LOOPBACK / LOOPBACK_PEER: the same
+ * two schemes between the systems of one process on one GPU (dem_step_group; tests). */
+enum { DEM_TRANSPORT_NCCL = 0, DEM_TRANSPORT_LOOPBACK = 1, DEM_TRANSPORT_PEER = 2, DEM_TRANSPORT_LOOPBACK_PEER = 3 };
 
 typedef struct {
   int64_t steps;             /* steps completed since dem_set_state */
@@ -243,6 +250,17 @@ dem_status dem_set_mesh_motion(dem_system* sys, int32_t mesh, const double pos[3
  * that step: force and torque about X (the sum over its contacts in a fixed order). */
 dem_status dem_get_mesh(dem_system* sys, int32_t mesh, double pos[3], double quat[4], double force[3],
                         double torque[3]);
+
+/* PEER transport link (after every dem_set_state, before stepping; collective in effect).  Each
+ * rank exports a packet — CUDA IPC handles of its two state arrays and its flag words, its clump
+ * count and its ghost receive lists — which the caller delivers to the left and right neighbours
+ * (any transport: torch.distributed all_gather in the Python binding); dem_peer_import maps the
+ * neighbours' arrays (peer access) and derives the neighbour ghost slot of every clump we send.
+ * dem_peer_export with out = NULL returns the packet size in *len.  left / right = NULL where
+ * there is no neighbour.  A rank's dem_set_state must not start while a neighbour is still
+ * stepping (with an NCCL id in dem_params the library runs that barrier itself). */
+dem_status dem_peer_export(dem_system* sys, int64_t cap, void* out, int64_t* len);
+dem_status dem_peer_import(dem_system* sys, const void* left, const void* right);
 
 /* Clump migration between slabs.  Collective over the n_ranks systems of an
  * NCCL decomposition (every rank calls it at the same point, between dem_step calls).  The

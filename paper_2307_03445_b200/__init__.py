@@ -3,6 +3,7 @@
 The product is `libdem_b200.so` (hand-written sm_100a CUDA behind the C-ABI in
 include/dem.h); `binding` marshals arguments and provides PyTorch's allocator and stream.
 """
-from .binding import (DEM_STATUS, EXPORTS, LIB_PATH, STAGES, TRANSPORT_LOOPBACK, TRANSPORT_NCCL,  # noqa: F401
+from .binding import (DEM_STATUS, EXPORTS, LIB_PATH, STAGES, TRANSPORT_LOOPBACK, TRANSPORT_LOOPBACK_PEER,  # noqa: F401
+                      TRANSPORT_NCCL, TRANSPORT_PEER,
                       DemError, System, halo_width, load_library, migrate_group, nccl_unique_id, partition_plan,
                       slab_bounds, step_group, system_from_scene)

@@ -59,13 +59,13 @@ class dem_stats(C.Structure):
                 ("cell_size", C.c_double), ("regrows", C.c_int64), ("kernel_launches_per_step", C.c_int64)]
 
 
-TRANSPORT_NCCL, TRANSPORT_LOOPBACK = 0, 1
+TRANSPORT_NCCL, TRANSPORT_LOOPBACK, TRANSPORT_PEER, TRANSPORT_LOOPBACK_PEER = 0, 1, 2, 3
 
 EXPORTS = ["dem_create", "dem_set_state", "dem_set_contact_history", "dem_step", "dem_synchronize",
            "dem_get_state", "dem_get_contacts", "dem_get_stats", "dem_set_profiling", "dem_get_stage_times",
            "dem_status_string", "dem_last_error", "dem_destroy", "dem_nccl_unique_id", "dem_partition_plan",
            "dem_step_group", "dem_migrate", "dem_migrate_group", "dem_add_mesh", "dem_set_mesh_motion",
-           "dem_get_mesh"]
+           "dem_get_mesh", "dem_peer_export", "dem_peer_import"]
 
 _lib = None
 
@@ -102,6 +102,8 @@ def load_library(path: str = LIB_PATH):
     L.dem_add_mesh.argtypes = [P, C.POINTER(dem_mesh), C.POINTER(I32)]
     L.dem_set_mesh_motion.argtypes = [P, I32, P, P, P, P]
     L.dem_get_mesh.argtypes = [P, I32, P, P, P, P]
+    L.dem_peer_export.argtypes = [P, I64, P, C.POINTER(I64)]
+    L.dem_peer_import.argtypes = [P, P, P]
     for f in EXPORTS:
         if f not in ("dem_destroy", "dem_status_string"):
             getattr(L, f).restype = C.c_int
@@ -271,11 +273,32 @@ class System:
                     "dem_get_mesh")
         return dict(pos=X, quat=q, force=f, torque=t)
 
+    def dem_peer_link(self, rank, world, group=None):
+        """PEER transport: exchange the IPC export packets with the neighbouring ranks over
+        torch.distributed (any backend) and map them (dem_peer_export / dem_peer_import).  Collective;
+        needed after every dem_set_state (dem_migrate re-links by itself)."""
+        import torch.distributed as dist
+
+        L = load_library()
+        n = C.c_int64()
+        self._check(L.dem_peer_export(self.sys, 0, None, C.byref(n)), "dem_peer_export")
+        buf = (C.c_ubyte * n.value)()
+        self._check(L.dem_peer_export(self.sys, n.value, buf, C.byref(n)), "dem_peer_export")
+        packets = [None] * world
+        dist.all_gather_object(packets, bytes(buf), group=group)
+        keep = [C.create_string_buffer(packets[r], len(packets[r])) if 0 <= r < world else None
+                for r in (rank - 1, rank + 1)]
+        self._check(L.dem_peer_import(self.sys, *[C.cast(k, C.c_void_p) if k is not None else None for k in keep]),
+                    "dem_peer_import")
+        self._peer = (rank, world, group)
+
     def dem_migrate(self, threshold=0.0) -> bool:
         """Collective (NCCL ranks): migrate clumps between slabs if an owned COM moved more than
         `threshold` [m] since the last partition (0 forces it).  True if a migration happened."""
         moved = C.c_int32(0)
         self._check(load_library().dem_migrate(self.sys, float(threshold), C.byref(moved)), "dem_migrate")
+        if moved.value and getattr(self, "_peer", None):
+            self.dem_peer_link(*self._peer)
         return bool(moved.value)
 
     def dem_get_state(self, out=None):

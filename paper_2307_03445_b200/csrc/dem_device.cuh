@@ -138,6 +138,12 @@ struct StepArgs {
   double* mesh_part;         // [6 n_mesh n_cta] per-CTA wrench partials (force on mesh, torque about X)
   int* mesh_flag;            // [n_cta] 1 if the CTA wrote a partial this step
   double* mesh_wrench;       // [6 n_mesh] the last step's wrench
+  // fused halo (peer transport): the integrating thread of a clump in a send list
+  // writes its new state straight into the neighbour's next-state array at the neighbour's ghost
+  // slot (NVLink peer stores), so there is no pack, no collective and no unpack
+  double* peer_state[2];     // [side] the neighbour's next-state SoA base (13 arrays of peer_n), or null
+  long long peer_n[2];       // [side] the neighbour's clump count (SoA stride)
+  const int* peer_idx[2];    // [side][n_own] the neighbour's ghost slot of each owned clump, or -1
   double half_margin;        // > 0 (cd_every > 1): displacement allowed since the last rebuild
   int n_own, ns_own;         // owned clumps / spheres come first; the rest are ghosts (§8e)
   const double* xref;        // [3 n_own] owned COMs at dem_set_state (distributed drift check)

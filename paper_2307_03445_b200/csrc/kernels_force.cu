@@ -111,7 +111,7 @@ __device__ __noinline__ bool mesh_entry(const MeshView a, int tri, int row_beg, 
   return true;
 }
 
-template <bool kMesh>
+template <bool kMesh, bool kPeer>
 __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArgs a) {
   __shared__ int rp[kMaxS + 1];
   __shared__ double4 own_p[kMaxS];
@@ -415,7 +415,24 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
   const double ry = qw * dy - qx * dz + qy * dw + qz * dx;
   const double rz = qw * dz + qx * dy - qy * dx + qz * dw;
   const double nrm = sqrt(rw * rw + rx * rx + ry * ry + rz * rz);
-  a.nxt.qw[c] = rw / nrm; a.nxt.qx[c] = rx / nrm; a.nxt.qy[c] = ry / nrm; a.nxt.qz[c] = rz / nrm;
+  const double q0 = rw / nrm, q1 = rx / nrm, q2 = ry / nrm, q3 = rz / nrm;
+  a.nxt.qw[c] = q0; a.nxt.qx[c] = q1; a.nxt.qy[c] = q2; a.nxt.qz[c] = q3;
+  // fused halo: the new state of a clump the neighbours hold as a ghost goes straight into their
+  // next-state arrays (peer stores over NVLink), then a system-scope fence before the signal
+  bool sent = false;
+#pragma unroll
+  for (int side = 0; side < 2; ++side) {
+    if (!kPeer || !a.peer_state[side]) continue;
+    const int g = a.peer_idx[side][c];
+    if (g < 0) continue;
+    double* R = a.peer_state[side];
+    const long long m = a.peer_n[side];
+    const double v[13] = {nxx, nxy, nxz, q0, q1, q2, q3, vx, vy, vz, n0, n1, n2};
+#pragma unroll
+    for (int k = 0; k < 13; ++k) R[(size_t)k * m + g] = v[k];
+    sent = true;
+  }
+  if (sent) __threadfence_system();
 }
 
 // canonical contacts held in a row set: entries whose own sphere key is the smaller one
@@ -433,10 +450,11 @@ __global__ void k_count_canonical(Rows r, const long long* __restrict__ s_key, i
 
 void launch_force_integrate(const StepArgs& a, cudaStream_t s) {
   if (a.n_cta <= 0) return;
+  const bool peer = a.peer_state[0] || a.peer_state[1];
   if (a.n_tri)
-    k_force_integrate<true><<<a.n_cta, kFT, 0, s>>>(a);
+    peer ? k_force_integrate<true, true><<<a.n_cta, kFT, 0, s>>>(a) : k_force_integrate<true, false><<<a.n_cta, kFT, 0, s>>>(a);
   else
-    k_force_integrate<false><<<a.n_cta, kFT, 0, s>>>(a);
+    peer ? k_force_integrate<false, true><<<a.n_cta, kFT, 0, s>>>(a) : k_force_integrate<false, false><<<a.n_cta, kFT, 0, s>>>(a);
 }
 void launch_count_canonical(const Rows& r, const long long* s_key, int ns, unsigned long long* out, cudaStream_t s) {
   if (ns) k_count_canonical<<<(ns + 255) / 256, 256, 0, s>>>(r, s_key, ns, out);
@@ -531,5 +549,53 @@ void launch_state_in(const State& st, const int* perm, int n, const double* pos,
 void launch_state_out(const State& st, const int* outpos, int n_own, double* pos, double* quat, double* vel,
                       double* om, cudaStream_t s) {
   if (n_own) k_state_out<<<(n_own + 255) / 256, 256, 0, s>>>(st, outpos, n_own, pos, quat, vel, om);
+}
+}  // namespace dem
+
+namespace dem {
+// Peer-transport step handshake: after its fused force kernel every rank writes its
+// completed-step count into both neighbours' flag words (release, system scope); before its
+// next step it waits until both its flag words reach its own count (acquire).  A rank is then
+// never more than one step ahead of a neighbour, so it writes a neighbour's next-state ghost
+// slots only after that neighbour stopped reading them as its current state, and reads its own
+// ghosts only after the neighbours wrote them.  Counts are monotonic (reset by dem_set_state
+// before the collective handle exchange), so graph replays need no per-step immediates.
+__global__ void k_peer_signal(const Ctl* ctl, int* r0, int* r1) {
+  if (ctl->abort) return;
+  const int v = (int)ctl->step;
+  if (r0) asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(r0), "r"(v) : "memory");
+  if (r1) asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(r1), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ int ld_acquire_sys(const int* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// one thread spins on the two flag words; gives up after ~20 s (a dead peer) with an error
+__global__ void k_peer_wait(Ctl* ctl, const int* f0, const int* f1) {
+  if (ctl->abort) return;
+  const int want = (int)ctl->step;
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    const bool ok = (!f0 || ld_acquire_sys(f0) >= want) && (!f1 || ld_acquire_sys(f1) >= want);
+    if (ok) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 20000000000ull) {
+      raise_error(ctl, -4, want, 0);  // DEM_ERR_NCCL: a neighbour stopped stepping
+      return;
+    }
+    __nanosleep(200);
+  }
+}
+
+void launch_peer_signal(const Ctl* ctl, int* r0, int* r1, cudaStream_t s) {
+  if (r0 || r1) k_peer_signal<<<1, 1, 0, s>>>(ctl, r0, r1);
+}
+void launch_peer_wait(Ctl* ctl, const int* f0, const int* f1, cudaStream_t s) {
+  if (f0 || f1) k_peer_wait<<<1, 1, 0, s>>>(ctl, f0, f1);
 }
 }  // namespace dem

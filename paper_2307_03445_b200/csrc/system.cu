@@ -34,6 +34,8 @@ void launch_pack(const State& st, const int* idx, int n, double* buf, cudaStream
 void launch_unpack(const State& st, const int* idx, int n, const double* buf, cudaStream_t s);
 void launch_max_drift(const State& st, const double* xref, int n, unsigned long long* out, cudaStream_t s);
 void launch_mesh_pose(const StepArgs&, cudaStream_t);
+void launch_peer_signal(const Ctl* ctl, int* r0, int* r1, cudaStream_t s);
+void launch_peer_wait(Ctl* ctl, const int* f0, const int* f1, cudaStream_t s);
 void launch_state_in(const State& st, const int* perm, int n, const double* pos, const double* quat,
                      const double* vel, const double* om, int* bad, cudaStream_t s);
 void launch_state_out(const State& st, const int* outpos, int n_own, double* pos, double* quat, double* vel,
@@ -150,7 +152,21 @@ struct dem_system {
   int *d_send_idx[2] = {nullptr, nullptr}, *d_recv_idx[2] = {nullptr, nullptr};
   double *d_sendbuf[2] = {nullptr, nullptr}, *d_recvbuf[2] = {nullptr, nullptr};
   double* d_xref = nullptr;                          // owned COM at dem_set_state (drift check)
+  // peer transports (fused halo): state arrays and flag words from cudaMalloc (IPC-exportable),
+  // the neighbours' next-state arrays / flag words / ghost slots of our send lists
+  bool peer = false;
+  double* raw_state[2] = {nullptr, nullptr};
+  int* d_flags = nullptr;                            // [0] written by the left, [1] by the right neighbour
+  double* remote_state[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [side][parity]
+  long long remote_n[2] = {0, 0};
+  int* remote_flag[2] = {nullptr, nullptr};
+  int* d_peer_idx[2] = {nullptr, nullptr};           // [side][n_own] neighbour ghost slot or -1
+  std::vector<int> h_send_list[2], h_recv_list[2];   // storage indices, ascending gid
+  std::vector<void*> ipc_open;                       // neighbour mappings to close
+  bool peer_linked = false;
 };
+
+static dem_status peer_release(dem_system* sys);
 
 // ------------------------------------------------------------------ helpers
 #define CK(call)                                                                  \
@@ -316,6 +332,11 @@ static StepArgs make_args(dem_system* sys, int kind, bool det = false) {
   a.mesh_part = sys->d_mesh_part;
   a.mesh_flag = sys->d_mesh_flag;
   a.mesh_wrench = sys->d_mesh_wrench;
+  for (int side = 0; side < 2; ++side) {
+    a.peer_state[side] = sys->peer ? sys->remote_state[side][p ^ 1] : nullptr;
+    a.peer_n[side] = sys->remote_n[side];
+    a.peer_idx[side] = sys->d_peer_idx[side];
+  }
   a.rec = sys->rec;
   a.record = sys->P.record_contacts ? 1 : 0;
   a.ctl = sys->d_ctl;
@@ -354,6 +375,9 @@ enum { PART_ALL = 0, PART_POSE = 1, PART_DET = 2, PART_FORCE = 3 };
 static void enqueue_pose(dem_system* sys, int kind, cudaStream_t s, cudaEvent_t* ev) {
   StepArgs a = make_args(sys, kind);
   if (ev) cudaEventRecord(ev[0], s);
+  if (sys->peer)  // the neighbours have written this step's ghost states (and read ours)
+    launch_peer_wait(sys->d_ctl, sys->remote_flag[0] ? sys->d_flags : nullptr,
+                     sys->remote_flag[1] ? sys->d_flags + 1 : nullptr, s);
   launch_mesh_pose(a, s);
   launch_pose_count(a, s);
   if (ev) cudaEventRecord(ev[1], s);
@@ -384,7 +408,9 @@ static void enqueue_force(dem_system* sys, int kind, cudaStream_t s, cudaEvent_t
   launch_force_integrate(a, s);
   launch_mesh_finish(a, s);
   if (ev) cudaEventRecord(ev[7], s);
-  if (sys->dist) {
+  if (sys->peer) {
+    launch_peer_signal(sys->d_ctl, sys->remote_flag[0], sys->remote_flag[1], s);
+  } else if (sys->dist) {
     enqueue_pack(sys, a, s);
     if (exchange && sys->P.transport == DEM_TRANSPORT_NCCL) {
       enqueue_nccl_exchange(sys, s);
@@ -493,7 +519,7 @@ extern "C" dem_status dem_create(const dem_params* params, const dem_material* m
   if (params->n_ranks > 1 &&
       (params->rank < 0 || params->rank >= params->n_ranks || !(params->slab_hi > params->slab_lo) ||
        !(params->halo > 0) || !(params->drift_max >= 0) ||
-       (params->transport != DEM_TRANSPORT_NCCL && params->transport != DEM_TRANSPORT_LOOPBACK)))
+       (params->transport < DEM_TRANSPORT_NCCL || params->transport > DEM_TRANSPORT_LOOPBACK_PEER)))
     return DEM_ERR_INVALID_ARG;
   for (int m = 0; m < n_mat; ++m)
     if (!material_ok(materials[m])) return DEM_ERR_BAD_MATERIAL;
@@ -595,7 +621,17 @@ extern "C" dem_status dem_create(const dem_params* params, const dem_material* m
   }
   if (params->n_ranks > 1) {
     sys->dist = true;
-    if (params->transport == DEM_TRANSPORT_NCCL) {
+    sys->peer = params->transport == DEM_TRANSPORT_PEER || params->transport == DEM_TRANSPORT_LOOPBACK_PEER;
+    if (sys->peer) {
+      if (cudaMalloc(&sys->d_flags, 2 * sizeof(int)) != cudaSuccess ||
+          cudaMemset(sys->d_flags, 0, 2 * sizeof(int)) != cudaSuccess) {
+        dem_destroy(sys);
+        return DEM_ERR_OOM;
+      }
+    }
+    bool have_id = false;
+    for (int k = 0; k < 128; ++k) have_id |= params->nccl_id[k] != 0;
+    if (params->transport == DEM_TRANSPORT_NCCL || (params->transport == DEM_TRANSPORT_PEER && have_id)) {
       ncclUniqueId id;
       static_assert(sizeof(id.internal) == 128, "ncclUniqueId size");
       std::memcpy(id.internal, params->nccl_id, 128);
@@ -623,6 +659,8 @@ extern "C" void dem_destroy(dem_system* sys) {
   if (!sys) return;
   if (sys->det_stream) cudaStreamSynchronize(sys->det_stream);
   cudaStreamSynchronize(sys->stream);
+  peer_release(sys);
+  if (sys->d_flags) cudaFree(sys->d_flags);
   if (sys->comm) ncclCommDestroy(sys->comm);
   free_graphs(sys);
   std::vector<void*> ptrs;
@@ -667,6 +705,122 @@ static dem_status alloc_rows(dem_system* sys, long long cap) {
   }
   sys->cap_entries = cap;
   free_graphs(sys);
+  return DEM_OK;
+}
+
+// ------------------------------------------------------------------ peer transports (fused halo)
+// Release the neighbour mappings and our IPC-exported state arrays (dem_set_state, dem_destroy).
+static dem_status peer_release(dem_system* sys) {
+  for (void* p : sys->ipc_open) cudaIpcCloseMemHandle(p);
+  sys->ipc_open.clear();
+  for (int p = 0; p < 2; ++p) {
+    if (sys->raw_state[p]) cudaFree(sys->raw_state[p]);
+    sys->raw_state[p] = nullptr;
+    sys->d_state[p] = nullptr;
+  }
+  for (int side = 0; side < 2; ++side) {
+    sys->remote_state[side][0] = sys->remote_state[side][1] = nullptr;
+    sys->remote_n[side] = 0;
+    sys->remote_flag[side] = nullptr;
+  }
+  return DEM_OK;
+}
+
+// our owned clumps' ghost slots in a neighbour: the k-th clump of our send list to that side
+// is the k-th of its receive list from us (both ascending gid)
+static dem_status peer_set_index(dem_system* sys, int side, const std::vector<int>& their_recv) {
+  std::vector<int> idx((size_t)std::max<int64_t>(sys->n_own, 1), -1);
+  if (their_recv.size() != sys->h_send_list[side].size()) {
+    sys->err = "peer halo: send and receive lists of neighbouring ranks differ";
+    return DEM_ERR_INVALID_ARG;
+  }
+  for (size_t k = 0; k < their_recv.size(); ++k) idx[sys->h_send_list[side][k]] = their_recv[k];
+  TRY(alloc_arr(sys, &sys->d_peer_idx[side], idx.size()));
+  CK(cudaMemcpy(sys->d_peer_idx[side], idx.data(), sizeof(int) * idx.size(), cudaMemcpyHostToDevice));
+  return DEM_OK;
+}
+
+// PEER (one process per GPU): every rank exports its IPC handles (two state arrays, flag words),
+// its clump count and its two receive lists; each rank imports its neighbours' packets (the
+// caller moves the bytes, e.g. torch.distributed all_gather) and maps their arrays with peer
+// access (NVLink)
+struct PeerHeader {
+  cudaIpcMemHandle_t state[2], flags;
+  long long n, len[2];
+};
+
+extern "C" dem_status dem_peer_export(dem_system* sys, int64_t cap, void* out, int64_t* len) {
+  if (!sys || !len || !sys->peer || sys->P.transport != DEM_TRANSPORT_PEER) return DEM_ERR_INVALID_ARG;
+  const int64_t need = (int64_t)(sizeof(PeerHeader) + sizeof(int) * (sys->h_recv_list[0].size() +
+                                                                       sys->h_recv_list[1].size()));
+  *len = need;
+  if (!out) return DEM_OK;
+  if (cap < need || !sys->raw_state[0]) return DEM_ERR_INVALID_ARG;
+  PeerHeader h{};
+  CK(cudaIpcGetMemHandle(&h.state[0], sys->raw_state[0]));
+  CK(cudaIpcGetMemHandle(&h.state[1], sys->raw_state[1]));
+  CK(cudaIpcGetMemHandle(&h.flags, sys->d_flags));
+  h.n = sys->n;
+  h.len[0] = (long long)sys->h_recv_list[0].size();
+  h.len[1] = (long long)sys->h_recv_list[1].size();
+  char* o = (char*)out;
+  std::memcpy(o, &h, sizeof h);
+  o += sizeof h;
+  for (int side = 0; side < 2; ++side) {
+    std::memcpy(o, sys->h_recv_list[side].data(), sizeof(int) * sys->h_recv_list[side].size());
+    o += sizeof(int) * sys->h_recv_list[side].size();
+  }
+  return DEM_OK;
+}
+
+extern "C" dem_status dem_peer_import(dem_system* sys, const void* left, const void* right) {
+  if (!sys || !sys->peer || sys->P.transport != DEM_TRANSPORT_PEER) return DEM_ERR_INVALID_ARG;
+  const int r = sys->P.rank, P = sys->P.n_ranks;
+  if ((r > 0) != (left != nullptr) || (r < P - 1) != (right != nullptr)) return DEM_ERR_INVALID_ARG;
+  for (void* p : sys->ipc_open) cudaIpcCloseMemHandle(p);
+  sys->ipc_open.clear();
+  for (int side = 0; side < 2; ++side) {
+    const char* pk = (const char*)(side == 0 ? left : right);
+    if (!pk) continue;
+    PeerHeader h;
+    std::memcpy(&h, pk, sizeof h);
+    // the neighbour's receive list from us: its list from the right if it is our left neighbour
+    const int theirs_side = side == 0 ? 1 : 0;
+    const int* lists = (const int*)(pk + sizeof h);
+    std::vector<int> their_recv(lists + (theirs_side == 0 ? 0 : h.len[0]),
+                                lists + (theirs_side == 0 ? 0 : h.len[0]) + h.len[theirs_side]);
+    TRY(peer_set_index(sys, side, their_recv));
+    for (int p = 0; p < 2; ++p) {
+      void* ptr = nullptr;
+      CK(cudaIpcOpenMemHandle(&ptr, h.state[p], cudaIpcMemLazyEnablePeerAccess));
+      sys->ipc_open.push_back(ptr);
+      sys->remote_state[side][p] = (double*)ptr;
+    }
+    void* fl = nullptr;
+    CK(cudaIpcOpenMemHandle(&fl, h.flags, cudaIpcMemLazyEnablePeerAccess));
+    sys->ipc_open.push_back(fl);
+    sys->remote_flag[side] = (int*)fl + (side == 0 ? 1 : 0);  // we are its right / left neighbour
+    sys->remote_n[side] = h.n;
+  }
+  sys->peer_linked = true;
+  free_graphs(sys);
+  return DEM_OK;
+}
+
+// LOOPBACK_PEER (one process, one GPU): the same links made with plain device pointers
+static dem_status peer_link_local(dem_system* const* systems, int n) {
+  for (int r = 0; r < n; ++r) {
+    dem_system* sys = systems[r];
+    for (int side = 0; side < 2; ++side) {
+      const int nb = side == 0 ? r - 1 : r + 1;
+      if (nb < 0 || nb >= n) continue;
+      dem_system* o = systems[nb];
+      for (int p = 0; p < 2; ++p) sys->remote_state[side][p] = o->d_state[p];
+      sys->remote_n[side] = o->n;
+      sys->remote_flag[side] = o->d_flags + (side == 0 ? 1 : 0);
+      TRY(peer_set_index(sys, side, o->h_recv_list[1 - side]));
+    }
+  }
   return DEM_OK;
 }
 
@@ -798,6 +952,15 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
   if (n > (1LL << 30)) return DEM_ERR_INVALID_ARG;
   CK(cudaStreamSynchronize(sys->stream));
   CK(cudaStreamSynchronize(sys->det_stream));
+  if (sys->peer && sys->P.transport == DEM_TRANSPORT_PEER && sys->raw_state[0] && sys->comm) {
+    // the neighbours may still be storing ghost states into our arrays: a barrier before the
+    // re-layout frees them (every rank calls dem_set_state; the steps before it are complete on
+    // each rank once its stream has passed this all-reduce)
+    CK(cudaMemsetAsync(sys->d_counter, 0, sizeof(unsigned long long), sys->stream));
+    if (ncclAllReduce(sys->d_counter, sys->d_counter, 1, ncclUint64, ncclMax, sys->comm, sys->stream) != ncclSuccess)
+      return DEM_ERR_NCCL;
+    CK(cudaStreamSynchronize(sys->stream));
+  }
   std::vector<long long> g(n);
   std::vector<int> t(n);
   std::vector<double> in[4];
@@ -994,6 +1157,10 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
     }
     for (auto& L : lists) std::sort(L.begin(), L.end(), [&](int x, int y) { return g[x] < g[y]; });
   }
+  for (int side = 0; side < 2; ++side) {
+    sys->h_send_list[side] = lists[side];
+    sys->h_recv_list[side] = lists[2 + side];
+  }
   n = n_hold;
   sys->n = n;
   sys->ns = ns;
@@ -1040,8 +1207,18 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
   TRY(alloc_arr(sys, &sys->d_gid, n));
   TRY(alloc_arr(sys, &sys->d_tid, n));
   TRY(alloc_arr(sys, &sys->d_sph_off, n + 1));
-  TRY(alloc_arr(sys, &sys->d_state[0], 13 * n));
-  TRY(alloc_arr(sys, &sys->d_state[1], 13 * n));
+  if (sys->peer) {
+    // IPC-exportable state (the neighbours store ghost states into it); the old mappings and
+    // arrays are released only after every rank has stopped stepping (barrier above)
+    TRY(peer_release(sys));
+    for (int p = 0; p < 2; ++p) {
+      CK(cudaMalloc(&sys->raw_state[p], sizeof(double) * 13 * std::max<int64_t>(n, 1)));
+      sys->d_state[p] = sys->raw_state[p];
+    }
+  } else {
+    TRY(alloc_arr(sys, &sys->d_state[0], 13 * n));
+    TRY(alloc_arr(sys, &sys->d_state[1], 13 * n));
+  }
   TRY(alloc_arr(sys, &sys->d_kin, (size_t)kKin * n));
   TRY(alloc_arr(sys, &sys->d_s_clump, ns));
   TRY(alloc_arr(sys, &sys->d_s_tc, ns));
@@ -1154,6 +1331,13 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
     if (n_own)
       CK(cudaMemcpyAsync(sys->d_outpos, sys->h_outpos.data(), sizeof(int) * n_own, cudaMemcpyHostToDevice, s));
     CK(cudaStreamSynchronize(s));
+  }
+  if (sys->peer) {
+    // step counts restart at 0: the flag words too, before the collective link below (a
+    // neighbour signals into them only after it has passed that link)
+    CK(cudaMemset(sys->d_flags, 0, 2 * sizeof(int)));
+    CK(cudaDeviceSynchronize());
+    sys->peer_linked = false;  // PEER: dem_peer_export / dem_peer_import before the next step
   }
   sys->launched = 0;
   sys->steps_done = 0;
@@ -1303,6 +1487,10 @@ static dem_status check_mesh_motion(dem_system* sys) {
 
 extern "C" dem_status dem_step(dem_system* sys, int64_t n_steps) {
   if (!sys || n_steps < 0) return DEM_ERR_INVALID_ARG;
+  if (sys->peer && sys->P.transport == DEM_TRANSPORT_PEER && !sys->peer_linked) {
+    sys->err = "PEER transport: call dem_peer_export / dem_peer_import after dem_set_state";
+    return DEM_ERR_INVALID_ARG;
+  }
   if (sys->h_ctl->err_code) return (dem_status)sys->h_ctl->err_code;
   TRY(check_mesh_motion(sys));
   int64_t remaining = n_steps;
@@ -1497,17 +1685,29 @@ extern "C" dem_status dem_partition_plan(int64_t n, const double* pos, double sl
 extern "C" dem_status dem_step_group(dem_system* const* systems, int32_t n, int64_t n_steps) {
   if (!systems || n < 1 || n_steps < 0) return DEM_ERR_INVALID_ARG;
   cudaStream_t s = systems[0]->stream;
+  const int tr = systems[0]->P.transport;
   for (int r = 0; r < n; ++r) {
     dem_system* sys = systems[r];
-    if (!sys || sys->stream != s || (n > 1 && (!sys->dist || sys->P.transport != DEM_TRANSPORT_LOOPBACK ||
-                                               sys->P.rank != r || sys->P.n_ranks != n)))
+    if (!sys || sys->stream != s ||
+        (n > 1 && (!sys->dist || sys->P.transport != tr ||
+                   (tr != DEM_TRANSPORT_LOOPBACK && tr != DEM_TRANSPORT_LOOPBACK_PEER) || sys->P.rank != r ||
+                   sys->P.n_ranks != n)))
       return DEM_ERR_INVALID_ARG;
     if (sys->h_ctl->err_code) return (dem_status)sys->h_ctl->err_code;
+  }
+  const bool peer = n > 1 && tr == DEM_TRANSPORT_LOOPBACK_PEER;
+  if (peer && !systems[0]->peer_linked) {
+    TRY(peer_link_local(systems, n));
+    for (int r = 0; r < n; ++r) systems[r]->peer_linked = true;
   }
   for (int64_t k = 0; k < n_steps; ++k) {
     for (int r = 0; r < n; ++r) {
       dem_system* sys = systems[r];
       enqueue_step(sys, step_kind(sys), s, nullptr, /*exchange=*/false);
+    }
+    if (peer) {  // the force kernels stored the ghost states into the neighbours already
+      for (int r = 0; r < n; ++r) advance_parities(systems[r], step_kind(systems[r]));
+      continue;
     }
     // ghost halo: rank r's left-side ghosts are rank r-1's right-side sends, and vice versa
     for (int r = 0; r < n; ++r) {
@@ -1727,8 +1927,8 @@ extern "C" dem_status dem_migrate(dem_system* sys, double threshold, int32_t* mo
   if (!sys || !(threshold >= 0)) return DEM_ERR_INVALID_ARG;
   if (moved) *moved = 0;
   if (!sys->dist || sys->launched == 0) return DEM_OK;  // nothing moved since the last partition
-  if (sys->P.transport != DEM_TRANSPORT_NCCL) {
-    sys->err = "dem_migrate needs the NCCL transport (loopback groups: dem_migrate_group)";
+  if ((sys->P.transport != DEM_TRANSPORT_NCCL && sys->P.transport != DEM_TRANSPORT_PEER) || !sys->comm) {
+    sys->err = "dem_migrate needs the NCCL or PEER transport (loopback groups: dem_migrate_group)";
     return DEM_ERR_INVALID_ARG;
   }
   TRY(dem_synchronize(sys));
@@ -1778,7 +1978,9 @@ extern "C" dem_status dem_migrate_group(dem_system* const* systems, int32_t n, d
   if (moved) *moved = 0;
   for (int r = 0; r < n; ++r) {
     dem_system* sys = systems[r];
-    if (!sys || (n > 1 && (!sys->dist || sys->P.transport != DEM_TRANSPORT_LOOPBACK || sys->P.rank != r ||
+    if (!sys || (n > 1 && (!sys->dist ||
+                           (sys->P.transport != DEM_TRANSPORT_LOOPBACK && sys->P.transport != DEM_TRANSPORT_LOOPBACK_PEER) ||
+                           sys->P.rank != r ||
                            sys->P.n_ranks != n)))
       return DEM_ERR_INVALID_ARG;
   }

@@ -31,13 +31,13 @@ def _strip(seed=0):
     return s
 
 
-def _group(dem, scene, P, drift_max=1e-3, record=True):
+def _group(dem, scene, P, drift_max=1e-3, record=True, transport=None):
     halo = dem.halo_width(scene, drift_max)
     b = dem.slab_bounds(scene.pos[:, 0], P, scene.domain_lo[0], scene.domain_hi[0])
     systems = []
     for r in range(P):
         d = dict(rank=r, n_ranks=P, slab_lo=b[r], slab_hi=b[r + 1], halo=halo, drift_max=drift_max,
-                 transport=dem.TRANSPORT_LOOPBACK)
+                 transport=dem.TRANSPORT_LOOPBACK if transport is None else transport)
         systems.append(dem.system_from_scene(scene, record_contacts=record, dist=d, entries_per_sphere=12))
     return systems
 
@@ -56,8 +56,10 @@ def _contacts(systems):
     return {k: v[order] for k, v in out.items()}
 
 
-@pytest.mark.parametrize("P", [2, 3])
-def test_loopback_decomposition_is_bitwise_identical(dem, P):
+@pytest.mark.parametrize("P,peer", [(2, False), (3, False), (2, True), (3, True)])
+def test_loopback_decomposition_is_bitwise_identical(dem, P, peer):
+    """peer: the fused halo (the force kernel stores ghost states straight into the neighbour's
+    arrays, flag handshake per step) instead of pack + copy + unpack."""
     scene = _strip()
     assert scene.n_clumps > 10_000
     ref = dem.system_from_scene(scene, record_contacts=True)
@@ -65,7 +67,7 @@ def test_loopback_decomposition_is_bitwise_identical(dem, P):
     sr = ref.dem_get_state()
     order = np.argsort(sr["gid"])
     sr = {k: v[order] for k, v in sr.items()}
-    systems = _group(dem, scene, P)
+    systems = _group(dem, scene, P, transport=dem.TRANSPORT_LOOPBACK_PEER if peer else None)
     stats = [s.dem_get_stats() for s in systems]
     assert sum(st["n_owned_clumps"] for st in stats) == scene.n_clumps
     assert all(st["n_ghost_clumps"] > 0 for st in stats)
@@ -89,7 +91,8 @@ def test_drift_beyond_halo_guard_is_reported(dem):
     assert e.value.status == -15
 
 
-def test_migration_keeps_the_trajectory_bitwise(dem):
+@pytest.mark.parametrize("peer", [False, True])
+def test_migration_keeps_the_trajectory_bitwise(dem, peer):
     """Clumps streaming across the slab face are migrated to their new owner with their
     tangential history (dem_migrate_group); the gathered P = 2 trajectory stays
     bitwise equal to the single-system run and no drift guard fires."""
@@ -97,7 +100,7 @@ def test_migration_keeps_the_trajectory_bitwise(dem):
     scene.vel[:, 0] += 1.5  # 1.5 m/s along x: ~0.15 mm per 100 steps, across the face
     ref = dem.system_from_scene(scene, record_contacts=True)
     drift = 0.1e-3
-    systems = _group(dem, scene, 2, drift_max=drift)
+    systems = _group(dem, scene, 2, drift_max=drift, transport=dem.TRANSPORT_LOOPBACK_PEER if peer else None)
     owned0 = [s.dem_get_stats()["n_owned_clumps"] for s in systems]
     moves = 0
     for _ in range(8):
