@@ -1815,7 +1815,8 @@ extern "C" dem_status dem_get_stats(dem_system* sys, dem_stats* out) {
   out->n_cells = sys->ncell;
   out->cell_size = sys->grid.cell;
   out->regrows = sys->regrows;
-  out->kernel_launches_per_step = kLaunchesPerStep + (sys->dist ? 4 : 0) + (sys->n_mesh ? 3 : 0);
+  out->kernel_launches_per_step =
+      kLaunchesPerStep + (sys->dist ? (sys->peer ? 2 : 4) : 0) + (sys->n_mesh ? 3 : 0);
   if (sys->launched > 0 && sys->ns > 0) {
     const RowBuf& R = sys->rows[sys->ep];
     int tot = 0, ins = 0;
