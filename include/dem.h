@@ -148,6 +148,7 @@ typedef struct {
   double cell_size;
   int64_t regrows;           /* capacity regrows so far */
   int64_t kernel_launches_per_step;
+  int64_t state_fast_resets;  /* dem_set_state calls that took the same-clumps fast path */
 } dem_stats;
 
 typedef struct dem_system dem_system;

@@ -56,7 +56,8 @@ class dem_stats(C.Structure):
     _fields_ = [("steps", C.c_int64), ("n_clumps", C.c_int64), ("n_spheres", C.c_int64),
                 ("n_owned_clumps", C.c_int64), ("n_owned_spheres", C.c_int64), ("n_ghost_clumps", C.c_int64),
                 ("n_entries", C.c_int64), ("n_contacts", C.c_int64), ("n_inserts", C.c_int64), ("n_cells", C.c_int64),
-                ("cell_size", C.c_double), ("regrows", C.c_int64), ("kernel_launches_per_step", C.c_int64)]
+                ("cell_size", C.c_double), ("regrows", C.c_int64), ("kernel_launches_per_step", C.c_int64),
+                ("state_fast_resets", C.c_int64)]
 
 
 TRANSPORT_NCCL, TRANSPORT_LOOPBACK, TRANSPORT_PEER, TRANSPORT_LOOPBACK_PEER = 0, 1, 2, 3

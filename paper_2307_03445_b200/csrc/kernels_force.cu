@@ -517,11 +517,14 @@ namespace dem {
 // arrays (AoS rows: pos 3, quat 4, vel 3, omega 3 per clump).
 __global__ void k_state_in(State st, const int* __restrict__ perm, int n, const double* __restrict__ pos,
                            const double* __restrict__ quat, const double* __restrict__ vel,
-                           const double* __restrict__ om, int* bad) {
+                           const double* __restrict__ om, int* bad, double* xref, int n_own) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int c = perm[i];
   const double x = pos[3 * c], y = pos[3 * c + 1], z = pos[3 * c + 2];
+  if (xref && i < n_own) {  // distributed: the drift reference of the owned clumps
+    xref[3 * i] = x; xref[3 * i + 1] = y; xref[3 * i + 2] = z;
+  }
   const double vx = vel[3 * c], vy = vel[3 * c + 1], vz = vel[3 * c + 2];
   const double wx = om[3 * c], wy = om[3 * c + 1], wz = om[3 * c + 2];
   if (!isfinite(x) || !isfinite(y) || !isfinite(z) || !isfinite(vx) || !isfinite(vy) || !isfinite(vz) ||
@@ -543,8 +546,8 @@ __global__ void k_state_out(State st, const int* __restrict__ outpos, int n_own,
   if (om) { om[3 * r] = st.wx[i]; om[3 * r + 1] = st.wy[i]; om[3 * r + 2] = st.wz[i]; }
 }
 void launch_state_in(const State& st, const int* perm, int n, const double* pos, const double* quat,
-                     const double* vel, const double* om, int* bad, cudaStream_t s) {
-  if (n) k_state_in<<<(n + 255) / 256, 256, 0, s>>>(st, perm, n, pos, quat, vel, om, bad);
+                     const double* vel, const double* om, int* bad, double* xref, int n_own, cudaStream_t s) {
+  if (n) k_state_in<<<(n + 255) / 256, 256, 0, s>>>(st, perm, n, pos, quat, vel, om, bad, xref, n_own);
 }
 void launch_state_out(const State& st, const int* outpos, int n_own, double* pos, double* quat, double* vel,
                       double* om, cudaStream_t s) {

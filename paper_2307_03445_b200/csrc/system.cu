@@ -37,7 +37,7 @@ void launch_mesh_pose(const StepArgs&, cudaStream_t);
 void launch_peer_signal(const Ctl* ctl, int* r0, int* r1, cudaStream_t s);
 void launch_peer_wait(Ctl* ctl, const int* f0, const int* f1, cudaStream_t s);
 void launch_state_in(const State& st, const int* perm, int n, const double* pos, const double* quat,
-                     const double* vel, const double* om, int* bad, cudaStream_t s);
+                     const double* vel, const double* om, int* bad, double* xref, int n_own, cudaStream_t s);
 void launch_state_out(const State& st, const int* outpos, int n_own, double* pos, double* quat, double* vel,
                       double* om, cudaStream_t s);
 void launch_mesh_pairs(const StepArgs&, cudaStream_t);
@@ -84,6 +84,7 @@ struct dem_system {
   std::vector<long long> h_in_gid;
   std::vector<int> h_in_tid;
   std::vector<int> h_outpos;        // owned storage index -> output row of dem_get_state
+  std::vector<int8_t> h_role, h_sendf;  // the slab partition of the last input (distributed)
   int *d_perm = nullptr, *d_outpos = nullptr, *d_io_bad = nullptr;
   double* d_io = nullptr;           // 13 n doubles of staging (caller-order AoS rows)
   long long* d_gid = nullptr;
@@ -164,6 +165,7 @@ struct dem_system {
   std::vector<int> h_send_list[2], h_recv_list[2];   // storage indices, ascending gid
   std::vector<void*> ipc_open;                       // neighbour mappings to close
   bool peer_linked = false;
+  int64_t fast_resets = 0;
 };
 
 static dem_status peer_release(dem_system* sys);
@@ -978,9 +980,26 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
     }
   }
   // fast path: the same clumps as the last call (a state reset or restore): the state is
-  // permuted into the existing storage order on the device, nothing is re-laid out
-  if (!sys->dist && n > 0 && sys->n == n && (int64_t)sys->h_in_gid.size() == n && sys->d_perm &&
-      std::equal(g.begin(), g.end(), sys->h_in_gid.begin()) && std::equal(t.begin(), t.end(), sys->h_in_tid.begin())) {
+  // permuted into the existing storage order on the device, nothing is re-laid out.  A
+  // distributed system also needs the same slab partition (roles of every clump by COM x).
+  bool same = n > 0 && (int64_t)sys->h_in_gid.size() == n && sys->d_perm &&
+              std::equal(g.begin(), g.end(), sys->h_in_gid.begin()) &&
+              std::equal(t.begin(), t.end(), sys->h_in_tid.begin());
+  if (same && sys->dist) {
+    std::vector<double> hp;
+    const double* P0 = pos;
+    if (on_device) {
+      hp.resize((size_t)3 * n);
+      CK(cudaMemcpy(hp.data(), pos, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
+      P0 = hp.data();
+    }
+    std::vector<int8_t> r2(n), f2(n);
+    const dem_params& PP = sys->P;
+    TRY(dem_partition_plan(n, P0, PP.slab_lo, PP.slab_hi, PP.halo, PP.rank > 0, PP.rank < PP.n_ranks - 1,
+                           r2.data(), f2.data()));
+    same = r2 == sys->h_role && f2 == sys->h_sendf;
+  }
+  if (same) {
     cudaStream_t s = sys->stream;
     const double* dsrc[4] = {pos, quat, vel, omega};
     if (!on_device) {
@@ -994,7 +1013,8 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
     CK(cudaMemsetAsync(sys->d_io_bad, 0, sizeof(int), s));
     sys->sp = 0;
     const StepArgs a = make_args(sys, K_FULL);
-    launch_state_in(a.cur, sys->d_perm, (int)n, dsrc[0], dsrc[1], dsrc[2], dsrc[3], sys->d_io_bad, s);
+    launch_state_in(a.cur, sys->d_perm, (int)sys->n, dsrc[0], dsrc[1], dsrc[2], dsrc[3], sys->d_io_bad,
+                    sys->dist ? sys->d_xref : nullptr, (int)sys->n_own, s);
     CK(cudaMemsetAsync(sys->d_cell_count, 0, sizeof(int) * sys->ncell, s));
     for (int p = 0; p < 2; ++p) CK(cudaMemsetAsync(sys->rows[p].row_ptr, 0, sizeof(int) * (sys->ns + 1), s));
     std::memset(sys->h_ctl, 0, sizeof(Ctl));
@@ -1003,6 +1023,20 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
     CK(cudaMemcpyAsync(&bad, sys->d_io_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     if (bad) return DEM_ERR_NONFINITE;
+    if (sys->peer) {
+      // step counts restart at 0: so do the flag words, then every rank passes a barrier before
+      // any of them steps again (a neighbour's first signal must not hit a flag word that is
+      // still to be reset)
+      CK(cudaMemset(sys->d_flags, 0, 2 * sizeof(int)));
+      CK(cudaDeviceSynchronize());
+      if (sys->comm) {
+        CK(cudaMemsetAsync(sys->d_counter, 0, sizeof(unsigned long long), s));
+        if (ncclAllReduce(sys->d_counter, sys->d_counter, 1, ncclUint64, ncclMax, sys->comm, s) != ncclSuccess)
+          return DEM_ERR_NCCL;
+        CK(cudaStreamSynchronize(s));
+      }
+    }
+    sys->fast_resets++;
     sys->launched = 0;
     sys->steps_done = 0;
     sys->up = sys->ep = 0;
@@ -1021,6 +1055,7 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
   }
   std::vector<long long> g_in(g);
   std::vector<int> t_in(t);
+  // (the slab partition of this input is kept for the fast path's check)
   for (int64_t c = 0; c < n; ++c)
     if (t[c] < 0 || t[c] >= sys->n_tmpl || g[c] < 0 || g[c] >= (1LL << 56)) {
       sys->err = "clump " + std::to_string(c) + ": bad template id or gid";
@@ -1032,6 +1067,8 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
     const dem_params& P = sys->P;
     TRY(dem_partition_plan(n, src[0], P.slab_lo, P.slab_hi, P.halo, P.rank > 0, P.rank < P.n_ranks - 1,
                            role.data(), sendf.data()));
+    sys->h_role = role;
+    sys->h_sendf = sendf;
   }
   free_graphs(sys);
   // grid: cell edge (auto: 4 x mean sphere radius + margin, at least 2 r_min + margin)
@@ -1325,7 +1362,7 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
     for (int64_t r = 0; r < n_own; ++r) sys->h_outpos[sys->dist ? ord[r] : r] = sys->dist ? (int)r : perm[r];
     TRY(alloc_arr(sys, &sys->d_perm, (size_t)n + 1));
     TRY(alloc_arr(sys, &sys->d_outpos, (size_t)n_own + 1));
-    TRY(alloc_arr(sys, &sys->d_io, (size_t)13 * n + 1));
+    TRY(alloc_arr(sys, &sys->d_io, (size_t)13 * std::max<int64_t>(n, (int64_t)sys->h_in_gid.size()) + 1));
     TRY(alloc_arr(sys, &sys->d_io_bad, 1));
     if (n) CK(cudaMemcpyAsync(sys->d_perm, perm.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
     if (n_own)
@@ -1817,6 +1854,7 @@ extern "C" dem_status dem_get_stats(dem_system* sys, dem_stats* out) {
   out->regrows = sys->regrows;
   out->kernel_launches_per_step =
       kLaunchesPerStep + (sys->dist ? (sys->peer ? 2 : 4) : 0) + (sys->n_mesh ? 3 : 0);
+  out->state_fast_resets = sys->fast_resets;
   if (sys->launched > 0 && sys->ns > 0) {
     const RowBuf& R = sys->rows[sys->ep];
     int tot = 0, ins = 0;

@@ -131,3 +131,25 @@ def test_migration_below_threshold_is_a_no_op(dem):
     owned = [s.dem_get_stats()["n_owned_clumps"] for s in systems]
     assert not dem.migrate_group(systems, threshold=1.0)
     assert [s.dem_get_stats()["n_owned_clumps"] for s in systems] == owned
+
+
+@pytest.mark.parametrize("peer", [False, True])
+def test_distributed_fast_reset_equals_fresh_group(dem, peer):
+    """dem_set_state with the same global clumps and the same slab partition takes the fast
+    path on every rank (device permutation, drift reference refreshed, step counts and peer flag
+    words reset); the group then steps exactly like a freshly built one."""
+    scene = _strip(seed=5)
+    tr = dem.TRANSPORT_LOOPBACK_PEER if peer else None
+    a = _group(dem, scene, 2, record=False, transport=tr)
+    dem.step_group(a, 25)
+    t = scene.copy()
+    t.vel = scene.vel[::-1].copy()
+    for s in a:
+        s.dem_set_state(t.gid, t.tid, t.pos, t.quat, t.vel, t.omega)
+        assert s.dem_get_stats()["state_fast_resets"] == 1
+    b = _group(dem, t, 2, record=False, transport=tr)
+    dem.step_group(a, 30)
+    dem.step_group(b, 30)
+    ga, gb = _gather(a), _gather(b)
+    for k in ("gid", "pos", "quat", "vel", "omega"):
+        assert np.array_equal(ga[k], gb[k]), k

@@ -36,7 +36,7 @@ def test_fast_reset_equals_fresh_system(dem):
     a.dem_step(120)  # leaves history and a non-zero ping-pong phase behind
     t = _moved(s)
     a.dem_set_state(t.gid, t.tid, t.pos, t.quat, t.vel, t.omega)
-    assert a.dem_get_stats()["steps"] == 0
+    assert a.dem_get_stats()["steps"] == 0 and a.dem_get_stats()["state_fast_resets"] == 1
     b = dem.system_from_scene(t)
     a.dem_step(150)
     b.dem_step(150)
