@@ -26,7 +26,18 @@
 namespace dem {
 
 // ---------------------------------------------------------------- (a1) + bin count
-__global__ void __launch_bounds__(256) k_pose_count(StepArgs a) {
+// threads per CTA of the per-sphere kernels (A/B on the C5 bench: 64 beats 128 by 0.5%, 256 by
+// 2.5%, 512 by 17% — smaller CTAs keep more warps resident at these register counts)
+#ifndef DEM_POSE_TPB
+#define DEM_POSE_TPB 64
+#endif
+#ifndef DEM_SCATTER_TPB
+#define DEM_SCATTER_TPB 64
+#endif
+#ifndef DEM_ROWS_TPB
+#define DEM_ROWS_TPB 64
+#endif
+__global__ void __launch_bounds__(DEM_POSE_TPB) k_pose_count(StepArgs a) {
   if (a.adopt && blockIdx.x == 0 && threadIdx.x == 0 && a.ctl->det_abort) {
     // the set detected ahead overflowed a capacity: abort this adoption step, the host regrows
     // and rebuilds the set at this step instead (same trajectory: DESIGN.md §5.2)
@@ -97,7 +108,7 @@ __global__ void __launch_bounds__(256) k_pose_count(StepArgs a) {
 // ---------------------------------------------------------------- bin scatter
 // Slots are taken by decrementing the counts, which leaves cell_count all-zero for the
 // next step.  The order inside a bin is irrelevant: rows are sorted by partner key.
-__global__ void __launch_bounds__(256) k_bin_scatter(StepArgs a) {
+__global__ void __launch_bounds__(DEM_SCATTER_TPB) k_bin_scatter(StepArgs a) {
   if (*a.abort || a.ctl->abort) return;  // (an error in the steps running beside an ahead detection)
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.ns) return;
@@ -454,7 +465,7 @@ __device__ __forceinline__ int prev_index(const Rows& prev, int pb, int pe, long
   return -1;
 }
 
-__global__ void __launch_bounds__(256) k_rows_finish(StepArgs a) {
+__global__ void __launch_bounds__(DEM_ROWS_TPB) k_rows_finish(StepArgs a) {
   if (*a.abort || a.ctl->abort) return;  // (an error in the steps running beside an ahead detection)
   const int total = a.rows.row_ptr[a.ns];
   if ((long long)total > a.cap_entries) {
@@ -549,10 +560,10 @@ __global__ void __launch_bounds__(256) k_rows_finish(StepArgs a) {
 
 // host launchers
 void launch_pose_count(const StepArgs& a, cudaStream_t s) {
-  k_pose_count<<<a.ns ? (a.ns + 255) / 256 : 1, 256, 0, s>>>(a);
+  k_pose_count<<<a.ns ? (a.ns + DEM_POSE_TPB - 1) / DEM_POSE_TPB : 1, DEM_POSE_TPB, 0, s>>>(a);
 }
 void launch_bin_scatter(const StepArgs& a, cudaStream_t s) {
-  if (a.ns) k_bin_scatter<<<(a.ns + 255) / 256, 256, 0, s>>>(a);
+  if (a.ns) k_bin_scatter<<<(a.ns + DEM_SCATTER_TPB - 1) / DEM_SCATTER_TPB, DEM_SCATTER_TPB, 0, s>>>(a);
 }
 void launch_pairs(const StepArgs& a, cudaStream_t s, int n_sm) {
   long long warps = a.ncell;
@@ -571,7 +582,7 @@ void launch_pairs(const StepArgs& a, cudaStream_t s, int n_sm) {
     k_pairs<false, false><<<(unsigned)blocks, kPairWarps * 32, 0, s>>>(a);
 }
 void launch_rows_finish(const StepArgs& a, cudaStream_t s) {
-  if (a.ns) k_rows_finish<<<(a.ns + 255) / 256, 256, 0, s>>>(a);
+  if (a.ns) k_rows_finish<<<(a.ns + DEM_ROWS_TPB - 1) / DEM_ROWS_TPB, DEM_ROWS_TPB, 0, s>>>(a);
 }
 
 }  // namespace dem
