@@ -144,7 +144,10 @@ __global__ void __launch_bounds__(DEM_SCATTER_TPB) k_bin_scatter(StepArgs a) {
 #ifndef DEM_PAIRS_CONTIG
 #define DEM_PAIRS_CONTIG 64  // bins per warp in a CTA span
 #endif
-constexpr int kPairWarps = 8;
+#ifndef DEM_PAIRS_WARPS
+#define DEM_PAIRS_WARPS 8
+#endif
+constexpr int kPairWarps = DEM_PAIRS_WARPS;
 constexpr int kPairBuf = DEM_PAIRS_BUF;
 
 // Members of a bin, staged in the warp's shared memory.  Both spheres of a pair overlap the
