@@ -544,3 +544,27 @@ def mesh_funnel(r_top: float, r_bottom: float, height: float, n: int = 32) -> np
         d = (r_top * np.cos(th[k]), r_top * np.sin(th[k]), height)
         tris += [(a, b, c), (a, c, d)]
     return np.array(tris, dtype=np.float64)
+
+
+def mesh_wheel(radius: float = 0.25, width: float = 0.15, n: int = 72, grousers: int = 24,
+               grouser_h: float = 0.01) -> np.ndarray:
+    """A rover-style wheel: the rolling surface of a cylinder about the body y axis
+    (n facets around), its two side disks, and `grousers` radial plates of height grouser_h
+    across the width.  Outward orientation is not needed (contacts are unsigned)."""
+    th = np.linspace(0.0, 2 * np.pi, n + 1)
+    y0, y1 = -0.5 * width, 0.5 * width
+    tris = []
+    for k in range(n):
+        a0, a1 = th[k], th[k + 1]
+        p = [(radius * np.cos(a), y, radius * np.sin(a)) for a in (a0, a1) for y in (y0, y1)]
+        tris += [(p[0], p[2], p[3]), (p[0], p[3], p[1])]
+        for y in (y0, y1):  # side disks as fans
+            tris.append(((0.0, y, 0.0), (radius * np.cos(a0), y, radius * np.sin(a0)),
+                         (radius * np.cos(a1), y, radius * np.sin(a1))))
+    for g in range(grousers):
+        a = 2 * np.pi * g / grousers
+        c, s_ = np.cos(a), np.sin(a)
+        r0, r1 = radius, radius + grouser_h
+        q = [(r * c, y, r * s_) for r in (r0, r1) for y in (y0, y1)]
+        tris += [(q[0], q[2], q[3]), (q[0], q[3], q[1])]
+    return np.array(tris, dtype=np.float64)
