@@ -46,6 +46,9 @@ int force_cta_spheres() { return kMaxS; }
 #ifndef DEM_FORCE_MINB
 #define DEM_FORCE_MINB (1024 / DEM_FORCE_FT)  // 64 registers
 #endif
+#ifndef DEM_FORCE_MINB_MESH
+#define DEM_FORCE_MINB_MESH DEM_FORCE_MINB  // 80 registers (6 CTAs) spill less but run slower
+#endif
 // A mesh entry (NEXT-3): the sphere's closest point on the triangle (R25), counted only if it is
 // its feature's contact among the sphere's entries on the same mesh (R26).  Outputs the contact
 // frame as for a wall (n from the sphere to the surface, the middle of the overlap), the mesh's
@@ -112,7 +115,7 @@ __device__ __noinline__ bool mesh_entry(const MeshView a, int tri, int row_beg, 
 }
 
 template <bool kMesh, bool kPeer>
-__global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArgs a) {
+__global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_MINB) k_force_integrate(StepArgs a) {
   __shared__ int rp[kMaxS + 1];
   __shared__ double4 own_p[kMaxS];
   __shared__ int own_mat[kMaxS];
@@ -124,7 +127,7 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
   __shared__ int emesh[kMesh ? kFT : 1];
   __shared__ double mtq[3][kMesh ? kFT : 1];
   __shared__ double cw[kMesh ? kMaxMeshes : 1][6];
-  bool cta_mesh = false;
+  __shared__ int chunk_mesh, cta_mesh;  // this chunk / this CTA holds mesh entries
   const int tid = threadIdx.x;
   const int2 b0 = a.cta_clump[blockIdx.x], b1 = a.cta_clump[blockIdx.x + 1];
   const int c0 = b0.x, c1 = b1.x;
@@ -159,6 +162,7 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
     for (int k = tid; k < ncl * (kKin / 2); k += kFT) reinterpret_cast<double2*>(ck)[k] = src[k];
   }
   if (kMesh && tid < kMaxMeshes * 6) cw[tid / 6][tid % 6] = 0.0;
+  if (kMesh && tid == 0) chunk_mesh = cta_mesh = 0;
   __syncthreads();
   const double h = a.h;
   const int E0 = rp[0], E1 = rp[nsph];
@@ -325,25 +329,25 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
         // reaction on the mesh: +F at p, torque (p - X_m) x F
         const double mx = px - Xjx, my = py - Xjy, mz = pz - Xjz;
         emesh[tid] = mesh;
+        chunk_mesh = 1;  // (a benign race: every writer stores 1)
         mtq[0][tid] = my * Fz - mz * Fy;
         mtq[1][tid] = mz * Fx - mx * Fz;
         mtq[2][tid] = mx * Fy - my * Fx;
       }
     }
-    if (kMesh) {
-      // the CTA's mesh wrench, entries in row order (deterministic)
-      if (__syncthreads_or(emesh[tid] >= 0)) {
-        cta_mesh = true;
-        if (tid == 0)
-          for (int q = 0; q < kFT; ++q) {
-            const int m = emesh[q];
-            if (m < 0) continue;
-            cw[m][0] -= part[0][q]; cw[m][1] -= part[1][q]; cw[m][2] -= part[2][q];
-            cw[m][3] += mtq[0][q]; cw[m][4] += mtq[1][q]; cw[m][5] += mtq[2][q];
-          }
+    __syncthreads();
+    if (kMesh && tid == 0 && chunk_mesh) {
+      // the CTA's mesh wrench, entries in row order (deterministic), beside the per-sphere sums
+      // of the other threads (both only read part[] until the next barrier)
+      cta_mesh = 1;
+      chunk_mesh = 0;
+      for (int q = 0; q < kFT; ++q) {
+        const int m = emesh[q];
+        if (m < 0) continue;
+        cw[m][0] -= part[0][q]; cw[m][1] -= part[1][q]; cw[m][2] -= part[2][q];
+        cw[m][3] += mtq[0][q]; cw[m][4] += mtq[1][q]; cw[m][5] += mtq[2][q];
       }
     }
-    __syncthreads();
     // (a9, first level) canonical per-sphere sums: entries in row (partner-key) order
     for (int ls = tid; ls < nsph; ls += kFT) {
       const int b = max(rp[ls], c0e), en = min(rp[ls + 1], c0e + kFT);
@@ -357,7 +361,7 @@ __global__ void __launch_bounds__(kFT, DEM_FORCE_MINB) k_force_integrate(StepArg
   if (kMesh) {
     if (cta_mesh && tid < a.n_mesh * 6)
       a.mesh_part[((size_t)blockIdx.x * a.n_mesh + tid / 6) * 6 + tid % 6] = cw[tid / 6][tid % 6];
-    if (tid == 0) a.mesh_flag[blockIdx.x] = cta_mesh ? 1 : 0;
+    if (tid == 0) a.mesh_flag[blockIdx.x] = cta_mesh;
   }
   if (tid >= ncl) return;
   // (a9, second level) + (a10): per clump, spheres in component order.

@@ -38,6 +38,7 @@ def main():
     s.meshes = [Mesh(wheel, 0, pos=(cx, cy, top + R - 0.02), vel=(v, 0.0, 0.0), omega=(0.0, w, 0.0))]
     g = dem.system_from_scene(s)
     g.dem_step(a.warmup)
+    g.dem_set_profiling(True)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(g.stream)
@@ -46,11 +47,15 @@ def main():
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / a.steps
     st = g.dem_get_stats()
+    stages = g.dem_get_stage_times()
+    g.dem_set_profiling(False)
     m = g.dem_get_mesh(0)
     out = dict(workload="C5 bed + grousered wheel mesh (P:441 single-wheel slip)", spheres=st["n_spheres"],
                triangles=int(wheel.shape[0]), steps=a.steps, warmup=a.warmup, ms_per_step=ms,
                sphere_steps_per_s=st["n_spheres"] / (ms * 1e-3), contacts=st["n_contacts"],
-               wheel_force_n=m["force"].tolist(), wheel_torque_nm=m["torque"].tolist())
+               wheel_force_n=m["force"].tolist(), wheel_torque_nm=m["torque"].tolist(), stage_ms=stages,
+               note="stage events between the kernels on the system stream (mesh pose in pose, mesh pairs in "
+                    "bin_scatter, mesh finish in force)")
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     json.dump(out, open(os.path.join(ROOT, "gpurun_out", "wheel_bench.json"), "w"), indent=1)
     print(json.dumps(out))
