@@ -32,6 +32,11 @@
  *     been checked); dem_last_error() names the clump/contact key and the step.  Capacity
  *     overflows (bins, contact rows) are handled internally by regrowing and re-running the
  *     aborted steps; a contact list is never silently truncated.
+ *   - Environment (test and diagnosis hooks, read at dem_create / dem_step; off by default):
+ *     DEM_FAULT_AHEAD_OVERFLOW=n  the next n ahead detections (overlapped cadence) report a
+ *                                 capacity overflow (exercises the recovery path);
+ *     DEM_DEBUG_SERIAL_DET=1      the force steps wait for an ahead detection (no overlap);
+ *     DEM_DEBUG_LOG=1             capacity regrows are logged to stderr.
  */
 #ifndef DEM_B200_H
 #define DEM_B200_H
