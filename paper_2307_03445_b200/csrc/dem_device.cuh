@@ -138,6 +138,13 @@ struct StepArgs {
   double* mesh_part;         // [6 n_mesh n_cta] per-CTA wrench partials (force on mesh, torque about X)
   int* mesh_flag;            // [n_cta] 1 if the CTA wrote a partial this step
   double* mesh_wrench;       // [6 n_mesh] the last step's wrench
+  // mesh entries of the set in use (k_mesh_geom) and of the set being detected (k_rows_finish):
+  // (entry, own sphere) pairs, and the per-entry closest point + "counts" flag of this step
+  const int2* mlist;         // [*mlist_n]
+  const int* mlist_n;
+  int2* mlist_out;
+  int* mlist_out_n;
+  double4* mgeom;            // [cap_entries] closest point (x, y, z), w = 1 if the contact counts (R26)
   // fused halo (peer transport): the integrating thread of a clump in a send list
   // writes its new state straight into the neighbour's next-state array at the neighbour's ghost
   // slot (NVLink peer stores), so there is no pack, no collective and no unpack

@@ -551,6 +551,9 @@ __global__ void __launch_bounds__(DEM_ROWS_TPB) k_rows_finish(StepArgs a) {
       R[u].prev = (pj < pe && a.prev.ent[pj].key == k) ? pj : -1;
     }
   }
+  if (a.n_tri)  // this set's mesh entries, for the per-step geometry pass (k_mesh_geom)
+    for (int u = 0; u < nc; ++u)
+      if (R[u].partner <= -1 - kMaxPlanes) a.mlist_out[atomicAdd(a.mlist_out_n, 1)] = make_int2(beg + u, i);
   for (int u = nc, p = a.tab.n_planes - 1; p >= 0; --p)
     if (wmask >> p & 1u) {
       Entry e;

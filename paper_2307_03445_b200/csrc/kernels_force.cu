@@ -49,69 +49,48 @@ int force_cta_spheres() { return kMaxS; }
 #ifndef DEM_FORCE_MINB_MESH
 #define DEM_FORCE_MINB_MESH DEM_FORCE_MINB  // 80 registers (6 CTAs) spill less but run slower
 #endif
-// A mesh entry (NEXT-3): the sphere's closest point on the triangle (R25), counted only if it is
-// its feature's contact among the sphere's entries on the same mesh (R26).  Outputs the contact
-// frame as for a wall (n from the sphere to the surface, the middle of the overlap), the mesh's
-// reference point, velocity and angular velocity (the point velocity of the boundary).
-// (the pointers it needs, by value: a reference to the kernel's StepArgs would make every thread
-// copy the whole parameter block to its stack)
-struct MeshView {
-  const double* tri_world;
-  const int* tri_mesh;
-  const int* tri_vid;
-  const double* mesh;
-  const int* mesh_mat;
-  const Entry* ent;
-};
-
-__device__ __noinline__ bool mesh_entry(const MeshView a, int tri, int row_beg, int row_end, double cx,
-                                        double cy, double cz, double ri, double& nx, double& ny, double& nz,
-                                        double& px, double& py, double& pz, double& delta, int& mj, double* Xvw,
-                                        int& mesh, bool& degenerate) {
-  const double* T = a.tri_world + 9 * tri;
-  double qx, qy, qz;
-  const int reg = closest_on_triangle(T, cx, cy, cz, qx, qy, qz);
-  const double dx = sub(cx, qx), dy = sub(cy, qy), dz = sub(cz, qz);
-  const double dist = sqrt(add(add(mul(dx, dx), mul(dy, dy)), mul(dz, dz)));
-  degenerate = dist == 0.0;
-  delta = ri - dist;
-  const double inv = 1.0 / dist;
-  nx = -(dx * inv);
-  ny = -(dy * inv);
-  nz = -(dz * inv);
-  const double arm = ri - 0.5 * delta;
-  px = cx + arm * nx;
-  py = cy + arm * ny;
-  pz = cz + arm * nz;
-  mesh = a.tri_mesh[tri];
-  mj = a.mesh_mat[mesh];
-  const double* M = a.mesh + kMeshRec * mesh;
-  Xvw[0] = M[0]; Xvw[1] = M[1]; Xvw[2] = M[2];
-  Xvw[3] = M[7]; Xvw[4] = M[8]; Xvw[5] = M[9];
-  Xvw[6] = M[10]; Xvw[7] = M[11]; Xvw[8] = M[12];
-  // one contact per feature: face > edge > vertex, ties to the lower triangle index
-  int kind, u, v;
-  tri_feature(a.tri_vid, tri, reg, kind, u, v);
-  if (kind == 2) return true;
-  for (int e = row_beg; e < row_end; ++e) {
-    const int code = a.ent[e].partner;
-    if (code > -1 - kMaxPlanes) continue;
-    const int tj = -1 - kMaxPlanes - code;
-    if (tj == tri || a.tri_mesh[tj] != mesh) continue;
-    double ox, oy, oz;
-    const int rj = closest_on_triangle(a.tri_world + 9 * tj, cx, cy, cz, ox, oy, oz);
-    int kj, uj, vj;
-    tri_feature(a.tri_vid, tj, rj, kj, uj, vj);
-    if (kind == 1) {
-      if (kj == 2 && tri_has(a.tri_vid, tj, u) && tri_has(a.tri_vid, tj, v)) return false;
-      if (kj == 1 && uj == u && vj == v && tj < tri) return false;
-    } else {
-      if (kj == 2 && tri_has(a.tri_vid, tj, u)) return false;
-      if (kj == 1 && (uj == u || vj == u)) return false;
-      if (kj == 0 && uj == u && tj < tri) return false;
-    }
+// Mesh entries (NEXT-3), per step, before the force kernel: the sphere's closest point on the
+// triangle (R25) and whether the contact counts under one contact per feature (R26: face >
+// edge > vertex among the sphere's entries on the same mesh, ties to the lower triangle).  The
+// force kernel then treats a mesh entry like a wall entry with this point.
+__global__ void __launch_bounds__(256) k_mesh_geom(StepArgs a) {
+  if (a.ctl->abort) return;
+  const int n = *a.mlist_n;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const int2 it = a.mlist[k];
+    const int e = it.x, i = it.y;
+    const int tri = -1 - kMaxPlanes - a.rows.ent[e].partner;
+    const double4 c = a.spos[i];
+    double qx, qy, qz;
+    const int reg = closest_on_triangle(a.tri_world + 9 * tri, c.x, c.y, c.z, qx, qy, qz);
+    const int mesh = a.tri_mesh[tri];
+    int kind, u, v;
+    tri_feature(a.tri_vid, tri, reg, kind, u, v);
+    bool counts = true;
+    if (kind != 2)
+      for (int f = a.rows.row_ptr[i], fe = a.rows.row_ptr[i + 1]; f < fe && counts; ++f) {
+        const int code = a.rows.ent[f].partner;
+        if (code > -1 - kMaxPlanes) continue;
+        const int tj = -1 - kMaxPlanes - code;
+        if (tj == tri || a.tri_mesh[tj] != mesh) continue;
+        double ox, oy, oz;
+        const int rj = closest_on_triangle(a.tri_world + 9 * tj, c.x, c.y, c.z, ox, oy, oz);
+        int kj, uj, vj;
+        tri_feature(a.tri_vid, tj, rj, kj, uj, vj);
+        if (kind == 1) {
+          if (kj == 2 && tri_has(a.tri_vid, tj, u) && tri_has(a.tri_vid, tj, v)) counts = false;
+          if (kj == 1 && uj == u && vj == v && tj < tri) counts = false;
+        } else {
+          if (kj == 2 && tri_has(a.tri_vid, tj, u)) counts = false;
+          if (kj == 1 && (uj == u || vj == u)) counts = false;
+          if (kj == 0 && uj == u && tj < tri) counts = false;
+        }
+      }
+    a.mgeom[e] = make_double4(qx, qy, qz, counts ? 1.0 : 0.0);
   }
-  return true;
+}
+void launch_mesh_geom(const StepArgs& a, cudaStream_t s) {
+  if (a.n_tri) k_mesh_geom<<<4 * 148, 256, 0, s>>>(a);
 }
 
 template <bool kMesh, bool kPeer>
@@ -205,15 +184,30 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
       bool active = true;
       int mesh = -1;
       if (kMesh && t <= -1 - kMaxPlanes) {
-        double Xvw[9];
-        const MeshView mv{a.tri_world, a.tri_mesh, a.tri_vid, a.mesh, a.mesh_mat, a.rows.ent};
-        active = mesh_entry(mv, -1 - kMaxPlanes - t, rp[ls], rp[ls + 1], cx, cy, cz, ri, nx, ny, nz, px, py, pz,
-                            delta, mj, Xvw, mesh, degenerate);
+        // the closest point and the feature rule come from k_mesh_geom; n from the sphere to
+        // the surface, the middle of the overlap, the flat-wall limit (R25-R27)
+        const double4 gq = a.mgeom[e];
+        const double dx = sub(cx, gq.x), dy = sub(cy, gq.y), dz = sub(cz, gq.z);
+        const double dist = sqrt(add(add(mul(dx, dx), mul(dy, dy)), mul(dz, dz)));
+        degenerate = dist == 0.0;
+        delta = ri - dist;
+        const double inv = 1.0 / dist;
+        nx = -(dx * inv);
+        ny = -(dy * inv);
+        nz = -(dz * inv);
+        const double arm = ri - 0.5 * delta;
+        px = cx + arm * nx;
+        py = cy + arm * ny;
+        pz = cz + arm * nz;
+        active = gq.w != 0.0;
+        mesh = a.tri_mesh[-1 - kMaxPlanes - t];
+        mj = a.mesh_mat[mesh];
+        const double* M = a.mesh + kMeshRec * mesh;
+        Xjx = M[0]; Xjy = M[1]; Xjz = M[2];
+        Vjx = M[7]; Vjy = M[8]; Vjz = M[9];
+        Wjx = M[10]; Wjy = M[11]; Wjz = M[12];
         rbar = ri;
         mbar = Mi;
-        Xjx = Xvw[0]; Xjy = Xvw[1]; Xjz = Xvw[2];
-        Vjx = Xvw[3]; Vjy = Xvw[4]; Vjz = Xvw[5];
-        Wjx = Xvw[6]; Wjy = Xvw[7]; Wjz = Xvw[8];
       } else if (!wall) {
         const double4 pj = a.spos[t];
         const double2* kj = reinterpret_cast<const double2*>(a.kin + (size_t)kKin * a.s_clump[t]);

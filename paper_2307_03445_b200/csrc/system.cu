@@ -42,6 +42,7 @@ void launch_state_out(const State& st, const int* outpos, int n_own, double* pos
                       double* om, cudaStream_t s);
 void launch_mesh_pairs(const StepArgs&, cudaStream_t);
 void launch_mesh_finish(const StepArgs&, cudaStream_t);
+void launch_mesh_geom(const StepArgs&, cudaStream_t);
 }  // namespace dem
 
 using namespace dem;
@@ -126,7 +127,10 @@ struct dem_system {
   double *d_tri_body = nullptr, *d_tri_world = nullptr, *d_tri_snap = nullptr, *d_mesh = nullptr,
          *d_mesh_part = nullptr, *d_mesh_wrench = nullptr;
   int *d_tri_vid = nullptr, *d_tri_mesh = nullptr, *d_mesh_mat = nullptr, *d_mesh_flag = nullptr;
-  int mesh_part_ctas = 0;  // test hook (env DEM_FAULT_AHEAD_OVERFLOW=n): the next n ahead detections report an overflow
+  int mesh_part_ctas = 0;
+  int2* d_mlist[2] = {nullptr, nullptr};  // mesh entries of entry set e (k_rows_finish)
+  int* d_mlist_n = nullptr;               // [2] their counts
+  double4* d_mgeom = nullptr;             // [cap_entries] per-step closest point + feature flag  // test hook (env DEM_FAULT_AHEAD_OVERFLOW=n): the next n ahead detections report an overflow
   long long cap_entries = 0;
   Record rec{};
   Ctl* d_ctl = nullptr;
@@ -334,6 +338,14 @@ static StepArgs make_args(dem_system* sys, int kind, bool det = false) {
   a.mesh_part = sys->d_mesh_part;
   a.mesh_flag = sys->d_mesh_flag;
   a.mesh_wrench = sys->d_mesh_wrench;
+  {
+    const int eu = rebuild ? sys->ep ^ 1 : sys->ep;  // the entry set the force kernel reads
+    a.mlist = sys->d_mlist[eu];
+    a.mlist_n = sys->d_mlist_n ? sys->d_mlist_n + eu : nullptr;
+    a.mlist_out = sys->d_mlist[sys->ep ^ 1];
+    a.mlist_out_n = sys->d_mlist_n ? sys->d_mlist_n + (sys->ep ^ 1) : nullptr;
+    a.mgeom = sys->d_mgeom;
+  }
   for (int side = 0; side < 2; ++side) {
     a.peer_state[side] = sys->peer ? sys->remote_state[side][p ^ 1] : nullptr;
     a.peer_n[side] = sys->remote_n[side];
@@ -392,6 +404,7 @@ static void enqueue_detect(dem_system* sys, int kind, cudaStream_t s, cudaEvent_
   // the same launch batch: the re-run must find the entry sets as they were)
   const int* abort = a.abort;
   const int* abort2 = &sys->d_ctl->abort;
+  if (run && sys->n_tri) cudaMemsetAsync(a.mlist_out_n, 0, sizeof(int), s);
   if (run) launch_excl_scan(sys->d_cell_count, sys->d_cell_start, sys->ncell, sys->d_scan_tmp, abort, s, abort2);
   if (ev) cudaEventRecord(ev[2], s);
   if (run) launch_bin_scatter(a, s);
@@ -407,6 +420,7 @@ static void enqueue_detect(dem_system* sys, int kind, cudaStream_t s, cudaEvent_
 
 static void enqueue_force(dem_system* sys, int kind, cudaStream_t s, cudaEvent_t* ev, bool exchange) {
   StepArgs a = make_args(sys, kind);
+  launch_mesh_geom(a, s);
   launch_force_integrate(a, s);
   launch_mesh_finish(a, s);
   if (ev) cudaEventRecord(ev[7], s);
@@ -679,6 +693,16 @@ extern "C" void dem_destroy(dem_system* sys) {
 }
 
 // ------------------------------------------------------------------ capacity
+// mesh-entry lists and the per-entry geometry (meshes only; sized like the entry arrays)
+static dem_status alloc_mesh_lists(dem_system* sys) {
+  if (!sys->n_mesh || !sys->cap_entries) return DEM_OK;
+  for (int e = 0; e < 2; ++e) TRY(alloc_arr(sys, &sys->d_mlist[e], (size_t)sys->cap_entries));
+  TRY(alloc_arr(sys, &sys->d_mgeom, (size_t)sys->cap_entries));
+  TRY(alloc_arr(sys, &sys->d_mlist_n, 2));
+  CK(cudaMemsetAsync(sys->d_mlist_n, 0, 2 * sizeof(int), sys->stream));
+  return DEM_OK;
+}
+
 static dem_status alloc_rows(dem_system* sys, long long cap) {
   // grow both row buffers to cap entries, preserving the contents of both
   for (int p = 0; p < 2; ++p) {
@@ -706,6 +730,7 @@ static dem_status alloc_rows(dem_system* sys, long long cap) {
     TRY(alloc_arr(sys, &sys->rec.delta, cap));
   }
   sys->cap_entries = cap;
+  TRY(alloc_mesh_lists(sys));
   free_graphs(sys);
   return DEM_OK;
 }
@@ -915,6 +940,7 @@ extern "C" dem_status dem_add_mesh(dem_system* sys, const dem_mesh* m, int32_t* 
   CK(cudaMemsetAsync(sys->d_mesh_wrench, 0, sizeof(double) * 6 * kMaxMeshes, sys->stream));
   sys->mesh_part_ctas = 0;
   TRY(ensure_mesh_buffers(sys));
+  TRY(alloc_mesh_lists(sys));
   CK(cudaStreamSynchronize(sys->stream));
   free_graphs(sys);
   if (mesh_id) *mesh_id = sys->n_mesh - 1;
