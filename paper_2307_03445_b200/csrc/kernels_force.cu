@@ -30,7 +30,7 @@ constexpr int kPairStride = 8;  // doubles per material pair in Tables::pair
 #define DEM_FORCE_FT 128
 #endif
 #ifndef DEM_FORCE_FC
-#define DEM_FORCE_FC (DEM_FORCE_FT / 4)
+#define DEM_FORCE_FC (DEM_FORCE_FT * 3 / 8)  // 48 clumps: CTAs are cut by entries (system.cu)
 #endif
 #ifndef DEM_FORCE_MAXS
 #define DEM_FORCE_MAXS (DEM_FORCE_FT * 5 / 4)
