@@ -37,37 +37,16 @@ namespace dem {
 #ifndef DEM_ROWS_TPB
 #define DEM_ROWS_TPB 64
 #endif
-__global__ void __launch_bounds__(DEM_POSE_TPB) k_pose_count(StepArgs a) {
-  if (a.adopt && blockIdx.x == 0 && threadIdx.x == 0 && a.ctl->det_abort) {
-    // the set detected ahead overflowed a capacity: abort this adoption step, the host regrows
-    // and rebuilds the set at this step instead (same trajectory: DESIGN.md §5.2)
-    atomicExch(&a.ctl->abort, 1);
-  }
-  if (a.ctl->abort) return;
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.ns) return;
-  const int c = a.s_clump[i];
-  const int tc = a.s_tc[i];
-  const double qw = a.cur.qw[c], qx = a.cur.qx[c], qy = a.cur.qy[c], qz = a.cur.qz[c];
-  double R[9];
-  quat_R(qw, qx, qy, qz, R);
+// one sphere of clump c: centre, record, domain and displacement checks, and on detection
+// steps its plane candidates, row count and bin counts
+__device__ __forceinline__ void pose_sphere(const StepArgs& a, int i, int c, int tc, const double* R, double X,
+                                            double Y, double Z) {
   const double ox = a.tab.tc_off[3 * tc], oy = a.tab.tc_off[3 * tc + 1], oz = a.tab.tc_off[3 * tc + 2];
-  const double X = a.cur.x[c], Y = a.cur.y[c], Z = a.cur.z[c];
   const double cx = add(X, row_dot(R, ox, oy, oz));
   const double cy = add(Y, row_dot(R + 3, ox, oy, oz));
   const double cz = add(Z, row_dot(R + 6, ox, oy, oz));
   const double r = a.tab.tc_rad[tc];
   a.spos[i] = make_double4(cx, cy, cz, r);
-  if (tc == a.tab.tpl_coff[a.tid[c]]) {
-    const double wx = a.cur.wx[c], wy = a.cur.wy[c], wz = a.cur.wz[c];
-    double* k = a.kin + (size_t)kKin * c;
-    k[0] = X; k[1] = Y; k[2] = Z;
-    k[3] = a.cur.vx[c]; k[4] = a.cur.vy[c]; k[5] = a.cur.vz[c];
-    k[6] = R[0] * wx + R[1] * wy + R[2] * wz;
-    k[7] = R[3] * wx + R[4] * wy + R[5] * wz;
-    k[8] = R[6] * wx + R[7] * wy + R[8] * wz;
-    k[9] = a.tab.tpl_mass[a.tid[c]];
-  }
   const Grid& g = a.grid;
   if (!(cx >= g.dom_lo[0] && cx <= g.dom_hi[0] && cy >= g.dom_lo[1] && cy <= g.dom_hi[1] &&
         cz >= g.dom_lo[2] && cz <= g.dom_hi[2])) {
@@ -104,6 +83,62 @@ __global__ void __launch_bounds__(DEM_POSE_TPB) k_pose_count(StepArgs a) {
       for (int x = lx; x <= hx; ++x) atomicAdd(&a.cell_count[base + x * g.st[0]], 1);
     }
 }
+
+__device__ __forceinline__ void kin_record(const StepArgs& a, int c, const double* R, double X, double Y, double Z) {
+  const double wx = a.cur.wx[c], wy = a.cur.wy[c], wz = a.cur.wz[c];
+  double* k = a.kin + (size_t)kKin * c;
+  k[0] = X; k[1] = Y; k[2] = Z;
+  k[3] = a.cur.vx[c]; k[4] = a.cur.vy[c]; k[5] = a.cur.vz[c];
+  k[6] = R[0] * wx + R[1] * wy + R[2] * wz;
+  k[7] = R[3] * wx + R[4] * wy + R[5] * wz;
+  k[8] = R[6] * wx + R[7] * wy + R[8] * wz;
+  k[9] = a.tab.tpl_mass[a.tid[c]];
+}
+
+__device__ __forceinline__ bool pose_prologue(const StepArgs& a) {
+  if (a.adopt && blockIdx.x == 0 && threadIdx.x == 0 && a.ctl->det_abort) {
+    // the set detected ahead overflowed a capacity: abort this adoption step, the host regrows
+    // and rebuilds the set at this step instead (same trajectory: DESIGN.md §5.2)
+    atomicExch(&a.ctl->abort, 1);
+  }
+  return !a.ctl->abort;
+}
+
+#ifndef DEM_POSE_PER_CLUMP
+#define DEM_POSE_PER_CLUMP 0
+#endif
+#if DEM_POSE_PER_CLUMP
+// one thread per clump: R(q) once for all its spheres
+__global__ void __launch_bounds__(DEM_POSE_TPB) k_pose_count(StepArgs a) {
+  if (!pose_prologue(a)) return;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= a.n) return;
+  double R[9];
+  quat_R(a.cur.qw[c], a.cur.qx[c], a.cur.qy[c], a.cur.qz[c], R);
+  const double X = a.cur.x[c], Y = a.cur.y[c], Z = a.cur.z[c];
+  kin_record(a, c, R, X, Y, Z);
+  for (int i = a.sph_off[c], e = a.sph_off[c + 1]; i < e; ++i) pose_sphere(a, i, c, a.s_tc[i], R, X, Y, Z);
+}
+void launch_pose_count(const StepArgs& a, cudaStream_t s) {
+  k_pose_count<<<a.n ? (a.n + DEM_POSE_TPB - 1) / DEM_POSE_TPB : 1, DEM_POSE_TPB, 0, s>>>(a);
+}
+#else
+__global__ void __launch_bounds__(DEM_POSE_TPB) k_pose_count(StepArgs a) {
+  if (!pose_prologue(a)) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.ns) return;
+  const int c = a.s_clump[i];
+  const int tc = a.s_tc[i];
+  double R[9];
+  quat_R(a.cur.qw[c], a.cur.qx[c], a.cur.qy[c], a.cur.qz[c], R);
+  const double X = a.cur.x[c], Y = a.cur.y[c], Z = a.cur.z[c];
+  if (tc == a.tab.tpl_coff[a.tid[c]]) kin_record(a, c, R, X, Y, Z);
+  pose_sphere(a, i, c, tc, R, X, Y, Z);
+}
+void launch_pose_count(const StepArgs& a, cudaStream_t s) {
+  k_pose_count<<<a.ns ? (a.ns + DEM_POSE_TPB - 1) / DEM_POSE_TPB : 1, DEM_POSE_TPB, 0, s>>>(a);
+}
+#endif
 
 // ---------------------------------------------------------------- bin scatter
 // Slots are taken by decrementing the counts, which leaves cell_count all-zero for the
@@ -565,9 +600,6 @@ __global__ void __launch_bounds__(DEM_ROWS_TPB) k_rows_finish(StepArgs a) {
 }
 
 // host launchers
-void launch_pose_count(const StepArgs& a, cudaStream_t s) {
-  k_pose_count<<<a.ns ? (a.ns + DEM_POSE_TPB - 1) / DEM_POSE_TPB : 1, DEM_POSE_TPB, 0, s>>>(a);
-}
 void launch_bin_scatter(const StepArgs& a, cudaStream_t s) {
   if (a.ns) k_bin_scatter<<<(a.ns + DEM_SCATTER_TPB - 1) / DEM_SCATTER_TPB, DEM_SCATTER_TPB, 0, s>>>(a);
 }
