@@ -489,7 +489,10 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
 // each entry's history index found in the sphere's previous row ("persist between
 // timesteps"; -1 for a contact born this step).  Rows of up to kRegRow candidates — nearly
 // all of them — are sorted and matched in registers; longer ones in place in memory.
-constexpr int kRegRow = 8;
+#ifndef DEM_REG_ROW
+#define DEM_REG_ROW 6  // A/B on the C5 bench: 6 beats 5, 7 and 8 (rows 1.80 vs 1.97-2.08 ms)
+#endif
+constexpr int kRegRow = DEM_REG_ROW;
 
 // key of a candidate partner: a sphere's key, or INT64_MAX - kMaxPlanes - t for triangle t
 // (partner code -1 - kMaxPlanes - t, written by k_mesh_pairs): sorts after every sphere
