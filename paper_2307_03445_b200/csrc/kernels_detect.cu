@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(DEM_SCATTER_TPB) k_bin_scatter(StepArgs a) {
 // tuning knobs (build-time; see build.py -D): buffered pairs per warp, min CTAs/SM for the
 // register budget, bins per CTA run
 #ifndef DEM_PAIRS_BUF
-#define DEM_PAIRS_BUF 64
+#define DEM_PAIRS_BUF 32  // A/B: 32 beats 64 by 4% (96, 128 much slower)
 #endif
 #ifndef DEM_PAIRS_MINB
 #define DEM_PAIRS_MINB 4
