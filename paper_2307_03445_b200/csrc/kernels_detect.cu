@@ -191,16 +191,50 @@ constexpr int kPairBuf = DEM_PAIRS_BUF;
 // axis d", the pair belongs to C iff (g_a | g_b) == 7: that is how each pair is found in
 // exactly one bin.
 constexpr int kFlatMax = 64;  // bins up to this size: member groups + flat pair enumeration
+#ifndef DEM_PAIRS_SOA
+#define DEM_PAIRS_SOA 1
+#endif
+#ifndef DEM_PAIRS_SPLIT
+#define DEM_PAIRS_SPLIT 1
+#endif
 struct Members {
+#if DEM_PAIRS_SOA
+  // x, y | z, r in two 16-byte arrays: consecutive members hit consecutive bank quads (a
+  // 32-byte double4 stride makes the 128-bit loads of 8 consecutive members conflict 2-way)
+  double2 xy[kFlatMax], zr[kFlatMax];
+  __device__ __forceinline__ double4 get(int q) const {
+    const double2 u = xy[q], v = zr[q];
+    return make_double4(u.x, u.y, v.x, v.y);
+  }
+  __device__ __forceinline__ void put(int q, const double4& p) {
+    xy[q] = make_double2(p.x, p.y);
+    zr[q] = make_double2(p.z, p.w);
+  }
+#else
   double4 p[kFlatMax];  // x, y, z, r
+  __device__ __forceinline__ double4 get(int q) const { return p[q]; }
+  __device__ __forceinline__ void put(int q, const double4& v) { p[q] = v; }
+#endif
+#if DEM_PAIRS_SPLIT
+  // clump and item apart: the pair test reads the clumps only, a hit its two items
+  int clump[kFlatMax], item[kFlatMax];
+  __device__ __forceinline__ int2 meta_get(int q) const { return make_int2(clump[q], item[q]); }
+  __device__ __forceinline__ void meta_put(int q, int2 v) {
+    clump[q] = v.x;
+    item[q] = v.y;
+  }
+#else
   int2 meta[kFlatMax];  // (clump, sphere index [| g << 29 on the large-bin path])
+  __device__ __forceinline__ int2 meta_get(int q) const { return meta[q]; }
+  __device__ __forceinline__ void meta_put(int q, int2 v) { meta[q] = v; }
+#endif
 };
 
 __device__ __forceinline__ void load_member(const StepArgs& a, Members& M, int slot, int item) {
   const int it = a.items[item];
   const int idx = it & 0x1fffffff;
-  M.p[slot] = a.dpos[idx];
-  M.meta[slot] = make_int2(a.s_clump[idx], it);
+  M.put(slot, a.dpos[idx]);
+  M.meta_put(slot, make_int2(a.s_clump[idx], it));
 }
 
 // Member order of the flat path: groups by g in the order 7, 6, 1, 5, 3, 2, 4, 0 (nibble g of
@@ -385,13 +419,13 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
         __syncwarp();
         if (lane < m) {
           const int q = byte_of(st, pos0) + byte_of(x0 - v0, pos0);
-          A.p[q] = u0;
-          A.meta[q] = mt0;
+          A.put(q, u0);
+          A.meta_put(q, mt0);
         }
         if (lane + 32 < m) {
           const int q = byte_of(st, pos1) + byte_of(t0, pos1) + byte_of(x1 - v1, pos1);
-          A.p[q] = u1;
-          A.meta[q] = mt1;
+          A.put(q, u1);
+          A.meta_put(q, mt1);
         }
         __syncwarp();
         const int n7 = byte_of(tot, 0), n6 = byte_of(tot, 1), n5 = byte_of(tot, 3), n3 = byte_of(tot, 4),
@@ -429,10 +463,19 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
               i = A0 + (q - r * W);
               j = B0 + r;
             }
+#if DEM_PAIRS_SPLIT
+            const int2 mi = make_int2(A.clump[i], 0), mj = make_int2(A.clump[j], 0);
+            hit = candidate<kGhosts, kMargin>(a, mi, mj, A.get(i), A.get(j));
+            if (hit) {
+              ia = A.item[i];
+              ib = A.item[j];
+            }
+#else
             const int2 mi = A.meta[i], mj = A.meta[j];
-            hit = candidate<kGhosts, kMargin>(a, mi, mj, A.p[i], A.p[j]);
+            hit = candidate<kGhosts, kMargin>(a, mi, mj, A.get(i), A.get(j));
             ia = mi.y;
             ib = mj.y;
+#endif
           }
           push_hits(a, bf, nbuf, hit, ia, ib, lane);
         }
@@ -465,10 +508,10 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
                   i = p / mj;
                   j = p - i * mj;
                 }
-                const int2 mu = A.meta[i];
-                const int2 mv = A.meta[ob + j];
+                const int2 mu = A.meta_get(i);
+                const int2 mv = A.meta_get(ob + j);
                 if (((unsigned)(mu.y | mv.y) >> 29) == 7u) {
-                  hit = candidate<kGhosts, kMargin>(a, mu, mv, A.p[i], A.p[ob + j]);
+                  hit = candidate<kGhosts, kMargin>(a, mu, mv, A.get(i), A.get(ob + j));
                   ia = mu.y & 0x1fffffff;
                   ibx = mv.y & 0x1fffffff;
                 }
