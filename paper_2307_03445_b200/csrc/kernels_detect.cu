@@ -34,6 +34,16 @@ namespace dem {
 #ifndef DEM_SCATTER_TPB
 #define DEM_SCATTER_TPB 64
 #endif
+// CTAs per SM for the register budget (A/B on the C5 bench: pose 24 -> 40 registers, 1.15 vs
+// 1.20 ms at 48 and 1.38 at 32 with spills; scatter 32 -> 32 registers, 1.00 vs 1.10 ms)
+#ifndef DEM_POSE_MINB
+#define DEM_POSE_MINB 24
+#endif
+#ifndef DEM_SCATTER_MINB
+#define DEM_SCATTER_MINB 32
+#endif
+#define DEM_POSE_LB DEM_POSE_TPB, DEM_POSE_MINB
+#define DEM_SCATTER_LB DEM_SCATTER_TPB, DEM_SCATTER_MINB
 #ifndef DEM_ROWS_TPB
 #define DEM_ROWS_TPB 64
 #endif
@@ -109,7 +119,7 @@ __device__ __forceinline__ bool pose_prologue(const StepArgs& a) {
 #endif
 #if DEM_POSE_PER_CLUMP
 // one thread per clump: R(q) once for all its spheres
-__global__ void __launch_bounds__(DEM_POSE_TPB) k_pose_count(StepArgs a) {
+__global__ void __launch_bounds__(DEM_POSE_LB) k_pose_count(StepArgs a) {
   if (!pose_prologue(a)) return;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= a.n) return;
@@ -123,7 +133,7 @@ void launch_pose_count(const StepArgs& a, cudaStream_t s) {
   k_pose_count<<<a.n ? (a.n + DEM_POSE_TPB - 1) / DEM_POSE_TPB : 1, DEM_POSE_TPB, 0, s>>>(a);
 }
 #else
-__global__ void __launch_bounds__(DEM_POSE_TPB) k_pose_count(StepArgs a) {
+__global__ void __launch_bounds__(DEM_POSE_LB) k_pose_count(StepArgs a) {
   if (!pose_prologue(a)) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.ns) return;
@@ -143,7 +153,7 @@ void launch_pose_count(const StepArgs& a, cudaStream_t s) {
 // ---------------------------------------------------------------- bin scatter
 // Slots are taken by decrementing the counts, which leaves cell_count all-zero for the
 // next step.  The order inside a bin is irrelevant: rows are sorted by partner key.
-__global__ void __launch_bounds__(DEM_SCATTER_TPB) k_bin_scatter(StepArgs a) {
+__global__ void __launch_bounds__(DEM_SCATTER_LB) k_bin_scatter(StepArgs a) {
   if (*a.abort || a.ctl->abort) return;  // (an error in the steps running beside an ahead detection)
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.ns) return;
@@ -344,6 +354,67 @@ __constant__ float c_rcp[kFlatMax + 8] = {1.0f,      DEM_R8(1),  DEM_R8(9),  DEM
                                           DEM_R8(33), DEM_R8(41), DEM_R8(49), DEM_R8(57)};
 #undef DEM_R8
 
+// one pair of the flat path: the predicate, and the two sphere indices of a hit
+template <bool kGhosts, bool kMargin>
+__device__ __forceinline__ bool flat_pair(const StepArgs& a, const Members& A, int i, int j, int& ia, int& ib) {
+#if DEM_PAIRS_SPLIT
+  const int2 mi = make_int2(A.clump[i], 0), mj = make_int2(A.clump[j], 0);
+  const bool hit = candidate<kGhosts, kMargin>(a, mi, mj, A.get(i), A.get(j));
+  if (hit) {
+    ia = A.item[i];
+    ib = A.item[j];
+  }
+#else
+  const int2 mi = A.meta[i], mj = A.meta[j];
+  const bool hit = candidate<kGhosts, kMargin>(a, mi, mj, A.get(i), A.get(j));
+  ia = mi.y;
+  ib = mj.y;
+#endif
+  return hit;
+}
+
+// The pair blocks of a bin's member order (see kGroupPos) from the group sizes `tot` and
+// starts `st` (byte k: position k): T (p < tri) from the triangle table, then R0..R3 as
+// pair = (A0 + q % W, B0 + q / W) with correctly rounded reciprocals of the block widths
+// (q < 64 * 64, so (q + 1/2) / W, at least 1/(2W) away from an integer, truncates right)
+struct PairBlocks {
+  int tri, e0, e1, e2, total, n7, n4, W1, W2, s1, s3, s4, s5, s6;
+  float r0, r1, r2, r3;
+  __device__ __forceinline__ PairBlocks(unsigned long long tot, unsigned long long st, int m) {
+    n7 = byte_of(tot, 0);
+    const int n6 = byte_of(tot, 1), n5 = byte_of(tot, 3), n3 = byte_of(tot, 4);
+    n4 = byte_of(tot, 6);
+    s6 = byte_of(st, 1); s1 = byte_of(st, 2); s5 = byte_of(st, 3); s3 = byte_of(st, 4);
+    const int s2 = byte_of(st, 5);
+    s4 = byte_of(st, 6);
+    tri = n7 * (n7 - 1) / 2;
+    W1 = s2 - s1;
+    W2 = s4 - s3;
+    e0 = tri + n7 * (m - n7);
+    e1 = e0 + n6 * W1;
+    e2 = e1 + n5 * W2;
+    total = e2 + n3 * n4;
+    r0 = c_rcp[n7]; r1 = c_rcp[W1]; r2 = c_rcp[W2]; r3 = c_rcp[n4];
+  }
+  __device__ __forceinline__ void decode(int p, const unsigned short* tri_ij, int& i, int& j) const {
+    if (p < tri) {
+      const int v = tri_ij[p];
+      i = v & 0xff;
+      j = v >> 8;
+    } else {
+      const bool b1 = p >= e0, b2 = p >= e1, b3 = p >= e2;
+      const int q = p - (b3 ? e2 : b2 ? e1 : b1 ? e0 : tri);
+      const int W = b3 ? n4 : b2 ? W2 : b1 ? W1 : n7;
+      const float rw = b3 ? r3 : b2 ? r2 : b1 ? r1 : r0;
+      const int A0 = b3 ? s4 : b2 ? s3 : b1 ? s1 : 0;
+      const int B0 = b3 ? s3 : b2 ? s5 : b1 ? s6 : n7;
+      const int r = __float2int_rz(((float)q + 0.5f) * rw);
+      i = A0 + (q - r * W);
+      j = B0 + r;
+    }
+  }
+};
+
 template <bool kGhosts, bool kMargin>
 __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepArgs a) {
   __shared__ Members smA[kPairWarps];
@@ -428,54 +499,15 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
           A.meta_put(q, mt1);
         }
         __syncwarp();
-        const int n7 = byte_of(tot, 0), n6 = byte_of(tot, 1), n5 = byte_of(tot, 3), n3 = byte_of(tot, 4),
-                  n4 = byte_of(tot, 6);
-        const int s6 = byte_of(st, 1), s1 = byte_of(st, 2), s5 = byte_of(st, 3), s3 = byte_of(st, 4),
-                  s2 = byte_of(st, 5), s4 = byte_of(st, 6);
-        // blocks after T: pair = (A0 + q % W, B0 + q / W)
-        const int tri = n7 * (n7 - 1) / 2;
-        const int W1 = s2 - s1, W2 = s4 - s3;
-        const int e0 = tri + n7 * (m - n7);
-        const int e1 = e0 + n6 * W1;
-        const int e2 = e1 + n5 * W2;
-        const int total = e2 + n3 * n4;
-        // correctly rounded reciprocals of the block widths: q < 64 * 64, so (q + 1/2) / W,
-        // which is at least 1/(2W) away from an integer, truncates right
-        const float r0 = c_rcp[n7], r1 = c_rcp[W1], r2 = c_rcp[W2], r3 = c_rcp[n4];
-        for (int base = 0; base < total; base += 32) {
+        const PairBlocks B(tot, st, m);
+        for (int base = 0; base < B.total; base += 32) {
           const int p = base + lane;
           bool hit = false;
           int ia = 0, ib = 0;
-          if (p < total) {
+          if (p < B.total) {
             int i, j;
-            if (p < tri) {
-              const int v = tri_ij[p];
-              i = v & 0xff;
-              j = v >> 8;
-            } else {
-              const bool b1 = p >= e0, b2 = p >= e1, b3 = p >= e2;
-              const int q = p - (b3 ? e2 : b2 ? e1 : b1 ? e0 : tri);
-              const int W = b3 ? n4 : b2 ? W2 : b1 ? W1 : n7;
-              const float rw = b3 ? r3 : b2 ? r2 : b1 ? r1 : r0;
-              const int A0 = b3 ? s4 : b2 ? s3 : b1 ? s1 : 0;
-              const int B0 = b3 ? s3 : b2 ? s5 : b1 ? s6 : n7;
-              const int r = __float2int_rz(((float)q + 0.5f) * rw);
-              i = A0 + (q - r * W);
-              j = B0 + r;
-            }
-#if DEM_PAIRS_SPLIT
-            const int2 mi = make_int2(A.clump[i], 0), mj = make_int2(A.clump[j], 0);
-            hit = candidate<kGhosts, kMargin>(a, mi, mj, A.get(i), A.get(j));
-            if (hit) {
-              ia = A.item[i];
-              ib = A.item[j];
-            }
-#else
-            const int2 mi = A.meta[i], mj = A.meta[j];
-            hit = candidate<kGhosts, kMargin>(a, mi, mj, A.get(i), A.get(j));
-            ia = mi.y;
-            ib = mj.y;
-#endif
+            B.decode(p, tri_ij, i, j);
+            hit = flat_pair<kGhosts, kMargin>(a, A, i, j, ia, ib);
           }
           push_hits(a, bf, nbuf, hit, ia, ib, lane);
         }
@@ -549,7 +581,10 @@ __device__ __forceinline__ int prev_index(const Rows& prev, int pb, int pe, long
   return -1;
 }
 
-__global__ void __launch_bounds__(DEM_ROWS_TPB) k_rows_finish(StepArgs a) {
+#ifndef DEM_ROWS_MINB
+#define DEM_ROWS_MINB 32  // A/B: 32 registers (a few spilled) 1.69 ms vs 1.80 at 40, 2.07 at 48
+#endif
+__global__ void __launch_bounds__(DEM_ROWS_TPB, DEM_ROWS_MINB) k_rows_finish(StepArgs a) {
   if (*a.abort || a.ctl->abort) return;  // (an error in the steps running beside an ahead detection)
   const int total = a.rows.row_ptr[a.ns];
   if ((long long)total > a.cap_entries) {
