@@ -41,7 +41,37 @@ struct Ctl {
 };
 
 constexpr int kUt = 4;    // doubles per entry of the tangential history (padded)
-constexpr int kKin = 10;  // doubles per clump in the packed kinematics record
+#ifndef DEM_V256
+#define DEM_V256 1  // 256-bit gathers of the 32-byte records (sm_100 LDG.256)
+#endif
+constexpr int kKinUsed = 10;  // doubles per clump in the packed kinematics record
+// record stride: padded to 96 bytes so a partner's record is three 256-bit loads
+constexpr int kKin = DEM_V256 ? 12 : 10;
+
+// 32-byte loads/stores in one instruction (sm_100: LDG.E.ENL2.256 / STG.E.ENL2.256); p must be
+// 32-byte aligned.  A random gather of a 32-byte record then costs one L1 wavefront per lane
+// instead of two.  The loads take the read-only path: only for data no thread of the same
+// launch writes.
+__device__ __forceinline__ double4 ldg256(const void* p) {
+#if DEM_V256
+  double4 v;
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+#else
+  const double2* q = reinterpret_cast<const double2*>(p);
+  const double2 u = __ldg(q), w = __ldg(q + 1);
+  return make_double4(u.x, u.y, w.x, w.y);
+#endif
+}
+__device__ __forceinline__ void stg256(void* p, double x, double y, double z, double w) {
+#if DEM_V256
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(x), "d"(y), "d"(z), "d"(w) : "memory");
+#else
+  double2* q = reinterpret_cast<double2*>(p);
+  q[0] = make_double2(x, y);
+  q[1] = make_double2(z, w);
+#endif
+}
 
 struct Tables {
   const double* tc_off;   // [3 * n_tc] body-frame offsets, AoS

@@ -97,12 +97,24 @@ __device__ __forceinline__ void pose_sphere(const StepArgs& a, int i, int c, int
 __device__ __forceinline__ void kin_record(const StepArgs& a, int c, const double* R, double X, double Y, double Z) {
   const double wx = a.cur.wx[c], wy = a.cur.wy[c], wz = a.cur.wz[c];
   double* k = a.kin + (size_t)kKin * c;
+  const double w0 = R[0] * wx + R[1] * wy + R[2] * wz;
+  const double w1 = R[3] * wx + R[4] * wy + R[5] * wz;
+  const double w2 = R[6] * wx + R[7] * wy + R[8] * wz;
+#ifndef DEM_KIN_ST256
+#define DEM_KIN_ST256 DEM_V256
+#endif
+#if DEM_KIN_ST256
+  stg256(k, X, Y, Z, a.cur.vx[c]);
+  stg256(k + 4, a.cur.vy[c], a.cur.vz[c], w0, w1);
+  stg256(k + 8, w2, a.tab.tpl_mass[a.tid[c]], 0.0, 0.0);
+#else
   k[0] = X; k[1] = Y; k[2] = Z;
   k[3] = a.cur.vx[c]; k[4] = a.cur.vy[c]; k[5] = a.cur.vz[c];
-  k[6] = R[0] * wx + R[1] * wy + R[2] * wz;
-  k[7] = R[3] * wx + R[4] * wy + R[5] * wz;
-  k[8] = R[6] * wx + R[7] * wy + R[8] * wz;
+  k[6] = w0;
+  k[7] = w1;
+  k[8] = w2;
   k[9] = a.tab.tpl_mass[a.tid[c]];
+#endif
 }
 
 __device__ __forceinline__ bool pose_prologue(const StepArgs& a) {
@@ -243,7 +255,7 @@ struct Members {
 __device__ __forceinline__ void load_member(const StepArgs& a, Members& M, int slot, int item) {
   const int it = a.items[item];
   const int idx = it & 0x1fffffff;
-  M.put(slot, a.dpos[idx]);
+  M.put(slot, ldg256(a.dpos + idx));
   M.meta_put(slot, make_int2(a.s_clump[idx], it));
 }
 
@@ -465,7 +477,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
         if (lane < m) {
           const int it = a.items[k0 + lane];
           const int idx = it & 0x1fffffff;
-          u0 = a.dpos[idx];
+          u0 = ldg256(a.dpos + idx);
           mt0 = make_int2(a.s_clump[idx], idx);
           pos0 = (kGroupPos >> (4 * ((unsigned)it >> 29))) & 7;
           v0 = 1ull << (8 * pos0);
@@ -473,7 +485,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
         if (lane + 32 < m) {
           const int it = a.items[k0 + 32 + lane];
           const int idx = it & 0x1fffffff;
-          u1 = a.dpos[idx];
+          u1 = ldg256(a.dpos + idx);
           mt1 = make_int2(a.s_clump[idx], idx);
           pos1 = (kGroupPos >> (4 * ((unsigned)it >> 29))) & 7;
           v1 = 1ull << (8 * pos1);

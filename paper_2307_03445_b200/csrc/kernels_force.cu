@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
   __shared__ double4 own_p[kMaxS];
   __shared__ int own_mat[kMaxS];
   __shared__ int own_lc[kMaxS];
-  __shared__ __align__(16) double ck[kFC * kKin];
+  __shared__ __align__(16) double ck[kFC * kKinUsed];
   __shared__ double part[6][kFT];
   __shared__ double acc[6][kMaxS];
   // mesh wrench (kMesh): per entry the mesh id (-1: not a mesh entry) and torque about its X
@@ -137,8 +137,12 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
     for (int q = 0; q < 6; ++q) acc[q][ls] = 0.0;
   }
   {
+    // the used 10 doubles of each record (global stride kKin, shared stride kKinUsed)
     const double2* src = reinterpret_cast<const double2*>(a.kin + (size_t)kKin * c0);
-    for (int k = tid; k < ncl * (kKin / 2); k += kFT) reinterpret_cast<double2*>(ck)[k] = src[k];
+    for (int k = tid; k < ncl * (kKinUsed / 2); k += kFT) {
+      const int c = k / (kKinUsed / 2), r = k - c * (kKinUsed / 2);
+      reinterpret_cast<double2*>(ck)[k] = src[c * (kKin / 2) + r];
+    }
   }
   if (kMesh && tid < kMaxMeshes * 6) cw[tid / 6][tid % 6] = 0.0;
   if (kMesh && tid == 0) chunk_mesh = cta_mesh = 0;
@@ -158,7 +162,7 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
       const int ls = lo;
       const double4 own = own_p[ls];
       const double cx = own.x, cy = own.y, cz = own.z, ri = own.w;
-      const double* ki = ck + kKin * own_lc[ls];
+      const double* ki = ck + kKinUsed * own_lc[ls];
       const double Xx = ki[0], Xy = ki[1], Xz = ki[2];
       const double Mi = ki[9];
       const Entry ent = a.rows.ent[e];
@@ -170,10 +174,10 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
       double ux = 0.0, uy = 0.0, uz = 0.0;
       const int pidx = a.remap ? ent.prev : e;
       if (pidx >= 0) {
-        const double2 u01 = *reinterpret_cast<const double2*>(a.prev.ut + kUt * pidx);
-        ux = u01.x;
-        uy = u01.y;
-        uz = a.prev.ut[kUt * pidx + 2];
+        const double4 u = ldg256(a.prev.ut + kUt * pidx);
+        ux = u.x;
+        uy = u.y;
+        uz = u.z;
       }
       // (a5) geometry: n from i (own) to j (partner)
       double nx, ny, nz, px, py, pz, delta, rbar, mbar;
@@ -209,8 +213,8 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
         rbar = ri;
         mbar = Mi;
       } else if (!wall) {
-        const double4 pj = a.spos[t];
-        const double2* kj = reinterpret_cast<const double2*>(a.kin + (size_t)kKin * a.s_clump[t]);
+        const double4 pj = ldg256(a.spos + t);
+        const double* kjp = a.kin + (size_t)kKin * a.s_clump[t];
         mj = a.s_mat[t];
         const double rj = pj.w;
         const double dx = pj.x - cx, dy = pj.y - cy, dz = pj.z - cz;
@@ -226,12 +230,22 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
         py = __fma_rn(hr, ny, 0.5 * (cy + pj.y));
         pz = __fma_rn(hr, nz, 0.5 * (cz + pj.z));
         rbar = (ri * rj) / (ri + rj);
+#if DEM_V256
+        const double4 k03 = ldg256(kjp), k47 = ldg256(kjp + 4), k8b = ldg256(kjp + 8);
+        const double Mj = k8b.y;
+        mbar = (Mi * Mj) / (Mi + Mj);
+        Xjx = k03.x; Xjy = k03.y; Xjz = k03.z;
+        Vjx = k03.w; Vjy = k47.x; Vjz = k47.y;
+        Wjx = k47.z; Wjy = k47.w; Wjz = k8b.x;
+#else
+        const double2* kj = reinterpret_cast<const double2*>(kjp);
         const double2 k01 = kj[0], k23 = kj[1], k45 = kj[2], k67 = kj[3], k89 = kj[4];
         const double Mj = k89.y;
         mbar = (Mi * Mj) / (Mi + Mj);
         Xjx = k01.x; Xjy = k01.y; Xjz = k23.x;
         Vjx = k23.y; Vjy = k45.x; Vjz = k45.y;
         Wjx = k67.x; Wjy = k67.y; Wjz = k89.x;
+#endif
       } else {
         const int pl = -1 - t;
         const double* pp = a.tab.plane_pt[pl];
@@ -303,8 +317,7 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
         Fy = fny + fty;
         Fz = fnz + ftz;
       }
-      *reinterpret_cast<double2*>(a.rows.ut + kUt * e) = make_double2(nux, nuy);
-      *reinterpret_cast<double2*>(a.rows.ut + kUt * e + 2) = make_double2(nuz, 0.0);
+      stg256(a.rows.ut + kUt * e, nux, nuy, nuz, 0.0);
       if (a.record) {
         a.rec.F[3 * e] = Fx; a.rec.F[3 * e + 1] = Fy; a.rec.F[3 * e + 2] = Fz;
         a.rec.p[3 * e] = px; a.rec.p[3 * e + 1] = py; a.rec.p[3 * e + 2] = pz;
@@ -363,7 +376,7 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
   // Omega += h I^-1 (tau - Omega x I Omega); q <- normalize(q (x) exp(h Omega)).
   const int c = c0 + tid;
   const int t = a.tid[c];
-  const double* kc = ck + kKin * tid;  // this clump's X, V, omega_world, M
+  const double* kc = ck + kKinUsed * tid;  // this clump's X, V, omega_world, M
   const double M = kc[9];
   const double I0 = a.tab.tpl_inertia[3 * t], I1 = a.tab.tpl_inertia[3 * t + 1], I2 = a.tab.tpl_inertia[3 * t + 2];
   double Fx = 0.0, Fy = 0.0, Fz = 0.0, Tx = 0.0, Ty = 0.0, Tz = 0.0;
