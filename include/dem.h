@@ -104,7 +104,9 @@ typedef struct {
   double domain_lo[3], domain_hi[3]; /* every sphere centre must stay inside */
   double cell_size;          /* bin edge [m]; 0 = automatic */
   int32_t record_contacts;   /* 1: keep per-contact force/point/normal/delta for dem_get_contacts */
-  dem_alloc_fn alloc;        /* NULL: cudaMallocAsync on the system stream */
+  dem_alloc_fn alloc;        /* NULL: cudaMallocAsync on the system stream.  Blocks must be 32-byte
+                                aligned (the kernels move 32-byte records with 256-bit accesses); a
+                                misaligned block fails the call that allocates it */
   dem_free_fn free;
   void* alloc_ctx;
   double entries_per_sphere; /* initial contact-row capacity per sphere (0 = 8); distributed systems

@@ -47,6 +47,8 @@ constexpr int kUt = 4;    // doubles per entry of the tangential history (padded
 constexpr int kKinUsed = 10;  // doubles per clump in the packed kinematics record
 // record stride: padded to 96 bytes so a partner's record is three 256-bit loads
 constexpr int kKin = DEM_V256 ? 12 : 10;
+static_assert(!DEM_V256 || (kKin * 8) % 32 == 0, "kinematics records must stay 32-byte aligned");
+static_assert(kUt * 8 == 32, "u_t records are one 32-byte access");
 
 // 32-byte loads/stores in one instruction (sm_100: LDG.E.ENL2.256 / STG.E.ENL2.256); p must be
 // 32-byte aligned.  A random gather of a 32-byte record then costs one L1 wavefront per lane

@@ -191,6 +191,11 @@ static void* dalloc(dem_system* sys, size_t bytes) {
   void* p = nullptr;
   if (sys->P.alloc) {
     p = sys->P.alloc(bytes, sys->P.alloc_ctx, (void*)sys->stream);
+    if (p && ((uintptr_t)p & 31)) {  // 256-bit record accesses need 32-byte alignment
+      if (sys->P.free) sys->P.free(p, bytes, sys->P.alloc_ctx, (void*)sys->stream);
+      sys->err = "params.alloc returned a block that is not 32-byte aligned";
+      return nullptr;
+    }
   } else {
     if (cudaMallocAsync(&p, bytes, sys->stream) != cudaSuccess) p = nullptr;
   }
@@ -214,7 +219,8 @@ static dem_status alloc_arr(dem_system* sys, T** out, size_t count) {
   dfree(sys, *out);
   *out = (T*)dalloc(sys, sizeof(T) * count);
   if (!*out) {
-    sys->err = "device allocation of " + std::to_string(sizeof(T) * count) + " bytes failed";
+    sys->err = "device allocation of " + std::to_string(sizeof(T) * count) + " bytes failed" +
+               (sys->err.find("32-byte") != std::string::npos ? " (" + sys->err + ")" : std::string());
     return DEM_ERR_OOM;
   }
   return DEM_OK;
