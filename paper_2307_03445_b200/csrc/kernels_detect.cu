@@ -219,6 +219,9 @@ constexpr int kFlatMax = 64;  // bins up to this size: member groups + flat pair
 #ifndef DEM_PAIRS_SPLIT
 #define DEM_PAIRS_SPLIT 1
 #endif
+#ifndef DEM_PAIRS_PIPE
+#define DEM_PAIRS_PIPE 1
+#endif
 struct Members {
 #if DEM_PAIRS_SOA
   // x, y | z, r in two 16-byte arrays: consecutive members hit consecutive bank quads (a
@@ -461,9 +464,46 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
       it_stop = min(ncell, it_stop + (long long)gridDim.x * kSpan);
     }
   };
+#if DEM_PAIRS_PIPE
+  // Software pipeline over the warp's bins: entering bin c its items are already in registers
+  // and the bounds of c + 1 too; the items of c + 1 and the bounds of c + 2 are issued before
+  // c's member records are awaited, so of the bounds -> items -> records chain only the last
+  // load is exposed per bin.
+  auto bounds = [&](long long c, int& b0, int& b1) {
+    b0 = b1 = 0;
+    if (c < ncell) {
+      b0 = a.cell_start[c];
+      b1 = a.cell_start[c + 1];
+    }
+  };
+  const long long cfirst = it;
+  int k0c, k1c, k0n, k1n;
+  bounds(it, k0c, k1c);
+  advance();
+  long long cnext = it;
+  bounds(it, k0n, k1n);
+  int itA = lane < k1c - k0c ? a.items[k0c + lane] : 0;
+  int itB = lane + 32 < k1c - k0c ? a.items[k0c + 32 + lane] : 0;
+  for (long long cid = cfirst; cid < ncell;) {
+    const int k0 = k0c;
+    const int m = k1c - k0c;
+    const int curA = itA, curB = itB;
+    const int mn = k1n - k0n;
+    itA = lane < mn ? a.items[k0n + lane] : 0;
+    itB = lane + 32 < mn ? a.items[k0n + 32 + lane] : 0;
+    k0c = k0n;
+    k1c = k1n;
+    cid = cnext;
+    advance();
+    cnext = it;
+    bounds(it, k0n, k1n);
+#else
   for (long long cid = it; cid < ncell; advance(), cid = it) {
     const int k0 = a.cell_start[cid];
     const int m = a.cell_start[cid + 1] - k0;
+    const int curA = lane < m ? a.items[k0 + lane] : 0;
+    const int curB = lane + 32 < m ? a.items[k0 + 32 + lane] : 0;
+#endif
     if (m >= 2) {
       if (m <= kFlatMax) {
         // Lane l loads members l and l + 32 and stores them at their place in the group order
@@ -475,7 +515,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
         int pos0 = 0, pos1 = 0;
         unsigned long long v0 = 0, v1 = 0;
         if (lane < m) {
-          const int it = a.items[k0 + lane];
+          const int it = curA;
           const int idx = it & 0x1fffffff;
           u0 = ldg256(a.dpos + idx);
           mt0 = make_int2(a.s_clump[idx], idx);
@@ -483,7 +523,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
           v0 = 1ull << (8 * pos0);
         }
         if (lane + 32 < m) {
-          const int it = a.items[k0 + 32 + lane];
+          const int it = curB;
           const int idx = it & 0x1fffffff;
           u1 = ldg256(a.dpos + idx);
           mt1 = make_int2(a.s_clump[idx], idx);
