@@ -45,7 +45,7 @@ namespace dem {
 #define DEM_POSE_LB DEM_POSE_TPB, DEM_POSE_MINB
 #define DEM_SCATTER_LB DEM_SCATTER_TPB, DEM_SCATTER_MINB
 #ifndef DEM_ROWS_TPB
-#define DEM_ROWS_TPB 64
+#define DEM_ROWS_TPB 128  // A/B: 1.58 ms vs 1.69 in 64-thread CTAs (same 32 registers)
 #endif
 // one sphere of clump c: centre, record, domain and displacement checks, and on detection
 // steps its plane candidates, row count and bin counts
@@ -634,7 +634,7 @@ __device__ __forceinline__ int prev_index(const Rows& prev, int pb, int pe, long
 }
 
 #ifndef DEM_ROWS_MINB
-#define DEM_ROWS_MINB 32  // A/B: 32 registers (a few spilled) 1.69 ms vs 1.80 at 40, 2.07 at 48
+#define DEM_ROWS_MINB (2048 / DEM_ROWS_TPB)  // 32 registers (a few spilled): 1.69 ms vs 1.80 at 40, 2.07 at 48
 #endif
 __global__ void __launch_bounds__(DEM_ROWS_TPB, DEM_ROWS_MINB) k_rows_finish(StepArgs a) {
   if (*a.abort || a.ctl->abort) return;  // (an error in the steps running beside an ahead detection)
