@@ -195,18 +195,19 @@ def run_ours(a):
     t_setup = time.perf_counter()
     scene = make_scene(a.config)
     dparams = None
-    if world > 1:
-        # spatial slab decomposition along x, equal clump counts; fixed bed = strong scaling
-        drift = 1e-3
-        b = dem.slab_bounds(scene.pos[:, 0], world, scene.domain_lo[0], scene.domain_hi[0])
-        dparams = dict(rank=rank, n_ranks=world, slab_lo=b[rank], slab_hi=b[rank + 1],
-                       halo=dem.halo_width(scene, drift), drift_max=drift,
-                       transport=dem.TRANSPORT_PEER if a.transport == "peer" else dem.TRANSPORT_NCCL,
-                       nccl_id=obj[0])
     # deferred rebuild (NEXT-1): margin = 2 v_max h k; k = 1 is the headline.
     # Overlapped cadence (NEXT-2): the set is used 2k - 2 steps after its detection.
     lag = (2 * a.cd_every - 2) if a.overlap else a.cd_every
     margin = 2.0 * a.vmax * scene.h * lag if a.cd_every > 1 else 0.0
+    if world > 1:
+        # spatial slab decomposition along x, equal clump counts; fixed bed = strong scaling.
+        # The ghost band covers the margin the system actually uses (dem_create checks it).
+        drift = 1e-3
+        b = dem.slab_bounds(scene.pos[:, 0], world, scene.domain_lo[0], scene.domain_hi[0])
+        dparams = dict(rank=rank, n_ranks=world, slab_lo=b[rank], slab_hi=b[rank + 1],
+                       halo=dem.halo_width(scene, drift, margin=margin), drift_max=drift,
+                       transport=dem.TRANSPORT_PEER if a.transport == "peer" else dem.TRANSPORT_NCCL,
+                       nccl_id=obj[0])
     sys_ = dem.system_from_scene(scene, record_contacts=False, cell_size=a.cell_size, dist=dparams,
                                  entries_per_sphere=12 if world > 1 else 0, margin=margin, cd_every=a.cd_every,
                                  overlap=a.overlap)

@@ -201,9 +201,13 @@ dem_status dem_get_stats(dem_system* sys, dem_stats* out);
 /* Stage profiling.  With enable = 1, dem_step launches the step kernels directly (no graph) with
  * CUDA events between the stages on the system stream and accumulates each stage's device time;
  * enable resets the accumulators.  dem_get_stage_times returns the mean ms per step of each stage,
- * in the order: pose+bin-count, bin-offset scan, bin scatter, per-bin pair tests, row-offset scan,
- * row scatter, wall entries + row sort, force + reduce + integrate (remap, contact forces,
- * canonical per-sphere and per-clump sums, Eq. 4 update) — 8 stages. */
+ * in the order (8 stages): (1) pose + bin counts (k_pose_count; with meshes also k_mesh_pose),
+ * (2) bin-offset scan, (3) bin scatter (k_bin_scatter; with meshes also k_mesh_pairs), (4) per-bin
+ * pair tests (k_pairs), (5) row-offset scan, (6) rows: candidate sort, wall entries, history remap
+ * (k_rows_finish), (7) force + reduce + integrate (k_force_integrate: remap, contact forces,
+ * canonical per-sphere and per-clump sums, Eq. 4 update; with meshes also k_mesh_geom before and
+ * k_mesh_finish after), (8) ghost halo (pack + exchange + unpack, or the peer handshake;
+ * distributed systems only).  Stages 2-6 are 0 on steps that reuse a deferred set. */
 dem_status dem_set_profiling(dem_system* sys, int32_t enable);
 dem_status dem_get_stage_times(dem_system* sys, int32_t n_stages, double* ms);
 

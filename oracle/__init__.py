@@ -19,12 +19,16 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "dem_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
+# tools/mutate_oracle.py points this at a deliberately broken build to show the pins catch it
+_LIB_OVERRIDE = os.environ.get("DEM_ORACLE_LIB")
 _lib = None
 
 ORC_ERRORS = {-1: "invalid argument", -10: "out of domain", -11: "non-finite", -12: "degenerate contact"}
 
 
 def build(force: bool = False) -> str:
+    if _LIB_OVERRIDE:
+        return _LIB_OVERRIDE
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(
             os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "dem_oracle.h"))):
         subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-std=c11", "-D_DEFAULT_SOURCE", "-fPIC",
@@ -36,8 +40,7 @@ def build(force: bool = False) -> str:
 def lib():
     global _lib
     if _lib is None:
-        build()
-        L = C.CDLL(_LIB)
+        L = C.CDLL(build())
         P, I64, I32, D = C.c_void_p, C.c_int64, C.c_int32, C.c_double
         L.orc_create.restype = P
         L.orc_create.argtypes = [D, P, D, P, P, C.c_int, P, C.c_int, P, P, P, P, P, P, C.c_int, P, P, P, C.c_int]

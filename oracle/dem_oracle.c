@@ -7,7 +7,11 @@
  *
  * Parity status of each part ("pins"):
  *   orc_pair_params    pinned  (SPEC examples S:64-66; series formulas)
- *   orc_contact_force  pinned  (static press S:119; Hertz closed forms; CoR identity)
+ *   orc_contact_force  pinned  (static press S:119; Hertz closed forms; CoR identity;
+ *                               tangential log decrement (c_t); Coulomb cap under a damped
+ *                               kick (Eq. 3c branch); tests/test_oracle_pins_contact.py)
+ *   contact point      pinned  (spin / impulse lever arms r - delta/2 of a polydisperse
+ *                               oblique impact; soft-sphere rolling radius on plane/mesh)
  *   contact set        pinned  (independent numpy brute force, grid == brute)
  *   accumulate/integr. pinned  (free fall closed form, tumbling invariants,
  *                               momentum conservation, incline closed forms)

@@ -415,10 +415,11 @@ def step_group(systems, n_steps=1):
         raise DemError(rc, f"dem_step_group: {buf.value.decode()}")
 
 
-def halo_width(scene, drift_max):
-    """Ghost band: 2 x the largest bounding radius + margin + 2 drift_max (include/dem.h)."""
+def halo_width(scene, drift_max, margin=None):
+    """Ghost band: 2 x the largest bounding radius + margin + 2 drift_max (include/dem.h); margin
+    defaults to the scene's (pass the system's own if it was overridden)."""
     rb = max(float(np.max(np.linalg.norm(t.offsets, axis=1) + t.radius)) for t in scene.templates)
-    return 2.0 * rb + float(scene.margin) + 2.0 * drift_max
+    return 2.0 * rb + float(scene.margin if margin is None else margin) + 2.0 * drift_max
 
 
 def migrate_group(systems, threshold=0.0) -> bool:

@@ -701,6 +701,7 @@ __global__ void __launch_bounds__(DEM_ROWS_TPB, DEM_ROWS_MINB) k_rows_finish(Ste
       Entry e;
       e.key = partner_key(a, t);
       e.partner = t;
+      e.prev = -1;  // set by the merge below
       R[u] = e;
     }
     for (int u = 1; u < nc; ++u) {

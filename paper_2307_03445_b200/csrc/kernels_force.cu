@@ -343,7 +343,9 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
       }
     }
     __syncthreads();
-    if (kMesh && tid == 0 && chunk_mesh) {
+    // only thread 0 reads or clears chunk_mesh between the barriers (the other threads set it
+    // before the barrier above and next after the barrier below)
+    if (kMesh && tid == 0 && *(volatile int*)&chunk_mesh) {
       // the CTA's mesh wrench, entries in row order (deterministic), beside the per-sphere sums
       // of the other threads (both only read part[] until the next barrier)
       cta_mesh = 1;

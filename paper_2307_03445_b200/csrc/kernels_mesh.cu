@@ -64,6 +64,9 @@ __global__ void __launch_bounds__(256) k_mesh_pairs(StepArgs a) {
   const int lane = threadIdx.x & 31, nw = (blockDim.x >> 5) * gridDim.y;
   const int warp = blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int code = -1 - kMaxPlanes - t;
+  // an insert overflow (k_bin_scatter stopped writing past cap_inserts; the host regrows and
+  // re-runs the step) leaves the bin bounds pointing past the items array: nothing to read
+  if ((long long)a.cell_start[a.ncell] > a.cap_inserts) return;
   for (long long b = warp; b < nb; b += nw) {
     const int bx = tlo[0] + (int)(b % nx), by = tlo[1] + (int)((b / nx) % ny), bz = tlo[2] + (int)(b / ((long long)nx * ny));
     const long long cid = bx * g.st[0] + by * g.st[1] + bz * g.st[2];

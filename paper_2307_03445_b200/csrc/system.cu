@@ -561,6 +561,18 @@ extern "C" dem_status dem_create(const dem_params* params, const dem_material* m
     for (int k = 0; k < T.n_comp; ++k)
       if (!(T.radius[k] > 0) || T.material[k] < 0 || T.material[k] >= n_mat) return DEM_ERR_BAD_TEMPLATE;
   }
+  if (params->n_ranks > 1) {
+    // the ghost band must hold every clump a owned sphere can touch before the next migration:
+    // 2 R_bound,max + margin + 2 drift_max; a thinner band misses contacts silently
+    double rb_max = 0.0;
+    for (int t = 0; t < n_tmpl; ++t)
+      for (int k = 0; k < templates[t].n_comp; ++k) {
+        const double* o = templates[t].offset + 3 * k;
+        rb_max = std::max(rb_max, std::sqrt(o[0] * o[0] + o[1] * o[1] + o[2] * o[2]) + templates[t].radius[k]);
+      }
+    const double need = 2.0 * rb_max + params->margin + 2.0 * params->drift_max;
+    if (params->halo < need * (1.0 - 1e-12)) return DEM_ERR_INVALID_ARG;
+  }
   dem_system* sys = new dem_system();
   sys->P = *params;
   if (const char* fi = std::getenv("DEM_FAULT_AHEAD_OVERFLOW")) sys->fault_ahead = std::atoi(fi);
@@ -722,6 +734,10 @@ static dem_status alloc_rows(dem_system* sys, long long cap) {
       sys->err = "row buffer allocation failed";
       return DEM_ERR_OOM;
     }
+    // zeroed once per (rare) growth, so no byte of a row buffer is ever read uninitialised
+    // (compute-sanitizer initcheck; the old contents are copied over the front below)
+    CK(cudaMemsetAsync(nb.ent, 0, sizeof(Entry) * cap, sys->stream));
+    CK(cudaMemsetAsync(nb.ut, 0, sizeof(double) * kUt * cap, sys->stream));
     if (sys->rows[p].ent && sys->cap_entries) {
       size_t m = (size_t)std::min(cap, sys->cap_entries);
       cudaMemcpyAsync(nb.ent, sys->rows[p].ent, sizeof(Entry) * m, cudaMemcpyDeviceToDevice, sys->stream);
@@ -1626,7 +1642,9 @@ extern "C" dem_status dem_step(dem_system* sys, int64_t n_steps) {
       const int kind = step_kind(sys);
       sched.push_back(Sched{sys->up, sys->ep, sys->since_rebuild, sys->pending});
       if (sys->profiling) {
-        // stage timing: every part in line on the system stream (same results)
+        // stage timing: every part in line on the system stream (same results); a set still being
+        // detected ahead on det_stream (launched before profiling was turned on) is joined first
+        if (kind == K_ADOPT) CK(cudaStreamWaitEvent(sys->stream, sys->ev_det, 0));
         enqueue_step(sys, kind, sys->stream, &sys->ev[(size_t)k * (kStages + 1)]);
       } else if (kind == K_AHEAD) {
         // the next window's detection forks off after this step's poses and runs on det_stream

@@ -65,3 +65,39 @@ def test_sm100a_cubin_and_no_oracle_link():
         if f.endswith(".py"):
             txt = open(os.path.join(ROOT, "paper_2307_03445_b200", f)).read()
             assert "import oracle" not in txt and "from oracle" not in txt
+
+
+def test_dem_create_rejects_a_thin_ghost_band_without_gpu():
+    """A distributed system's ghost band must be >= 2 R_bound,max + margin + 2 drift_max
+    (include/dem.h): dem_create refuses a thinner one before touching the GPU."""
+    import ctypes as C
+
+    import numpy as np
+
+    import paper_2307_03445_b200 as pkg
+    from paper_2307_03445_b200 import binding as B
+
+    L = pkg.load_library()
+    mats = (B.dem_material * 1)(B.dem_material(1e9, 0.3, 0.4, 0.5))
+    off, rad, mat = np.array([0.0, 0.0, 0.0, 1e-3, 0.0, 0.0]), np.array([1e-3, 1e-3]), np.zeros(2, np.int32)
+    tp = (B.dem_template * 1)()
+    tp[0].n_comp = 2
+    tp[0].offset = off.ctypes.data_as(C.POINTER(C.c_double))
+    tp[0].radius = rad.ctypes.data_as(C.POINTER(C.c_double))
+    tp[0].material = mat.ctypes.data_as(C.POINTER(C.c_int32))
+    tp[0].mass = 1e-5
+    tp[0].inertia[:] = [1e-11, 1e-11, 1e-11]
+    p = B.dem_params()
+    p.h = 1e-6
+    p.gravity[:] = [0, 0, -9.81]
+    p.cd_every = 2
+    p.margin = 1e-5
+    p.domain_lo[:] = [-1, -1, -1]
+    p.domain_hi[:] = [1, 1, 1]
+    p.rank, p.n_ranks, p.slab_lo, p.slab_hi, p.drift_max = 0, 2, -1.0, 0.0, 1e-4
+    p.transport = B.TRANSPORT_LOOPBACK
+    need = 2 * 2e-3 + 1e-5 + 2 * 1e-4  # R_bound = 2 mm
+    out = C.c_void_p()
+    p.halo = need * (1 - 1e-6)
+    assert L.dem_create(C.byref(p), mats, 1, tp, 1, None, 0, None, C.byref(out)) == -1
+    assert not out.value
