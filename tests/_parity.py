@@ -12,6 +12,13 @@ def force_ref(scene):
     return min(t.mass for t in scene.templates) * g
 
 
+def u_floor(scene):
+    """Floor of the per-contact u_t comparison: h x v_ref, v_ref = the rms clump speed (>= 1 cm/s)."""
+    v = np.asarray(scene.vel, float)
+    vref = max(float(np.sqrt(np.mean(np.sum(v ** 2, axis=1)))) if v.size else 0.0, 0.01)
+    return float(scene.h) * vref
+
+
 def assert_same_contact_set(cg, co):
     assert np.array_equal(cg["key_a"], co["key_a"]) and np.array_equal(cg["key_b"], co["key_b"]), (
         f"contact sets differ: gpu {len(cg['key_a'])} vs oracle {len(co['key_a'])}")
@@ -27,8 +34,14 @@ def assert_forces_close(cg, co, scene, rtol=FORCE_RTOL):
         a, b = cg[k], co[k]
         scale = np.abs(b).max() + 1e-30
         assert np.abs(a - b).max() <= 1e-9 * scale, k
-    uscale = np.abs(co["u_t"]).max() + 1e-30
-    assert np.abs(cg["u_t"] - co["u_t"]).max() <= rtol * uscale
+    # u_t per contact (relative + a floor): the floor is the history one step of tangential
+    # motion adds at the scene's speed scale (h v_ref), so a wrong or sign-flipped small u_t
+    # fails even when the largest u_t of the scene is far bigger
+    uo, ug = co["u_t"], cg["u_t"]
+    uerr = np.linalg.norm(ug - uo, axis=1)
+    ubound = rtol * np.linalg.norm(uo, axis=1) + rtol * u_floor(scene)
+    ubad = np.nonzero(uerr > ubound)[0]
+    assert ubad.size == 0, f"{ubad.size} u_t out of tolerance; worst {uerr[ubad].max()} vs {ubound[ubad].min()}"
     return float((err / (np.linalg.norm(Fo, axis=1) + force_ref(scene))).max()) if err.size else 0.0
 
 

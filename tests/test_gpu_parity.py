@@ -222,6 +222,46 @@ def test_out_of_domain_is_reported(dem):
     assert e.value.status == -10 and "gid 1" in str(e.value)
 
 
+def _two_spheres(pos_b, vel_a=(0.0, 0.0, 0.0), vel_b=(0.0, 0.0, 0.0)):
+    t = w.sphere_template(1e-3)
+    return w.Scene(materials=np.array([w.M0]), templates=[t], planes=[], h=1e-6, gravity=np.zeros(3),
+                   domain_lo=np.full(3, -0.01), domain_hi=np.full(3, 0.01), gid=np.array([4, 9], np.int64),
+                   tid=np.zeros(2, np.int32), pos=np.array([[0.0, 0.0, 0.0], pos_b]),
+                   quat=np.array([[1.0, 0, 0, 0]] * 2), vel=np.array([vel_a, vel_b], float), omega=np.zeros((2, 3)))
+
+
+def test_degenerate_contact_is_reported(dem):
+    """Coincident centres of two spheres of different clumps (S:107): no contact normal exists;
+    the step reports DEM_ERR_DEGENERATE_CONTACT (-12) naming both sphere keys, as the oracle
+    reports its degenerate-contact error."""
+    scene = _two_spheres((0.0, 0.0, 0.0))
+    o = oracle.Oracle(scene)
+    with pytest.raises(oracle.OracleError, match="degenerate|coincident"):
+        o.step(1)
+    g = dem.system_from_scene(scene)
+    with pytest.raises(dem.DemError) as e:
+        g.dem_step(3)
+    assert e.value.status == -12
+    assert "256" in str(e.value) and "576" in str(e.value)  # sphere keys 4*64 and 9*64
+    with pytest.raises(dem.DemError):  # the error is latched: later calls report it again
+        g.dem_step(1)
+
+
+def test_nonfinite_wrench_in_step_is_reported(dem):
+    """Finite inputs whose contact force overflows inside the step (relative speed 2e308: the
+    normal damping term is inf) give DEM_ERR_NONFINITE (-11) naming the clump, as the
+    oracle's non-finite-wrench error; the state is not advanced past the bad step."""
+    scene = _two_spheres((1.9e-3, 0.0, 0.0), vel_a=(1e308, 0.0, 0.0), vel_b=(-1e308, 0.0, 0.0))
+    o = oracle.Oracle(scene)
+    with pytest.raises(oracle.OracleError, match="non-finite"):
+        o.step(1)
+    g = dem.system_from_scene(scene)
+    with pytest.raises(dem.DemError) as e:
+        g.dem_step(2)
+    assert e.value.status == -11 and ("gid 4" in str(e.value) or "gid 9" in str(e.value))
+    assert g.dem_get_stats()["steps"] <= 1
+
+
 def test_capacity_regrow_keeps_parity(dem):
     """A very dense overlapping scene overflows the initial row capacity (8 per sphere):
     the library regrows and re-runs; results still match the oracle."""

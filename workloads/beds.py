@@ -139,3 +139,48 @@ def patch_mesh(cone_speed: float = 0.5, spin: float = 0.0, depth: float = 1.0e-3
     s.domain_hi = np.array(s.domain_hi, dtype=float) + np.array([0.0, 0.0, hc + 0.02])
     s.name = "patch-mesh"
     return s
+
+
+def c3_impact(seed: int = 33) -> Scene:
+    """Config 3 at impact (a parity case, not a bench line): the C3 column (100k DS clumps, RSA
+    in the r = 6 cm cylinder) lowered onto a settled base layer — the oracle-settled patch tiled
+    under the column and cut to the same cylinder, as the first arrivals of the pour would have
+    built it — every column clump falling at 2 m/s (a 20 cm drop) with +-2 m/s of random relative
+    motion and +-200 rad/s of random spin.  Its lowest sphere starts 2 um into the top of the
+    base layer, so high-speed impacts on a dense layer begin at once while the sparse column
+    above keeps falling."""
+    from scipy.spatial.transform import Rotation
+
+    from .scenes import c3_repose
+
+    col = c3_repose()
+    rng = np.random.default_rng(seed)
+    base = tiled_bed(60_000, footprint=(0.125, 0.125), seed=seed)
+    c = 0.5 * (base.domain_lo[:2] + base.domain_hi[:2])
+    keep = np.nonzero(np.hypot(base.pos[:, 0] - c[0], base.pos[:, 1] - c[1]) < 0.06)[0]
+    base = base.subset(keep)
+    base.pos = base.pos - np.array([c[0], c[1], 0.0])
+
+    def sphere_extent(s, sel, lowest):
+        R = Rotation.from_quat(s.quat[sel][:, [1, 2, 3, 0]]).as_matrix()
+        z = [float(s.pos[i, 2] + (R[k] @ o)[2] + (-r if lowest else r)) for k, i in enumerate(sel)
+             for o, r in zip(s.templates[s.tid[i]].offsets, s.templates[s.tid[i]].radius)]
+        return min(z) if lowest else max(z)
+
+    top = sphere_extent(base, np.argsort(base.pos[:, 2])[-500:], False)
+    bottom = sphere_extent(col, np.argsort(col.pos[:, 2])[:500], True)
+    col.pos = col.pos + np.array([0.0, 0.0, top - bottom - 2e-6])
+    n0 = base.n_clumps
+    vel = np.concatenate([base.vel, np.column_stack([np.zeros(col.n_clumps), np.zeros(col.n_clumps),
+                                                     np.full(col.n_clumps, -2.0)])
+                          + rng.uniform(-2.0, 2.0, size=(col.n_clumps, 3))])
+    om = np.concatenate([base.omega, rng.uniform(-200.0, 200.0, size=(col.n_clumps, 3))])
+    s = col.copy()
+    s.gid = np.concatenate([np.arange(n0, dtype=np.int64), col.gid + n0])
+    s.tid = np.concatenate([base.tid, col.tid]).astype(np.int32)
+    s.pos = np.concatenate([base.pos, col.pos])
+    s.quat = np.concatenate([base.quat, col.quat])
+    s.vel, s.omega = vel, om
+    s.domain_hi = np.array([s.domain_hi[0], s.domain_hi[1], float(col.pos[:, 2].max()) + 0.05])
+    s.name = "C3-impact"
+    return s

@@ -256,50 +256,58 @@ def rsa_bed(seed: int, n_clumps: int, lo, hi, per_comp_mat: bool = False, vz: fl
     (fact 0.1-5).  If `cylinder_r` > 0 the centres are restricted to a vertical
     cylinder about the box's x-y centre (C3 repose column).
     """
+    from scipy.spatial import cKDTree
+
     rng = np.random.default_rng(seed)
     templates = ds_templates(per_component_materials=per_comp_mat)
     rb = np.array([t.bounding_radius for t in templates])
     counts = ds_type_counts(n_clumps)
     types = np.concatenate([np.full(c, t, dtype=np.int32) for t, c in enumerate(counts)])
     lo, hi = np.asarray(lo, float), np.asarray(hi, float)
-    cell = 2 * rb.max()
-    dims = np.maximum(1, np.ceil((hi - lo) / cell).astype(int))
-    grid: dict = {}
-    P = np.zeros((n_clumps, 3))
-    R = rb[types]
     cx, cy = 0.5 * (lo[0] + hi[0]), 0.5 * (lo[1] + hi[1])
-    placed = 0
-    for k in range(n_clumps):
-        r = R[k]
-        ok = False
-        for _ in range(max_tries):
-            p = rng.uniform(lo + r, hi - r)
+    # batched RSA, one radius at a time (largest first): propose a batch of centres, drop those
+    # that overlap a placed sphere (k-d tree query) or an earlier accepted proposal of the same
+    # batch, keep what is needed; a seeded, valid non-overlapping packing
+    P = np.zeros((0, 3))
+    Rp = np.zeros(0)
+    for t in np.argsort(-rb, kind="stable"):
+        r, need = rb[t], int(counts[t])
+        fails = 0
+        while need > 0:
+            m = int(min(max(4 * need, 2048), 400_000))
+            q = rng.uniform(lo + r, hi - r, size=(m, 3))
             if cylinder_r > 0:
-                if (p[0] - cx) ** 2 + (p[1] - cy) ** 2 > (cylinder_r - r) ** 2:
-                    continue
-            c = np.minimum(((p - lo) / cell).astype(int), dims - 1)
-            clash = False
-            for dx in (-1, 0, 1):
-                for dy in (-1, 0, 1):
-                    for dz in (-1, 0, 1):
-                        for j in grid.get((c[0] + dx, c[1] + dy, c[2] + dz), ()):
-                            if np.sum((P[j] - p) ** 2) < (R[j] + r) ** 2:
-                                clash = True
-                                break
-                        if clash:
-                            break
-                    if clash:
-                        break
-                if clash:
-                    break
-            if not clash:
-                ok = True
-                break
-        if not ok:
-            raise RuntimeError(f"RSA could not place clump {k} of {n_clumps}; box too small")
-        P[k] = p
-        grid.setdefault((c[0], c[1], c[2]), []).append(k)
-        placed += 1
+                q = q[(q[:, 0] - cx) ** 2 + (q[:, 1] - cy) ** 2 <= (cylinder_r - r) ** 2]
+            if P.shape[0]:
+                tree = cKDTree(P)
+                near = tree.query_ball_point(q, r + Rp.max(), workers=-1)
+                ok = np.ones(q.shape[0], bool)
+                for i, js in enumerate(near):
+                    if js:
+                        js = np.asarray(js)
+                        if np.any(np.sum((P[js] - q[i]) ** 2, axis=1) < (Rp[js] + r) ** 2):
+                            ok[i] = False
+                q = q[ok]
+            if q.shape[0]:
+                clash = cKDTree(q).query_pairs(2 * r, output_type="ndarray")
+                keep = np.ones(q.shape[0], bool)
+                if clash.size:
+                    bad_with = {}
+                    for a, b in clash:
+                        bad_with.setdefault(int(max(a, b)), []).append(int(min(a, b)))
+                    for i in sorted(bad_with):
+                        if any(keep[j] for j in bad_with[i]):
+                            keep[i] = False
+                q = q[keep][:need]
+            if q.shape[0] == 0:
+                fails += 1
+                if fails > max_tries // 100 + 3:
+                    raise RuntimeError(f"RSA could not place {need} clumps of type {t}; box too small")
+                continue
+            P = np.concatenate([P, q])
+            Rp = np.concatenate([Rp, np.full(q.shape[0], r)])
+            need -= q.shape[0]
+    types = np.repeat(np.argsort(-rb, kind="stable"), counts[np.argsort(-rb, kind="stable")]).astype(np.int32)
     gid, tid, pos, quat, vel, om = _mk_state(n_clumps)
     perm = rng.permutation(n_clumps)
     tid[:] = types[perm]
