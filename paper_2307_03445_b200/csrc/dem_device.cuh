@@ -40,7 +40,10 @@ struct Ctl {
   int pad_;
 };
 
-constexpr int kUt = 4;    // doubles per entry of the tangential history (padded)
+#ifndef DEM_UT_PAD
+#define DEM_UT_PAD 0  // 1: u_t padded to 32 bytes (one 256-bit access per entry)
+#endif
+constexpr int kUt = DEM_UT_PAD ? 4 : 3;  // doubles per entry of the tangential history (x, y, z[, 0]), AoS
 #ifndef DEM_V256
 #define DEM_V256 1  // 256-bit gathers of the 32-byte records (sm_100 LDG.256)
 #endif
@@ -48,7 +51,6 @@ constexpr int kKinUsed = 10;  // doubles per clump in the packed kinematics reco
 // record stride: padded to 96 bytes so a partner's record is three 256-bit loads
 constexpr int kKin = DEM_V256 ? 12 : 10;
 static_assert(!DEM_V256 || (kKin * 8) % 32 == 0, "kinematics records must stay 32-byte aligned");
-static_assert(kUt * 8 == 32, "u_t records are one 32-byte access");
 
 // 32-byte loads/stores in one instruction (sm_100: LDG.E.ENL2.256 / STG.E.ENL2.256); p must be
 // 32-byte aligned.  A random gather of a 32-byte record then costs one L1 wavefront per lane
@@ -106,8 +108,9 @@ struct Grid {
   double pad;  // r + pad is the half-extent of a sphere's bin AABB (margin/2 + eps)
 };
 
-struct __align__(16) Entry {
-  long long key;    // partner key (sphere key, or INT64_MAX - plane)
+// A row entry as the force kernel reads it (8 bytes); the partner keys live in their own array
+// (Rows::key), read only by the row build/merge, dem_get_contacts and error reports.
+struct __align__(8) Entry {
   int partner;      // partner local sphere index, or -1 - plane
   int prev;         // index of the same key in the previous step's rows (its u_t), or -1
 };
@@ -115,7 +118,8 @@ struct __align__(16) Entry {
 struct Rows {
   int* row_ptr;     // [ns + 1]
   Entry* ent;       // [cap]
-  double* ut;       // [kUt * cap] AoS (x, y, z, 0): one 32-byte sector per entry, oriented own -> partner
+  long long* key;   // [cap] partner key (sphere key, or INT64_MAX - plane), ascending within a row
+  double* ut;       // [kUt * cap] AoS (x, y, z), oriented own -> partner
 };
 
 struct Record {

@@ -629,7 +629,7 @@ __device__ __forceinline__ long long partner_key(const StepArgs& a, int code) {
 
 __device__ __forceinline__ int prev_index(const Rows& prev, int pb, int pe, long long key) {
   for (int v = pb; v < pe; ++v)
-    if (prev.ent[v].key == key) return v;
+    if (prev.key[v] == key) return v;
   return -1;
 }
 
@@ -652,6 +652,7 @@ __global__ void __launch_bounds__(DEM_ROWS_TPB, DEM_ROWS_MINB) k_rows_finish(Ste
   const int m = a.rows.row_ptr[i + 1] - beg;
   const int pb = a.prev.row_ptr[i], pe = a.prev.row_ptr[i + 1];
   Entry* R = a.rows.ent + beg;
+  long long* K = a.rows.key + beg;
   const unsigned wmask = a.wall_mask[i];  // the pose kernel's sphere-plane candidates
   const int w = __popc(wmask);
   const int nc = m - w;  // k_pairs handed out slots [w, m) of the candidate list
@@ -681,7 +682,7 @@ __global__ void __launch_bounds__(DEM_ROWS_TPB, DEM_ROWS_MINB) k_rows_finish(Ste
         }
 #pragma unroll 4
     for (int v = pb; v < pe; ++v) {
-      const long long pk = a.prev.ent[v].key;
+      const long long pk = a.prev.key[v];
 #pragma unroll
       for (int q = 0; q < kRegRow; ++q)
         if (kk[q] == pk) hh[q] = v;
@@ -690,34 +691,37 @@ __global__ void __launch_bounds__(DEM_ROWS_TPB, DEM_ROWS_MINB) k_rows_finish(Ste
     for (int q = 0; q < kRegRow; ++q)
       if (q < nc) {
         Entry e;
-        e.key = kk[q];
         e.partner = tt[q];
         e.prev = hh[q];
         R[q] = e;
+        K[q] = kk[q];
       }
   } else {
     for (int u = 0; u < nc; ++u) {
       const int t = S[(size_t)u * a.ns_own];
       Entry e;
-      e.key = partner_key(a, t);
       e.partner = t;
       e.prev = -1;  // set by the merge below
       R[u] = e;
+      K[u] = partner_key(a, t);
     }
     for (int u = 1; u < nc; ++u) {
       const Entry x = R[u];
+      const long long xk = K[u];
       int v = u - 1;
-      while (v >= 0 && R[v].key > x.key) {
+      while (v >= 0 && K[v] > xk) {
         R[v + 1] = R[v];
+        K[v + 1] = K[v];
         --v;
       }
       R[v + 1] = x;
+      K[v + 1] = xk;
     }
     int pj = pb;  // merge with the previous row (both sorted by key)
     for (int u = 0; u < nc; ++u) {
-      const long long k = R[u].key;
-      while (pj < pe && a.prev.ent[pj].key < k) ++pj;
-      R[u].prev = (pj < pe && a.prev.ent[pj].key == k) ? pj : -1;
+      const long long k = K[u];
+      while (pj < pe && a.prev.key[pj] < k) ++pj;
+      R[u].prev = (pj < pe && a.prev.key[pj] == k) ? pj : -1;
     }
   }
   if (a.n_tri)  // this set's mesh entries, for the per-step geometry pass (k_mesh_geom)
@@ -725,10 +729,11 @@ __global__ void __launch_bounds__(DEM_ROWS_TPB, DEM_ROWS_MINB) k_rows_finish(Ste
       if (R[u].partner <= -1 - kMaxPlanes) a.mlist_out[atomicAdd(a.mlist_out_n, 1)] = make_int2(beg + u, i);
   for (int u = nc, p = a.tab.n_planes - 1; p >= 0; --p)
     if (wmask >> p & 1u) {
+      const long long key = (long long)(0x7fffffffffffffffLL - p);
       Entry e;
-      e.key = (long long)(0x7fffffffffffffffLL - p);
       e.partner = -1 - p;
-      e.prev = prev_index(a.prev, pb, pe, e.key);
+      e.prev = prev_index(a.prev, pb, pe, key);
+      K[u] = key;
       R[u++] = e;
     }
 }

@@ -26,6 +26,12 @@
 namespace dem {
 
 constexpr int kPairStride = 8;  // doubles per material pair in Tables::pair
+#ifndef DEM_FORCE_OWNER
+#define DEM_FORCE_OWNER 1  // owner sphere of each entry from a shared table (else a binary search)
+#endif
+#ifndef DEM_FORCE_ASYNC_EPI
+#define DEM_FORCE_ASYNC_EPI 0  // 1: own clumps' q, Omega, inertia staged by cp.async in the prologue
+#endif
 #ifndef DEM_FORCE_FT
 #define DEM_FORCE_FT 128
 #endif
@@ -102,6 +108,8 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
   __shared__ __align__(16) double ck[kFC * kKinUsed];
   __shared__ double part[6][kFT];
   __shared__ double acc[6][kMaxS];
+  __shared__ unsigned char own_of[DEM_FORCE_OWNER ? kFT : 1];  // entry of the chunk -> its own sphere
+  __shared__ double cq[DEM_FORCE_ASYNC_EPI ? 10 : 1][kFC];     // own clumps' q, Omega_body, inertia (Eq. 4)
   // mesh wrench (kMesh): per entry the mesh id (-1: not a mesh entry) and torque about its X
   __shared__ int emesh[kMesh ? kFT : 1];
   __shared__ double mtq[3][kMesh ? kFT : 1];
@@ -125,8 +133,15 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
   if (blockIdx.x == 0 && tid == 0) a.ctl->step += 1;  // no other thread of this launch reads it
   const int s0 = b0.y;
   const int nsph = b1.y - s0;
+  const int E0g = a.rows.row_ptr[s0];
   for (int k = tid; k <= nsph; k += kFT) {
-    rp[k] = a.rows.row_ptr[s0 + k];
+    const int r0 = a.rows.row_ptr[s0 + k];
+    rp[k] = r0;
+    if (k < nsph) {  // owner of each entry of the first chunk (later chunks: built beside the sums)
+      const int r1 = a.rows.row_ptr[s0 + k + 1];
+      if (DEM_FORCE_OWNER)
+        for (int q = max(r0, E0g); q < min(r1, E0g + kFT); ++q) own_of[q - E0g] = (unsigned char)k;
+    }
   }
   for (int ls = tid; ls < nsph; ls += kFT) {
     const int i = s0 + ls;
@@ -144,6 +159,20 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
       reinterpret_cast<double2*>(ck)[k] = src[c * (kKin / 2) + r];
     }
   }
+  if (DEM_FORCE_ASYNC_EPI && tid < ncl) {
+    // the integrating thread's q, Omega (body) and inertia, copied to shared memory in the
+    // background (cp.async, no registers held) and awaited only after the entry loop
+    const int c = c0 + tid, t = a.tid[c];
+    const double* src[10] = {a.cur.qw + c, a.cur.qx + c, a.cur.qy + c, a.cur.qz + c, a.cur.wx + c,
+                             a.cur.wy + c, a.cur.wz + c, a.tab.tpl_inertia + 3 * t, a.tab.tpl_inertia + 3 * t + 1,
+                             a.tab.tpl_inertia + 3 * t + 2};
+#pragma unroll
+    for (int k = 0; k < 10; ++k) {
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(&cq[k][tid]);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src[k]) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   if (kMesh && tid < kMaxMeshes * 6) cw[tid / 6][tid % 6] = 0.0;
   if (kMesh && tid == 0) chunk_mesh = cta_mesh = 0;
   __syncthreads();
@@ -153,20 +182,22 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
     const int e = c0e + tid;
     if (kMesh) emesh[tid] = -1;
     if (e < E1) {
-      // owner: last ls with rp[ls] <= e
-      int lo = 0, hi = nsph - 1;
+#if DEM_FORCE_OWNER
+      const int ls = own_of[tid];
+#else
+      int lo = 0, hi = nsph - 1;  // owner: last ls with rp[ls] <= e
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
         if (rp[mid] <= e) lo = mid; else hi = mid - 1;
       }
       const int ls = lo;
+#endif
       const double4 own = own_p[ls];
       const double cx = own.x, cy = own.y, cz = own.z, ri = own.w;
       const double* ki = ck + kKinUsed * own_lc[ls];
       const double Xx = ki[0], Xy = ki[1], Xz = ki[2];
       const double Mi = ki[9];
       const Entry ent = a.rows.ent[e];
-      const long long key = ent.key;
       const int t = ent.partner;
       // (a4) history remap: the slot of this key in the previous rows was found by the
       // row merge in k_rows_finish (-1: contact born this step, u_t = 0)
@@ -174,10 +205,15 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
       double ux = 0.0, uy = 0.0, uz = 0.0;
       const int pidx = a.remap ? ent.prev : e;
       if (pidx >= 0) {
-        const double4 u = ldg256(a.prev.ut + kUt * pidx);
-        ux = u.x;
-        uy = u.y;
-        uz = u.z;
+#if DEM_UT_PAD
+        const double4 u = ldg256(a.prev.ut + (size_t)kUt * pidx);
+        ux = u.x; uy = u.y; uz = u.z;
+#else
+        const double* u = a.prev.ut + (size_t)kUt * pidx;
+        ux = __ldg(u);
+        uy = __ldg(u + 1);
+        uz = __ldg(u + 2);
+#endif
       }
       // (a5) geometry: n from i (own) to j (partner)
       double nx, ny, nz, px, py, pz, delta, rbar, mbar;
@@ -264,7 +300,7 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
         mj = a.tab.plane_mat[pl];
       }
       if (degenerate) {
-        raise_error(a.ctl, -12, a.s_key[s0 + ls], key);
+        raise_error(a.ctl, -12, a.s_key[s0 + ls], a.rows.key[e]);
         delta = 0.0;
       }
       double Fx = 0.0, Fy = 0.0, Fz = 0.0, nux = 0.0, nuy = 0.0, nuz = 0.0;
@@ -317,7 +353,16 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
         Fy = fny + fty;
         Fz = fnz + ftz;
       }
-      stg256(a.rows.ut + kUt * e, nux, nuy, nuz, 0.0);
+      {
+#if DEM_UT_PAD
+        stg256(a.rows.ut + (size_t)kUt * e, nux, nuy, nuz, 0.0);
+#else
+        double* u = a.rows.ut + (size_t)kUt * e;
+        u[0] = nux;
+        u[1] = nuy;
+        u[2] = nuz;
+#endif
+      }
       if (a.record) {
         a.rec.F[3 * e] = Fx; a.rec.F[3 * e + 1] = Fy; a.rec.F[3 * e + 2] = Fz;
         a.rec.p[3 * e] = px; a.rec.p[3 * e + 1] = py; a.rec.p[3 * e + 2] = pz;
@@ -357,13 +402,18 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
         cw[m][3] += mtq[0][q]; cw[m][4] += mtq[1][q]; cw[m][5] += mtq[2][q];
       }
     }
-    // (a9, first level) canonical per-sphere sums: entries in row (partner-key) order
+    // (a9, first level) canonical per-sphere sums: entries in row (partner-key) order; then the
+    // owners of this sphere's entries in the next chunk
     for (int ls = tid; ls < nsph; ls += kFT) {
-      const int b = max(rp[ls], c0e), en = min(rp[ls + 1], c0e + kFT);
+      const int r0 = rp[ls], r1 = rp[ls + 1];
+      const int b = max(r0, c0e), en = min(r1, c0e + kFT);
       for (int q = b - c0e; q < en - c0e; ++q) {
 #pragma unroll
         for (int d = 0; d < 6; ++d) acc[d][ls] += part[d][q];
       }
+      const int nb = c0e + kFT;
+      if (DEM_FORCE_OWNER)
+        for (int q = max(r0, nb); q < min(r1, nb + kFT); ++q) own_of[q - nb] = (unsigned char)ls;
     }
     __syncthreads();
   }
@@ -377,10 +427,19 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
   // F = sum_k f_k + M g; tau_body = R^T sum_k tau_k; V += h F/M; X += h V;
   // Omega += h I^-1 (tau - Omega x I Omega); q <- normalize(q (x) exp(h Omega)).
   const int c = c0 + tid;
-  const int t = a.tid[c];
+#if DEM_FORCE_ASYNC_EPI
+  asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's own cq[.][tid]
+  const double I0 = cq[7][tid], I1 = cq[8][tid], I2 = cq[9][tid];
+  const double qw = cq[0][tid], qx = cq[1][tid], qy = cq[2][tid], qz = cq[3][tid];
+  const double w0 = cq[4][tid], w1 = cq[5][tid], w2 = cq[6][tid];
+#else
+  const int tt = a.tid[c];
+  const double I0 = a.tab.tpl_inertia[3 * tt], I1 = a.tab.tpl_inertia[3 * tt + 1], I2 = a.tab.tpl_inertia[3 * tt + 2];
+  const double qw = a.cur.qw[c], qx = a.cur.qx[c], qy = a.cur.qy[c], qz = a.cur.qz[c];
+  const double w0 = a.cur.wx[c], w1 = a.cur.wy[c], w2 = a.cur.wz[c];
+#endif
   const double* kc = ck + kKinUsed * tid;  // this clump's X, V, omega_world, M
   const double M = kc[9];
-  const double I0 = a.tab.tpl_inertia[3 * t], I1 = a.tab.tpl_inertia[3 * t + 1], I2 = a.tab.tpl_inertia[3 * t + 2];
   double Fx = 0.0, Fy = 0.0, Fz = 0.0, Tx = 0.0, Ty = 0.0, Tz = 0.0;
   for (int s = a.sph_off[c] - s0, e = a.sph_off[c + 1] - s0; s < e; ++s) {
     Fx += acc[0][s]; Fy += acc[1][s]; Fz += acc[2][s];
@@ -389,7 +448,6 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
   Fx = __dadd_rn(Fx, __dmul_rn(M, a.g[0]));
   Fy = __dadd_rn(Fy, __dmul_rn(M, a.g[1]));
   Fz = __dadd_rn(Fz, __dmul_rn(M, a.g[2]));
-  const double qw = a.cur.qw[c], qx = a.cur.qx[c], qy = a.cur.qy[c], qz = a.cur.qz[c];
   double R[9];
   quat_R(qw, qx, qy, qz, R);
   const double tbx = R[0] * Tx + R[3] * Ty + R[6] * Tz;
@@ -408,7 +466,6 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
     const double dx = nxx - a.xref[3 * c], dy = nxy - a.xref[3 * c + 1], dz = nxz - a.xref[3 * c + 2];
     if (dx * dx + dy * dy + dz * dz > a.drift_max * a.drift_max) raise_error(a.ctl, -15, a.gid[c], 0);
   }
-  const double w0 = a.cur.wx[c], w1 = a.cur.wy[c], w2 = a.cur.wz[c];
   const double L0 = I0 * w0, L1 = I1 * w1, L2 = I2 * w2;
   const double g0 = w1 * L2 - w2 * L1, g1 = w2 * L0 - w0 * L2, g2 = w0 * L1 - w1 * L0;
   const double n0 = w0 + h * ((tbx - g0) / I0);
@@ -455,7 +512,7 @@ __global__ void k_count_canonical(Rows r, const long long* __restrict__ s_key, i
   unsigned c = 0;
   if (i < ns) {
     const long long own = s_key[i];
-    for (int e = r.row_ptr[i]; e < r.row_ptr[i + 1]; ++e) c += r.ent[e].key > own;
+    for (int e = r.row_ptr[i]; e < r.row_ptr[i + 1]; ++e) c += r.key[e] > own;
   }
   c = __reduce_add_sync(0xffffffffu, c);
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (unsigned long long)c);

@@ -56,6 +56,7 @@ static const int kOne = 1;  // 5 stage kernels + 2 x 3 scan kernels
 struct RowBuf {
   int* row_ptr = nullptr;
   Entry* ent = nullptr;
+  long long* key = nullptr;
   double* ut = nullptr;
 };
 
@@ -322,8 +323,8 @@ static StepArgs make_args(dem_system* sys, int kind, bool det = false) {
   a.wall_mask = sys->d_wall_mask;
   const RowBuf& E = sys->rows[rebuild ? sys->ep ^ 1 : sys->ep];
   const RowBuf& Q = sys->rows[sys->ep];
-  a.rows = Rows{E.row_ptr, E.ent, sys->rows[sys->up ^ 1].ut};
-  a.prev = Rows{Q.row_ptr, Q.ent, sys->rows[sys->up].ut};
+  a.rows = Rows{E.row_ptr, E.ent, E.key, sys->rows[sys->up ^ 1].ut};
+  a.prev = Rows{Q.row_ptr, Q.ent, Q.key, sys->rows[sys->up].ut};
   const bool deferred = sys->P.cd_every > 1;
   a.count = (kind == K_FULL || kind == K_AHEAD) ? 1 : 0;
   a.remap = rebuild ? 1 : 0;
@@ -729,21 +730,25 @@ static dem_status alloc_rows(dem_system* sys, long long cap) {
     RowBuf nb;
     nb.row_ptr = sys->rows[p].row_ptr;
     nb.ent = (Entry*)dalloc(sys, sizeof(Entry) * cap);
+    nb.key = (long long*)dalloc(sys, sizeof(long long) * cap);
     nb.ut = (double*)dalloc(sys, sizeof(double) * kUt * cap);
-    if (!nb.ent || !nb.ut) {
+    if (!nb.ent || !nb.key || !nb.ut) {
       sys->err = "row buffer allocation failed";
       return DEM_ERR_OOM;
     }
     // zeroed once per (rare) growth, so no byte of a row buffer is ever read uninitialised
     // (compute-sanitizer initcheck; the old contents are copied over the front below)
     CK(cudaMemsetAsync(nb.ent, 0, sizeof(Entry) * cap, sys->stream));
+    CK(cudaMemsetAsync(nb.key, 0, sizeof(long long) * cap, sys->stream));
     CK(cudaMemsetAsync(nb.ut, 0, sizeof(double) * kUt * cap, sys->stream));
     if (sys->rows[p].ent && sys->cap_entries) {
       size_t m = (size_t)std::min(cap, sys->cap_entries);
       cudaMemcpyAsync(nb.ent, sys->rows[p].ent, sizeof(Entry) * m, cudaMemcpyDeviceToDevice, sys->stream);
+      cudaMemcpyAsync(nb.key, sys->rows[p].key, sizeof(long long) * m, cudaMemcpyDeviceToDevice, sys->stream);
       cudaMemcpyAsync(nb.ut, sys->rows[p].ut, sizeof(double) * kUt * m, cudaMemcpyDeviceToDevice, sys->stream);
     }
     dfree(sys, sys->rows[p].ent);
+    dfree(sys, sys->rows[p].key);
     dfree(sys, sys->rows[p].ut);
     sys->rows[p] = nb;
   }
@@ -1365,6 +1370,7 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
   sys->cap_entries = 0;
   for (int p = 0; p < 2; ++p) {
     dfree(sys, sys->rows[p].ent); sys->rows[p].ent = nullptr;
+    dfree(sys, sys->rows[p].key); sys->rows[p].key = nullptr;
     dfree(sys, sys->rows[p].ut); sys->rows[p].ut = nullptr;
   }
   TRY(alloc_rows(sys, cap));
@@ -1458,16 +1464,17 @@ extern "C" dem_status dem_set_contact_history(dem_system* sys, int64_t n, const 
   }
   std::vector<int> rp(sys->ns + 1, 0);
   std::vector<Entry> ents;
+  std::vector<long long> keys;
   std::vector<double> ut;
   for (int64_t s = 0; s < sys->ns; ++s) {
     auto& v = per[s];
     std::sort(v.begin(), v.end(), [](const E& x, const E& y) { return x.key < y.key; });
     for (auto& e : v) {
       Entry en;
-      en.key = e.key;
       en.partner = -1;  // only the key and u_t of the previous rows are read
       en.prev = -1;
       ents.push_back(en);
+      keys.push_back(e.key);
       for (int d = 0; d < kUt; ++d) ut.push_back(d < 3 ? e.u[d] : 0.0);
     }
     rp[s + 1] = (int)ents.size();
@@ -1480,6 +1487,7 @@ extern "C" dem_status dem_set_contact_history(dem_system* sys, int64_t n, const 
   CK(cudaMemcpyAsync(R.row_ptr, rp.data(), sizeof(int) * (sys->ns + 1), cudaMemcpyHostToDevice, s));
   if (m) {
     CK(cudaMemcpyAsync(R.ent, ents.data(), sizeof(Entry) * m, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(R.key, keys.data(), sizeof(long long) * m, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(sys->rows[sys->up].ut, ut.data(), sizeof(double) * kUt * m, cudaMemcpyHostToDevice, s));
   }
   CK(cudaStreamSynchronize(s));
@@ -1899,10 +1907,8 @@ extern "C" dem_status dem_get_contacts(dem_system* sys, int64_t cap, int64_t* n,
   std::vector<int> rp(ns + 1);
   CK(cudaMemcpy(rp.data(), R.row_ptr, sizeof(int) * (ns + 1), cudaMemcpyDeviceToHost));
   const int64_t m = rp[ns];
-  std::vector<Entry> ents(m);
-  if (m) CK(cudaMemcpy(ents.data(), R.ent, sizeof(Entry) * m, cudaMemcpyDeviceToHost));
   std::vector<long long> keys(m);
-  for (int64_t e = 0; e < m; ++e) keys[e] = ents[e].key;
+  if (m) CK(cudaMemcpy(keys.data(), R.key, sizeof(long long) * m, cudaMemcpyDeviceToHost));
   // canonical entries: own key < partner key
   std::vector<std::pair<int64_t, int64_t>> sel;  // (own sphere, entry)
   for (int64_t s = 0; s < ns; ++s)
@@ -1962,7 +1968,7 @@ extern "C" dem_status dem_get_stats(dem_system* sys, dem_stats* out) {
     CK(cudaMemcpyAsync(&ins, sys->d_cell_start + sys->ncell, sizeof(int), cudaMemcpyDeviceToHost, sys->stream));
     CK(cudaMemsetAsync(sys->d_counter, 0, sizeof(unsigned long long), sys->stream));
     // canonical contacts held here: entries whose own key is the smaller (walls included)
-    launch_count_canonical(Rows{R.row_ptr, R.ent, R.ut}, sys->d_s_key, (int)sys->ns_own, sys->d_counter, sys->stream);
+    launch_count_canonical(Rows{R.row_ptr, R.ent, R.key, R.ut}, sys->d_s_key, (int)sys->ns_own, sys->d_counter, sys->stream);
     unsigned long long canon = 0;
     CK(cudaMemcpyAsync(&canon, sys->d_counter, sizeof(canon), cudaMemcpyDeviceToHost, sys->stream));
     CK(cudaStreamSynchronize(sys->stream));

@@ -38,18 +38,28 @@ def main():
     ap.add_argument("--vstop", type=float, default=0.02)
     ap.add_argument("--max-steps", type=int, default=400000)
     ap.add_argument("--chunk", type=int, default=2000)
+    ap.add_argument("--resume", default=None,
+                    help="continue settling a saved patch (its state, no history) instead of spawning")
     a = ap.parse_args()
     import workloads as w
 
-    n = int(round(a.density * a.side * a.side * a.depth))
-    vol = sum(c * t.mass / w.GRAIN_DENSITY for c, t in zip(w.ds_type_counts(n), w.ds_templates()))
-    H = vol / a.fraction / (a.side * a.side)
     t0 = time.time()
-    s = rsa_bed_exact(a.seed, n, (0.0, 0.0, 0.0), (a.side, a.side, H), vz=a.vz)
-    print(f"spawned {n} clumps / {s.n_spheres} spheres in a {H:.3f} m column ({time.time() - t0:.1f}s)",
-          flush=True)
+    if a.resume:
+        from workloads.scenes import load_scene
+
+        s = load_scene(a.resume)
+        steps = int(s.name.rsplit("-", 1)[-1]) if s.name.rsplit("-", 1)[-1].isdigit() else 0
+        print(f"resuming {s.name}: {s.n_clumps} clumps, vmax {np.linalg.norm(s.vel, axis=1).max():.4f}", flush=True)
+        a.max_steps += steps
+    else:
+        n = int(round(a.density * a.side * a.side * a.depth))
+        vol = sum(c * t.mass / w.GRAIN_DENSITY for c, t in zip(w.ds_type_counts(n), w.ds_templates()))
+        H = vol / a.fraction / (a.side * a.side)
+        s = rsa_bed_exact(a.seed, n, (0.0, 0.0, 0.0), (a.side, a.side, H), vz=a.vz)
+        print(f"spawned {n} clumps / {s.n_spheres} spheres in a {H:.3f} m column ({time.time() - t0:.1f}s)",
+              flush=True)
+        steps = 0
     o = oracle.Oracle(s, detect=1)
-    steps = 0
     while steps < a.max_steps:
         o.step(a.chunk)
         steps += a.chunk
@@ -59,7 +69,7 @@ def main():
         print(f"step {steps}: vmax {vmax:.4f} m/s, zmax {st['pos'][:, 2].max():.4f} m, "
               f"contacts {len(c['key_a'])} ({(c['delta'] > 0).sum()} touching), {time.time() - t0:.0f}s",
               flush=True)
-        if steps % 20000 == 0 or (steps > 50000 and vmax < a.vstop):
+        if steps % 20000 == 0 or (steps > 50000 and vmax < a.vstop) or steps >= a.max_steps:
             out = s.copy()
             out.pos, out.quat, out.vel, out.omega = st["pos"], st["quat"], st["vel"], st["omega"]
             out.domain_hi = np.array([a.side + 1e-3, a.side + 1e-3, st["pos"][:, 2].max() + 0.02])
