@@ -41,10 +41,19 @@ def peaks():
 
 
 # ---------------------------------------------------------------- workloads
-def make_scene(name: str):
+def make_scene(name: str, slab: float = 1.0):
     import workloads as w
     from workloads import beds
 
+    if name == "c5" and slab < 1.0:
+        # an x-slab of the bed (full y extent and depth), centred: the per-rank share of a
+        # P-GPU slab decomposition (slab = 1/P) run as one system — the size curve of §8e
+        bed = beds.c5_bed()
+        xlo, xhi = float(bed.pos[:, 0].min()), float(bed.pos[:, 0].max())
+        xc, wd = 0.5 * (xlo + xhi), slab * (xhi - xlo)
+        s = beds.crop(bed, [xc - wd / 2, -1.0, -1.0], [xc + wd / 2, 10.0, 10.0])
+        s.name = f"{bed.name} x-slab {slab:g}"
+        return s
     if name == "c5":
         return beds.c5_bed()
     if name == "c4":
@@ -193,7 +202,7 @@ def run_ours(a):
         td.broadcast_object_list(obj, src=0)
         dist = td
     t_setup = time.perf_counter()
-    scene = make_scene(a.config)
+    scene = make_scene(a.config, a.slab)
     dparams = None
     # deferred rebuild (NEXT-1): margin = 2 v_max h k; k = 1 is the headline.
     # Overlapped cadence (NEXT-2): the set is used 2k - 2 steps after its detection.
@@ -397,6 +406,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="c5", choices=["c5", "c4", "c3", "c1"])
     ap.add_argument("--cell-size", type=float, default=0.0)
+    ap.add_argument("--slab", type=float, default=1.0,
+                    help="c5 only: time a centred x-slab of this fraction of the bed (size curve; 1 = whole bed)")
     ap.add_argument("--cd-every", type=int, default=1, help="contact-set rebuild period k (1 = headline)")
     ap.add_argument("--vmax", type=float, default=1.0, help="speed bound for the k > 1 margin [m/s]")
     ap.add_argument("--overlap", action="store_true",

@@ -1,0 +1,128 @@
+"""NEXT-4 as SURVEY §8f specifies: the repose angle of config C3 (BASELINE config 3).
+
+C3 = 100k GRC-1-like DS clumps (Table-1 mix, seeded RSA in a vertical r = 6 cm cylinder at a
+bounding-sphere solid fraction of 0.25) released from rest above the plane z = 0 (P:277, P:299:
+"the angle of repose ... 30 degrees").  The column collapses onto the floor and spreads into a
+pile; the run continues until the pile is at rest, then the free-surface angle is fitted.
+
+Reproducible from the seed: the scene is workloads.c3_repose(seed), the solver runs the paper's
+deferred cadence (rebuild every k steps with the margin 2 v_max h k; the device
+reports DEM_ERR_VMAX if any sphere outruns it) on the GPU (the oracle is far too slow for the
+millions of steps), and the angle is fitted over several radial ranges; the acceptance band is
+30 +- 5 degrees.  Writes gpurun_out/<out>.json (+ the final state .npz).
+
+    python tools/repose_c3.py [--seed 3] [--max-steps 4000000] [--out r02/repose_c3]
+"""
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+FIT_RANGES = [(0.2, 0.8), (0.3, 0.7), (0.25, 0.75), (0.2, 0.6), (0.4, 0.8)]
+BAND = (25.0, 35.0)
+
+
+def surface_profile(pos, top_r, dr=4e-3):
+    """Free surface of a pile about the x-y centroid of its clumps: in rings of width dr the
+    surface height is the 2nd-highest clump top (COM z + bounding radius) of the ring."""
+    cx, cy = float(np.median(pos[:, 0])), float(np.median(pos[:, 1]))
+    rho = np.hypot(pos[:, 0] - cx, pos[:, 1] - cy)
+    top = pos[:, 2] + top_r
+    edges = np.arange(0.0, rho.max() + dr, dr)
+    idx = np.digitize(rho, edges) - 1
+    r_mid, surf = [], []
+    for k in range(len(edges) - 1):
+        m = idx == k
+        if m.sum() >= 3:
+            r_mid.append(0.5 * (edges[k] + edges[k + 1]))
+            surf.append(float(np.sort(top[m])[-2]))
+    return np.array(r_mid), np.array(surf), (cx, cy)
+
+
+def fit_angles(r_mid, surf, min_layer=6e-3):
+    thick = surf > min_layer
+    R = float(r_mid[thick].max()) if thick.any() else float(r_mid.max())
+    out = {}
+    for lo, hi in FIT_RANGES:
+        sel = (r_mid >= lo * R) & (r_mid <= hi * R)
+        if sel.sum() >= 3:
+            slope = np.polyfit(r_mid[sel], surf[sel], 1)[0]
+            out[f"{lo:g}-{hi:g}"] = float(math.degrees(math.atan(-slope)))
+    return R, out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--seed", type=int, default=3)
+    ap.add_argument("--max-steps", type=int, default=4_000_000)
+    ap.add_argument("--chunk", type=int, default=100_000)
+    ap.add_argument("--cd-every", type=int, default=20)
+    ap.add_argument("--vmax", type=float, default=8.0, help="speed bound of the deferred margin [m/s]")
+    ap.add_argument("--cell", type=float, default=4.0e-3, help="bin edge [m]")
+    ap.add_argument("--out", default="r02/repose_c3")
+    a = ap.parse_args()
+    import torch
+
+    import paper_2307_03445_b200 as dem
+    import workloads as w
+
+    torch.cuda.set_device(0)
+    s = w.c3_repose(seed=a.seed)
+    k = a.cd_every
+    margin = 2.0 * a.vmax * s.h * k
+    g = dem.system_from_scene(s, margin=margin, cd_every=k, cell_size=a.cell)
+    rb = np.array([t.bounding_radius for t in s.templates])[s.tid]
+    mass = np.array([t.mass for t in s.templates])[s.tid]
+    out_base = os.path.join(ROOT, "gpurun_out", a.out)
+    os.makedirs(os.path.dirname(out_base), exist_ok=True)
+    log, t0, steps, rest = [], time.time(), 0, 0
+    order = np.argsort(s.gid)
+    while steps < a.max_steps:
+        g.dem_step(a.chunk)
+        steps += a.chunk
+        st = g.dem_get_state()
+        o = np.argsort(st["gid"])
+        v, pos = st["vel"][o], st["pos"][o]
+        speed = np.linalg.norm(v, axis=1)
+        ke = float(0.5 * np.sum(mass * speed ** 2))
+        st_ = g.dem_get_stats()
+        rec = dict(step=steps, t_s=round(steps * s.h, 4), ke_j=ke, vmax=float(speed.max()),
+                   v99=float(np.quantile(speed, 0.99)), zmax=float(pos[:, 2].max()),
+                   contacts=int(st_["n_contacts"]), wall_s=round(time.time() - t0, 1))
+        if steps % (5 * a.chunk) == 0:
+            r_mid, surf, _ = surface_profile(pos, rb[order])
+            rec["R"], rec["angles"] = fit_angles(r_mid, surf)
+        log.append(rec)
+        print(json.dumps(rec), flush=True)
+        rest = rest + 1 if (rec["v99"] < 0.01 and rec["vmax"] < 0.2 and steps * s.h > 0.8) else 0
+        if rest >= 3:
+            break
+    st = g.dem_get_state()
+    o = np.argsort(st["gid"])
+    pos = st["pos"][o]
+    np.savez_compressed(out_base + "_final.npz", gid=st["gid"][o], tid=s.tid[order], pos=pos, quat=st["quat"][o],
+                        vel=st["vel"][o], omega=st["omega"][o])
+    r_mid, surf, centre = surface_profile(pos, rb[order])
+    R, angles = fit_angles(r_mid, surf)
+    vals = list(angles.values())
+    wall = time.time() - t0
+    res = dict(scene=s.name, seed=a.seed, clumps=s.n_clumps, spheres=s.n_spheres, steps=steps,
+               sim_time_s=steps * s.h, h=s.h, cd_every=k, margin_m=margin, cell_m=a.cell, gpu_wall_s=wall,
+               sphere_steps_per_s=s.n_spheres * steps / wall, at_rest=rest >= 3, pile_radius_m=R,
+               pile_centre=centre, angle_deg=float(np.median(vals)), angle_fits_deg=angles,
+               angle_spread_deg=[float(min(vals)), float(max(vals))], band_deg=BAND,
+               in_band=bool(BAND[0] <= np.median(vals) <= BAND[1]), paper_angle_deg=30.0,
+               profile=[(float(x), float(y)) for x, y in zip(r_mid, surf)], log=log)
+    json.dump(res, open(out_base + ".json", "w"), indent=1)
+    print(json.dumps({k_: v_ for k_, v_ in res.items() if k_ not in ("profile", "log")}))
+
+
+if __name__ == "__main__":
+    main()
