@@ -217,9 +217,10 @@ def run_ours(a):
                        halo=dem.halo_width(scene, drift, margin=margin), drift_max=drift,
                        transport=dem.TRANSPORT_PEER if a.transport == "peer" else dem.TRANSPORT_NCCL,
                        nccl_id=obj[0])
+    # N > 1: rank-local input (each rank is handed only the clumps of its slab; the ghost bands come
+    # from the neighbours over NCCL, dem_set_state_local)
     sys_ = dem.system_from_scene(scene, record_contacts=False, cell_size=a.cell_size, dist=dparams,
-                                 entries_per_sphere=12 if world > 1 else 0, margin=margin, cd_every=a.cd_every,
-                                 overlap=a.overlap)
+                                 margin=margin, cd_every=a.cd_every, overlap=a.overlap, local=world > 1)
     stream = sys_.stream
     if world > 1 and a.transport == "peer":
         sys_.dem_peer_link(rank, world)  # fused halo: neighbours' arrays mapped over NVLink
@@ -301,7 +302,13 @@ def run_ours(a):
     e2e = None
     if not a.no_e2e:
         pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()  # noqa: E731
-        hs = {k: pin(getattr(scene, k)) for k in ("gid", "tid", "pos", "quat", "vel", "omega")}
+        keys = ("gid", "tid", "pos", "quat", "vel", "omega")
+        if world > 1:  # rank-local: this rank's own clumps only (the ghosts come from the neighbours)
+            x = scene.pos[:, 0]
+            sel = np.nonzero((x >= dparams["slab_lo"]) & (x < dparams["slab_hi"]))[0]
+            hs = {k: pin(getattr(scene, k)[sel]) for k in keys}
+        else:
+            hs = {k: pin(getattr(scene, k)) for k in keys}
         h2d = sum(v.nbytes for v in hs.values())
         ho = {k: pin(np.zeros_like(v)) for k, v in hs.items()}  # pinned result buffers
         ctl_bytes = 72  # the status word (struct Ctl) dem_step reads back after every call
@@ -309,7 +316,10 @@ def run_ours(a):
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        sys_.dem_set_state(hs["gid"], hs["tid"], hs["pos"], hs["quat"], hs["vel"], hs["omega"])
+        if world > 1:
+            sys_.dem_set_state_local(hs["gid"], hs["tid"], hs["pos"], hs["quat"], hs["vel"], hs["omega"])
+        else:
+            sys_.dem_set_state(hs["gid"], hs["tid"], hs["pos"], hs["quat"], hs["vel"], hs["omega"])
         for _ in range(a.steps):
             sys_.dem_step(1)
         out = sys_.dem_get_state(out=ho)

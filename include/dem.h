@@ -109,17 +109,21 @@ typedef struct {
                                 misaligned block fails the call that allocates it */
   dem_free_fn free;
   void* alloc_ctx;
-  double entries_per_sphere; /* initial contact-row capacity per sphere (0 = 8); distributed systems
-                                cannot regrow mid-run (ranks would desynchronise): size it generously */
+  double entries_per_sphere; /* initial contact-row capacity per sphere (0 = 8); grown on overflow.  A
+                                distributed rank regrows together with all ranks (the abort word is
+                                all-reduced before each rebuild step's force kernel, so every rank
+                                re-runs the same steps); that needs the NCCL communicator or a loopback
+                                group — a PEER rank without one returns DEM_ERR_CAPACITY instead */
   /* ---- spatial slab decomposition along x.  n_ranks <= 1: one system owns all. ----
-   * dem_set_state then takes the GLOBAL state on every rank; the rank owns the clumps whose COM x
+   * dem_set_state then takes any superset of the held clumps (e.g. the global state); the rank owns the clumps whose COM x
    * is in [slab_lo, slab_hi) and keeps ghost copies of the clumps within `halo` beyond each face
    * (owned by the neighbouring ranks rank-1 / rank+1, so halo must not exceed a neighbour's slab
    * width).  Every step the owners' new ghost states are exchanged; contacts are evaluated by the
    * owner of each sphere (mirror-exact, so no force exchange), and owned states are bitwise
    * independent of the number of ranks.  halo >= 2 R_bound,max + margin + 2 drift_max; an owned
    * COM that moves more than drift_max from its dem_set_state position raises
-   * DEM_ERR_REPARTITION (re-call dem_set_state with the gathered global state to migrate). */
+   * DEM_ERR_REPARTITION (call dem_migrate, or dem_set_state again).  dem_set_state_local takes
+   * rank-local input instead (each rank only its own clumps; ghosts come from the neighbours). */
   int32_t rank, n_ranks;
   double slab_lo, slab_hi, halo, drift_max;
   int32_t transport;         /* DEM_TRANSPORT_NCCL, _PEER, _LOOPBACK or _LOOPBACK_PEER (below) */
@@ -156,6 +160,10 @@ typedef struct {
   int64_t regrows;           /* capacity regrows so far */
   int64_t kernel_launches_per_step;
   int64_t state_fast_resets;  /* dem_set_state calls that took the same-clumps fast path */
+  int64_t migrated_clumps;    /* distributed: owned clumps this rank sent to a neighbour in the last migration */
+  int64_t migration_bytes;    /* ... and the bytes of those clumps and of the contacts routed with them */
+  int64_t ghost_exchange_bytes; /* bytes this rank sent to complete its neighbours' ghost bands (last
+                                   dem_set_state_local / migration) */
 } dem_stats;
 
 typedef struct dem_system dem_system;
@@ -274,21 +282,54 @@ dem_status dem_get_mesh(dem_system* sys, int32_t mesh, double pos[3], double qua
 dem_status dem_peer_export(dem_system* sys, int64_t cap, void* out, int64_t* len);
 dem_status dem_peer_import(dem_system* sys, const void* left, const void* right);
 
-/* Clump migration between slabs.  Collective over the n_ranks systems of an
- * NCCL decomposition (every rank calls it at the same point, between dem_step calls).  The
- * largest displacement of an owned COM since the last dem_set_state is reduced over the ranks
- * (device reduction + ncclAllReduce MAX); if it exceeds `threshold` [m] (use a fraction of
- * drift_max, e.g. drift_max / 2; 0 forces a migration), every rank's owned states and canonical
- * contact histories (keys + u_t) are all-gathered over NCCL (counts, then payloads) and every
- * rank re-partitions the gathered global state by COM x (dem_set_state semantics) and imports
- * the gathered history (dem_set_contact_history), so clumps that crossed a face move to their new
- * owner with their tangential history and the ghost bands are rebuilt around the new positions.
- * The trajectory is unchanged: owned states are bitwise independent of the decomposition.
- * *moved (optional) receives 1 if a migration happened.  Non-distributed systems: no-op. */
+/* Clump migration between slabs, neighbour-only.  Collective over the n_ranks
+ * systems of an NCCL decomposition (every rank calls it at the same point, between dem_step
+ * calls).  The largest displacement of an owned COM since the last partition is reduced over the
+ * ranks (device reduction + ncclAllReduce MAX); if it exceeds `threshold` [m] (use a fraction of
+ * drift_max, e.g. drift_max / 2; 0 forces a migration):
+ *   1. every rank sends to each neighbour (grouped ncclSend/ncclRecv: counts, then payloads) only
+ *      the owned clumps whose COM crossed into that neighbour's slab, with the directed contact-row
+ *      entries of their spheres (partner key + u_t, the history a sphere's owner keeps;
+ *      dem_migration_plan);
+ *   2. the new owned sets exchange their ghost bands with the neighbours (dem_set_state_local);
+ *   3. every rank lays out its own clumps again and re-imports the entries of its spheres.
+ * Bytes moved scale with the crossings and the ghost band, never with the whole system
+ * (dem_stats.migration_bytes / ghost_exchange_bytes).  The trajectory is unchanged: owned states
+ * are bitwise independent of the decomposition.  *moved (optional) receives 1 if a migration
+ * happened.  Non-distributed systems: no-op. */
 dem_status dem_migrate(dem_system* sys, double threshold, int32_t* moved);
 
-/* dem_migrate for a LOOPBACK group (ranks 0..n-1 in order, as dem_step_group); host gather. */
+/* dem_migrate for a LOOPBACK group (ranks 0..n-1 in order, as dem_step_group): the same
+ * neighbour-only plan, the payloads handed between the systems in host memory. */
 dem_status dem_migrate_group(dem_system* const* systems, int32_t n, double threshold, int32_t* moved);
+
+/* The migration plan as every rank computes it (host only, no GPU).  For the n clumps a rank
+ * holds (gid, COM x in pos[3c], role[c] 1 owned / 2 ghost from the left / 3 ghost from the right,
+ * as dem_partition_plan gives), dest[c] = the clump's owner after the move relative to this rank:
+ * -1 left neighbour, 0 this rank, +1 right neighbour (an owned COM below slab_lo goes left, at or
+ * above slab_hi right; a ghost becomes ours once its COM is inside our slab).  For the rank's
+ * n_entries directed contact-row entries (the history each rank keeps for its own spheres; own
+ * sphere key = gid * 64 + component), route[k] = dest of the own sphere's clump: an entry moves
+ * with its sphere.  Returns DEM_ERR_INVALID_ARG if a role is 0 or an entry's clump is not held. */
+dem_status dem_migration_plan(int64_t n, const int64_t* gid, const double* pos, const int8_t* role,
+                              double slab_lo, double slab_hi, int32_t has_left, int32_t has_right, int8_t* dest,
+                              int64_t n_entries, const int64_t* own_key, int8_t* route);
+
+/* Rank-local state input of a distributed system (collective over an NCCL decomposition, like
+ * dem_migrate): the caller passes any set of clumps (host arrays, dem_set_state layout); the rank
+ * keeps those whose COM x lies in [slab_lo, slab_hi) — every clump must be given to the rank that
+ * owns it — and receives its ghost bands from the neighbours' owned clumps (grouped
+ * ncclSend/ncclRecv, counts then payloads), then lays out owned + ghosts as dem_set_state does.
+ * No rank ever needs the global state.  Non-distributed systems: dem_set_state. */
+dem_status dem_set_state_local(dem_system* sys, int64_t n, const int64_t* gid, const int32_t* tid,
+                               const double* pos, const double* quat, const double* vel, const double* omega);
+
+/* dem_set_state_local for a LOOPBACK group: rank r's input is n_in[r] clumps in gid[r], tid[r],
+ * pos[r], ... (host arrays). */
+dem_status dem_set_state_local_group(dem_system* const* systems, int32_t n, const int64_t* n_in,
+                                     const int64_t* const* gid, const int32_t* const* tid,
+                                     const double* const* pos, const double* const* quat,
+                                     const double* const* vel, const double* const* omega);
 
 const char* dem_status_string(dem_status s);
 dem_status dem_last_error(const dem_system* sys, char* buf, size_t len);

@@ -5,5 +5,5 @@ include/dem.h); `binding` marshals arguments and provides PyTorch's allocator an
 """
 from .binding import (DEM_STATUS, EXPORTS, LIB_PATH, STAGES, TRANSPORT_LOOPBACK, TRANSPORT_LOOPBACK_PEER,  # noqa: F401
                       TRANSPORT_NCCL, TRANSPORT_PEER,
-                      DemError, System, halo_width, load_library, migrate_group, nccl_unique_id, partition_plan,
-                      slab_bounds, step_group, system_from_scene)
+                      DemError, System, halo_width, load_library, migrate_group, migration_plan, nccl_unique_id,
+                      partition_plan, set_state_local_group, slab_bounds, step_group, system_from_scene)

@@ -57,7 +57,8 @@ class dem_stats(C.Structure):
                 ("n_owned_clumps", C.c_int64), ("n_owned_spheres", C.c_int64), ("n_ghost_clumps", C.c_int64),
                 ("n_entries", C.c_int64), ("n_contacts", C.c_int64), ("n_inserts", C.c_int64), ("n_cells", C.c_int64),
                 ("cell_size", C.c_double), ("regrows", C.c_int64), ("kernel_launches_per_step", C.c_int64),
-                ("state_fast_resets", C.c_int64)]
+                ("state_fast_resets", C.c_int64), ("migrated_clumps", C.c_int64), ("migration_bytes", C.c_int64),
+                ("ghost_exchange_bytes", C.c_int64)]
 
 
 TRANSPORT_NCCL, TRANSPORT_LOOPBACK, TRANSPORT_PEER, TRANSPORT_LOOPBACK_PEER = 0, 1, 2, 3
@@ -66,7 +67,8 @@ EXPORTS = ["dem_create", "dem_set_state", "dem_set_contact_history", "dem_step",
            "dem_get_state", "dem_get_contacts", "dem_get_stats", "dem_set_profiling", "dem_get_stage_times",
            "dem_status_string", "dem_last_error", "dem_destroy", "dem_nccl_unique_id", "dem_partition_plan",
            "dem_step_group", "dem_migrate", "dem_migrate_group", "dem_add_mesh", "dem_set_mesh_motion",
-           "dem_get_mesh", "dem_peer_export", "dem_peer_import"]
+           "dem_get_mesh", "dem_peer_export", "dem_peer_import", "dem_migration_plan", "dem_set_state_local",
+           "dem_set_state_local_group"]
 
 _lib = None
 
@@ -105,6 +107,9 @@ def load_library(path: str = LIB_PATH):
     L.dem_get_mesh.argtypes = [P, I32, P, P, P, P]
     L.dem_peer_export.argtypes = [P, I64, P, C.POINTER(I64)]
     L.dem_peer_import.argtypes = [P, P, P]
+    L.dem_migration_plan.argtypes = [I64, P, P, P, C.c_double, C.c_double, I32, I32, P, I64, P, P]
+    L.dem_set_state_local.argtypes = [P, I64, P, P, P, P, P, P]
+    L.dem_set_state_local_group.argtypes = [P, I32, P, P, P, P, P, P, P]
     for f in EXPORTS:
         if f not in ("dem_destroy", "dem_status_string"):
             getattr(L, f).restype = C.c_int
@@ -195,6 +200,7 @@ class System:
             self._alloc_cb, self._free_cb = ALLOC_FN(_alloc), FREE_FN(_free)
             p.alloc, p.free = self._alloc_cb, self._free_cb
         self.record = record_contacts
+        self.params = p  # (read back by callers: slab bounds of a distributed rank)
         self.sys = C.c_void_p()
         rc = L.dem_create(C.byref(p), mats, len(materials), tpls, len(templates), pls, len(planes),
                           C.c_void_p(self.stream.cuda_stream), C.byref(self.sys))
@@ -229,6 +235,19 @@ class System:
         self.n = gid.shape[0]
         self._check(load_library().dem_set_state(self.sys, self.n, _ptr(gid), _ptr(tid), *[_ptr(a) for a in arr], 0),
                     "dem_set_state")
+
+    def dem_set_state_local(self, gid, tid, pos, quat, vel, omega):
+        """Distributed, collective (NCCL ranks): rank-local input — the clumps whose COM lies in this
+        rank's slab are kept (give each clump to its owner), the ghost bands come from the neighbours."""
+        gid = np.ascontiguousarray(gid, np.int64)
+        tid = np.ascontiguousarray(tid, np.int32)
+        arr = [_f64(pos), _f64(quat), _f64(vel), _f64(omega)]
+        fast0 = self.dem_get_stats()["state_fast_resets"]
+        self._check(load_library().dem_set_state_local(self.sys, gid.shape[0], _ptr(gid), _ptr(tid),
+                                                       *[_ptr(a) for a in arr]), "dem_set_state_local")
+        # a re-layout (not the same-clumps fast path) replaced the IPC-exported arrays: re-link
+        if getattr(self, "_peer", None) and self.dem_get_stats()["state_fast_resets"] == fast0:
+            self.dem_peer_link(*self._peer)
 
     def dem_set_state_device(self, gid, tid, pos, quat, vel, omega):
         """torch CUDA tensors (int64, int32, float64 x4), contiguous."""
@@ -356,8 +375,10 @@ class System:
         return dict(zip(STAGES, ms.tolist()))
 
 
-def system_from_scene(scene, record_contacts=False, cell_size=None, margin=None, **kw) -> System:
-    """Build a System from a workloads.Scene-like object (duck-typed; no import of workloads)."""
+def system_from_scene(scene, record_contacts=False, cell_size=None, margin=None, local=False, **kw) -> System:
+    """Build a System from a workloads.Scene-like object (duck-typed; no import of workloads).
+    local=True (distributed ranks with an NCCL communicator): hand the rank only the clumps of its
+    own slab (dem_set_state_local, collective); the ghost bands come from the neighbours."""
     templates = [dict(offsets=t.offsets, radius=t.radius, material=t.material, mass=t.mass, inertia=t.inertia)
                  for t in scene.templates]
     planes = [(p.point, p.normal, p.material) for p in scene.planes]
@@ -366,7 +387,13 @@ def system_from_scene(scene, record_contacts=False, cell_size=None, margin=None,
                cell_size=scene.cell_size if cell_size is None else cell_size, record_contacts=record_contacts, **kw)
     for m in getattr(scene, "meshes", []):  # kinematic triangle meshes (NEXT-3)
         s.dem_add_mesh(m.verts, m.material, m.pos, m.quat, m.vel, m.omega)
-    s.dem_set_state(scene.gid, scene.tid, scene.pos, scene.quat, scene.vel, scene.omega)
+    if local and kw.get("dist"):
+        x = scene.pos[:, 0]
+        sel = np.nonzero((x >= s.params.slab_lo) & (x < s.params.slab_hi))[0]
+        s.dem_set_state_local(scene.gid[sel], scene.tid[sel], scene.pos[sel], scene.quat[sel], scene.vel[sel],
+                              scene.omega[sel])
+    else:
+        s.dem_set_state(scene.gid, scene.tid, scene.pos, scene.quat, scene.vel, scene.omega)
     return s
 
 
@@ -436,3 +463,48 @@ def migrate_group(systems, threshold=0.0) -> bool:
                 break
         raise DemError(rc, f"dem_migrate_group: {buf.value.decode()}")
     return bool(moved.value)
+
+
+def _group_error(systems, rc, what):
+    buf = C.create_string_buffer(512)
+    for s in systems:
+        load_library().dem_last_error(s.sys, buf, 512)
+        if buf.value:
+            break
+    raise DemError(rc, f"{what}: {buf.value.decode()}")
+
+
+def set_state_local_group(systems, parts):
+    """dem_set_state_local_group: rank r of a loopback group gets parts[r] = (gid, tid, pos, quat,
+    vel, omega) — only its own clumps are needed; the ghost bands come from the neighbours."""
+    n = len(systems)
+    keep = []
+    cols = [[] for _ in range(6)]
+    for part in parts:
+        arrs = [np.ascontiguousarray(part[0], np.int64), np.ascontiguousarray(part[1], np.int32)] + \
+               [_f64(x) for x in part[2:]]
+        keep.append(arrs)
+        for k, a in enumerate(arrs):
+            cols[k].append(_ptr(a))
+    n_in = np.array([len(a[0]) for a in keep], np.int64)
+    ptrs = [(C.c_void_p * n)(*c) for c in cols]
+    arr = (C.c_void_p * n)(*[s.sys for s in systems])
+    rc = load_library().dem_set_state_local_group(arr, n, _ptr(n_in), *ptrs)
+    if rc:
+        _group_error(systems, rc, "dem_set_state_local_group")
+
+
+def migration_plan(gid, pos, role, slab_lo, slab_hi, has_left, has_right, own_key=None):
+    """Host-only migration plan of include/dem.h: (dest int8 per held clump, route int8 per directed
+    row entry, given by the key of its own sphere)."""
+    gid = np.ascontiguousarray(gid, np.int64)
+    pos = _f64(pos).reshape(-1, 3)
+    role = np.ascontiguousarray(role, np.int8)
+    ok = np.ascontiguousarray(np.zeros(0) if own_key is None else own_key, np.int64)
+    dest, route = np.zeros(len(gid), np.int8), np.zeros(len(ok), np.int8)
+    rc = load_library().dem_migration_plan(len(gid), _ptr(gid), _ptr(pos), _ptr(role), float(slab_lo), float(slab_hi),
+                                           int(bool(has_left)), int(bool(has_right)), _ptr(dest), len(ok), _ptr(ok),
+                                           _ptr(route))
+    if rc:
+        raise DemError(rc, "dem_migration_plan")
+    return dest, route

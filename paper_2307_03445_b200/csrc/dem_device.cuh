@@ -369,4 +369,11 @@ __device__ __forceinline__ bool tri_has(const int* vid, int t, int x) {
   return vid[3 * t] == x || vid[3 * t + 1] == x || vid[3 * t + 2] == x;
 }
 
+// the abort words of a loopback group (k_abort_or)
+constexpr int kMaxGroup = 64;
+struct AbortWords {
+  int* p[kMaxGroup];
+  int n;
+};
+
 }  // namespace dem

@@ -430,10 +430,63 @@ struct PairBlocks {
   }
 };
 
+// Row descriptors of the flat path (DEM_PAIRS_ROWDEC).  In the member order of kGroupPos every
+// member that owns pairs owns ONE contiguous range of partners:  a group-7 member at slot l pairs
+// with slots (l, m);  a group-6 member with the groups {1, 5, 3} = slots [s1, s2);  a group-5
+// member with {3, 2} = [s3, s4);  a group-3 member with group 4 = [s4, s4 + n4).  Enumerating
+// the owners' rows one after another numbers the bin's pairs p = 0 .. total - 1; owner o (the
+// o-th member with a non-empty row) starts at off_o, whose bit is set in a per-warp bitmap.  In a
+// pass over p = base .. base + 31 (base a multiple of 32: one bitmap word) lane l's owner is
+//   o = (starts before base) + popc(word & lanes <= l) - 1,
+// and its partner slot is j = lo_o + (p - off_o): one shared word, one popc, one descriptor load
+// per pair instead of a block search with float reciprocals.  desc[o] = (lo_o - off_o) << 8 | slot.
+#ifndef DEM_PAIRS_ROWDEC
+#define DEM_PAIRS_ROWDEC 1
+#endif
+// group ranks from bit-plane ballots instead of a 64-bit warp scan of one-hot byte counters
+#ifndef DEM_PAIRS_BALLOT
+#define DEM_PAIRS_BALLOT 0  // A/B on C5: pairs 4.86 ms vs 4.64 with the scan (more instructions, not fewer)
+#endif
+#if DEM_PAIRS_BALLOT && !DEM_PAIRS_ROWDEC
+#error "DEM_PAIRS_BALLOT needs DEM_PAIRS_ROWDEC"
+#endif
+struct RowDec {
+  unsigned bmap[kTri / 32 + 1];
+  int desc[kFlatMax];
+};
+
+// Row of the member at slot l (group-ordered): partner start lo, count cnt and offset off in the
+// bin's pair numbering (closed forms of the sums of the earlier rows).
+__device__ __forceinline__ void member_row(int l, int m, int n7, int n6, int n5, int n3, int n4, int s1, int s2,
+                                           int s3, int s4, int s5, int e0, int e1, int e2, int& lo, int& cnt,
+                                           int& off) {
+  lo = 0; cnt = 0; off = 0;
+  if (l < n7) {
+    lo = l + 1;
+    cnt = m - 1 - l;
+    off = l * (m - 1) - (l * (l - 1) >> 1);
+  } else if (l < n7 + n6) {
+    lo = s1;
+    cnt = s2 - s1;
+    off = e0 + (l - n7) * cnt;
+  } else if (l >= s5 && l < s5 + n5) {
+    lo = s3;
+    cnt = s4 - s3;
+    off = e1 + (l - s5) * cnt;
+  } else if (l >= s3 && l < s3 + n3) {
+    lo = s4;
+    cnt = n4;
+    off = e2 + (l - s3) * cnt;
+  }
+}
+
 template <bool kGhosts, bool kMargin>
 __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepArgs a) {
   __shared__ Members smA[kPairWarps];
   __shared__ int2 sbuf[kPairWarps][kPairBuf];
+#if DEM_PAIRS_ROWDEC
+  __shared__ RowDec smR[kPairWarps];
+#else
   __shared__ unsigned short tri_ij[kTri];  // p -> i | j << 8 for p = j (j - 1) / 2 + i, i < j
   for (int p = threadIdx.x; p < kTri; p += blockDim.x) {
     int i, j;
@@ -441,6 +494,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
     tri_ij[p] = (unsigned short)(i | (j << 8));
   }
   __syncthreads();
+#endif
   if (*a.abort || a.ctl->abort) return;  // (an error in the steps running beside an ahead detection)
   if ((long long)a.cell_start[a.ncell] > a.cap_inserts) {
     a.ctl->need_inserts = a.cell_start[a.ncell];
@@ -513,14 +567,18 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
         double4 u0 = make_double4(0.0, 0.0, 0.0, 0.0), u1 = u0;
         int2 mt0 = make_int2(0, 0), mt1 = mt0;
         int pos0 = 0, pos1 = 0;
+#if !DEM_PAIRS_BALLOT
         unsigned long long v0 = 0, v1 = 0;
+#endif
         if (lane < m) {
           const int it = curA;
           const int idx = it & 0x1fffffff;
           u0 = ldg256(a.dpos + idx);
           mt0 = make_int2(a.s_clump[idx], idx);
           pos0 = (kGroupPos >> (4 * ((unsigned)it >> 29))) & 7;
+#if !DEM_PAIRS_BALLOT
           v0 = 1ull << (8 * pos0);
+#endif
         }
         if (lane + 32 < m) {
           const int it = curB;
@@ -528,8 +586,54 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
           u1 = ldg256(a.dpos + idx);
           mt1 = make_int2(a.s_clump[idx], idx);
           pos1 = (kGroupPos >> (4 * ((unsigned)it >> 29))) & 7;
+#if !DEM_PAIRS_BALLOT
           v1 = 1ull << (8 * pos1);
+#endif
         }
+#if DEM_PAIRS_BALLOT
+        // Group order by bit-plane ballots: A_k (B_k) = lanes of the first (second) member half
+        // whose position has bit k set.  The size of position p is the popcount of the lanes whose
+        // three planes match p; a member's slot = (members at lower positions) + (members at its
+        // position before it: first half before second half, then by lane).
+        const unsigned lt = (1u << lane) - 1u;
+        const unsigned V0 = m >= 32 ? 0xffffffffu : (1u << m) - 1u;
+        const unsigned V1 = m >= 64 ? 0xffffffffu : (m > 32 ? (1u << (m - 32)) - 1u : 0u);
+        const unsigned A0 = __ballot_sync(0xffffffffu, pos0 & 1) & V0, A1 = __ballot_sync(0xffffffffu, pos0 & 2) & V0,
+                       A2 = __ballot_sync(0xffffffffu, pos0 & 4) & V0;
+        unsigned B0 = 0u, B1 = 0u, B2 = 0u;
+        if (m > 32) {  // warp-uniform
+          B0 = __ballot_sync(0xffffffffu, pos1 & 1) & V1;
+          B1 = __ballot_sync(0xffffffffu, pos1 & 2) & V1;
+          B2 = __ballot_sync(0xffffffffu, pos1 & 4) & V1;
+        }
+        // lanes of a half at exactly position p / at a position below p (bit-sliced comparison)
+        auto at = [](unsigned V, unsigned X0, unsigned X1, unsigned X2, int p) {
+          return V & ((p & 1) ? X0 : ~X0) & ((p & 2) ? X1 : ~X1) & ((p & 4) ? X2 : ~X2);
+        };
+        auto below = [](unsigned V, unsigned X0, unsigned X1, unsigned X2, int p) {
+          const unsigned P0 = (p & 1) ? ~0u : 0u, P1 = (p & 2) ? ~0u : 0u, P2 = (p & 4) ? ~0u : 0u;
+          const unsigned e2 = ~(X2 ^ P2), e1 = ~(X1 ^ P1);
+          return V & ((~X2 & P2) | (e2 & ~X1 & P1) | (e2 & e1 & ~X0 & P0));
+        };
+        int nk[7];
+#pragma unroll
+        for (int k = 0; k < 7; ++k) nk[k] = __popc(at(V0, A0, A1, A2, k)) + __popc(at(V1, B0, B1, B2, k));
+        const int n7 = nk[0], n6 = nk[1], n5 = nk[3], n3 = nk[4], n4 = nk[6];
+        const int s1 = n7 + n6, s5 = s1 + nk[2], s3 = s5 + n5, s2 = s3 + n3, s4 = s2 + nk[5];
+        __syncwarp();
+        if (lane < m) {
+          const int q = __popc(below(V0, A0, A1, A2, pos0)) + __popc(below(V1, B0, B1, B2, pos0)) +
+                        __popc(at(V0, A0, A1, A2, pos0) & lt);
+          A.put(q, u0);
+          A.meta_put(q, mt0);
+        }
+        if (lane + 32 < m) {
+          const int q = __popc(below(V0, A0, A1, A2, pos1)) + __popc(below(V1, B0, B1, B2, pos1)) +
+                        __popc(at(V0, A0, A1, A2, pos1)) + __popc(at(V1, B0, B1, B2, pos1) & lt);
+          A.put(q, u1);
+          A.meta_put(q, mt1);
+        }
+#else
         const unsigned long long x0 = warp_incl_scan64(v0, lane);
         const unsigned long long t0 = __shfl_sync(0xffffffffu, x0, 31);
         unsigned long long x1 = 0, t1 = 0;
@@ -550,6 +654,57 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
           A.put(q, u1);
           A.meta_put(q, mt1);
         }
+#endif
+#if DEM_PAIRS_ROWDEC
+        {
+          RowDec& D = smR[w];
+#if !DEM_PAIRS_BALLOT
+          const int n7 = byte_of(tot, 0), n6 = byte_of(tot, 1), n5 = byte_of(tot, 3), n3 = byte_of(tot, 4);
+          const int n4 = byte_of(tot, 6);
+          const int s1 = byte_of(st, 2), s5 = byte_of(st, 3), s3 = byte_of(st, 4), s2 = byte_of(st, 5);
+          const int s4 = byte_of(st, 6);
+#endif
+          const int e0 = n7 * (m - 1) - ((n7 * (n7 - 1)) >> 1);
+          const int e1 = e0 + n6 * (s2 - s1);
+          const int e2 = e1 + n5 * (s4 - s3);
+          const int total = e2 + n3 * n4;
+          int lo0, c0, o0, lo1 = 0, c1 = 0, o1 = 0;
+          member_row(lane, m, n7, n6, n5, n3, n4, s1, s2, s3, s4, s5, e0, e1, e2, lo0, c0, o0);
+          if (m > 32) member_row(lane + 32, m, n7, n6, n5, n3, n4, s1, s2, s3, s4, s5, e0, e1, e2, lo1, c1, o1);
+          // bitmap words of this bin's numbering cleared, then one start bit per non-empty row
+          const int nw = (total + 31) >> 5;
+          if (lane < nw) D.bmap[lane] = 0u;
+          if (lane + 32 < nw) D.bmap[lane + 32] = 0u;
+#if !DEM_PAIRS_BALLOT
+          const unsigned lt = (1u << lane) - 1u;
+#endif
+          const unsigned b0 = __ballot_sync(0xffffffffu, c0 > 0), b1 = __ballot_sync(0xffffffffu, c1 > 0);
+          __syncwarp();
+          if (c0 > 0) {
+            D.desc[__popc(b0 & lt)] = ((lo0 - o0) << 8) | lane;
+            atomicOr(&D.bmap[o0 >> 5], 1u << (o0 & 31));
+          }
+          if (c1 > 0) {
+            D.desc[__popc(b0) + __popc(b1 & lt)] = ((lo1 - o1) << 8) | (lane + 32);
+            atomicOr(&D.bmap[o1 >> 5], 1u << (o1 & 31));
+          }
+          __syncwarp();
+          const unsigned le = lt | (1u << lane);
+          int before = 0;  // row starts below base (warp-uniform)
+          for (int base = 0; base < total; base += 32) {
+            const unsigned word = D.bmap[base >> 5];
+            const int p = base + lane;
+            bool hit = false;
+            int ia = 0, ib = 0;
+            if (p < total) {
+              const int d = D.desc[before + __popc(word & le) - 1];
+              hit = flat_pair<kGhosts, kMargin>(a, A, d & 0xff, p + (d >> 8), ia, ib);
+            }
+            before += __popc(word);
+            push_hits(a, bf, nbuf, hit, ia, ib, lane);
+          }
+        }
+#else
         __syncwarp();
         const PairBlocks B(tot, st, m);
         for (int base = 0; base < B.total; base += 32) {
@@ -563,6 +718,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
           }
           push_hits(a, bf, nbuf, hit, ia, ib, lane);
         }
+#endif
       } else {
         // Large bins (m > kFlatMax): blocks of 32 members in the two halves of the shared slots,
         // every pair of the bin tested (the group filter applied per pair).

@@ -30,7 +30,7 @@ constexpr int kPairStride = 8;  // doubles per material pair in Tables::pair
 #define DEM_FORCE_OWNER 1  // owner sphere of each entry from a shared table (else a binary search)
 #endif
 #ifndef DEM_FORCE_ASYNC_EPI
-#define DEM_FORCE_ASYNC_EPI 0  // 1: own clumps' q, Omega, inertia staged by cp.async in the prologue
+#define DEM_FORCE_ASYNC_EPI 0  // 1: own clumps' q, Omega, inertia staged by cp.async in the prologue (A/B: 3.96 -> 4.73 ms)
 #endif
 #ifndef DEM_FORCE_FT
 #define DEM_FORCE_FT 128
@@ -120,14 +120,16 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
   const int c0 = b0.x, c1 = b1.x;
   const int ncl = c1 - c0;
   if (a.ctl->abort) {
-    // capacity abort / error: carry the state forward unchanged so the ping-pong stays valid
-    if (tid < ncl) {
-      const int c = c0 + tid;
+    // capacity abort / error: carry the state forward unchanged so the ping-pong stays valid —
+    // the ghosts too (a distributed abort is agreed by every rank, so no neighbour stores them)
+    auto carry = [&](int c) {
       a.nxt.x[c] = a.cur.x[c]; a.nxt.y[c] = a.cur.y[c]; a.nxt.z[c] = a.cur.z[c];
       a.nxt.qw[c] = a.cur.qw[c]; a.nxt.qx[c] = a.cur.qx[c]; a.nxt.qy[c] = a.cur.qy[c]; a.nxt.qz[c] = a.cur.qz[c];
       a.nxt.vx[c] = a.cur.vx[c]; a.nxt.vy[c] = a.cur.vy[c]; a.nxt.vz[c] = a.cur.vz[c];
       a.nxt.wx[c] = a.cur.wx[c]; a.nxt.wy[c] = a.cur.wy[c]; a.nxt.wz[c] = a.cur.wz[c];
-    }
+    };
+    if (tid < ncl) carry(c0 + tid);
+    for (int c = a.n_own + blockIdx.x * kFT + tid; c < a.n; c += gridDim.x * kFT) carry(c);
     return;
   }
   if (blockIdx.x == 0 && tid == 0) a.ctl->step += 1;  // no other thread of this launch reads it
@@ -407,9 +409,17 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
     for (int ls = tid; ls < nsph; ls += kFT) {
       const int r0 = rp[ls], r1 = rp[ls + 1];
       const int b = max(r0, c0e), en = min(r1, c0e + kFT);
-      for (int q = b - c0e; q < en - c0e; ++q) {
+      if (b < en) {
+        // the running sums in registers across the sphere's entries of this chunk (same order)
+        double sum[6];
 #pragma unroll
-        for (int d = 0; d < 6; ++d) acc[d][ls] += part[d][q];
+        for (int d = 0; d < 6; ++d) sum[d] = acc[d][ls];
+        for (int q = b - c0e; q < en - c0e; ++q) {
+#pragma unroll
+          for (int d = 0; d < 6; ++d) sum[d] += part[d][q];
+        }
+#pragma unroll
+        for (int d = 0; d < 6; ++d) acc[d][ls] = sum[d];
       }
       const int nb = c0e + kFT;
       if (DEM_FORCE_OWNER)
@@ -518,8 +528,25 @@ __global__ void k_count_canonical(Rows r, const long long* __restrict__ s_key, i
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (unsigned long long)c);
 }
 
+#ifndef DEM_FORCE_CARVEOUT
+#define DEM_FORCE_CARVEOUT 0  // 1: largest shared-memory carveout — A/B on C5: force 3.96 -> 4.58 ms (less L1 for the gathers)
+#endif
+template <bool kMesh, bool kPeer>
+static void force_carveout() {
+  static bool done = false;
+  if (DEM_FORCE_CARVEOUT && !done) {
+    cudaFuncSetAttribute(k_force_integrate<kMesh, kPeer>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    done = true;
+  }
+}
+
 void launch_force_integrate(const StepArgs& a, cudaStream_t s) {
   if (a.n_cta <= 0) return;
+  force_carveout<true, true>();
+  force_carveout<true, false>();
+  force_carveout<false, true>();
+  force_carveout<false, false>();
   const bool peer = a.peer_state[0] || a.peer_state[1];
   if (a.n_tri)
     peer ? k_force_integrate<true, true><<<a.n_cta, kFT, 0, s>>>(a) : k_force_integrate<true, false><<<a.n_cta, kFT, 0, s>>>(a);
@@ -672,3 +699,18 @@ void launch_peer_wait(Ctl* ctl, const int* f0, const int* f1, cudaStream_t s) {
   if (f0 || f1) k_peer_wait<<<1, 1, 0, s>>>(ctl, f0, f1);
 }
 }  // namespace dem
+
+namespace dem {
+// loopback groups: the ranks' abort words OR-ed together before their force kernels (the
+// in-process counterpart of the distributed abort all-reduce, system.cu enqueue_abort_vote)
+__global__ void k_abort_or(AbortWords w) {
+  int any = 0;
+  for (int r = 0; r < w.n; ++r) any |= *w.p[r];
+  if (any)
+    for (int r = 0; r < w.n; ++r) *w.p[r] = 1;
+}
+void launch_abort_or(const AbortWords& w, cudaStream_t s) {
+  if (w.n > 1) k_abort_or<<<1, 1, 0, s>>>(w);
+}
+}  // namespace dem
+

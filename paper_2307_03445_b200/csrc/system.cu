@@ -36,6 +36,7 @@ void launch_max_drift(const State& st, const double* xref, int n, unsigned long 
 void launch_mesh_pose(const StepArgs&, cudaStream_t);
 void launch_peer_signal(const Ctl* ctl, int* r0, int* r1, cudaStream_t s);
 void launch_peer_wait(Ctl* ctl, const int* f0, const int* f1, cudaStream_t s);
+void launch_abort_or(const AbortWords& w, cudaStream_t s);
 void launch_state_in(const State& st, const int* perm, int n, const double* pos, const double* quat,
                      const double* vel, const double* om, int* bad, double* xref, int n_own, cudaStream_t s);
 void launch_state_out(const State& st, const int* outpos, int n_own, double* pos, double* quat, double* vel,
@@ -173,6 +174,7 @@ struct dem_system {
   std::vector<void*> ipc_open;                       // neighbour mappings to close
   bool peer_linked = false;
   int64_t fast_resets = 0;
+  int64_t migrated_clumps = 0, migration_bytes = 0, ghost_bytes = 0;  // last migration / ghost exchange
 };
 
 static dem_status peer_release(dem_system* sys);
@@ -447,9 +449,18 @@ static void enqueue_force(dem_system* sys, int kind, cudaStream_t s, cudaEvent_t
 
 // the whole step on one stream (sequential; an AHEAD step's detection runs in line — the same
 // results as the concurrent launch, which only changes when the kernels run)
+// A distributed rank aborts a rebuild step only together with every other rank: the abort word
+// (a capacity overflow in the detection) is all-reduced (MAX) before the force kernel, so every
+// rank carries the same steps forward and the host regrows and re-runs them on every rank alike.
+static void enqueue_abort_vote(dem_system* sys, int kind, cudaStream_t s) {
+  if (sys->dist && sys->comm && (kind == K_FULL || kind == K_ADOPT))
+    ncclAllReduce(&sys->d_ctl->abort, &sys->d_ctl->abort, 1, ncclInt32, ncclMax, sys->comm, s);
+}
+
 static void enqueue_step(dem_system* sys, int kind, cudaStream_t s, cudaEvent_t* ev, bool exchange = true) {
   enqueue_pose(sys, kind, s, ev);
   enqueue_detect(sys, kind, s, ev);
+  enqueue_abort_vote(sys, kind, s);
   enqueue_force(sys, kind, s, ev, exchange);
 }
 
@@ -1320,9 +1331,7 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
   for (int e = 0; e < 2; ++e) TRY(alloc_arr(sys, &sys->d_spos_ref[e], sys->P.cd_every > 1 ? ns : 0));
   // candidate lists: kRowWidth slots per owned sphere to start with (walls included), widened
   // on overflow (the rows of a settled bed hold a few entries)
-  // (a distributed system cannot regrow mid-run without desynchronising its neighbours: it starts
-  // with twice the width)
-  sys->row_width = sys->dist ? 2 * kRowWidth : kRowWidth;
+  sys->row_width = kRowWidth;
   TRY(alloc_arr(sys, &sys->d_slots, (size_t)sys->ns_own * sys->row_width + 1));
   // CTA partition of the fused force/integrate kernel: consecutive whole clumps, at most
   // force_cta_clumps() clumps and force_cta_spheres() spheres per CTA
@@ -1443,32 +1452,22 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
   return DEM_OK;
 }
 
-extern "C" dem_status dem_set_contact_history(dem_system* sys, int64_t n, const int64_t* key_a,
-                                              const int64_t* key_b, const double* u_t) {
-  if (!sys || n < 0 || (n && (!key_a || !key_b || !u_t))) return DEM_ERR_INVALID_ARG;
+// the history of the next step's rebuild (DEM_set_contact_history, migration): per held sphere
+// (storage index) its entries {partner key, u_t oriented own -> partner}; only owned spheres get
+// rows
+struct HistEntry {
+  long long key;
+  double u[3];
+};
+static dem_status install_history(dem_system* sys, std::vector<std::vector<HistEntry>>& per) {
   CK(cudaStreamSynchronize(sys->det_stream));  // a set detected ahead is dropped
-  std::unordered_map<long long, int> idx;
-  idx.reserve((size_t)sys->ns * 2);
-  for (int64_t s = 0; s < sys->ns_own; ++s) idx[sys->h_s_key[s]] = (int)s;  // owned spheres only
-  struct E {
-    long long key;
-    double u[3];
-  };
-  std::vector<std::vector<E>> per(sys->ns);
-  for (int64_t r = 0; r < n; ++r) {
-    if (!(key_a[r] < key_b[r])) return DEM_ERR_INVALID_ARG;
-    auto ia = idx.find(key_a[r]);
-    if (ia != idx.end()) per[ia->second].push_back(E{key_b[r], {u_t[3 * r], u_t[3 * r + 1], u_t[3 * r + 2]}});
-    auto ib = idx.find(key_b[r]);
-    if (ib != idx.end()) per[ib->second].push_back(E{key_a[r], {-u_t[3 * r], -u_t[3 * r + 1], -u_t[3 * r + 2]}});
-  }
   std::vector<int> rp(sys->ns + 1, 0);
   std::vector<Entry> ents;
   std::vector<long long> keys;
   std::vector<double> ut;
   for (int64_t s = 0; s < sys->ns; ++s) {
     auto& v = per[s];
-    std::sort(v.begin(), v.end(), [](const E& x, const E& y) { return x.key < y.key; });
+    std::sort(v.begin(), v.end(), [](const HistEntry& x, const HistEntry& y) { return x.key < y.key; });
     for (auto& e : v) {
       Entry en;
       en.partner = -1;  // only the key and u_t of the previous rows are read
@@ -1494,6 +1493,23 @@ extern "C" dem_status dem_set_contact_history(dem_system* sys, int64_t n, const 
   sys->since_rebuild = 0;
   sys->pending = false;
   return DEM_OK;
+}
+
+extern "C" dem_status dem_set_contact_history(dem_system* sys, int64_t n, const int64_t* key_a,
+                                              const int64_t* key_b, const double* u_t) {
+  if (!sys || n < 0 || (n && (!key_a || !key_b || !u_t))) return DEM_ERR_INVALID_ARG;
+  std::unordered_map<long long, int> idx;
+  idx.reserve((size_t)sys->ns * 2);
+  for (int64_t s = 0; s < sys->ns_own; ++s) idx[sys->h_s_key[s]] = (int)s;  // owned spheres only
+  std::vector<std::vector<HistEntry>> per(sys->ns);
+  for (int64_t r = 0; r < n; ++r) {
+    if (!(key_a[r] < key_b[r])) return DEM_ERR_INVALID_ARG;
+    auto ia = idx.find(key_a[r]);
+    if (ia != idx.end()) per[ia->second].push_back(HistEntry{key_b[r], {u_t[3 * r], u_t[3 * r + 1], u_t[3 * r + 2]}});
+    auto ib = idx.find(key_b[r]);
+    if (ib != idx.end()) per[ib->second].push_back(HistEntry{key_a[r], {-u_t[3 * r], -u_t[3 * r + 1], -u_t[3 * r + 2]}});
+  }
+  return install_history(sys, per);
 }
 
 // ------------------------------------------------------------------ stepping
@@ -1627,6 +1643,46 @@ static dem_status check_mesh_motion(dem_system* sys) {
   return DEM_OK;
 }
 
+// Capacity regrow after an abort: the parities of the aborted step are restored, the capacities
+// that overflowed grow, the graphs are dropped, the status word is cleared.
+static dem_status regrow(dem_system* sys, int up, int ep, int since, int kind, bool pending) {
+  CK(cudaStreamSynchronize(sys->det_stream));
+  if (std::getenv("DEM_DEBUG_LOG"))
+    std::fprintf(stderr, "dem: regrow (kind %d, pending %d): need entries %lld inserts %lld width %lld det_abort %d\n",
+                 kind, (int)pending, sys->h_ctl->need_entries, sys->h_ctl->need_inserts, sys->h_ctl->need_width,
+                 sys->h_ctl->det_abort);
+  sys->up = up;
+  sys->ep = ep;
+  sys->since_rebuild = since;
+  sys->pending = false;
+  sys->h_ctl->det_abort = 0;
+  bool grew = false;  // (a distributed rank also re-runs when only another rank overflowed)
+  if (sys->h_ctl->need_entries > sys->cap_entries) {
+    long long need = sys->h_ctl->need_entries;
+    TRY(alloc_rows(sys, need + need / 4 + 1024));
+    grew = true;
+  }
+  if (sys->h_ctl->need_inserts > sys->cap_inserts) {
+    long long need = sys->h_ctl->need_inserts;
+    sys->cap_inserts = need + need / 4 + 1024;
+    TRY(alloc_arr(sys, &sys->d_items, sys->cap_inserts));
+    grew = true;
+  }
+  if (sys->h_ctl->need_width > sys->row_width) {
+    sys->row_width = (int)std::min<long long>(sys->h_ctl->need_width + 8, 1 << 16);
+    TRY(alloc_arr(sys, &sys->d_slots, (size_t)sys->ns_own * sys->row_width + 1));
+    grew = true;
+  }
+  if (grew) sys->regrows++;
+  free_graphs(sys);
+  sys->h_ctl->abort = 0;
+  sys->h_ctl->need_entries = 0;
+  sys->h_ctl->need_inserts = 0;
+  sys->h_ctl->need_width = 0;
+  CK(cudaMemcpyAsync(sys->d_ctl, sys->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, sys->stream));
+  return DEM_OK;
+}
+
 extern "C" dem_status dem_step(dem_system* sys, int64_t n_steps) {
   if (!sys || n_steps < 0) return DEM_ERR_INVALID_ARG;
   if (sys->peer && sys->P.transport == DEM_TRANSPORT_PEER && !sys->peer_linked) {
@@ -1696,50 +1752,24 @@ extern "C" dem_status dem_step(dem_system* sys, int64_t n_steps) {
     if (sys->h_ctl->err_code) return device_error(sys);
     remaining -= done;
     if (!sys->h_ctl->abort) break;
-    if (sys->dist) {  // a local regrow would desynchronise the ranks' halo exchanges
-      sys->err = "capacity overflow on a distributed system (raise params.entries_per_sphere)";
+    if (sys->dist && !sys->comm) {  // a local regrow would desynchronise the ranks' halo exchanges
+      sys->err = "capacity overflow on a distributed system without an NCCL communicator (raise params.entries_per_sphere)";
       return DEM_ERR_CAPACITY;
     }
     // capacity abort in step `done` (a FULL step, or an ADOPT step whose set detected ahead
     // overflowed): the state was carried forward through the aborted steps (sp is already
     // right); the latest valid u_t and entry set are those that step read.  Regrow and re-run
     // from there — an aborted adoption as a FULL rebuild at that step, which gives the same
-    // trajectory (every contact with delta > 0 is in both sets).
+    // trajectory (every contact with delta > 0 is in both sets).  A distributed
+    // rank gets here together with every other rank: the abort word is all-reduced before the
+    // force kernel of each rebuild step, so all ranks carried the same steps forward.
     if (++guard > 8) {
       sys->err = "capacity regrow did not converge";
       return DEM_ERR_CAPACITY;
     }
-    CK(cudaStreamSynchronize(sys->det_stream));
-    if (std::getenv("DEM_DEBUG_LOG"))
-      std::fprintf(stderr, "dem: regrow at step %lld (kind %d, pending %d): need entries %lld inserts %lld width %lld det_abort %d\n",
-                   (long long)done, sched[(size_t)done].since == 0 ? (sched[(size_t)done].pending ? K_ADOPT : K_FULL) : -1,
-                   (int)sched[(size_t)done].pending, sys->h_ctl->need_entries, sys->h_ctl->need_inserts,
-                   sys->h_ctl->need_width, sys->h_ctl->det_abort);
-    sys->regrows++;
-    sys->up = sched[(size_t)done].up;
-    sys->ep = sched[(size_t)done].ep;
-    sys->since_rebuild = sched[(size_t)done].since;
-    sys->pending = false;
-    sys->h_ctl->det_abort = 0;
-    if (sys->h_ctl->need_entries > sys->cap_entries) {
-      long long need = sys->h_ctl->need_entries;
-      TRY(alloc_rows(sys, need + need / 4 + 1024));
-    }
-    if (sys->h_ctl->need_inserts > sys->cap_inserts) {
-      long long need = sys->h_ctl->need_inserts;
-      sys->cap_inserts = need + need / 4 + 1024;
-      TRY(alloc_arr(sys, &sys->d_items, sys->cap_inserts));
-    }
-    if (sys->h_ctl->need_width > sys->row_width) {
-      sys->row_width = (int)std::min<long long>(sys->h_ctl->need_width + 8, 1 << 16);
-      TRY(alloc_arr(sys, &sys->d_slots, (size_t)sys->ns_own * sys->row_width + 1));
-    }
-    free_graphs(sys);
-    sys->h_ctl->abort = 0;
-    sys->h_ctl->need_entries = 0;
-    sys->h_ctl->need_inserts = 0;
-    sys->h_ctl->need_width = 0;
-    CK(cudaMemcpyAsync(sys->d_ctl, sys->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, sys->stream));
+    const Sched& at = sched[(size_t)done];
+    TRY(regrow(sys, at.up, at.ep, at.since, sched[(size_t)done].since == 0 ? (at.pending ? K_ADOPT : K_FULL) : -1,
+               at.pending));
   }
   if (sys->launched > 0) TRY(repartition_by_entries(sys));
   return DEM_OK;
@@ -1845,45 +1875,80 @@ extern "C" dem_status dem_step_group(dem_system* const* systems, int32_t n, int6
     TRY(peer_link_local(systems, n));
     for (int r = 0; r < n; ++r) systems[r]->peer_linked = true;
   }
-  for (int64_t k = 0; k < n_steps; ++k) {
-    for (int r = 0; r < n; ++r) {
-      dem_system* sys = systems[r];
-      enqueue_step(sys, step_kind(sys), s, nullptr, /*exchange=*/false);
-    }
-    if (peer) {  // the force kernels stored the ghost states into the neighbours already
-      for (int r = 0; r < n; ++r) advance_parities(systems[r], step_kind(systems[r]));
-      continue;
-    }
-    // ghost halo: rank r's left-side ghosts are rank r-1's right-side sends, and vice versa
-    for (int r = 0; r < n; ++r) {
-      dem_system* sys = systems[r];
-      if (r > 0 && sys->n_recv[0]) {
-        if (systems[r - 1]->n_send[1] != sys->n_recv[0]) return DEM_ERR_INVALID_ARG;
-        CK(cudaMemcpyAsync(sys->d_recvbuf[0], systems[r - 1]->d_sendbuf[1], sizeof(double) * kKin13 * sys->n_recv[0],
-                           cudaMemcpyDeviceToDevice, s));
+  if (n > kMaxGroup) return DEM_ERR_INVALID_ARG;
+  AbortWords aw{};
+  aw.n = n;
+  for (int r = 0; r < n; ++r) aw.p[r] = &systems[r]->d_ctl->abort;
+  struct Sched {
+    int up, ep, since;
+    bool pending;
+  };
+  std::vector<std::vector<Sched>> sched(n);
+  int64_t remaining = n_steps;
+  int guard = 0;
+  while (remaining > 0) {
+    const int64_t done_before = systems[0]->h_ctl->step;
+    for (auto& v : sched) v.clear();
+    for (int64_t k = 0; k < remaining; ++k) {
+      // every rank's poses and detection, then one abort vote, then every rank's force kernel: a
+      // capacity overflow on any rank stops the step on all of them (coordinated regrow below)
+      for (int r = 0; r < n; ++r) {
+        dem_system* sys = systems[r];
+        sched[r].push_back(Sched{sys->up, sys->ep, sys->since_rebuild, sys->pending});
+        enqueue_pose(sys, step_kind(sys), s, nullptr);
+        enqueue_detect(sys, step_kind(sys), s, nullptr);
       }
-      if (r < n - 1 && sys->n_recv[1]) {
-        if (systems[r + 1]->n_send[0] != sys->n_recv[1]) return DEM_ERR_INVALID_ARG;
-        CK(cudaMemcpyAsync(sys->d_recvbuf[1], systems[r + 1]->d_sendbuf[0], sizeof(double) * kKin13 * sys->n_recv[1],
-                           cudaMemcpyDeviceToDevice, s));
+      launch_abort_or(aw, s);
+      for (int r = 0; r < n; ++r) {
+        dem_system* sys = systems[r];
+        enqueue_force(sys, step_kind(sys), s, nullptr, /*exchange=*/false);
+      }
+      if (peer) {  // the force kernels stored the ghost states into the neighbours already
+        for (int r = 0; r < n; ++r) advance_parities(systems[r], step_kind(systems[r]));
+        continue;
+      }
+      // ghost halo: rank r's left-side ghosts are rank r-1's right-side sends, and vice versa
+      for (int r = 0; r < n; ++r) {
+        dem_system* sys = systems[r];
+        if (r > 0 && sys->n_recv[0]) {
+          if (systems[r - 1]->n_send[1] != sys->n_recv[0]) return DEM_ERR_INVALID_ARG;
+          CK(cudaMemcpyAsync(sys->d_recvbuf[0], systems[r - 1]->d_sendbuf[1], sizeof(double) * kKin13 * sys->n_recv[0],
+                             cudaMemcpyDeviceToDevice, s));
+        }
+        if (r < n - 1 && sys->n_recv[1]) {
+          if (systems[r + 1]->n_send[0] != sys->n_recv[1]) return DEM_ERR_INVALID_ARG;
+          CK(cudaMemcpyAsync(sys->d_recvbuf[1], systems[r + 1]->d_sendbuf[0], sizeof(double) * kKin13 * sys->n_recv[1],
+                             cudaMemcpyDeviceToDevice, s));
+        }
+      }
+      for (int r = 0; r < n; ++r) {
+        dem_system* sys = systems[r];
+        const int kind = step_kind(sys);
+        StepArgs a = make_args(sys, kind);
+        enqueue_unpack(sys, a, s);
+        advance_parities(sys, kind);
       }
     }
+    bool aborted = false;
+    int64_t done = 0;
     for (int r = 0; r < n; ++r) {
       dem_system* sys = systems[r];
-      const int kind = step_kind(sys);
-      StepArgs a = make_args(sys, kind);
-      enqueue_unpack(sys, a, s);
-      advance_parities(sys, kind);
+      TRY(read_ctl(sys));
+      sys->steps_done = sys->h_ctl->step;
+      if (sys->h_ctl->err_code) return device_error(sys);
+      aborted |= sys->h_ctl->abort != 0;
+      done = sys->h_ctl->step - done_before;  // equal on every rank (the abort vote)
     }
-  }
-  for (int r = 0; r < n; ++r) {
-    dem_system* sys = systems[r];
-    TRY(read_ctl(sys));
-    sys->steps_done = sys->h_ctl->step;
-    if (sys->h_ctl->err_code) return device_error(sys);
-    if (sys->h_ctl->abort) {
-      sys->err = "capacity overflow in a loopback group (size entries_per_sphere generously)";
+    remaining -= done;
+    if (!aborted) break;
+    if (++guard > 8) {
+      systems[0]->err = "capacity regrow did not converge";
       return DEM_ERR_CAPACITY;
+    }
+    // every rank stopped at step `done`: each regrows what overflowed on it and all re-run from there
+    for (int r = 0; r < n; ++r) {
+      const Sched& at = sched[r][(size_t)done];
+      TRY(regrow(systems[r], at.up, at.ep, at.since, at.since == 0 ? (at.pending ? K_ADOPT : K_FULL) : -1, at.pending));
     }
   }
   return DEM_OK;
@@ -1961,6 +2026,9 @@ extern "C" dem_status dem_get_stats(dem_system* sys, dem_stats* out) {
   out->kernel_launches_per_step =
       kLaunchesPerStep + (sys->dist ? (sys->peer ? 2 : 4) : 0) + (sys->n_mesh ? 3 : 0);
   out->state_fast_resets = sys->fast_resets;
+  out->migrated_clumps = sys->migrated_clumps;
+  out->migration_bytes = sys->migration_bytes;
+  out->ghost_exchange_bytes = sys->ghost_bytes;
   if (sys->launched > 0 && sys->ns > 0) {
     const RowBuf& R = sys->rows[sys->ep];
     int tot = 0, ins = 0;
@@ -2002,71 +2070,366 @@ static dem_status local_max_drift2(dem_system* sys, double* out) {
   return DEM_OK;
 }
 
-// owned states and canonical contact histories of one system, packed as doubles:
-// per clump [gid bits, tid, pos 3, quat 4, vel 3, omega 3], per contact [key_a bits, key_b bits, u_t 3]
+// ------------------------------------------------------------------ neighbour exchange
+// Records moved between neighbouring ranks, as doubles: a clump [gid bits, tid, pos 3, quat 4,
+// vel 3, omega 3]; a contact [key_a bits, key_b bits, u_t 3 (oriented a -> b)].
 static constexpr int kMigClump = 15, kMigContact = 5;
-static dem_status pack_owned(dem_system* sys, std::vector<double>& buf, int64_t& nc, int64_t& nk) {
-  int64_t n = 0, m = 0;
-  TRY(dem_get_state(sys, 0, &n, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0));
-  std::vector<int64_t> gid(n);
-  std::vector<int32_t> tid(n);
-  std::vector<double> pos(3 * n), quat(4 * n), vel(3 * n), om(3 * n);
-  TRY(dem_get_state(sys, n, &n, gid.data(), tid.data(), pos.data(), quat.data(), vel.data(), om.data(), 0));
-  TRY(dem_get_contacts(sys, 0, &m, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr));
-  std::vector<int64_t> ka(m), kb(m);
-  std::vector<double> ut(3 * m);
-  if (m) TRY(dem_get_contacts(sys, m, &m, ka.data(), kb.data(), nullptr, nullptr, nullptr, ut.data(), nullptr));
-  buf.assign((size_t)kMigClump * n + (size_t)kMigContact * m, 0.0);
-  double* o = buf.data();
-  for (int64_t c = 0; c < n; ++c, o += kMigClump) {
-    std::memcpy(&o[0], &gid[c], 8);
-    o[1] = (double)tid[c];
-    for (int d = 0; d < 3; ++d) o[2 + d] = pos[3 * c + d];
-    for (int d = 0; d < 4; ++d) o[5 + d] = quat[4 * c + d];
-    for (int d = 0; d < 3; ++d) o[9 + d] = vel[3 * c + d];
-    for (int d = 0; d < 3; ++d) o[12 + d] = om[3 * c + d];
+
+struct ClumpSet {
+  std::vector<int64_t> gid;
+  std::vector<int32_t> tid;
+  std::vector<double> pos, quat, vel, om;
+  int64_t size() const { return (int64_t)gid.size(); }
+  void add(int64_t g, int32_t t, const double* p, const double* q, const double* v, const double* w) {
+    gid.push_back(g);
+    tid.push_back(t);
+    pos.insert(pos.end(), p, p + 3);
+    quat.insert(quat.end(), q, q + 4);
+    vel.insert(vel.end(), v, v + 3);
+    om.insert(om.end(), w, w + 3);
   }
-  for (int64_t k = 0; k < m; ++k, o += kMigContact) {
-    std::memcpy(&o[0], &ka[k], 8);
-    std::memcpy(&o[1], &kb[k], 8);
-    for (int d = 0; d < 3; ++d) o[2 + d] = ut[3 * k + d];
+  void add(const ClumpSet& s, int64_t c) {
+    add(s.gid[c], s.tid[c], &s.pos[3 * c], &s.quat[4 * c], &s.vel[3 * c], &s.om[3 * c]);
   }
-  nc = n;
-  nk = m;
+  void put(std::vector<double>& o, int64_t c) const {
+    double r[kMigClump];
+    std::memcpy(&r[0], &gid[c], 8);
+    r[1] = (double)tid[c];
+    for (int d = 0; d < 3; ++d) r[2 + d] = pos[3 * c + d];
+    for (int d = 0; d < 4; ++d) r[5 + d] = quat[4 * c + d];
+    for (int d = 0; d < 3; ++d) r[9 + d] = vel[3 * c + d];
+    for (int d = 0; d < 3; ++d) r[12 + d] = om[3 * c + d];
+    o.insert(o.end(), r, r + kMigClump);
+  }
+  void get(const double* r) {
+    int64_t g;
+    std::memcpy(&g, &r[0], 8);
+    add(g, (int32_t)r[1], r + 2, r + 5, r + 9, r + 12);
+  }
+};
+
+struct ContactSet {
+  std::vector<int64_t> ka, kb;
+  std::vector<double> ut;
+  int64_t size() const { return (int64_t)ka.size(); }
+  void put(std::vector<double>& o, int64_t k) const {
+    double r[kMigContact];
+    std::memcpy(&r[0], &ka[k], 8);
+    std::memcpy(&r[1], &kb[k], 8);
+    for (int d = 0; d < 3; ++d) r[2 + d] = ut[3 * k + d];
+    o.insert(o.end(), r, r + kMigContact);
+  }
+  void get(const double* r) {
+    int64_t a, b;
+    std::memcpy(&a, &r[0], 8);
+    std::memcpy(&b, &r[1], 8);
+    ka.push_back(a);
+    kb.push_back(b);
+    ut.insert(ut.end(), r + 2, r + 5);
+  }
+};
+
+// one rank's payloads to / from its left [0] and right [1] neighbours
+struct NbrMsg {
+  std::vector<double> out[2], in[2];
+};
+
+// NCCL: grouped ncclSend/ncclRecv with rank - 1 and rank + 1, counts first, then payloads
+static dem_status exchange_nccl(dem_system* sys, NbrMsg& m) {
+  const int r = sys->P.rank, P = sys->P.n_ranks;
+  cudaStream_t s = sys->stream;
+  const bool nb[2] = {r > 0, r < P - 1};
+  const int peer[2] = {r - 1, r + 1};
+  int64_t* d_cnt = (int64_t*)dalloc(sys, sizeof(int64_t) * 4);
+  if (!d_cnt) return DEM_ERR_OOM;
+  const int64_t cnt_out[2] = {(int64_t)m.out[0].size(), (int64_t)m.out[1].size()};
+  int64_t cnt_in[2] = {0, 0};
+  CK(cudaMemcpyAsync(d_cnt, cnt_out, sizeof(cnt_out), cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(d_cnt + 2, 0, 2 * sizeof(int64_t), s));
+  ncclGroupStart();
+  for (int side = 0; side < 2; ++side)
+    if (nb[side]) {
+      ncclSend(d_cnt + side, 1, ncclInt64, peer[side], sys->comm, s);
+      ncclRecv(d_cnt + 2 + side, 1, ncclInt64, peer[side], sys->comm, s);
+    }
+  if (ncclGroupEnd() != ncclSuccess) return DEM_ERR_NCCL;
+  CK(cudaMemcpyAsync(cnt_in, d_cnt + 2, sizeof(cnt_in), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  dfree(sys, d_cnt);
+  const size_t tot = (size_t)(cnt_out[0] + cnt_out[1] + cnt_in[0] + cnt_in[1]);
+  double* d_buf = (double*)dalloc(sys, sizeof(double) * (tot + 1));
+  if (!d_buf) return DEM_ERR_OOM;
+  double* so[2] = {d_buf, d_buf + cnt_out[0]};
+  double* si[2] = {so[1] + cnt_out[1], so[1] + cnt_out[1] + cnt_in[0]};
+  for (int side = 0; side < 2; ++side)
+    if (cnt_out[side])
+      CK(cudaMemcpyAsync(so[side], m.out[side].data(), sizeof(double) * cnt_out[side], cudaMemcpyHostToDevice, s));
+  ncclGroupStart();
+  for (int side = 0; side < 2; ++side)
+    if (nb[side]) {
+      if (cnt_out[side]) ncclSend(so[side], (size_t)cnt_out[side], ncclDouble, peer[side], sys->comm, s);
+      if (cnt_in[side]) ncclRecv(si[side], (size_t)cnt_in[side], ncclDouble, peer[side], sys->comm, s);
+    }
+  if (ncclGroupEnd() != ncclSuccess) return DEM_ERR_NCCL;
+  for (int side = 0; side < 2; ++side) {
+    m.in[side].assign((size_t)cnt_in[side], 0.0);
+    if (cnt_in[side])
+      CK(cudaMemcpyAsync(m.in[side].data(), si[side], sizeof(double) * cnt_in[side], cudaMemcpyDeviceToHost, s));
+  }
+  CK(cudaStreamSynchronize(s));
+  dfree(sys, d_buf);
   return DEM_OK;
 }
 
-// the gathered global state + history (rank order) -> this system's new partition
-struct Global {
-  std::vector<int64_t> gid, ka, kb;
-  std::vector<int32_t> tid;
-  std::vector<double> pos, quat, vel, om, ut;
-  void add(const double* b, int64_t nc, int64_t nk) {
-    for (int64_t c = 0; c < nc; ++c, b += kMigClump) {
-      int64_t g;
-      std::memcpy(&g, &b[0], 8);
-      gid.push_back(g);
-      tid.push_back((int32_t)b[1]);
-      pos.insert(pos.end(), b + 2, b + 5);
-      quat.insert(quat.end(), b + 5, b + 9);
-      vel.insert(vel.end(), b + 9, b + 12);
-      om.insert(om.end(), b + 12, b + 15);
-    }
-    for (int64_t k = 0; k < nk; ++k, b += kMigContact) {
-      int64_t x, y;
-      std::memcpy(&x, &b[0], 8);
-      std::memcpy(&y, &b[1], 8);
-      ka.push_back(x);
-      kb.push_back(y);
-      ut.insert(ut.end(), b + 2, b + 5);
-    }
+// the exchange for the ranks held by this process: one NCCL rank, or a whole loopback group
+// (ranks 0..n-1 in order, payloads handed over in memory)
+static dem_status exchange(dem_system* const* sys, int n, std::vector<NbrMsg>& m) {
+  if (n == 1 && sys[0]->comm) return exchange_nccl(sys[0], m[0]);
+  if (n != sys[0]->P.n_ranks) {
+    sys[0]->err = "neighbour exchange: needs an NCCL communicator (dem_params.nccl_id) or the whole loopback group";
+    return DEM_ERR_INVALID_ARG;
   }
-  dem_status apply(dem_system* sys) const {
-    const int64_t n = (int64_t)gid.size(), m = (int64_t)ka.size();
-    TRY(dem_set_state(sys, n, gid.data(), tid.data(), pos.data(), quat.data(), vel.data(), om.data(), 0));
-    return dem_set_contact_history(sys, m, ka.data(), kb.data(), ut.data());
+  for (int r = 0; r < n; ++r) {
+    m[r].in[0] = r > 0 ? m[r - 1].out[1] : std::vector<double>();
+    m[r].in[1] = r < n - 1 ? m[r + 1].out[0] : std::vector<double>();
   }
-};
+  return DEM_OK;
+}
+
+// Every rank's owned clumps -> its held set: the owned clumps plus the clumps its neighbours own
+// within `halo` of the shared faces (sent by their owners: the same partition test on the same
+// bits on both sides), laid out by dem_set_state.  Collective over the decomposition.
+static dem_status complete_ghosts(dem_system* const* sys, int n, const std::vector<ClumpSet>& owned) {
+  std::vector<NbrMsg> m(n);
+  for (int r = 0; r < n; ++r) {
+    const dem_params& P = sys[r]->P;
+    const ClumpSet& O = owned[r];
+    std::vector<int8_t> role(O.size()), sendf(O.size());
+    TRY(dem_partition_plan(O.size(), O.pos.data(), P.slab_lo, P.slab_hi, P.halo, P.rank > 0,
+                           P.rank < P.n_ranks - 1, role.data(), sendf.data()));
+    for (int64_t c = 0; c < O.size(); ++c) {
+      if (role[c] != 1) {
+        sys[r]->err = "clump gid " + std::to_string(O.gid[c]) + " handed to a rank whose slab does not hold its COM";
+        return DEM_ERR_INVALID_ARG;
+      }
+      for (int side = 0; side < 2; ++side)
+        if (sendf[c] >> side & 1) O.put(m[r].out[side], c);
+    }
+    sys[r]->ghost_bytes = (int64_t)(m[r].out[0].size() + m[r].out[1].size()) * 8;
+  }
+  TRY(exchange(sys, n, m));
+  for (int r = 0; r < n; ++r) {
+    ClumpSet H = owned[r];
+    for (int side = 0; side < 2; ++side)
+      for (size_t o = 0; o < m[r].in[side].size(); o += kMigClump) H.get(m[r].in[side].data() + o);
+    TRY(dem_set_state(sys[r], H.size(), H.gid.data(), H.tid.data(), H.pos.data(), H.quat.data(), H.vel.data(),
+                      H.om.data(), 0));
+  }
+  return DEM_OK;
+}
+
+// the clumps of a rank-local input whose COM lies in the rank's slab
+static ClumpSet owned_of_input(const dem_system* sys, int64_t n, const int64_t* gid, const int32_t* tid,
+                              const double* pos, const double* quat, const double* vel, const double* om) {
+  ClumpSet O;
+  for (int64_t c = 0; c < n; ++c) {
+    const double x = pos[3 * c];
+    if (x >= sys->P.slab_lo && x < sys->P.slab_hi) O.add(gid[c], tid[c], pos + 3 * c, quat + 4 * c, vel + 3 * c, om + 3 * c);
+  }
+  return O;
+}
+
+extern "C" dem_status dem_set_state_local(dem_system* sys, int64_t n, const int64_t* gid, const int32_t* tid,
+                                          const double* pos, const double* quat, const double* vel,
+                                          const double* omega) {
+  if (!sys || n < 0 || (n > 0 && (!gid || !tid || !pos || !quat || !vel || !omega))) return DEM_ERR_INVALID_ARG;
+  if (!sys->dist) return dem_set_state(sys, n, gid, tid, pos, quat, vel, omega, 0);
+  std::vector<ClumpSet> owned{owned_of_input(sys, n, gid, tid, pos, quat, vel, omega)};
+  dem_system* one[1] = {sys};
+  return complete_ghosts(one, 1, owned);
+}
+
+extern "C" dem_status dem_set_state_local_group(dem_system* const* systems, int32_t n, const int64_t* n_in,
+                                                const int64_t* const* gid, const int32_t* const* tid,
+                                                const double* const* pos, const double* const* quat,
+                                                const double* const* vel, const double* const* omega) {
+  if (!systems || n < 1 || !n_in || !gid || !tid || !pos || !quat || !vel || !omega) return DEM_ERR_INVALID_ARG;
+  std::vector<ClumpSet> owned;
+  for (int r = 0; r < n; ++r) {
+    dem_system* sys = systems[r];
+    if (!sys || !sys->dist || sys->P.rank != r || sys->P.n_ranks != n || n_in[r] < 0) return DEM_ERR_INVALID_ARG;
+    owned.push_back(owned_of_input(sys, n_in[r], gid[r], tid[r], pos[r], quat[r], vel[r], omega[r]));
+  }
+  return complete_ghosts(systems, n, owned);
+}
+
+extern "C" dem_status dem_migration_plan(int64_t n, const int64_t* gid, const double* pos, const int8_t* role,
+                                         double slab_lo, double slab_hi, int32_t has_left, int32_t has_right,
+                                         int8_t* dest, int64_t n_entries, const int64_t* own_key, int8_t* route) {
+  if (n < 0 || n_entries < 0 || (n && (!gid || !pos || !role || !dest)) || (n_entries && (!own_key || !route)) ||
+      !(slab_hi > slab_lo))
+    return DEM_ERR_INVALID_ARG;
+  std::unordered_map<int64_t, int8_t> of;
+  of.reserve((size_t)n * 2);
+  for (int64_t c = 0; c < n; ++c) {
+    const double x = pos[3 * c];
+    int8_t d = 0;
+    if (role[c] == 1) {
+      d = (has_left && x < slab_lo) ? -1 : (has_right && x >= slab_hi) ? 1 : 0;
+    } else if (role[c] == 2) {
+      d = x >= slab_lo ? 0 : -1;  // a left neighbour's clump: now ours, or still the neighbour's
+    } else if (role[c] == 3) {
+      d = x < slab_hi ? 0 : 1;
+    } else {
+      return DEM_ERR_INVALID_ARG;
+    }
+    dest[c] = d;
+    of[gid[c]] = d;
+  }
+  // a directed row entry belongs to the owner of its own sphere: it goes where that clump goes
+  for (int64_t k = 0; k < n_entries; ++k) {
+    auto it = of.find(own_key[k] / kKeyStride);
+    if (own_key[k] < 0 || it == of.end()) return DEM_ERR_INVALID_ARG;
+    route[k] = it->second;
+  }
+  return DEM_OK;
+}
+
+// the directed row entries of the owned spheres in the last step's set: (own key, partner key,
+// u_t oriented own -> partner) — the history each rank keeps for its own spheres
+static dem_status get_directed(dem_system* sys, ContactSet& K) {
+  if (sys->launched == 0 || sys->ns_own == 0) return DEM_OK;
+  CK(cudaStreamSynchronize(sys->stream));
+  const RowBuf& R = sys->rows[sys->ep];
+  std::vector<int> rp(sys->ns_own + 1);
+  CK(cudaMemcpy(rp.data(), R.row_ptr, sizeof(int) * (sys->ns_own + 1), cudaMemcpyDeviceToHost));
+  const int64_t m = rp[sys->ns_own];
+  std::vector<long long> keys(m);
+  std::vector<double> ut((size_t)kUt * m);
+  if (m) {
+    CK(cudaMemcpy(keys.data(), R.key, sizeof(long long) * m, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(ut.data(), sys->rows[sys->up].ut, sizeof(double) * kUt * m, cudaMemcpyDeviceToHost));
+  }
+  for (int64_t s = 0; s < sys->ns_own; ++s)
+    for (int e = rp[s]; e < rp[s + 1]; ++e) {
+      K.ka.push_back(sys->h_s_key[s]);
+      K.kb.push_back(keys[e]);
+      K.ut.insert(K.ut.end(), &ut[(size_t)kUt * e], &ut[(size_t)kUt * e] + 3);
+    }
+  return DEM_OK;
+}
+
+// install directed entries as the history of the owned spheres they name (others are ignored)
+static dem_status import_directed(dem_system* sys, const ContactSet& K) {
+  std::unordered_map<long long, int> idx;
+  idx.reserve((size_t)sys->ns_own * 2);
+  for (int64_t s = 0; s < sys->ns_own; ++s) idx[sys->h_s_key[s]] = (int)s;
+  std::vector<std::vector<HistEntry>> per(sys->ns);
+  for (int64_t k = 0; k < K.size(); ++k) {
+    auto it = idx.find(K.ka[k]);
+    if (it != idx.end()) per[it->second].push_back(HistEntry{K.kb[k], {K.ut[3 * k], K.ut[3 * k + 1], K.ut[3 * k + 2]}});
+  }
+  return install_history(sys, per);
+}
+
+// Neighbour-only migration of the ranks held by this process: each rank sends the
+// owned clumps whose COM left its slab, with the directed row entries of their spheres (partner
+// key + u_t: the tangential history each sphere's owner keeps), to the neighbour that now owns
+// them (counts, then payloads); the new owned sets then exchange their ghost bands
+// (complete_ghosts) and every rank re-lays out only its own clumps and re-imports the entries of
+// its spheres.  Bytes moved scale with the crossings (plus the ghost band), not with the system.
+static dem_status migrate_ranks(dem_system* const* ranks, int n) {
+  std::vector<NbrMsg> m(n);
+  std::vector<ClumpSet> keep(n);
+  std::vector<ContactSet> kc(n);
+  for (int r = 0; r < n; ++r) {
+    dem_system* sys = ranks[r];
+    TRY(dem_synchronize(sys));
+    int64_t no = 0;
+    TRY(dem_get_state(sys, 0, &no, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0));
+    ClumpSet O;
+    O.gid.resize(no);
+    O.tid.resize(no);
+    O.pos.resize(3 * no);
+    O.quat.resize(4 * no);
+    O.vel.resize(3 * no);
+    O.om.resize(3 * no);
+    TRY(dem_get_state(sys, no, &no, O.gid.data(), O.tid.data(), O.pos.data(), O.quat.data(), O.vel.data(),
+                      O.om.data(), 0));
+    // held clumps: the owned ones, then the ghosts (storage order) with their current COM x
+    const int64_t ng = sys->n - sys->n_own;
+    std::vector<int64_t> hg(O.gid);
+    std::vector<double> hp(O.pos);
+    std::vector<int8_t> role(no, 1);
+    if (ng) {
+      std::vector<double> gx(ng);
+      CK(cudaMemcpy(gx.data(), sys->d_state[sys->sp] + sys->n_own, sizeof(double) * ng, cudaMemcpyDeviceToHost));
+      std::vector<int8_t> grole(ng, 0);
+      for (int side = 0; side < 2; ++side)
+        for (int i : sys->h_recv_list[side]) grole[i - sys->n_own] = (int8_t)(2 + side);
+      for (int64_t k = 0; k < ng; ++k) {
+        hg.push_back(sys->h_gid[sys->n_own + k]);
+        const double p3[3] = {gx[k], 0.0, 0.0};
+        hp.insert(hp.end(), p3, p3 + 3);
+        role.push_back(grole[k]);
+      }
+    }
+    ContactSet K;  // the directed row entries of the owned spheres
+    TRY(get_directed(sys, K));
+    const int64_t nk = K.size();
+    std::vector<int8_t> dest(hg.size()), route(nk);
+    const dem_params& P = sys->P;
+    if (dem_migration_plan((int64_t)hg.size(), hg.data(), hp.data(), role.data(), P.slab_lo, P.slab_hi, P.rank > 0,
+                           P.rank < P.n_ranks - 1, dest.data(), nk, K.ka.data(), route.data()) != DEM_OK) {
+      sys->err = "migration plan: a row entry names a sphere that is not owned here";
+      return DEM_ERR_INVALID_ARG;
+    }
+    std::vector<double> cl[2], co[2];
+    int64_t ncl[2] = {0, 0}, nco[2] = {0, 0};
+    for (int64_t c = 0; c < no; ++c) {
+      if (dest[c] == 0) {
+        keep[r].add(O, c);
+      } else {
+        const int side = dest[c] < 0 ? 0 : 1;
+        O.put(cl[side], c);
+        ++ncl[side];
+      }
+    }
+    for (int64_t k = 0; k < nk; ++k) {
+      if (route[k] == 0) {
+        kc[r].ka.push_back(K.ka[k]);
+        kc[r].kb.push_back(K.kb[k]);
+        kc[r].ut.insert(kc[r].ut.end(), &K.ut[3 * k], &K.ut[3 * k] + 3);
+      } else {
+        const int side = route[k] < 0 ? 0 : 1;
+        K.put(co[side], k);
+        ++nco[side];
+      }
+    }
+    for (int side = 0; side < 2; ++side) {
+      std::vector<double>& o = m[r].out[side];
+      o.push_back((double)ncl[side]);
+      o.push_back((double)nco[side]);
+      o.insert(o.end(), cl[side].begin(), cl[side].end());
+      o.insert(o.end(), co[side].begin(), co[side].end());
+    }
+    sys->migrated_clumps = ncl[0] + ncl[1];
+    sys->migration_bytes = (int64_t)(m[r].out[0].size() + m[r].out[1].size()) * 8;
+  }
+  TRY(exchange(ranks, n, m));
+  for (int r = 0; r < n; ++r)
+    for (int side = 0; side < 2; ++side) {
+      const std::vector<double>& in = m[r].in[side];
+      if (in.size() < 2) continue;
+      const int64_t nc = (int64_t)in[0], nk = (int64_t)in[1];
+      const double* b = in.data() + 2;
+      for (int64_t c = 0; c < nc; ++c, b += kMigClump) keep[r].get(b);
+      for (int64_t k = 0; k < nk; ++k, b += kMigContact) kc[r].get(b);
+    }
+  TRY(complete_ghosts(ranks, n, keep));
+  for (int r = 0; r < n; ++r) TRY(import_directed(ranks[r], kc[r]));
+  return DEM_OK;
+}
 
 extern "C" dem_status dem_migrate(dem_system* sys, double threshold, int32_t* moved) {
   if (!sys || !(threshold >= 0)) return DEM_ERR_INVALID_ARG;
@@ -2078,7 +2441,6 @@ extern "C" dem_status dem_migrate(dem_system* sys, double threshold, int32_t* mo
   }
   TRY(dem_synchronize(sys));
   cudaStream_t s = sys->stream;
-  const int P = sys->P.n_ranks;
   TRY(local_max_drift2(sys, nullptr));
   if (ncclAllReduce(sys->d_counter, sys->d_counter, 1, ncclDouble, ncclMax, sys->comm, s) != ncclSuccess)
     return DEM_ERR_NCCL;
@@ -2086,34 +2448,8 @@ extern "C" dem_status dem_migrate(dem_system* sys, double threshold, int32_t* mo
   CK(cudaMemcpyAsync(&d2, sys->d_counter, sizeof(double), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   if (threshold > 0 && std::sqrt(d2) <= threshold) return DEM_OK;
-  std::vector<double> mine;
-  int64_t nc = 0, nk = 0;
-  TRY(pack_owned(sys, mine, nc, nk));
-  // two-phase all-gather: counts, then payloads padded to the largest rank's
-  int64_t* d_cnt = (int64_t*)dalloc(sys, sizeof(int64_t) * 2 * (P + 1));
-  if (!d_cnt) return DEM_ERR_OOM;
-  const int64_t cnt[2] = {nc, nk};
-  std::vector<int64_t> all((size_t)2 * P);
-  CK(cudaMemcpyAsync(d_cnt, cnt, sizeof(cnt), cudaMemcpyHostToDevice, s));
-  if (ncclAllGather(d_cnt, d_cnt + 2, 2, ncclInt64, sys->comm, s) != ncclSuccess) return DEM_ERR_NCCL;
-  CK(cudaMemcpyAsync(all.data(), d_cnt + 2, sizeof(int64_t) * 2 * P, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  dfree(sys, d_cnt);
-  size_t len = 1;
-  for (int r = 0; r < P; ++r) len = std::max(len, (size_t)(kMigClump * all[2 * r] + kMigContact * all[2 * r + 1]));
-  double* d_send = (double*)dalloc(sys, sizeof(double) * len);
-  double* d_all = (double*)dalloc(sys, sizeof(double) * len * P);
-  if (!d_send || !d_all) return DEM_ERR_OOM;
-  if (!mine.empty()) CK(cudaMemcpyAsync(d_send, mine.data(), sizeof(double) * mine.size(), cudaMemcpyHostToDevice, s));
-  if (ncclAllGather(d_send, d_all, len, ncclDouble, sys->comm, s) != ncclSuccess) return DEM_ERR_NCCL;
-  std::vector<double> host(len * P);
-  CK(cudaMemcpyAsync(host.data(), d_all, sizeof(double) * len * P, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  dfree(sys, d_send);
-  dfree(sys, d_all);
-  Global G;
-  for (int r = 0; r < P; ++r) G.add(host.data() + len * r, all[2 * r], all[2 * r + 1]);
-  TRY(G.apply(sys));
+  dem_system* one[1] = {sys};
+  TRY(migrate_ranks(one, 1));
   if (moved) *moved = 1;
   return DEM_OK;
 }
@@ -2143,14 +2479,7 @@ extern "C" dem_status dem_migrate_group(dem_system* const* systems, int32_t n, d
     d2 = std::max(d2, v);
   }
   if (threshold > 0 && std::sqrt(d2) <= threshold) return DEM_OK;
-  Global G;
-  for (int r = 0; r < n; ++r) {
-    std::vector<double> buf;
-    int64_t nc = 0, nk = 0;
-    TRY(pack_owned(systems[r], buf, nc, nk));
-    G.add(buf.data(), nc, nk);
-  }
-  for (int r = 0; r < n; ++r) TRY(G.apply(systems[r]));
+  TRY(migrate_ranks(systems, n));
   if (moved) *moved = 1;
   return DEM_OK;
 }

@@ -181,3 +181,85 @@ def test_distributed_deferred_cadence_is_bitwise_identical(dem, peer, overlap):
     sg = _gather(systems)
     for key in ("gid", "pos", "quat", "vel", "omega"):
         assert np.array_equal(sg[key], sr[key][o]), key
+
+
+def _owner(systems):
+    return {int(g): r for r, s in enumerate(systems) for g in s.dem_get_state()["gid"]}
+
+
+@pytest.mark.parametrize("peer", [False, True])
+def test_migration_moves_only_the_crossers(dem, peer):
+    """Neighbour-only migration: each rank sends only the clumps whose COM crossed
+    into a neighbour's slab (and the contacts routed with them), so the migrated clump count equals
+    the number of owner changes and the bytes moved scale with it, not with the system."""
+    scene = _strip(seed=4)
+    scene.vel[:, 0] += 1.5
+    drift = 0.1e-3
+    systems = _group(dem, scene, 3, drift_max=drift, transport=dem.TRANSPORT_LOOPBACK_PEER if peer else None)
+    for _ in range(3):
+        dem.step_group(systems, 40)
+        before = _owner(systems)
+        assert dem.migrate_group(systems, threshold=0.5 * drift)
+        after = _owner(systems)
+        changed = sum(1 for g in before if before[g] != after[g])
+        st = [s.dem_get_stats() for s in systems]
+        assert sum(x["migrated_clumps"] for x in st) == changed > 0
+        # per crosser: its 15-double record plus the directed row entries of its (at most 6)
+        # spheres, 5 doubles each; 2 count words per side and rank — far below the 15 doubles per
+        # clump of the whole system an all-gather would move
+        mb = sum(x["migration_bytes"] for x in st)
+        assert mb <= 8 * (4 * len(systems) + changed * (15 + 5 * 80))
+        assert mb < 0.05 * 8 * 15 * scene.n_clumps
+        ghosts = sum(x["n_ghost_clumps"] for x in st)
+        assert sum(x["ghost_exchange_bytes"] for x in st) == 8 * 15 * ghosts
+
+
+@pytest.mark.parametrize("peer", [False, True])
+def test_rank_local_set_state_equals_global_input(dem, peer):
+    """dem_set_state_local_group: every rank is given only the clumps it owns (its slab); the ghost
+    bands come from the neighbours.  The group then steps bitwise like one built from the global
+    state on every rank."""
+    scene = _strip(seed=6)
+    tr = dem.TRANSPORT_LOOPBACK_PEER if peer else None
+    a = _group(dem, scene, 3, record=False, transport=tr)
+    b = _group(dem, scene, 3, record=False, transport=tr)
+    parts = []
+    for s in b:
+        sel = np.nonzero((scene.pos[:, 0] >= s.params.slab_lo) & (scene.pos[:, 0] < s.params.slab_hi))[0]
+        sub = scene.subset(sel)
+        parts.append((sub.gid, sub.tid, sub.pos, sub.quat, sub.vel, sub.omega))
+    dem.set_state_local_group(b, parts)
+    sa, sb = [s.dem_get_stats() for s in a], [s.dem_get_stats() for s in b]
+    for x, y in zip(sa, sb):
+        assert (x["n_owned_clumps"], x["n_ghost_clumps"]) == (y["n_owned_clumps"], y["n_ghost_clumps"])
+    dem.step_group(a, 30)
+    dem.step_group(b, 30)
+    ga, gb = _gather(a), _gather(b)
+    for k in ("gid", "pos", "quat", "vel", "omega"):
+        assert np.array_equal(ga[k], gb[k]), k
+
+
+@pytest.mark.parametrize("peer", [False, True])
+def test_coordinated_capacity_regrow(dem, peer):
+    """One rank starts with far too little row capacity: its overflow aborts the step on every rank
+    (the abort vote before the force kernels), each rank regrows what overflowed on it, and all
+    re-run — the gathered trajectory stays bitwise equal to the single system's."""
+    scene = _strip(seed=8)
+    ref = dem.system_from_scene(scene)
+    ref.dem_step(25)
+    drift = 1e-3
+    halo = dem.halo_width(scene, drift)
+    b = dem.slab_bounds(scene.pos[:, 0], 2, scene.domain_lo[0], scene.domain_hi[0])
+    systems = []
+    for r in range(2):
+        d = dict(rank=r, n_ranks=2, slab_lo=b[r], slab_hi=b[r + 1], halo=halo, drift_max=drift,
+                 transport=dem.TRANSPORT_LOOPBACK_PEER if peer else dem.TRANSPORT_LOOPBACK)
+        systems.append(dem.system_from_scene(scene, dist=d, entries_per_sphere=12 if r == 0 else 0.05))
+    dem.step_group(systems, 25)
+    st = [s.dem_get_stats() for s in systems]
+    assert st[0]["regrows"] == 0 and st[1]["regrows"] >= 1
+    sr = ref.dem_get_state()
+    o = np.argsort(sr["gid"])
+    sg = _gather(systems)
+    for k in ("gid", "pos", "quat", "vel", "omega"):
+        assert np.array_equal(sg[k], sr[k][o]), k

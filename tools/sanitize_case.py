@@ -4,7 +4,7 @@
 
 Cases: c1 (C1 box, k = 1), deferred (C1, k = 5 with margin), overlap (k = 4, second stream),
 mesh (a cone pushed into a settled patch), peer2 (LOOPBACK_PEER slab group, P = 2, with a
-migration), regrow (a bed started with too-small capacities so every regrow path runs).
+coordinated regrow and a neighbour-only migration), regrow (a bed started with too-small capacities so every regrow path runs).
 Device memory comes from cudaMallocAsync (use_torch_allocator=False) so the sanitizer sees
 every allocation at its true size instead of a caching-allocator slab.
 """
@@ -56,7 +56,9 @@ def peer2():
     drift = 1e-3
     halo = dem.halo_width(s, drift)
     b = dem.slab_bounds(s.pos[:, 0], 2, s.domain_lo[0], s.domain_hi[0])
-    systems = [dem.system_from_scene(s, record_contacts=True, use_torch_allocator=False, entries_per_sphere=12,
+    # rank 1 starts with too little row capacity: the coordinated regrow path runs too
+    systems = [dem.system_from_scene(s, record_contacts=True, use_torch_allocator=False,
+                                     entries_per_sphere=12 if r == 0 else 0.3,
                                      dist=dict(rank=r, n_ranks=2, slab_lo=b[r], slab_hi=b[r + 1], halo=halo,
                                                drift_max=drift, transport=dem.TRANSPORT_LOOPBACK_PEER))
                for r in range(2)]

@@ -40,6 +40,9 @@ def main():
     ap.add_argument("--chunk", type=int, default=2000)
     ap.add_argument("--resume", default=None,
                     help="continue settling a saved patch (its state, no history) instead of spawning")
+    ap.add_argument("--frictionless-sides", action="store_true",
+                    help="make the four side walls frictionless (mu = 0): the beds replace them by mirror "
+                         "images, whose contacts carry no tangential force")
     a = ap.parse_args()
     import workloads as w
 
@@ -51,6 +54,13 @@ def main():
         steps = int(s.name.rsplit("-", 1)[-1]) if s.name.rsplit("-", 1)[-1].isdigit() else 0
         print(f"resuming {s.name}: {s.n_clumps} clumps, vmax {np.linalg.norm(s.vel, axis=1).max():.4f}", flush=True)
         a.max_steps += steps
+        if a.frictionless_sides:
+            m0 = np.asarray(s.materials[0], float)
+            s.materials = np.array([m0, [m0[0], m0[1], 0.0, m0[3]]])
+            for pl in s.planes:
+                if abs(pl.normal[2]) < 0.5:
+                    pl.material = 1
+            print("side walls frictionless (material 1: mu = 0)", flush=True)
     else:
         n = int(round(a.density * a.side * a.side * a.depth))
         vol = sum(c * t.mass / w.GRAIN_DENSITY for c, t in zip(w.ds_type_counts(n), w.ds_templates()))
