@@ -267,7 +267,12 @@ dem_status dem_set_mesh_motion(dem_system* sys, int32_t mesh, const double pos[3
                                const double vel[3], const double omega[3]);
 
 /* The mesh pose after the last step, and the wrench the granular material exerted on it during
- * that step: force and torque about X (the sum over its contacts in a fixed order). */
+ * that step: force and torque about X (the sum over its contacts in a fixed order).  The
+ * order is the fused force kernel's CTA partition (partials per CTA in row order, then CTA order
+ * and a fixed tree), which is re-cut when the contact-entry count moves by more than a quarter at
+ * the end of a dem_step call: the wrench bits are reproducible for a given sequence of dem_step
+ * calls, and may differ in the last place between dem_step(100) and 100 x dem_step(1).  Clump
+ * states do not depend on the cut. */
 dem_status dem_get_mesh(dem_system* sys, int32_t mesh, double pos[3], double quat[4], double force[3],
                         double torque[3]);
 

@@ -47,10 +47,17 @@ constexpr int kUt = DEM_UT_PAD ? 4 : 3;  // doubles per entry of the tangential 
 #ifndef DEM_V256
 #define DEM_V256 1  // 256-bit gathers of the 32-byte records (sm_100 LDG.256)
 #endif
-constexpr int kKinUsed = 10;  // doubles per clump in the packed kinematics record
+#ifndef DEM_KIN_TID
+#define DEM_KIN_TID 1  // the clump's template id rides in the kinematics record (slot 10)
+#endif
+// doubles per clump of the packed kinematics record read by the force kernel (with DEM_KIN_TID
+// the template id bits in slot 10 and a pad: the integrating thread finds its inertia without a
+// dependent global load)
+constexpr int kKinUsed = DEM_KIN_TID ? 12 : 10;
 // record stride: padded to 96 bytes so a partner's record is three 256-bit loads
 constexpr int kKin = DEM_V256 ? 12 : 10;
 static_assert(!DEM_V256 || (kKin * 8) % 32 == 0, "kinematics records must stay 32-byte aligned");
+static_assert(!DEM_KIN_TID || kKin >= kKinUsed, "DEM_KIN_TID needs the 12-double (DEM_V256) record");
 
 // 32-byte loads/stores in one instruction (sm_100: LDG.E.ENL2.256 / STG.E.ENL2.256); p must be
 // 32-byte aligned.  A random gather of a 32-byte record then costs one L1 wavefront per lane

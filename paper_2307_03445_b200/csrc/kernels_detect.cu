@@ -106,7 +106,8 @@ __device__ __forceinline__ void kin_record(const StepArgs& a, int c, const doubl
 #if DEM_KIN_ST256
   stg256(k, X, Y, Z, a.cur.vx[c]);
   stg256(k + 4, a.cur.vy[c], a.cur.vz[c], w0, w1);
-  stg256(k + 8, w2, a.tab.tpl_mass[a.tid[c]], 0.0, 0.0);
+  const int t = a.tid[c];
+  stg256(k + 8, w2, a.tab.tpl_mass[t], __longlong_as_double((long long)t), 0.0);
 #else
   k[0] = X; k[1] = Y; k[2] = Z;
   k[3] = a.cur.vx[c]; k[4] = a.cur.vy[c]; k[5] = a.cur.vz[c];

@@ -29,6 +29,12 @@ constexpr int kPairStride = 8;  // doubles per material pair in Tables::pair
 #ifndef DEM_FORCE_OWNER
 #define DEM_FORCE_OWNER 1  // owner sphere of each entry from a shared table (else a binary search)
 #endif
+#ifndef DEM_FORCE_UT_ASYNC
+#define DEM_FORCE_UT_ASYNC 1  // previous u_t staged by cp.async into the thread's part[] slots
+#endif
+#ifndef DEM_FORCE_LAZY_OWN
+#define DEM_FORCE_LAZY_OWN 1  // own clump's record read from shared memory at its uses (fewer spills)
+#endif
 #ifndef DEM_FORCE_ASYNC_EPI
 #define DEM_FORCE_ASYNC_EPI 0  // 1: own clumps' q, Omega, inertia staged by cp.async in the prologue (A/B: 3.96 -> 4.73 ms)
 #endif
@@ -154,7 +160,7 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
     for (int q = 0; q < 6; ++q) acc[q][ls] = 0.0;
   }
   {
-    // the used 10 doubles of each record (global stride kKin, shared stride kKinUsed)
+    // the used doubles of each record (global stride kKin, shared stride kKinUsed)
     const double2* src = reinterpret_cast<const double2*>(a.kin + (size_t)kKin * c0);
     for (int k = tid; k < ncl * (kKinUsed / 2); k += kFT) {
       const int c = k / (kKinUsed / 2), r = k - c * (kKinUsed / 2);
@@ -196,16 +202,35 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
 #endif
       const double4 own = own_p[ls];
       const double cx = own.x, cy = own.y, cz = own.z, ri = own.w;
+#if DEM_FORCE_LAZY_OWN
+      // the own clump's record is read from shared memory where it is used (volatile: the
+      // compiler would otherwise hoist these loads above the partner gathers and spill them)
+      const volatile double* ki = ck + kKinUsed * own_lc[ls];
+#define Mi (ki[9])
+#else
       const double* ki = ck + kKinUsed * own_lc[ls];
-      const double Xx = ki[0], Xy = ki[1], Xz = ki[2];
       const double Mi = ki[9];
+#endif
       const Entry ent = a.rows.ent[e];
       const int t = ent.partner;
       // (a4) history remap: the slot of this key in the previous rows was found by the
       // row merge in k_rows_finish (-1: contact born this step, u_t = 0)
       // (between rebuilds the set is unchanged: the entry's own slot of the previous u_t)
-      double ux = 0.0, uy = 0.0, uz = 0.0;
       const int pidx = a.remap ? ent.prev : e;
+#if DEM_FORCE_UT_ASYNC
+      // the previous u_t is copied into this thread's slots of part[0..2] (written by this thread
+      // only after its last use) with cp.async: no registers are held across the partner gathers
+      if (pidx >= 0) {
+        const double* u = a.prev.ut + (size_t)kUt * pidx;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          const unsigned dst = (unsigned)__cvta_generic_to_shared(&part[d][tid]);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(u + d) : "memory");
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+#else
+      double ux = 0.0, uy = 0.0, uz = 0.0;
       if (pidx >= 0) {
 #if DEM_UT_PAD
         const double4 u = ldg256(a.prev.ut + (size_t)kUt * pidx);
@@ -217,6 +242,7 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
         uz = __ldg(u + 2);
 #endif
       }
+#endif
       // (a5) geometry: n from i (own) to j (partner)
       double nx, ny, nz, px, py, pz, delta, rbar, mbar;
       double Xjx = 0, Xjy = 0, Xjz = 0, Vjx = 0, Vjy = 0, Vjz = 0, Wjx = 0, Wjy = 0, Wjz = 0;
@@ -301,12 +327,15 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
         mbar = Mi;
         mj = a.tab.plane_mat[pl];
       }
+#if DEM_FORCE_LAZY_OWN
+#undef Mi
+#endif
       if (degenerate) {
         raise_error(a.ctl, -12, a.s_key[s0 + ls], a.rows.key[e]);
         delta = 0.0;
       }
       double Fx = 0.0, Fy = 0.0, Fz = 0.0, nux = 0.0, nuy = 0.0, nuz = 0.0;
-      const double rix = px - Xx, riy = py - Xy, riz = pz - Xz;
+      const double rix = px - ki[0], riy = py - ki[1], riz = pz - ki[2];
       if (delta > 0.0 && active) {
         // contact-point velocities (Eq. 2a); a mesh point moves with its mesh
         double vix, viy, viz, vjx = 0.0, vjy = 0.0, vjz = 0.0;
@@ -329,6 +358,11 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
         if (mu != 0.0) {
           // (a7) Eq. 3a-3b, Eq. 1b, Eq. 3c
           const double vtx = vrx - vn * nx, vty = vry - vn * ny, vtz = vrz - vn * nz;
+#if DEM_FORCE_UT_ASYNC
+          asm volatile("cp.async.wait_all;" ::: "memory");
+          const double ux = pidx >= 0 ? part[0][tid] : 0.0, uy = pidx >= 0 ? part[1][tid] : 0.0,
+                       uz = pidx >= 0 ? part[2][tid] : 0.0;
+#endif
           const double upx = ux + h * vtx, upy = uy + h * vty, upz = uz + h * vtz;
           const double upn = upx * nx + upy * ny + upz * nz;
           const double utx = upx - upn * nx, uty = upy - upn * ny, utz = upz - upn * nz;
@@ -373,6 +407,9 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
       }
       // force on own sphere is -F, torque r_i x (-F) (Eq. 4, reading R11)
       const double fx = -Fx, fy = -Fy, fz = -Fz;
+#if DEM_FORCE_UT_ASYNC
+      asm volatile("cp.async.wait_all;" ::: "memory");  // (the u_t copy into these slots has landed)
+#endif
       part[0][tid] = fx;
       part[1][tid] = fy;
       part[2][tid] = fz;
@@ -443,7 +480,7 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
   const double qw = cq[0][tid], qx = cq[1][tid], qy = cq[2][tid], qz = cq[3][tid];
   const double w0 = cq[4][tid], w1 = cq[5][tid], w2 = cq[6][tid];
 #else
-  const int tt = a.tid[c];
+  const int tt = DEM_KIN_TID ? (int)__double_as_longlong(ck[kKinUsed * tid + 10]) : a.tid[c];
   const double I0 = a.tab.tpl_inertia[3 * tt], I1 = a.tab.tpl_inertia[3 * tt + 1], I2 = a.tab.tpl_inertia[3 * tt + 2];
   const double qw = a.cur.qw[c], qx = a.cur.qx[c], qy = a.cur.qy[c], qz = a.cur.qz[c];
   const double w0 = a.cur.wx[c], w1 = a.cur.wy[c], w2 = a.cur.wz[c];

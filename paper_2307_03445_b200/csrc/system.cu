@@ -65,6 +65,7 @@ struct dem_system {
   dem_params P{};
   cudaStream_t stream = nullptr;
   cudaStream_t cap_stream = nullptr;
+  cudaStream_t cap_hi = nullptr;  // capture stream of the overlapped cadence's force graphs (highest priority)
   std::string err;
   // host tables
   int n_mat = 0, n_tmpl = 0, n_planes = 0;
@@ -471,6 +472,9 @@ static void enqueue_part(dem_system* sys, int kind, int part, cudaStream_t s) {
   if (part == PART_FORCE) enqueue_force(sys, kind, s, nullptr, true);
 }
 
+#ifndef DEM_OVERLAP_PRIORITY
+#define DEM_OVERLAP_PRIORITY 1
+#endif
 static int graph_key(const dem_system* sys, int kind, int part) {
   return sys->sp | (sys->up << 1) | (sys->ep << 2) | (kind << 3) | (part << 5);
 }
@@ -480,10 +484,31 @@ static dem_status step_graph(dem_system* sys, int kind, int part, cudaGraphExec_
   const int key = graph_key(sys, kind, part);
   if (!sys->graph[key]) {
     cudaGraph_t g;
-    CK(cudaStreamBeginCapture(sys->cap_stream, cudaStreamCaptureModeThreadLocal));
-    enqueue_part(sys, kind, part, sys->cap_stream);
-    CK(cudaStreamEndCapture(sys->cap_stream, &g));
-    cudaError_t e = cudaGraphInstantiate(&sys->graph[key], g, 0);
+    // overlapped cadence: the force steps' kernels are captured on a high-priority stream and the
+    // graphs instantiated with per-node priorities, so the detection running beside them on
+    // det_stream (default = lowest priority) only takes the SM slots the force kernels leave
+    const bool prio = DEM_OVERLAP_PRIORITY && sys->P.overlap && part != PART_DET && sys->cap_hi;
+    cudaStream_t cs = prio ? sys->cap_hi : sys->cap_stream;
+    CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    enqueue_part(sys, kind, part, cs);
+    CK(cudaStreamEndCapture(cs, &g));
+    if (prio) {  // every kernel node at the highest priority (explicitly, not only by capture stream)
+      size_t nn = 0;
+      CK(cudaGraphGetNodes(g, nullptr, &nn));
+      std::vector<cudaGraphNode_t> nodes(nn);
+      if (nn) CK(cudaGraphGetNodes(g, nodes.data(), &nn));
+      int least = 0, greatest = 0;
+      CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+      cudaLaunchAttributeValue v{};
+      v.priority = greatest;
+      for (cudaGraphNode_t nd : nodes) {
+        cudaGraphNodeType t;
+        CK(cudaGraphNodeGetType(nd, &t));
+        if (t == cudaGraphNodeTypeKernel) CK(cudaGraphKernelNodeSetAttribute(nd, cudaLaunchAttributePriority, &v));
+      }
+    }
+    cudaError_t e = cudaGraphInstantiate(&sys->graph[key], g,
+                                         DEM_OVERLAP_PRIORITY && sys->P.overlap ? cudaGraphInstantiateFlagUseNodePriority : 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) {
       sys->err = std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e);
@@ -625,6 +650,11 @@ extern "C" dem_status dem_create(const dem_params* params, const dem_material* m
     }
   cudaError_t e = cudaStreamCreateWithFlags(&sys->cap_stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&sys->det_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess && params->overlap) {
+    int least = 0, greatest = 0;
+    e = cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&sys->cap_hi, cudaStreamNonBlocking, greatest);
+  }
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sys->ev_fork, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sys->ev_det, cudaEventDisableTiming);
   if (e != cudaSuccess) {
@@ -718,6 +748,7 @@ extern "C" void dem_destroy(dem_system* sys) {
   if (sys->h_ctl) cudaFreeHost(sys->h_ctl);
   for (auto e : sys->ev) cudaEventDestroy(e);
   if (sys->cap_stream) cudaStreamDestroy(sys->cap_stream);
+  if (sys->cap_hi) cudaStreamDestroy(sys->cap_hi);
   if (sys->det_stream) cudaStreamDestroy(sys->det_stream);
   if (sys->ev_fork) cudaEventDestroy(sys->ev_fork);
   if (sys->ev_det) cudaEventDestroy(sys->ev_det);

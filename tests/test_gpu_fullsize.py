@@ -30,12 +30,12 @@ def dem():
 
 def _sample_clumps(scene, k, seed):
     """k sampled clumps spread over the bed: random interior clumps, large types (most contacts),
-    clumps at the copy-paste tile seams (tiles of the 30 mm patch + 0.2 mm gap), at the
+    clumps at the copy-paste tile seams (mirror-image tiles of the 30 mm patch), at the
     side walls, on the floor and at the free top surface."""
     rng = np.random.default_rng(seed)
     x, y, z = scene.pos[:, 0], scene.pos[:, 1], scene.pos[:, 2]
     patch = beds.load_patch()
-    L = max(pl.point[0] for pl in patch.planes if pl.normal[0] < 0) + 0.2e-3
+    L = max(pl.point[0] for pl in patch.planes if pl.normal[0] < 0)  # mirror-image tiles, no gap
     fx, fy = np.mod(x, L), np.mod(y, L)
     lo, hi = scene.domain_lo + 1e-3, scene.domain_hi - np.array([1e-3, 1e-3, 0.05])
     pools = [

@@ -150,6 +150,8 @@ def patch_mesh(cone_speed: float = 0.5, spin: float = 0.0, depth: float = 1.0e-3
     s = load_patch()
     floor = [p for p in s.planes if p.normal[2] > 0.5][0]
     s.planes = [p for p in s.planes if not p.normal[2] > 0.5]
+    for p in s.planes:  # the side walls in M0 (the patch settled against frictionless ones)
+        p.material = 0
     s.materials = np.array([M0, MAT_B])
     side_x = max(pl.point[0] for pl in s.planes if pl.normal[0] < 0)
     side_y = max(pl.point[1] for pl in s.planes if pl.normal[1] < 0)

@@ -4,9 +4,12 @@ Recipe (DESIGN.md §"Input recipe"): spawn DS clumps (Table-1 number
 fractions) by exact-geometry RSA in a 30 x 30 mm column at ~27% solid fraction,
 all moving down at 1 m/s, and let them settle under gravity in a 5-wall box with
 the CPU oracle at h = 1e-6 s (material M0) until the fastest clump is slower than
-`--vstop`.  The result is a dense settled patch (~0.15 m deep, the base-patch
-density of P:233-234) that `workloads.scenes.tile_scene` copy-pastes into
-the multi-million-clump benchmark beds.  Since the state is produced by the oracle,
+`--vstop`, then (``--resume ... --frictionless-sides``) settle it further with the four side walls
+frictionless, because the beds replace those walls by the patch's mirror images, whose contacts
+carry no tangential force.  The result is a dense settled patch that `workloads.beds.tiled_bed`
+copy-pastes into the multi-million-clump benchmark beds.  The committed patch:
+140,000 steps in the 5-wall box, then 100,000 steps with frictionless side walls (0.24 s of
+settling; mean speed 0.8 mm/s, 1.09 contacts per sphere).  Since the state is produced by the oracle,
 no benchmark or parity input ever comes from the CUDA path.
 
     python -m workloads.make_patch --out workloads/data/ds_patch_30mm.npz
