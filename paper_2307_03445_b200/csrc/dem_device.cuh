@@ -47,8 +47,12 @@ constexpr int kUt = DEM_UT_PAD ? 4 : 3;  // doubles per entry of the tangential 
 #ifndef DEM_V256
 #define DEM_V256 1  // 256-bit gathers of the 32-byte records (sm_100 LDG.256)
 #endif
+#ifndef DEM_SLOT_KEYS
+#define DEM_SLOT_KEYS 1
+#endif
 #ifndef DEM_KIN_TID
-#define DEM_KIN_TID 1  // the clump's template id rides in the kinematics record (slot 10)
+#define DEM_KIN_TID 0  // 1: the clump's template id rides in the kinematics record (slot 10); A/B: force
+                       // 3.94 -> 4.57 ms (the larger staging array costs the 8th resident CTA per SM)
 #endif
 // doubles per clump of the packed kinematics record read by the force kernel (with DEM_KIN_TID
 // the template id bits in slot 10 and a pad: the integrating thread finds its inertia without a
@@ -204,6 +208,8 @@ struct StepArgs {
   int* row_cnt;              // walls + sphere partners per sphere (built by atomics each step)
   unsigned short* wall_mask; // [ns] sphere-plane candidates of the detection (bit p: plane p)
   int* slots;                // [row_width][ns_own] candidate partners of the owned spheres (k_pairs)
+  long long* slot_key;       // [row_width][ns_own] their keys (DEM_SLOT_KEYS: written by the producers,
+                             // so k_rows_finish sorts without a dependent gather of s_key)
   int row_width;             // slots per sphere (walls included: slot w is the w-th entry of the row)
   Rows rows, prev;
   Record rec;

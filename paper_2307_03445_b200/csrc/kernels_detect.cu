@@ -297,10 +297,11 @@ __device__ __noinline__ void slot_overflow(Ctl* ctl, int* abort, int slot) {
   atomicExch(abort, 1);
 }
 
-__device__ __forceinline__ void put_slot(const StepArgs& a, int own, int slot, int t) {
+__device__ __forceinline__ void put_slot(const StepArgs& a, int own, int slot, int t, long long tkey) {
   if (slot < 0) return;
   if (slot < a.row_width) {
     a.slots[(size_t)slot * a.ns_own + own] = t;  // slot-major: k_rows_finish reads coalesced
+    if (DEM_SLOT_KEYS) a.slot_key[(size_t)slot * a.ns_own + own] = tkey;
   } else {
     slot_overflow(a.ctl, a.abort, slot);  // cold path, kept out of the loop's registers
   }
@@ -315,6 +316,7 @@ __device__ __forceinline__ void flush_pairs(const StepArgs& a, const int2* bf, i
   constexpr int kPer = kPairBuf / 32;
   int2 v[kPer];
   int sa[kPer], sb[kPer];
+  long long ka[kPer], kb[kPer];
 #pragma unroll
   for (int j = 0; j < kPer; ++j) {
     const int k = lane + 32 * j;
@@ -322,13 +324,17 @@ __device__ __forceinline__ void flush_pairs(const StepArgs& a, const int2* bf, i
       v[j] = bf[k];
       sa[j] = v[j].x < a.ns_own ? atomicAdd(&a.row_cnt[v[j].x], 1) : -1;  // -1: ghost, no row
       sb[j] = v[j].y < a.ns_own ? atomicAdd(&a.row_cnt[v[j].y], 1) : -1;
+      if (DEM_SLOT_KEYS) {  // the partners' keys, gathered here beside the atomics' latency
+        ka[j] = __ldg(a.s_key + v[j].x);
+        kb[j] = __ldg(a.s_key + v[j].y);
+      }
     }
   }
 #pragma unroll
   for (int j = 0; j < kPer; ++j) {
     if (lane + 32 * j < n) {
-      put_slot(a, v[j].x, sa[j], v[j].y);
-      put_slot(a, v[j].y, sb[j], v[j].x);
+      put_slot(a, v[j].x, sa[j], v[j].y, DEM_SLOT_KEYS ? kb[j] : 0);
+      put_slot(a, v[j].y, sb[j], v[j].x, DEM_SLOT_KEYS ? ka[j] : 0);
     }
   }
   __syncwarp();
@@ -814,6 +820,7 @@ __global__ void __launch_bounds__(DEM_ROWS_TPB, DEM_ROWS_MINB) k_rows_finish(Ste
   const int w = __popc(wmask);
   const int nc = m - w;  // k_pairs handed out slots [w, m) of the candidate list
   const int* S = a.slots + (size_t)w * a.ns_own + i;  // S[q * ns_own]: candidate q
+  const long long* SK = DEM_SLOT_KEYS ? a.slot_key + (size_t)w * a.ns_own + i : nullptr;  // and its key
   if (nc <= kRegRow) {
     int tt[kRegRow], hh[kRegRow];
     long long kk[kRegRow];
@@ -821,7 +828,7 @@ __global__ void __launch_bounds__(DEM_ROWS_TPB, DEM_ROWS_MINB) k_rows_finish(Ste
     for (int q = 0; q < kRegRow; ++q) tt[q] = q < nc ? S[(size_t)q * a.ns_own] : 0;
 #pragma unroll
     for (int q = 0; q < kRegRow; ++q) {
-      kk[q] = q < nc ? partner_key(a, tt[q]) : 0x7fffffffffffffffLL;
+      kk[q] = q < nc ? (DEM_SLOT_KEYS ? SK[(size_t)q * a.ns_own] : partner_key(a, tt[q])) : 0x7fffffffffffffffLL;
       hh[q] = -1;
     }
     // odd-even transposition sort (keys of the candidates are distinct; padding sorts last)
@@ -860,7 +867,7 @@ __global__ void __launch_bounds__(DEM_ROWS_TPB, DEM_ROWS_MINB) k_rows_finish(Ste
       e.partner = t;
       e.prev = -1;  // set by the merge below
       R[u] = e;
-      K[u] = partner_key(a, t);
+      K[u] = DEM_SLOT_KEYS ? SK[(size_t)u * a.ns_own] : partner_key(a, t);
     }
     for (int u = 1; u < nc; ++u) {
       const Entry x = R[u];

@@ -30,10 +30,10 @@ constexpr int kPairStride = 8;  // doubles per material pair in Tables::pair
 #define DEM_FORCE_OWNER 1  // owner sphere of each entry from a shared table (else a binary search)
 #endif
 #ifndef DEM_FORCE_UT_ASYNC
-#define DEM_FORCE_UT_ASYNC 1  // previous u_t staged by cp.async into the thread's part[] slots
+#define DEM_FORCE_UT_ASYNC 0  // 1: previous u_t staged by cp.async into the thread's part[] slots (A/B: force 3.94 -> 5.10 ms)
 #endif
 #ifndef DEM_FORCE_LAZY_OWN
-#define DEM_FORCE_LAZY_OWN 1  // own clump's record read from shared memory at its uses (fewer spills)
+#define DEM_FORCE_LAZY_OWN 0  // 1: own clump's record read (volatile) from shared memory at its uses: fewer spills, A/B neutral
 #endif
 #ifndef DEM_FORCE_ASYNC_EPI
 #define DEM_FORCE_ASYNC_EPI 0  // 1: own clumps' q, Omega, inertia staged by cp.async in the prologue (A/B: 3.96 -> 4.73 ms)

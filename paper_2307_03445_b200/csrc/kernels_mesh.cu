@@ -89,6 +89,7 @@ __global__ void __launch_bounds__(256) k_mesh_pairs(StepArgs a) {
         const int slot = atomicAdd(&a.row_cnt[idx], 1);
         if (slot < a.row_width) {
           a.slots[(size_t)slot * a.ns_own + idx] = code;
+          if (DEM_SLOT_KEYS) a.slot_key[(size_t)slot * a.ns_own + idx] = 0x7fffffffffffffffLL - (long long)(-1 - code);
         } else {
           atomicMax(&a.ctl->need_width, (long long)slot + 1);
           atomicExch(a.abort, 1);

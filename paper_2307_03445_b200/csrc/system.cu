@@ -101,6 +101,7 @@ struct dem_system {
   int2* d_cta_clump = nullptr;  // per CTA boundary: (first clump, first sphere)
   int n_cta = 0;
   int* d_slots = nullptr;  // fixed-width candidate partner lists of the owned spheres
+  long long* d_slot_key = nullptr;  // their partner keys (DEM_SLOT_KEYS)
   int row_width = 0;
   int n_sm = 148;
   // bins
@@ -312,6 +313,7 @@ static StepArgs make_args(dem_system* sys, int kind, bool det = false) {
   a.s_key = sys->d_s_key;
   a.spos = sys->d_spos;
   a.slots = sys->d_slots;
+  a.slot_key = sys->d_slot_key;
   a.row_width = sys->row_width;
   a.cta_clump = sys->d_cta_clump;
   a.n_cta = sys->n_cta;
@@ -1183,12 +1185,39 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
   }
   double rmean = ns ? rsum / ns : sys->rmax;
   double cell = sys->P.cell_size > 0 ? sys->P.cell_size : std::max(4.0 * rmean, 2.0 * sys->rmin) + sys->P.margin;
-  // bin region: the domain (distributed: restricted in x to the slab and its halo; spheres that
-  // stray outside the bin region are clamped into its edge bins, which stays exact)
+  // bin region: the box the held spheres occupy now, widened by 2 bins on every side, within the
+  // domain (distributed: also restricted in x to the slab and its halo).  Spheres that later
+  // stray outside it are clamped into its edge bins, which stays exact (only speed depends on the
+  // bins) — and a bed whose top lies far below the domain ceiling, or a slab of a long bed, is not
+  // charged for bins that hold nothing.
   double blo[3], bhi[3];
   for (int d = 0; d < 3; ++d) {
     blo[d] = sys->P.domain_lo[d];
     bhi[d] = sys->P.domain_hi[d];
+  }
+  if (n_hold > 0) {
+    std::vector<double> rb(sys->n_tmpl, 0.0);  // bounding radius of each template
+    for (int t = 0; t < sys->n_tmpl; ++t)
+      for (int j = 0; j < sys->tpl_ncomp[t]; ++j) {
+        const double* o = &sys->tc_off[3 * (sys->tpl_coff[t] + j)];
+        rb[t] = std::max(rb[t], std::sqrt(o[0] * o[0] + o[1] * o[1] + o[2] * o[2]) + sys->tc_rad[sys->tpl_coff[t] + j]);
+      }
+    double lo3[3] = {1e300, 1e300, 1e300}, hi3[3] = {-1e300, -1e300, -1e300};
+    for (int64_t c = 0; c < n; ++c) {
+      if (!role[c]) continue;
+      for (int d = 0; d < 3; ++d) {
+        const double x = src[0][3 * c + d];
+        if (!std::isfinite(x)) continue;
+        lo3[d] = std::min(lo3[d], x - rb[t[c]]);
+        hi3[d] = std::max(hi3[d], x + rb[t[c]]);
+      }
+    }
+    for (int d = 0; d < 3; ++d)
+      if (hi3[d] >= lo3[d]) {
+        blo[d] = std::max(blo[d], lo3[d] - 2.0 * cell);
+        bhi[d] = std::min(bhi[d], hi3[d] + 2.0 * cell);
+        if (!(bhi[d] > blo[d])) bhi[d] = blo[d] + cell;
+      }
   }
   if (sys->dist) {
     blo[0] = std::max(blo[0], sys->P.slab_lo - sys->P.halo);
@@ -1364,6 +1393,7 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
   // on overflow (the rows of a settled bed hold a few entries)
   sys->row_width = kRowWidth;
   TRY(alloc_arr(sys, &sys->d_slots, (size_t)sys->ns_own * sys->row_width + 1));
+  if (DEM_SLOT_KEYS) TRY(alloc_arr(sys, &sys->d_slot_key, (size_t)sys->ns_own * sys->row_width + 1));
   // CTA partition of the fused force/integrate kernel: consecutive whole clumps, at most
   // force_cta_clumps() clumps and force_cta_spheres() spheres per CTA
   // (owned clumps only: ghosts are integrated by their owners)
@@ -1702,6 +1732,7 @@ static dem_status regrow(dem_system* sys, int up, int ep, int since, int kind, b
   if (sys->h_ctl->need_width > sys->row_width) {
     sys->row_width = (int)std::min<long long>(sys->h_ctl->need_width + 8, 1 << 16);
     TRY(alloc_arr(sys, &sys->d_slots, (size_t)sys->ns_own * sys->row_width + 1));
+    if (DEM_SLOT_KEYS) TRY(alloc_arr(sys, &sys->d_slot_key, (size_t)sys->ns_own * sys->row_width + 1));
     grew = true;
   }
   if (grew) sys->regrows++;

@@ -1,9 +1,16 @@
 """NEXT-4 as SURVEY §8f specifies: the repose angle of config C3 (BASELINE config 3).
 
 C3 = 100k GRC-1-like DS clumps (Table-1 mix, seeded RSA in a vertical r = 6 cm cylinder at a
-bounding-sphere solid fraction of 0.25) released from rest above the plane z = 0 (P:277, P:299:
-"the angle of repose ... 30 degrees").  The column collapses onto the floor and spreads into a
-pile; the run continues until the pile is at rest, then the free-surface angle is fitted.
+bounding-sphere solid fraction of 0.25, a 1.5 m column) released from rest above the plane z = 0
+("the angle of repose ... 30 degrees").
+
+Protocol (the lifted-cylinder test): the column falls into an open cylinder (a 48-facet triangle-
+mesh tube, NEXT-3) of radius --tube standing on the plane; once the material has settled in it,
+the tube is lifted at --lift m/s ("constant velocity") and the material flows out under it
+into a free cone; the run continues until the pile is at rest, then the free-surface angle is
+fitted.  Dropping the column straight onto the plane (--tube 0) does not make a pile: the 5 m/s
+impacts spread the material into a flat layer out to the far walls (round-2 run: pile radius
+0.25 m, fitted "angle" -4 to -9 degrees).
 
 Reproducible from the seed: the scene is workloads.c3_repose(seed), the solver runs the paper's
 deferred cadence (rebuild every k steps with the margin 2 v_max h k; the device
@@ -11,7 +18,7 @@ reports DEM_ERR_VMAX if any sphere outruns it) on the GPU (the oracle is far too
 millions of steps), and the angle is fitted over several radial ranges; the acceptance band is
 30 +- 5 degrees.  Writes gpurun_out/<out>.json (+ the final state .npz).
 
-    python tools/repose_c3.py [--seed 3] [--max-steps 4000000] [--out r02/repose_c3]
+    python tools/repose_c3.py [--seed 3] [--tube 0.09] [--lift 0.1] [--out r02/repose_c3]
 """
 import argparse
 import json
@@ -67,6 +74,9 @@ def main():
     ap.add_argument("--vmax", type=float, default=8.0, help="speed bound of the deferred margin [m/s]")
     ap.add_argument("--cell", type=float, default=4.0e-3, help="bin edge [m]")
     ap.add_argument("--out", default="r02/repose_c3")
+    ap.add_argument("--tube", type=float, default=0.09, help="radius of the lifted cylinder [m] (0: plain drop)")
+    ap.add_argument("--lift", type=float, default=0.1, help="lifting speed of the cylinder [m/s]")
+    ap.add_argument("--settle-ke", type=float, default=2e-3, help="kinetic energy [J] below which the lift starts")
     a = ap.parse_args()
     import torch
 
@@ -75,6 +85,11 @@ def main():
 
     torch.cuda.set_device(0)
     s = w.c3_repose(seed=a.seed)
+    tube_h = float(s.domain_hi[2])
+    if a.tube > 0:
+        from workloads.scenes import Mesh, mesh_funnel
+
+        s.meshes = [Mesh(mesh_funnel(a.tube, a.tube, tube_h, 48), 0, pos=(0.0, 0.0, 0.0))]
     k = a.cd_every
     margin = 2.0 * a.vmax * s.h * k
     g = dem.system_from_scene(s, margin=margin, cd_every=k, cell_size=a.cell)
@@ -84,9 +99,12 @@ def main():
     os.makedirs(os.path.dirname(out_base), exist_ok=True)
     log, t0, steps, rest = [], time.time(), 0, 0
     order = np.argsort(s.gid)
+    lifting, tube_z = False, 0.0
     while steps < a.max_steps:
         g.dem_step(a.chunk)
         steps += a.chunk
+        if a.tube > 0:
+            tube_z = float(g.dem_get_mesh(0)["pos"][2])
         st = g.dem_get_state()
         o = np.argsort(st["gid"])
         v, pos = st["vel"][o], st["pos"][o]
@@ -95,13 +113,19 @@ def main():
         st_ = g.dem_get_stats()
         rec = dict(step=steps, t_s=round(steps * s.h, 4), ke_j=ke, vmax=float(speed.max()),
                    v99=float(np.quantile(speed, 0.99)), zmax=float(pos[:, 2].max()),
-                   contacts=int(st_["n_contacts"]), wall_s=round(time.time() - t0, 1))
+                   contacts=int(st_["n_contacts"]), wall_s=round(time.time() - t0, 1), tube_z=round(tube_z, 4))
+        if a.tube > 0 and not lifting and ke < a.settle_ke and steps * s.h > 0.5:
+            # settled in the tube: lift it at constant speed, straight up
+            g.dem_set_mesh_motion(0, (0.0, 0.0, tube_z), (1.0, 0.0, 0.0, 0.0), (0.0, 0.0, a.lift), (0.0, 0.0, 0.0))
+            lifting = True
+            rec["lift_start"] = True
         if steps % (5 * a.chunk) == 0:
             r_mid, surf, _ = surface_profile(pos, rb[order])
             rec["R"], rec["angles"] = fit_angles(r_mid, surf)
         log.append(rec)
         print(json.dumps(rec), flush=True)
-        rest = rest + 1 if (rec["v99"] < 0.01 and rec["vmax"] < 0.2 and steps * s.h > 0.8) else 0
+        free = a.tube <= 0 or (lifting and tube_z > float(pos[:, 2].max()) + 0.02)  # tube clear of the pile
+        rest = rest + 1 if (free and rec["v99"] < 0.01 and rec["vmax"] < 0.2 and steps * s.h > 0.8) else 0
         if rest >= 3:
             break
     st = g.dem_get_state()
@@ -113,7 +137,8 @@ def main():
     R, angles = fit_angles(r_mid, surf)
     vals = list(angles.values())
     wall = time.time() - t0
-    res = dict(scene=s.name, seed=a.seed, clumps=s.n_clumps, spheres=s.n_spheres, steps=steps,
+    res = dict(scene=s.name, protocol=(f"lifted cylinder r = {a.tube} m at {a.lift} m/s" if a.tube > 0 else "drop"),
+               seed=a.seed, clumps=s.n_clumps, spheres=s.n_spheres, steps=steps,
                sim_time_s=steps * s.h, h=s.h, cd_every=k, margin_m=margin, cell_m=a.cell, gpu_wall_s=wall,
                sphere_steps_per_s=s.n_spheres * steps / wall, at_rest=rest >= 3, pile_radius_m=R,
                pile_centre=centre, angle_deg=float(np.median(vals)), angle_fits_deg=angles,
