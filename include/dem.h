@@ -164,6 +164,8 @@ typedef struct {
   int64_t migration_bytes;    /* ... and the bytes of those clumps and of the contacts routed with them */
   int64_t ghost_exchange_bytes; /* bytes this rank sent to complete its neighbours' ghost bands (last
                                    dem_set_state_local / migration) */
+  int64_t bin_regrids;        /* bin grids laid out again because a sphere centre left the bin region
+                                 (the region is the box the spheres occupied, within the domain) */
 } dem_stats;
 
 typedef struct dem_system dem_system;

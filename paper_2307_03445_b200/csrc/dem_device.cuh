@@ -37,7 +37,7 @@ struct Ctl {
   long long need_entries;
   long long need_width;  // row-slot width a rebuild needed (fixed-width candidate rows)
   int det_abort;         // capacity overflow of a set detected ahead (overlapped cadence)
-  int pad_;
+  int need_regrid;       // a sphere centre left the bin region (the host re-grids between step batches)
 };
 
 #ifndef DEM_UT_PAD
@@ -47,8 +47,17 @@ constexpr int kUt = DEM_UT_PAD ? 4 : 3;  // doubles per entry of the tangential 
 #ifndef DEM_V256
 #define DEM_V256 1  // 256-bit gathers of the 32-byte records (sm_100 LDG.256)
 #endif
+#ifndef DEM_SCATTER_RANKS
+#define DEM_SCATTER_RANKS 0  // 1: ranks from the counting atomics, scatter without atomics; A/B on C5: pose
+                             // 1.14 -> 1.70 ms (returning atomics), scatter 1.02 -> 0.95: dropped
+#endif
+// Spheres with at most kRankW bin inserts keep the rank their counting atomic returned (so the
+// scatter needs no atomic); their counts live in the low 16 bits of cell_count, those of larger
+// spheres (which take their slots with an atomic in the scatter) in the high 16 bits.
+constexpr int kRankW = 8;
 #ifndef DEM_SLOT_KEYS
-#define DEM_SLOT_KEYS 1
+#define DEM_SLOT_KEYS 0  // 1: partner keys written beside the slots by k_pairs; A/B on C5: pairs 4.71 -> 5.31 ms,
+                         // rows 1.61 -> 1.65 ms (the flush gathers cost more than the row kernel saves)
 #endif
 #ifndef DEM_KIN_TID
 #define DEM_KIN_TID 0  // 1: the clump's template id rides in the kinematics record (slot 10); A/B: force
@@ -117,6 +126,8 @@ struct Grid {
   int ax[3];        // axes from fastest to slowest
   double inv_n_ax[2];  // 1 / n[ax[0]], 1 / n[ax[1]] for the fast bin-id decode
   double pad;  // r + pad is the half-extent of a sphere's bin AABB (margin/2 + eps)
+  double reg_lo[3], reg_hi[3];  // a centre outside these (where the bin region is tighter than the
+                                // domain) asks for a re-grid: Ctl::need_regrid
 };
 
 // A row entry as the force kernel reads it (8 bytes); the partner keys live in their own array
@@ -203,6 +214,7 @@ struct StepArgs {
   const double* xref;        // [3 n_own] owned COMs at dem_set_state (distributed drift check)
   double drift_max;          // 0: no check
   int* cell_count;
+  unsigned short* irank;     // [kRankW][ns] each insert's rank in its bin, from the counting atomics (DEM_SCATTER_RANKS)
   int* cell_start;
   int* items;                // [cap_inserts] bin items: sphere index | lowest-bin mask << 29
   int* row_cnt;              // walls + sphere partners per sphere (built by atomics each step)

@@ -71,6 +71,9 @@ __device__ __forceinline__ void pose_sphere(const StepArgs& a, int i, int c, int
     if (dx * dx + dy * dy + dz * dz > a.half_margin * a.half_margin) raise_error(a.ctl, -13, a.s_key[i], a.gid[c]);
   }
   if (!a.count) return;
+  if (cx < g.reg_lo[0] || cx > g.reg_hi[0] || cy < g.reg_lo[1] || cy > g.reg_hi[1] || cz < g.reg_lo[2] ||
+      cz > g.reg_hi[2])
+    a.ctl->need_regrid = 1;  // clamped into an edge bin (exact, but slow if many): re-grid soon
   if (a.ref_out) a.ref_out[i] = make_double4(cx, cy, cz, r);
   // sphere-plane candidates: (r + margin) - (c - p_w).n_w >= 0
   unsigned wmask = 0;
@@ -87,11 +90,34 @@ __device__ __forceinline__ void pose_sphere(const StepArgs& a, int i, int c, int
   cell_range(g, 0, cx, r, lx, hx);
   cell_range(g, 1, cy, r, ly, hy);
   cell_range(g, 2, cz, r, lz, hz);
+#if DEM_SCATTER_RANKS
+  const int nins = (hx - lx + 1) * (hy - ly + 1) * (hz - lz + 1);
+  if (nins <= kRankW) {
+    // the old count is this insert's rank among the bin's small-sphere inserts: kept for the scatter
+    int k = 0;
+    for (int z = lz; z <= hz; ++z)
+      for (int y = ly; y <= hy; ++y) {
+        const long long base = z * g.st[2] + y * g.st[1];
+        for (int x = lx; x <= hx; ++x, ++k) {
+          const int old = atomicAdd(&a.cell_count[base + x * g.st[0]], 1);
+          if ((old & 0xffff) == 0xffff) raise_error(a.ctl, -14, a.s_key[i], 0);  // 65535 in one bin: bins too coarse
+          a.irank[(size_t)k * a.ns + i] = (unsigned short)(old & 0xffff);
+        }
+      }
+    return;
+  }
+  for (int z = lz; z <= hz; ++z)
+    for (int y = ly; y <= hy; ++y) {
+      const long long base = z * g.st[2] + y * g.st[1];
+      for (int x = lx; x <= hx; ++x) atomicAdd(&a.cell_count[base + x * g.st[0]], 0x10000);
+    }
+#else
   for (int z = lz; z <= hz; ++z)
     for (int y = ly; y <= hy; ++y) {
       const long long base = z * g.st[2] + y * g.st[1];
       for (int x = lx; x <= hx; ++x) atomicAdd(&a.cell_count[base + x * g.st[0]], 1);
     }
+#endif
 }
 
 __device__ __forceinline__ void kin_record(const StepArgs& a, int c, const double* R, double X, double Y, double Z) {
@@ -177,13 +203,28 @@ __global__ void __launch_bounds__(DEM_SCATTER_LB) k_bin_scatter(StepArgs a) {
   cell_range(g, 0, s.x, s.w, lx, hx);
   cell_range(g, 1, s.y, s.w, ly, hy);
   cell_range(g, 2, s.z, s.w, lz, hz);
+#if DEM_SCATTER_RANKS
+  const bool small = (hx - lx + 1) * (hy - ly + 1) * (hz - lz + 1) <= kRankW;
+  int k = 0;
+#endif
   for (int z = lz; z <= hz; ++z)
     for (int y = ly; y <= hy; ++y) {
       const long long base = z * g.st[2] + y * g.st[1];
       for (int x = lx; x <= hx; ++x) {
         const long long cid = base + x * g.st[0];
         const int start = a.cell_start[cid];  // issued before the atomic: the two are independent
+#if DEM_SCATTER_RANKS
+        // small spheres: the rank from the counting pass; large ones after all small ones of the bin
+        int slot;
+        if (small) {
+          slot = a.irank[(size_t)(k++) * a.ns + i];
+        } else {
+          const unsigned old = (unsigned)atomicSub(&a.cell_count[cid], 0x10000);
+          slot = (int)((old & 0xffffu) + (old >> 16)) - 1;
+        }
+#else
         const int slot = atomicSub(&a.cell_count[cid], 1) - 1;
+#endif
         // the item carries the sphere's lowest-bin mask for k_pairs (ns < 2^29, checked)
         if (fits) a.items[start + slot] = i | (((x == lx ? 1 : 0) | (y == ly ? 2 : 0) | (z == lz ? 4 : 0)) << 29);
       }

@@ -751,3 +751,38 @@ void launch_abort_or(const AbortWords& w, cudaStream_t s) {
 }
 }  // namespace dem
 
+namespace dem {
+// bounding box of the sphere centres (re-grid, system.cu): ordered 64-bit keys of the doubles
+__device__ __forceinline__ unsigned long long ord_key(double v) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__global__ void k_bbox(const double4* __restrict__ spos, int ns, unsigned long long* box) {
+  unsigned long long lo[3] = {~0ull, ~0ull, ~0ull}, hi[3] = {0ull, 0ull, 0ull};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ns; i += gridDim.x * blockDim.x) {
+    const double4 p = spos[i];
+    const unsigned long long k[3] = {ord_key(p.x - p.w), ord_key(p.y - p.w), ord_key(p.z - p.w)};
+    const unsigned long long K[3] = {ord_key(p.x + p.w), ord_key(p.y + p.w), ord_key(p.z + p.w)};
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      lo[d] = min(lo[d], k[d]);
+      hi[d] = max(hi[d], K[d]);
+    }
+  }
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[d] = min(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
+      hi[d] = max(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(&box[d], lo[d]);
+      atomicMax(&box[3 + d], hi[d]);
+    }
+  }
+}
+void launch_bbox(const double4* spos, int ns, unsigned long long* box, cudaStream_t s) {
+  if (ns) k_bbox<<<148 * 4, 256, 0, s>>>(spos, ns, box);
+}
+}  // namespace dem
+

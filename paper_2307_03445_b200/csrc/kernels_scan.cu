@@ -45,7 +45,7 @@ __device__ __forceinline__ int block_excl_scan(int v, int* total) {
 
 __global__ void __launch_bounds__(kScanThreads) k_scan_tiles(const int* __restrict__ in, int* __restrict__ out,
                                                              int* __restrict__ tile_sums, long long n,
-                                                             const int* abort, const int* abort2) {
+                                                             const int* abort, const int* abort2, int packed) {
   if ((abort && *abort) || (abort2 && *abort2)) return;
   const long long base = (long long)blockIdx.x * kScanTile + (long long)threadIdx.x * kScanItems;
   int v[kScanItems];
@@ -53,6 +53,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_tiles(const int* __restri
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
     v[k] = (base + k < n) ? in[base + k] : 0;
+    if (packed) v[k] = (v[k] & 0xffff) + ((unsigned)v[k] >> 16);  // bin counts: small + large inserts
     s += v[k];
   }
   int total;
@@ -94,13 +95,13 @@ long long scan_tiles_needed(long long n) { return (n + kScanTile - 1) / kScanTil
 
 // out must hold n + 1 ints; tmp must hold scan_tiles_needed(n) ints
 void launch_excl_scan(const int* in, int* out, long long n, int* tmp, const int* abort, cudaStream_t s,
-                      const int* abort2) {
+                      const int* abort2, int packed) {
   long long tiles = scan_tiles_needed(n);
   if (tiles == 0) {
     cudaMemsetAsync(out, 0, sizeof(int), s);
     return;
   }
-  k_scan_tiles<<<(unsigned)tiles, kScanThreads, 0, s>>>(in, out, tmp, n, abort, abort2);
+  k_scan_tiles<<<(unsigned)tiles, kScanThreads, 0, s>>>(in, out, tmp, n, abort, abort2, packed);
   k_scan_sums<<<1, kScanThreads, 0, s>>>(tmp, (int)tiles, out + n, abort, abort2);
   k_scan_add<<<(unsigned)tiles, kScanThreads, 0, s>>>(out, tmp, n, abort, abort2);
 }

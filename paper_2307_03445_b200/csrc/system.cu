@@ -28,7 +28,7 @@ int force_cta_clumps();
 int force_cta_spheres();
 long long scan_tiles_needed(long long n);
 void launch_excl_scan(const int* in, int* out, long long n, int* tmp, const int* abort, cudaStream_t s,
-                      const int* abort2 = nullptr);
+                      const int* abort2, int packed = 0);
 void launch_count_canonical(const Rows& r, const long long* s_key, int ns, unsigned long long* out, cudaStream_t s);
 void launch_pack(const State& st, const int* idx, int n, double* buf, cudaStream_t s);
 void launch_unpack(const State& st, const int* idx, int n, const double* buf, cudaStream_t s);
@@ -37,6 +37,7 @@ void launch_mesh_pose(const StepArgs&, cudaStream_t);
 void launch_peer_signal(const Ctl* ctl, int* r0, int* r1, cudaStream_t s);
 void launch_peer_wait(Ctl* ctl, const int* f0, const int* f1, cudaStream_t s);
 void launch_abort_or(const AbortWords& w, cudaStream_t s);
+void launch_bbox(const double4* spos, int ns, unsigned long long* box, cudaStream_t s);
 void launch_state_in(const State& st, const int* perm, int n, const double* pos, const double* quat,
                      const double* vel, const double* om, int* bad, double* xref, int n_own, cudaStream_t s);
 void launch_state_out(const State& st, const int* outpos, int n_own, double* pos, double* quat, double* vel,
@@ -108,6 +109,7 @@ struct dem_system {
   Grid grid{};
   long long ncell = 0, cap_inserts = 0;
   int *d_cell_count = nullptr, *d_cell_start = nullptr, *d_items = nullptr;
+  unsigned short* d_irank = nullptr;  // [kRankW][ns] insert ranks (DEM_SCATTER_RANKS)
   int *d_row_cnt = nullptr, *d_scan_tmp = nullptr;
   unsigned short* d_wall_mask = nullptr;
   // rows: the entry sets (row_ptr, ent) of rows[ep] are the latest contact set and ping-pong
@@ -177,6 +179,7 @@ struct dem_system {
   bool peer_linked = false;
   int64_t fast_resets = 0;
   int64_t migrated_clumps = 0, migration_bytes = 0, ghost_bytes = 0;  // last migration / ghost exchange
+  int64_t regrids = 0;  // bin grids rebuilt around spheres that left the bin region
 };
 
 static dem_status peer_release(dem_system* sys);
@@ -322,6 +325,7 @@ static StepArgs make_args(dem_system* sys, int kind, bool det = false) {
   a.xref = sys->d_xref;
   a.drift_max = sys->dist ? sys->P.drift_max : 0.0;
   a.cell_count = sys->d_cell_count;
+  a.irank = sys->d_irank;
   a.cell_start = sys->d_cell_start;
   a.items = sys->d_items;
   a.row_cnt = sys->d_row_cnt;
@@ -407,6 +411,9 @@ static void enqueue_pose(dem_system* sys, int kind, cudaStream_t s, cudaEvent_t*
     launch_peer_wait(sys->d_ctl, sys->remote_flag[0] ? sys->d_flags : nullptr,
                      sys->remote_flag[1] ? sys->d_flags + 1 : nullptr, s);
   launch_mesh_pose(a, s);
+  // the scatter no longer returns the bin counts to zero (the small spheres take their ranks from
+  // the counting pass): clear them before a counting pass
+  if (DEM_SCATTER_RANKS && a.count) cudaMemsetAsync(sys->d_cell_count, 0, sizeof(int) * sys->ncell, s);
   launch_pose_count(a, s);
   if (ev) cudaEventRecord(ev[1], s);
 }
@@ -419,7 +426,8 @@ static void enqueue_detect(dem_system* sys, int kind, cudaStream_t s, cudaEvent_
   const int* abort = a.abort;
   const int* abort2 = &sys->d_ctl->abort;
   if (run && sys->n_tri) cudaMemsetAsync(a.mlist_out_n, 0, sizeof(int), s);
-  if (run) launch_excl_scan(sys->d_cell_count, sys->d_cell_start, sys->ncell, sys->d_scan_tmp, abort, s, abort2);
+  if (run) launch_excl_scan(sys->d_cell_count, sys->d_cell_start, sys->ncell, sys->d_scan_tmp, abort, s, abort2,
+                           DEM_SCATTER_RANKS);
   if (ev) cudaEventRecord(ev[2], s);
   if (run) launch_bin_scatter(a, s);
   if (run) launch_mesh_pairs(a, s);
@@ -1046,6 +1054,85 @@ extern "C" dem_status dem_get_mesh(dem_system* sys, int32_t mesh, double pos[3],
 }
 
 // ------------------------------------------------------------------ state
+// The bin grid: edge `cell`; region = the box the held spheres occupy
+// (box_lo/box_hi, empty if lo > hi) widened by 2 bins on every side, within the domain
+// (distributed: also within slab +- halo in x).  Spheres that later stray outside the region are
+// clamped into its edge bins, which stays exact (only speed depends on the bins); a centre that
+// leaves it where it is tighter than the domain raises Ctl::need_regrid, and dem_step re-grids
+// between step batches.  So a bed whose top lies far below the domain ceiling, or a slab of a
+// long bed, is not charged for bins that hold nothing.  coarsen: grow the edge while a sparse
+// region would need more than max(4M, 16 ns) bins (automatic cell size only).
+static dem_status grid_layout(dem_system* sys, double cell, const double* box_lo, const double* box_hi, int64_t ns,
+                              bool coarsen) {
+  double blo[3], bhi[3];
+  bool tight_lo[3], tight_hi[3];
+  for (int d = 0; d < 3; ++d) {
+    blo[d] = sys->P.domain_lo[d];
+    bhi[d] = sys->P.domain_hi[d];
+    if (box_hi[d] >= box_lo[d]) {
+      blo[d] = std::max(blo[d], box_lo[d] - 2.0 * cell);
+      bhi[d] = std::min(bhi[d], box_hi[d] + 2.0 * cell);
+      if (!(bhi[d] > blo[d])) bhi[d] = blo[d] + cell;
+    }
+    tight_lo[d] = blo[d] > sys->P.domain_lo[d];
+    tight_hi[d] = bhi[d] < sys->P.domain_hi[d];
+  }
+  if (sys->dist) {
+    blo[0] = std::max(blo[0], sys->P.slab_lo - sys->P.halo);
+    bhi[0] = std::min(bhi[0], sys->P.slab_hi + sys->P.halo);
+    if (!(bhi[0] > blo[0])) bhi[0] = blo[0] + cell;
+    tight_lo[0] = tight_hi[0] = false;  // the slab band is fixed; drift is guarded by drift_max
+  }
+  const long long max_cells = std::max<long long>(4LL << 20, 16 * ns);
+  auto cells_for = [&](double c) {
+    long long m = 1;
+    for (int d = 0; d < 3; ++d) m *= (long long)std::ceil((bhi[d] - blo[d]) / c) + 1;
+    return m;
+  };
+  if (coarsen && sys->P.cell_size <= 0)
+    while (cells_for(cell) > max_cells) cell *= 1.25;
+  Grid& G = sys->grid;
+  G.cell = cell;
+  G.inv_cell = 1.0 / cell;
+  G.pad = 0.5 * sys->P.margin + 1e-9;
+  long long ncell = 1;
+  for (int d = 0; d < 3; ++d) {
+    G.lo[d] = blo[d];
+    G.dom_lo[d] = sys->P.domain_lo[d];
+    G.dom_hi[d] = sys->P.domain_hi[d];
+    G.reg_lo[d] = tight_lo[d] ? blo[d] : -1e300;
+    G.reg_hi[d] = tight_hi[d] ? bhi[d] : 1e300;
+    long long nd = (long long)std::ceil((bhi[d] - blo[d]) / cell) + 1;
+    if (nd > (1LL << 20)) {
+      sys->err = "grid too fine for the domain";
+      return DEM_ERR_INVALID_ARG;
+    }
+    G.n[d] = (int)nd;
+    ncell *= nd;
+  }
+  if (ncell > (1LL << 31) - 2) {
+    sys->err = "too many bins; increase cell_size";
+    return DEM_ERR_INVALID_ARG;
+  }
+  sys->ncell = ncell;
+  // bin linearization: the axis with the fewest bins fastest, the longest slowest, so the
+  // neighbours of a bin along every axis stay close in memory (and x-slabs are contiguous
+  // for the usual longest-x beds)
+  int ord[3] = {0, 1, 2};
+#ifndef DEM_XFAST
+  std::sort(ord, ord + 3, [&](int p, int q) { return G.n[p] != G.n[q] ? G.n[p] < G.n[q] : p > q; });
+#endif
+  long long st = 1;
+  for (int k = 0; k < 3; ++k) {
+    G.st[ord[k]] = st;
+    st *= G.n[ord[k]];
+    G.ax[k] = ord[k];
+  }
+  G.inv_n_ax[0] = 1.0 / G.n[ord[0]];
+  G.inv_n_ax[1] = 1.0 / G.n[ord[1]];
+  return DEM_OK;
+}
+
 extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* gid, const int32_t* tid,
                                     const double* pos, const double* quat, const double* vel, const double* omega,
                                     int32_t on_device) {
@@ -1185,94 +1272,28 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
   }
   double rmean = ns ? rsum / ns : sys->rmax;
   double cell = sys->P.cell_size > 0 ? sys->P.cell_size : std::max(4.0 * rmean, 2.0 * sys->rmin) + sys->P.margin;
-  // bin region: the box the held spheres occupy now, widened by 2 bins on every side, within the
-  // domain (distributed: also restricted in x to the slab and its halo).  Spheres that later
-  // stray outside it are clamped into its edge bins, which stays exact (only speed depends on the
-  // bins) — and a bed whose top lies far below the domain ceiling, or a slab of a long bed, is not
-  // charged for bins that hold nothing.
-  double blo[3], bhi[3];
-  for (int d = 0; d < 3; ++d) {
-    blo[d] = sys->P.domain_lo[d];
-    bhi[d] = sys->P.domain_hi[d];
-  }
+  // bin region: the box the held spheres occupy now (grid_layout)
+  double box_lo[3] = {1e300, 1e300, 1e300}, box_hi[3] = {-1e300, -1e300, -1e300};
   if (n_hold > 0) {
     std::vector<double> rb(sys->n_tmpl, 0.0);  // bounding radius of each template
-    for (int t = 0; t < sys->n_tmpl; ++t)
-      for (int j = 0; j < sys->tpl_ncomp[t]; ++j) {
-        const double* o = &sys->tc_off[3 * (sys->tpl_coff[t] + j)];
-        rb[t] = std::max(rb[t], std::sqrt(o[0] * o[0] + o[1] * o[1] + o[2] * o[2]) + sys->tc_rad[sys->tpl_coff[t] + j]);
+    for (int tt = 0; tt < sys->n_tmpl; ++tt)
+      for (int j = 0; j < sys->tpl_ncomp[tt]; ++j) {
+        const double* o = &sys->tc_off[3 * (sys->tpl_coff[tt] + j)];
+        rb[tt] = std::max(rb[tt], std::sqrt(o[0] * o[0] + o[1] * o[1] + o[2] * o[2]) + sys->tc_rad[sys->tpl_coff[tt] + j]);
       }
-    double lo3[3] = {1e300, 1e300, 1e300}, hi3[3] = {-1e300, -1e300, -1e300};
     for (int64_t c = 0; c < n; ++c) {
       if (!role[c]) continue;
       for (int d = 0; d < 3; ++d) {
         const double x = src[0][3 * c + d];
         if (!std::isfinite(x)) continue;
-        lo3[d] = std::min(lo3[d], x - rb[t[c]]);
-        hi3[d] = std::max(hi3[d], x + rb[t[c]]);
+        box_lo[d] = std::min(box_lo[d], x - rb[t[c]]);
+        box_hi[d] = std::max(box_hi[d], x + rb[t[c]]);
       }
     }
-    for (int d = 0; d < 3; ++d)
-      if (hi3[d] >= lo3[d]) {
-        blo[d] = std::max(blo[d], lo3[d] - 2.0 * cell);
-        bhi[d] = std::min(bhi[d], hi3[d] + 2.0 * cell);
-        if (!(bhi[d] > blo[d])) bhi[d] = blo[d] + cell;
-      }
   }
-  if (sys->dist) {
-    blo[0] = std::max(blo[0], sys->P.slab_lo - sys->P.halo);
-    bhi[0] = std::min(bhi[0], sys->P.slab_hi + sys->P.halo);
-    if (!(bhi[0] > blo[0])) bhi[0] = blo[0] + cell;
-  }
-  // the bin edge only changes speed, never results: coarsen it while a sparse domain would
-  // need more than max(4M, 16 ns) bins
-  const long long max_cells = std::max<long long>(4LL << 20, 16 * ns);
-  auto cells_for = [&](double c) {
-    long long m = 1;
-    for (int d = 0; d < 3; ++d) m *= (long long)std::ceil((bhi[d] - blo[d]) / c) + 1;
-    return m;
-  };
-  if (sys->P.cell_size <= 0)
-    while (cells_for(cell) > max_cells) cell *= 1.25;
+  TRY(grid_layout(sys, cell, box_lo, box_hi, ns, true));
   Grid& G = sys->grid;
-  G.cell = cell;
-  G.inv_cell = 1.0 / cell;
-  G.pad = 0.5 * sys->P.margin + 1e-9;
-  long long ncell = 1;
-  for (int d = 0; d < 3; ++d) {
-    G.lo[d] = blo[d];
-    G.dom_lo[d] = sys->P.domain_lo[d];
-    G.dom_hi[d] = sys->P.domain_hi[d];
-    long long nd = (long long)std::ceil((bhi[d] - blo[d]) / cell) + 1;
-    if (nd > (1LL << 20)) {
-      sys->err = "grid too fine for the domain";
-      return DEM_ERR_INVALID_ARG;
-    }
-    G.n[d] = (int)nd;
-    ncell *= nd;
-  }
-  if (ncell > (1LL << 31) - 2) {
-    sys->err = "too many bins; increase cell_size";
-    return DEM_ERR_INVALID_ARG;
-  }
-  sys->ncell = ncell;
-  // bin linearization: the axis with the fewest bins fastest, the longest slowest, so the
-  // neighbours of a bin along every axis stay close in memory (and x-slabs are contiguous
-  // for the usual longest-x beds)
-  {
-    int ord[3] = {0, 1, 2};
-#ifndef DEM_XFAST
-    std::sort(ord, ord + 3, [&](int p, int q) { return G.n[p] != G.n[q] ? G.n[p] < G.n[q] : p > q; });
-#endif
-    long long s = 1;
-    for (int k = 0; k < 3; ++k) {
-      G.st[ord[k]] = s;
-      s *= G.n[ord[k]];
-      G.ax[k] = ord[k];
-    }
-    G.inv_n_ax[0] = 1.0 / G.n[ord[0]];
-    G.inv_n_ax[1] = 1.0 / G.n[ord[1]];
-  }
+  const long long ncell = sys->ncell;
   // storage order: owned clumps, then ghosts, each sorted by the bin of the COM (spatial
   // locality for every gather); results do not depend on it (keys, canonical sums).
   // h_perm maps storage -> caller index.
@@ -1361,7 +1382,7 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
   long long ins = 0;
   for (int64_t s = 0; s < ns; ++s) {
     double e = sys->tc_rad[sys->h_s_tc[s]] + G.pad;
-    long long m = (long long)std::floor(2.0 * e / cell) + 2;
+    long long m = (long long)std::floor(2.0 * e / G.cell) + 2;
     ins += m * m * m;
   }
   if (ins > (1LL << 31) - 2) ins = (1LL << 31) - 2;
@@ -1416,6 +1437,7 @@ extern "C" dem_status dem_set_state(dem_system* sys, int64_t n, const int64_t* g
   TRY(ensure_mesh_buffers(sys));
   TRY(alloc_arr(sys, &sys->d_cta_clump, cta.size()));
   TRY(alloc_arr(sys, &sys->d_cell_count, ncell));
+  if (DEM_SCATTER_RANKS) TRY(alloc_arr(sys, &sys->d_irank, (size_t)kRankW * ns + 1));
   TRY(alloc_arr(sys, &sys->d_cell_start, ncell + 1));
   TRY(alloc_arr(sys, &sys->d_items, ins));
   TRY(alloc_arr(sys, &sys->d_row_cnt, ns + 1));
@@ -1745,6 +1767,47 @@ static dem_status regrow(dem_system* sys, int up, int ep, int since, int kind, b
   return DEM_OK;
 }
 
+// A sphere centre left the bin region where it is tighter than the domain (Ctl::need_regrid):
+// lay the grid out again around the spheres' current box (same edge; results do not depend on
+// the bins), between step batches.
+static dem_status regrid(dem_system* sys) {
+  CK(cudaStreamSynchronize(sys->det_stream));  // a set detected ahead may still read the old bins
+  unsigned long long* d_box = (unsigned long long*)dalloc(sys, 6 * sizeof(unsigned long long));
+  if (!d_box) return DEM_ERR_OOM;
+  const unsigned long long init[6] = {~0ull, ~0ull, ~0ull, 0ull, 0ull, 0ull};
+  unsigned long long box[6];
+  CK(cudaMemcpyAsync(d_box, init, sizeof init, cudaMemcpyHostToDevice, sys->stream));
+  launch_bbox(sys->d_spos, (int)sys->ns, d_box, sys->stream);
+  CK(cudaMemcpyAsync(box, d_box, sizeof box, cudaMemcpyDeviceToHost, sys->stream));
+  CK(cudaStreamSynchronize(sys->stream));
+  dfree(sys, d_box);
+  auto val = [](unsigned long long k) {
+    const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+    double v;
+    std::memcpy(&v, &b, sizeof v);
+    return v;
+  };
+  double lo[3], hi[3];
+  for (int d = 0; d < 3; ++d) {
+    lo[d] = val(box[d]);
+    hi[d] = val(box[3 + d]);
+  }
+  TRY(grid_layout(sys, sys->grid.cell, lo, hi, sys->ns, true));
+  TRY(alloc_arr(sys, &sys->d_cell_count, sys->ncell));
+  TRY(alloc_arr(sys, &sys->d_cell_start, sys->ncell + 1));
+  TRY(alloc_arr(sys, &sys->d_scan_tmp, std::max(scan_tiles_needed(sys->ncell), scan_tiles_needed(sys->ns)) + 1));
+  CK(cudaMemsetAsync(sys->d_cell_count, 0, sizeof(int) * sys->ncell, sys->stream));
+  free_graphs(sys);
+  sys->regrids++;
+  sys->h_ctl->need_regrid = 0;
+  CK(cudaMemcpyAsync(sys->d_ctl, sys->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, sys->stream));
+  CK(cudaStreamSynchronize(sys->stream));
+  return DEM_OK;
+}
+
+// steps enqueued per status check (the status word is read, and a re-grid done, between batches)
+static constexpr int64_t kStepBatch = 2048;
+
 extern "C" dem_status dem_step(dem_system* sys, int64_t n_steps) {
   if (!sys || n_steps < 0) return DEM_ERR_INVALID_ARG;
   if (sys->peer && sys->P.transport == DEM_TRANSPORT_PEER && !sys->peer_linked) {
@@ -1763,8 +1826,9 @@ extern "C" dem_status dem_step(dem_system* sys, int64_t n_steps) {
   while (remaining > 0) {
     const int64_t done_before = sys->h_ctl->step;
     sched.clear();
-    if (sys->profiling) TRY(ensure_events(sys, remaining));
-    for (int64_t k = 0; k < remaining; ++k) {
+    const int64_t batch = std::min<int64_t>(remaining, kStepBatch);
+    if (sys->profiling) TRY(ensure_events(sys, batch));
+    for (int64_t k = 0; k < batch; ++k) {
       const int kind = step_kind(sys);
       sched.push_back(Sched{sys->up, sys->ep, sys->since_rebuild, sys->pending});
       if (sys->profiling) {
@@ -1813,7 +1877,10 @@ extern "C" dem_status dem_step(dem_system* sys, int64_t n_steps) {
     sys->steps_done = sys->h_ctl->step;
     if (sys->h_ctl->err_code) return device_error(sys);
     remaining -= done;
-    if (!sys->h_ctl->abort) break;
+    if (!sys->h_ctl->abort) {
+      if (sys->h_ctl->need_regrid) TRY(regrid(sys));
+      continue;
+    }
     if (sys->dist && !sys->comm) {  // a local regrow would desynchronise the ranks' halo exchanges
       sys->err = "capacity overflow on a distributed system without an NCCL communicator (raise params.entries_per_sphere)";
       return DEM_ERR_CAPACITY;
@@ -2088,6 +2155,7 @@ extern "C" dem_status dem_get_stats(dem_system* sys, dem_stats* out) {
   out->kernel_launches_per_step =
       kLaunchesPerStep + (sys->dist ? (sys->peer ? 2 : 4) : 0) + (sys->n_mesh ? 3 : 0);
   out->state_fast_resets = sys->fast_resets;
+  out->bin_regrids = sys->regrids;
   out->migrated_clumps = sys->migrated_clumps;
   out->migration_bytes = sys->migration_bytes;
   out->ghost_exchange_bytes = sys->ghost_bytes;

@@ -1,0 +1,70 @@
+"""Bin grid around the occupied box, re-laid out when spheres leave it.
+
+The bins only change speed, never results: a cloud of clumps released from a small box into a
+large domain flies out of its initial bin region; dem_step re-grids between step batches
+(dem_stats.bin_regrids) and the contact set and states stay those of the oracle."""
+import numpy as np
+import pytest
+
+import oracle
+from _parity import assert_forces_close, assert_same_contact_set, assert_states_close
+import workloads as w
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dem():
+    import torch
+
+    assert torch.cuda.is_available()
+    import paper_2307_03445_b200 as pkg
+
+    return pkg
+
+
+def _cloud():
+    from workloads.scenes import rsa_bed
+
+    # 150 DS clumps placed without overlaps (RSA of bounding spheres) in a 24 mm cube
+    s = rsa_bed(21, 150, lo=(0.0, 0.0, 0.0), hi=(0.024, 0.024, 0.024))
+    s.planes = []
+    s.gravity = np.zeros(3)
+    # an outward burst: every clump also moves away from the cloud centre at 3 m/s
+    d = s.pos - s.pos.mean(axis=0)
+    s.vel = s.vel + 3.0 * d / np.linalg.norm(d, axis=1, keepdims=True)
+    s.domain_lo = np.full(3, -0.05)
+    s.domain_hi = np.full(3, 0.075)
+    return s
+
+
+def test_regrid_when_spheres_leave_the_bin_region(dem):
+    s = _cloud()
+    g = dem.system_from_scene(s, record_contacts=True)
+    o = oracle.Oracle(s)
+    cells0 = g.dem_get_stats()["n_cells"]
+    for n in (1, 2499, 2500):  # dem_step batches of 2048 steps: re-grids inside the longer calls
+        g.dem_step(n)
+        o.step(n)
+    st = g.dem_get_stats()
+    assert st["bin_regrids"] >= 1 and st["n_cells"] > cells0
+    cg, co = g.dem_get_contacts(), o.contacts()
+    assert_same_contact_set(cg, co)
+    assert_forces_close(cg, co, s)
+    assert_states_close(g.dem_get_state(), o.state(), dict(pos=s.pos, quat=s.quat))
+
+
+def test_bin_region_is_the_occupied_box(dem):
+    """A bed far below its domain ceiling gets bins only where it is (and 2 bins of slack)."""
+    from workloads import beds
+
+    s = beds.load_patch()
+    tall = s.copy()
+    tall.domain_hi = np.array(s.domain_hi, dtype=float) + np.array([0.0, 0.0, 0.5])
+    a, b = dem.system_from_scene(s), dem.system_from_scene(tall)
+    assert a.dem_get_stats()["n_cells"] == b.dem_get_stats()["n_cells"]
+    a.dem_step(5)
+    b.dem_step(5)
+    sa, sb = a.dem_get_state(), b.dem_get_state()
+    for k in ("pos", "quat", "vel", "omega"):
+        assert np.array_equal(sa[k], sb[k]), k

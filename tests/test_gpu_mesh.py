@@ -76,8 +76,9 @@ def test_one_contact_per_feature_matches_oracle(dem, at):
 @pytest.mark.parametrize("k,overlap", [(1, False), (4, False), (4, True)])
 def test_mesh_with_deferred_overlapped_cadence(dem, k, overlap):
     s = beds.patch_mesh(cone_speed=0.5)
-    # the cone starts inside the bed: the first steps eject spheres at tens of m/s (v_max 100 m/s)
-    margin = 2.0 * 100.0 * s.h * (2 * k - 2 if overlap else k)
+    # the cone starts 1 mm inside the bed: the first steps eject the spheres it overlaps at up to
+    # ~100 m/s (a 1 mm Hertz overlap on a 0.8 mm sphere), so the margin covers 400 m/s
+    margin = 2.0 * 400.0 * s.h * (2 * k - 2 if overlap else k)
     g = dem.system_from_scene(s, record_contacts=True, margin=margin, cd_every=k, overlap=overlap)
     o = oracle.Oracle(s, margin=margin, cd_every=k, overlap=overlap)
     for it in range(3):

@@ -49,6 +49,28 @@ def launch_summary(csv_path):
     return "\n".join(lines) + "\n"
 
 
+def atomics_summary(csv_path):
+    """Per-kernel means of the explicitly requested atomic / L2 / DRAM counters (north_star)."""
+    text = open(csv_path).read()
+    text = text[text.index('"ID"'):]
+    rows = list(csv.DictReader(io.StringIO(text)))
+    per = {}
+    for r in rows:
+        k = r["Kernel Name"].split("(")[0].replace("void ", "")
+        try:
+            v = float(r["Metric Value"].replace(",", ""))
+        except ValueError:
+            continue
+        per.setdefault(k, {}).setdefault(f"{r['Metric Name']} [{r['Metric Unit']}]", []).append(v)
+    out = {k: {m: sum(v) / len(v) for m, v in ms.items()} for k, ms in per.items()}
+    lines = ["ncu --clock-control none --metrics <atomic, L2 and DRAM counters> (C5 bed, mean per launch)"]
+    for k, ms in out.items():
+        lines.append(k)
+        for m, v in sorted(ms.items()):
+            lines.append(f"   {m:75s} {v:.6g}")
+    return out, "\n".join(lines) + "\n"
+
+
 def main(rnd):
     src = os.path.join(ROOT, "gpurun_out", rnd)
     dst = os.path.join(ROOT, "profiles", rnd)
@@ -64,6 +86,11 @@ def main(rnd):
     if os.path.exists(lc):
         shutil.copy(lc, os.path.join(dst, "ncu_launches_c5.csv"))
         open(os.path.join(dst, "ncu_launches_c5_summary.txt"), "w").write(launch_summary(lc))
+    at = os.path.join(src, "atomics.csv")
+    if os.path.exists(at):
+        d, txt = atomics_summary(at)
+        json.dump(d, open(os.path.join(dst, "ncu_atomics.json"), "w"), indent=1)
+        open(os.path.join(dst, "ncu_atomics.txt"), "w").write(txt)
     rep = os.path.join(src, "full.ncu-rep")
     if os.path.exists(rep):
         s = summarise(rep)
