@@ -820,6 +820,9 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
 // each entry's history index found in the sphere's previous row ("persist between
 // timesteps"; -1 for a contact born this step).  Rows of up to kRegRow candidates — nearly
 // all of them — are sorted and matched in registers; longer ones in place in memory.
+#ifndef DEM_ROWS_LOCAL
+#define DEM_ROWS_LOCAL 24  // rows up to this long sorted in a thread-local array (0: in place in the row)
+#endif
 #ifndef DEM_REG_ROW
 #define DEM_REG_ROW 6  // A/B on the C5 bench: 6 beats 5, 7 and 8 (rows 1.80 vs 1.97-2.08 ms)
 #endif
@@ -901,6 +904,35 @@ __global__ void __launch_bounds__(DEM_ROWS_TPB, DEM_ROWS_MINB) k_rows_finish(Ste
         R[q] = e;
         K[q] = kk[q];
       }
+#if DEM_ROWS_LOCAL
+  } else if (nc <= DEM_ROWS_LOCAL) {
+    // longer rows (the big spheres): sorted in a thread-local array (local memory, cached in L1
+    // write-back) instead of in place in the global row
+    long long kl[DEM_ROWS_LOCAL];
+    int tl[DEM_ROWS_LOCAL];
+    for (int u = 0; u < nc; ++u) {
+      const int t = S[(size_t)u * a.ns_own];
+      const long long xk = DEM_SLOT_KEYS ? SK[(size_t)u * a.ns_own] : partner_key(a, t);
+      int v = u - 1;
+      while (v >= 0 && kl[v] > xk) {
+        kl[v + 1] = kl[v];
+        tl[v + 1] = tl[v];
+        --v;
+      }
+      kl[v + 1] = xk;
+      tl[v + 1] = t;
+    }
+    int pj = pb;  // merge with the previous row (both sorted by key)
+    for (int u = 0; u < nc; ++u) {
+      const long long k = kl[u];
+      while (pj < pe && a.prev.key[pj] < k) ++pj;
+      Entry e;
+      e.partner = tl[u];
+      e.prev = (pj < pe && a.prev.key[pj] == k) ? pj : -1;
+      R[u] = e;
+      K[u] = k;
+    }
+#endif
   } else {
     for (int u = 0; u < nc; ++u) {
       const int t = S[(size_t)u * a.ns_own];

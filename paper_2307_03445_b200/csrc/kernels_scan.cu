@@ -8,6 +8,9 @@
 
 namespace dem {
 
+#ifndef DEM_SCAN_V4
+#define DEM_SCAN_V4 1  // 16-byte loads and stores of whole 4-count groups (the arrays are 256-byte aligned)
+#endif
 constexpr int kScanThreads = 1024;
 constexpr int kScanItems = 4;
 constexpr int kScanTile = kScanThreads * kScanItems;
@@ -50,18 +53,29 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_tiles(const int* __restri
   const long long base = (long long)blockIdx.x * kScanTile + (long long)threadIdx.x * kScanItems;
   int v[kScanItems];
   int s = 0;
+  const bool whole = DEM_SCAN_V4 && base + kScanItems <= n;  // one 16-byte load / store per thread
+  if (whole) {
+    const int4 q = *reinterpret_cast<const int4*>(in + base);
+    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+  }
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
-    v[k] = (base + k < n) ? in[base + k] : 0;
+    if (!whole) v[k] = (base + k < n) ? in[base + k] : 0;
     if (packed) v[k] = (v[k] & 0xffff) + ((unsigned)v[k] >> 16);  // bin counts: small + large inserts
     s += v[k];
   }
   int total;
   int off = block_excl_scan(s, &total);
+  if (whole) {
+    int4 q;
+    q.x = off; q.y = off + v[0]; q.z = q.y + v[1]; q.w = q.z + v[2];
+    *reinterpret_cast<int4*>(out + base) = q;
+  } else {
 #pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    if (base + k < n) out[base + k] = off;
-    off += v[k];
+    for (int k = 0; k < kScanItems; ++k) {
+      if (base + k < n) out[base + k] = off;
+      off += v[k];
+    }
   }
   if (threadIdx.x == 0) tile_sums[blockIdx.x] = total;
 }
@@ -87,6 +101,15 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_add(int* out, const int* 
   const int add = tile_sums[blockIdx.x];
   if (add == 0) return;
   const long long base = (long long)blockIdx.x * kScanTile;
+  if (DEM_SCAN_V4 && base + kScanTile <= n) {
+    int4* o = reinterpret_cast<int4*>(out + base);
+    for (int k = threadIdx.x; k < kScanTile / 4; k += kScanThreads) {
+      int4 q = o[k];
+      q.x += add; q.y += add; q.z += add; q.w += add;
+      o[k] = q;
+    }
+    return;
+  }
   for (int k = threadIdx.x; k < kScanTile; k += kScanThreads)
     if (base + k < n) out[base + k] += add;
 }

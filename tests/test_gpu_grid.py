@@ -27,14 +27,17 @@ def _cloud():
     from workloads.scenes import rsa_bed
 
     # 150 DS clumps placed without overlaps (RSA of bounding spheres) in a 24 mm cube
+    from workloads.scenes import box_planes
+
     s = rsa_bed(21, 150, lo=(0.0, 0.0, 0.0), hi=(0.024, 0.024, 0.024))
-    s.planes = []
     s.gravity = np.zeros(3)
-    # an outward burst: every clump also moves away from the cloud centre at 3 m/s
+    # an outward burst at 6 m/s into walls 12 mm outside the cube: the clumps leave the bin region
+    # (the cube + 2 bins) within ~1.5 ms and hit the walls after ~2 ms
     d = s.pos - s.pos.mean(axis=0)
-    s.vel = s.vel + 3.0 * d / np.linalg.norm(d, axis=1, keepdims=True)
-    s.domain_lo = np.full(3, -0.05)
-    s.domain_hi = np.full(3, 0.075)
+    s.vel = s.vel + 6.0 * d / np.linalg.norm(d, axis=1, keepdims=True)
+    s.planes = box_planes(np.full(3, -0.012), np.full(3, 0.036), 0)
+    s.domain_lo = np.full(3, -0.013)
+    s.domain_hi = np.full(3, 0.037)
     return s
 
 
@@ -43,14 +46,20 @@ def test_regrid_when_spheres_leave_the_bin_region(dem):
     g = dem.system_from_scene(s, record_contacts=True)
     o = oracle.Oracle(s)
     cells0 = g.dem_get_stats()["n_cells"]
-    for n in (1, 2499, 2500):  # dem_step batches of 2048 steps: re-grids inside the longer calls
-        g.dem_step(n)
-        o.step(n)
+    g.dem_step(2000)  # one batch (dem_step checks the status word every 2048 steps): re-grid after it
+    o.step(2000)
     st = g.dem_get_stats()
     assert st["bin_regrids"] >= 1 and st["n_cells"] > cells0
-    cg, co = g.dem_get_contacts(), o.contacts()
-    assert_same_contact_set(cg, co)
-    assert_forces_close(cg, co, s)
+    seen = 0
+    for _ in range(16):  # the clumps bounce off the walls: compare every contact set met on the way
+        g.dem_step(150)
+        o.step(150)
+        cg, co = g.dem_get_contacts(), o.contacts()
+        assert_same_contact_set(cg, co)
+        if len(co["key_a"]):
+            assert_forces_close(cg, co, s)
+        seen += len(co["key_a"])
+    assert seen > 10
     assert_states_close(g.dem_get_state(), o.state(), dict(pos=s.pos, quat=s.quat))
 
 
