@@ -105,10 +105,14 @@ def stage_bytes(st):
         # 2 row-count atomics (read + write) per pair
         "pairs": nc * 4 + ins * 4 + ns * 36 + pairs * 24,
         "row_scan": ns * 8,
-        # row bounds of the new and previous rows, the pose kernel's wall mask; entries written and
-        # the previous row's entries read once; per pair 2 candidate slots + 2 partner keys
-        "rows_finish": ns * 18 + ent * 32 + pairs * 2 * 12,
-        "force+integrate": ns * (32 + 8 + 8) + n * (80 + 56 + 4 + 104) + ent * 72,
+        # row bounds of the new and previous rows, the pose kernel's wall mask; entries written
+        # (8-byte {partner, prev} + 8-byte key) and the previous row's keys read once; per pair 2
+        # candidate slots + 2 partner keys
+        "rows_finish": ns * 18 + ent * 24 + pairs * 2 * 12,
+        # own spheres' record, material, clump; the clumps' kinematics records + q, Omega, template
+        # read and the new state written; per entry its 8-byte record, the old u_t read and the new
+        # one written (24 bytes each)
+        "force+integrate": ns * (32 + 8 + 8) + n * (80 + 56 + 4 + 104) + ent * 56,
     }
 
 
