@@ -18,7 +18,7 @@ reports DEM_ERR_VMAX if any sphere outruns it) on the GPU (the oracle is far too
 millions of steps), and the angle is fitted over several radial ranges; the acceptance band is
 30 +- 5 degrees.  Writes gpurun_out/<out>.json (+ the final state .npz).
 
-    python tools/repose_c3.py [--seed 3] [--tube 0.09] [--lift 0.1] [--out r02/repose_c3]
+    python tools/repose_c3.py [--seed 3] [--tube 0.09] [--lift 0.02] [--cd-every 10] [--vmax 16] [--out r02/repose_c3]
 """
 import argparse
 import json
@@ -68,14 +68,14 @@ def fit_angles(r_mid, surf, min_layer=6e-3):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seed", type=int, default=3)
-    ap.add_argument("--max-steps", type=int, default=4_000_000)
+    ap.add_argument("--max-steps", type=int, default=8_000_000)
     ap.add_argument("--chunk", type=int, default=100_000)
-    ap.add_argument("--cd-every", type=int, default=20)
-    ap.add_argument("--vmax", type=float, default=8.0, help="speed bound of the deferred margin [m/s]")
+    ap.add_argument("--cd-every", type=int, default=10)
+    ap.add_argument("--vmax", type=float, default=16.0, help="speed bound of the deferred margin [m/s]")
     ap.add_argument("--cell", type=float, default=4.0e-3, help="bin edge [m]")
     ap.add_argument("--out", default="r02/repose_c3")
     ap.add_argument("--tube", type=float, default=0.09, help="radius of the lifted cylinder [m] (0: plain drop)")
-    ap.add_argument("--lift", type=float, default=0.1, help="lifting speed of the cylinder [m/s]")
+    ap.add_argument("--lift", type=float, default=0.02, help="lifting speed of the cylinder [m/s]")
     ap.add_argument("--settle-ke", type=float, default=2e-3, help="kinetic energy [J] below which the lift starts")
     a = ap.parse_args()
     import torch
