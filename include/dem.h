@@ -166,6 +166,8 @@ typedef struct {
                                    dem_set_state_local / migration) */
   int64_t bin_regrids;        /* bin grids laid out again because a sphere centre left the bin region
                                  (the region is the box the spheres occupied, within the domain) */
+  int64_t reruns;             /* re-runs after an aborted step: a capacity regrow, an overflowed set
+                                 detected ahead (overlapped cadence), or another rank's overflow */
 } dem_stats;
 
 typedef struct dem_system dem_system;

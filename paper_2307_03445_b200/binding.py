@@ -58,7 +58,7 @@ class dem_stats(C.Structure):
                 ("n_entries", C.c_int64), ("n_contacts", C.c_int64), ("n_inserts", C.c_int64), ("n_cells", C.c_int64),
                 ("cell_size", C.c_double), ("regrows", C.c_int64), ("kernel_launches_per_step", C.c_int64),
                 ("state_fast_resets", C.c_int64), ("migrated_clumps", C.c_int64), ("migration_bytes", C.c_int64),
-                ("ghost_exchange_bytes", C.c_int64), ("bin_regrids", C.c_int64)]
+                ("ghost_exchange_bytes", C.c_int64), ("bin_regrids", C.c_int64), ("reruns", C.c_int64)]
 
 
 TRANSPORT_NCCL, TRANSPORT_LOOPBACK, TRANSPORT_PEER, TRANSPORT_LOOPBACK_PEER = 0, 1, 2, 3

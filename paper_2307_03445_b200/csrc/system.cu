@@ -179,6 +179,7 @@ struct dem_system {
   bool peer_linked = false;
   int64_t fast_resets = 0;
   int64_t migrated_clumps = 0, migration_bytes = 0, ghost_bytes = 0;  // last migration / ghost exchange
+  int64_t reruns = 0;   // aborted steps re-run (regrow, ahead-set overflow, another rank's overflow)
   int64_t regrids = 0;  // bin grids rebuilt around spheres that left the bin region
 };
 
@@ -1758,6 +1759,7 @@ static dem_status regrow(dem_system* sys, int up, int ep, int since, int kind, b
     grew = true;
   }
   if (grew) sys->regrows++;
+  sys->reruns++;
   free_graphs(sys);
   sys->h_ctl->abort = 0;
   sys->h_ctl->need_entries = 0;
@@ -2156,6 +2158,7 @@ extern "C" dem_status dem_get_stats(dem_system* sys, dem_stats* out) {
       kLaunchesPerStep + (sys->dist ? (sys->peer ? 2 : 4) : 0) + (sys->n_mesh ? 3 : 0);
   out->state_fast_resets = sys->fast_resets;
   out->bin_regrids = sys->regrids;
+  out->reruns = sys->reruns;
   out->migrated_clumps = sys->migrated_clumps;
   out->migration_bytes = sys->migration_bytes;
   out->ghost_exchange_bytes = sys->ghost_bytes;
