@@ -38,6 +38,12 @@ constexpr int kPairStride = 8;  // doubles per material pair in Tables::pair
 #ifndef DEM_FORCE_ASYNC_EPI
 #define DEM_FORCE_ASYNC_EPI 0  // 1: own clumps' q, Omega, inertia staged by cp.async in the prologue (A/B: 3.96 -> 4.73 ms)
 #endif
+#ifndef DEM_FORCE_PRO
+#define DEM_FORCE_PRO 1  // batched prologue loads + the first chunk's entries issued before the barrier
+#endif
+#ifndef DEM_FORCE_EPI_EARLY
+#define DEM_FORCE_EPI_EARLY 0  // 1: q, Omega, template id cp.async-ed into own_p during the last sums (A/B on C5: force 3.84 -> 3.94 ms)
+#endif
 #ifndef DEM_FORCE_FT
 #define DEM_FORCE_FT 128
 #endif
@@ -142,6 +148,71 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
   const int s0 = b0.y;
   const int nsph = b1.y - s0;
   const int E0g = a.rows.row_ptr[s0];
+#if DEM_FORCE_PRO
+  // Batched prologue: every load of the CTA's staging (row bounds, own sphere records, materials,
+  // clumps, kinematics records) and the first chunk's row entry are issued before any of them is
+  // stored, so the prologue costs one memory round trip instead of one per staging loop.
+  static_assert(kMaxS < 2 * kFT && kFC * (kKinUsed / 2) <= 2 * kFT, "two staging loads per thread");
+  Entry ent_first;
+  ent_first.partner = -1;
+  ent_first.prev = -1;
+  {
+    const double2* src = reinterpret_cast<const double2*>(a.kin + (size_t)kKin * c0);
+    int r0v[2], r1v[2], mv[2], cv[2];
+    double4 pv[2];
+    double2 kv[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int k = tid + u * kFT;
+      r0v[u] = k <= nsph ? a.rows.row_ptr[s0 + k] : 0;
+      r1v[u] = k < nsph ? a.rows.row_ptr[s0 + k + 1] : 0;
+      if (k < nsph) {
+        pv[u] = ldg256(a.spos + s0 + k);
+        mv[u] = a.s_mat[s0 + k];
+        cv[u] = a.s_clump[s0 + k];
+      }
+      if (k < ncl * (kKinUsed / 2)) {
+        const int c = k / (kKinUsed / 2), r = k - c * (kKinUsed / 2);
+        kv[u] = src[c * (kKin / 2) + r];
+      }
+    }
+    const int E1g = a.rows.row_ptr[s0 + nsph];
+    if (E0g + tid < E1g) ent_first = a.rows.ent[E0g + tid];
+#if DEM_FORCE_PRO >= 2
+    // and the first chunk's partner sphere record, clump and material, copied into this thread's
+    // column of part[] in the background (written by this thread only after it read them)
+    if (ent_first.partner >= 0) {
+      const int t = ent_first.partner;
+      const double* ps = reinterpret_cast<const double*>(a.spos + t);
+#pragma unroll
+      for (int d = 0; d < 4; ++d) {
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(&part[d][tid]);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(ps + d) : "memory");
+      }
+      int* pi = reinterpret_cast<int*>(&part[4][tid]);
+      const unsigned d0 = (unsigned)__cvta_generic_to_shared(pi), d1 = (unsigned)__cvta_generic_to_shared(pi + 1);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d0), "l"(a.s_clump + t) : "memory");
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d1), "l"(a.s_mat + t) : "memory");
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+#endif
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int k = tid + u * kFT;
+      if (k <= nsph) rp[k] = r0v[u];
+      if (k < nsph) {
+        if (DEM_FORCE_OWNER)
+          for (int q = max(r0v[u], E0g); q < min(r1v[u], E0g + kFT); ++q) own_of[q - E0g] = (unsigned char)k;
+        own_p[k] = pv[u];
+        own_mat[k] = mv[u];
+        own_lc[k] = cv[u] - c0;
+#pragma unroll
+        for (int q = 0; q < 6; ++q) acc[q][k] = 0.0;
+      }
+      if (k < ncl * (kKinUsed / 2)) reinterpret_cast<double2*>(ck)[k] = kv[u];
+    }
+  }
+#else
   for (int k = tid; k <= nsph; k += kFT) {
     const int r0 = a.rows.row_ptr[s0 + k];
     rp[k] = r0;
@@ -167,6 +238,7 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
       reinterpret_cast<double2*>(ck)[k] = src[c * (kKin / 2) + r];
     }
   }
+#endif
   if (DEM_FORCE_ASYNC_EPI && tid < ncl) {
     // the integrating thread's q, Omega (body) and inertia, copied to shared memory in the
     // background (cp.async, no registers held) and awaited only after the entry loop
@@ -186,6 +258,10 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
   __syncthreads();
   const double h = a.h;
   const int E0 = rp[0], E1 = rp[nsph];
+#if DEM_FORCE_EPI_EARLY
+  static_assert(8 * kFC <= 4 * kMaxS, "q, Omega and the template id of the CTA's clumps fit in own_p");
+  bool epi = false;  // this thread's epilogue loads were issued (cp.async into own_p)
+#endif
   for (int c0e = E0; c0e < E1; c0e += kFT) {
     const int e = c0e + tid;
     if (kMesh) emesh[tid] = -1;
@@ -211,7 +287,11 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
       const double* ki = ck + kKinUsed * own_lc[ls];
       const double Mi = ki[9];
 #endif
+#if DEM_FORCE_PRO
+      const Entry ent = c0e == E0 ? ent_first : a.rows.ent[e];
+#else
       const Entry ent = a.rows.ent[e];
+#endif
       const int t = ent.partner;
       // (a4) history remap: the slot of this key in the previous rows was found by the
       // row merge in k_rows_finish (-1: contact born this step, u_t = 0)
@@ -277,9 +357,25 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
         rbar = ri;
         mbar = Mi;
       } else if (!wall) {
+#if DEM_FORCE_PRO >= 2
+        double4 pj;
+        const double* kjp;
+        if (c0e == E0) {  // the prologue's copies of this partner
+          asm volatile("cp.async.wait_all;" ::: "memory");
+          pj = make_double4(part[0][tid], part[1][tid], part[2][tid], part[3][tid]);
+          const int* pi = reinterpret_cast<const int*>(&part[4][tid]);
+          kjp = a.kin + (size_t)kKin * pi[0];
+          mj = pi[1];
+        } else {
+          pj = ldg256(a.spos + t);
+          kjp = a.kin + (size_t)kKin * a.s_clump[t];
+          mj = a.s_mat[t];
+        }
+#else
         const double4 pj = ldg256(a.spos + t);
         const double* kjp = a.kin + (size_t)kKin * a.s_clump[t];
         mj = a.s_mat[t];
+#endif
         const double rj = pj.w;
         const double dx = pj.x - cx, dy = pj.y - cy, dz = pj.z - cz;
         const double dist = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
@@ -427,6 +523,26 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
       }
     }
     __syncthreads();
+#if DEM_FORCE_EPI_EARLY
+    if (c0e + kFT >= E1 && tid < ncl) {
+      // the last chunk is evaluated, so own_p[] is free: the integrating thread's q, Omega and
+      // template id are copied into it in the background (cp.async: no registers held) while
+      // the per-sphere sums run, and awaited at the integration
+      const int c = c0 + tid;
+      const double* src[7] = {a.cur.qw + c, a.cur.qx + c, a.cur.qy + c, a.cur.qz + c, a.cur.wx + c, a.cur.wy + c,
+                              a.cur.wz + c};
+      double* eq = reinterpret_cast<double*>(own_p);
+#pragma unroll
+      for (int k = 0; k < 7; ++k) {
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(eq + k * kFC + tid);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src[k]) : "memory");
+      }
+      const unsigned dt = (unsigned)__cvta_generic_to_shared(reinterpret_cast<int*>(eq + 7 * kFC) + tid);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dt), "l"(a.tid + c) : "memory");
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      epi = true;
+    }
+#endif
     // only thread 0 reads or clears chunk_mesh between the barriers (the other threads set it
     // before the barrier above and next after the barrier below)
     if (kMesh && tid == 0 && *(volatile int*)&chunk_mesh) {
@@ -479,6 +595,23 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
   const double I0 = cq[7][tid], I1 = cq[8][tid], I2 = cq[9][tid];
   const double qw = cq[0][tid], qx = cq[1][tid], qy = cq[2][tid], qz = cq[3][tid];
   const double w0 = cq[4][tid], w1 = cq[5][tid], w2 = cq[6][tid];
+#elif DEM_FORCE_EPI_EARLY
+  double eq[7];
+  int et;
+  if (epi) {
+    asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's own copies
+    const double* sq = reinterpret_cast<const double*>(own_p);
+#pragma unroll
+    for (int k = 0; k < 7; ++k) eq[k] = sq[k * kFC + tid];
+    et = reinterpret_cast<const int*>(sq + 7 * kFC)[tid];
+  } else {
+    eq[0] = a.cur.qw[c]; eq[1] = a.cur.qx[c]; eq[2] = a.cur.qy[c]; eq[3] = a.cur.qz[c];
+    eq[4] = a.cur.wx[c]; eq[5] = a.cur.wy[c]; eq[6] = a.cur.wz[c];
+    et = a.tid[c];
+  }
+  const double I0 = a.tab.tpl_inertia[3 * et], I1 = a.tab.tpl_inertia[3 * et + 1], I2 = a.tab.tpl_inertia[3 * et + 2];
+  const double qw = eq[0], qx = eq[1], qy = eq[2], qz = eq[3];
+  const double w0 = eq[4], w1 = eq[5], w2 = eq[6];
 #else
   const int tt = DEM_KIN_TID ? (int)__double_as_longlong(ck[kKinUsed * tid + 10]) : a.tid[c];
   const double I0 = a.tab.tpl_inertia[3 * tt], I1 = a.tab.tpl_inertia[3 * tt + 1], I2 = a.tab.tpl_inertia[3 * tt + 2];
@@ -578,8 +711,15 @@ static void force_carveout() {
   }
 }
 
+// a system that holds no owned clump (empty, or a rank whose slab is empty) still counts its steps
+__global__ void k_step_tick(Ctl* ctl) {
+  if (!ctl->abort) ctl->step += 1;
+}
 void launch_force_integrate(const StepArgs& a, cudaStream_t s) {
-  if (a.n_cta <= 0) return;
+  if (a.n_cta <= 0) {
+    k_step_tick<<<1, 1, 0, s>>>(a.ctl);
+    return;
+  }
   force_carveout<true, true>();
   force_carveout<true, false>();
   force_carveout<false, true>();

@@ -1880,6 +1880,10 @@ extern "C" dem_status dem_step(dem_system* sys, int64_t n_steps) {
     if (sys->h_ctl->err_code) return device_error(sys);
     remaining -= done;
     if (!sys->h_ctl->abort) {
+      if (done == 0) {  // (never: every enqueued step either completes or aborts)
+        sys->err = "dem_step: a batch of steps completed none without an abort";
+        return DEM_ERR_CUDA;
+      }
       if (sys->h_ctl->need_regrid) TRY(regrid(sys));
       continue;
     }
