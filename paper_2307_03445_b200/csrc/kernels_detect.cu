@@ -488,7 +488,8 @@ __device__ __forceinline__ bool candidate(const StepArgs& a, const int2& mi, con
   // (r_a + r_b) + 0 is r_a + r_b exactly: the margin add is skipped when there is none
   const double s = kMargin ? add(add(pi.w, pj.w), a.margin) : add(pi.w, pj.w);
   // ghost-ghost pairs belong to other ranks (only a distributed system holds ghosts)
-  return mi.x != mj.x && (!kGhosts || min(mi.x, mj.x) < a.n_own) && d2 <= mul(s, s);
+  // (bitwise &: the pair arithmetic runs unconditionally, no branch around it)
+  return (mi.x != mj.x) & (!kGhosts || min(mi.x, mj.x) < a.n_own) & (d2 <= mul(s, s));
 }
 
 constexpr int kTri = kFlatMax * (kFlatMax - 1) / 2;
@@ -500,8 +501,12 @@ __constant__ float c_rcp[kFlatMax + 8] = {1.0f,      DEM_R8(1),  DEM_R8(9),  DEM
 #undef DEM_R8
 
 // one pair of the flat path: the predicate, and the two sphere indices of a hit
+#ifndef DEM_PAIRS_NODIV
+#define DEM_PAIRS_NODIV 1
+#endif
 template <bool kGhosts, bool kMargin>
-__device__ __forceinline__ bool flat_pair(const StepArgs& a, const Members& A, int i, int j, int& ia, int& ib) {
+__device__ __forceinline__ bool flat_pair(const StepArgs& a, const Members& A, int i, int j, int& ia, int& ib,
+                                          bool valid = true) {
 #if DEM_PAIRS_F32
   // different clumps, at least one owned, and the conservative fp32 pre-test (exact test at the flush)
   const int ci = A.clump[i], cj = A.clump[j];
@@ -517,7 +522,7 @@ __device__ __forceinline__ bool flat_pair(const StepArgs& a, const Members& A, i
   }
 #elif DEM_PAIRS_SPLIT
   const int2 mi = make_int2(A.clump[i], 0), mj = make_int2(A.clump[j], 0);
-  const bool hit = candidate<kGhosts, kMargin>(a, mi, mj, A.get(i), A.get(j));
+  const bool hit = valid & candidate<kGhosts, kMargin>(a, mi, mj, A.get(i), A.get(j));
   if (hit) {
     ia = A.item[i];
     ib = A.item[j];
@@ -600,9 +605,22 @@ struct RowDec {
 
 // Row of the member at slot l (group-ordered): partner start lo, count cnt and offset off in the
 // bin's pair numbering (closed forms of the sums of the earlier rows).
+#ifndef DEM_PAIRS_ROWSEL
+#define DEM_PAIRS_ROWSEL 1  // member_row by selects instead of an if-else chain (no divergent branches)
+#endif
 __device__ __forceinline__ void member_row(int l, int m, int n7, int n6, int n5, int n3, int n4, int s1, int s2,
                                            int s3, int s4, int s5, int e0, int e1, int e2, int& lo, int& cnt,
                                            int& off) {
+#if DEM_PAIRS_ROWSEL
+  (void)n6; (void)n5;
+  const bool c0 = l < n7, c1 = !c0 & (l < s1), c2 = (l >= s5) & (l < s3), c3 = (l >= s3) & (l < s2);
+  lo = c0 ? l + 1 : c1 ? s1 : c2 ? s3 : s4;
+  cnt = c0 ? m - 1 - l : c1 ? s2 - s1 : c2 ? s4 - s3 : c3 ? n4 : 0;
+  const int base = c1 ? e0 : c2 ? e1 : e2, l0 = c1 ? n7 : c2 ? s5 : s3;
+  off = c0 ? l * (m - 1) - ((l * (l - 1)) >> 1) : base + (l - l0) * cnt;
+  (void)n3;
+  return;
+#endif
   lo = 0; cnt = 0; off = 0;
   if (l < n7) {
     lo = l + 1;
@@ -652,13 +670,15 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
   // round-robin and their warps interleave inside the span, so concurrent warps work on
   // adjacent bins (shared L1 lines of multiply-inserted spheres) and a warp's buffered pairs
   // — so the slot writes that follow — stay spatially local.
-  constexpr long long kSpan = (long long)kPairWarps * DEM_PAIRS_CONTIG;
-  const long long ncell = a.ncell;
-  long long it = (long long)blockIdx.x * kSpan + w, it_stop = min(ncell, (long long)blockIdx.x * kSpan + kSpan);
+  // (32-bit bin ids: ncell + the overshoot of the last spans < 2^31, checked by grid_layout)
+  using bin_t = int;
+  constexpr bin_t kSpan = (bin_t)kPairWarps * DEM_PAIRS_CONTIG;
+  const bin_t ncell = (bin_t)a.ncell;
+  bin_t it = (bin_t)blockIdx.x * kSpan + w, it_stop = min(ncell, (bin_t)blockIdx.x * kSpan + kSpan);
   auto advance = [&]() {
     if ((it += kPairWarps) >= it_stop) {
-      it += (long long)(gridDim.x - 1) * kSpan;
-      it_stop = min(ncell, it_stop + (long long)gridDim.x * kSpan);
+      it += (bin_t)(gridDim.x - 1) * kSpan;
+      it_stop = min(ncell, it_stop + (bin_t)gridDim.x * kSpan);
     }
   };
 #if DEM_PAIRS_PIPE
@@ -666,22 +686,22 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
   // and the bounds of c + 1 too; the items of c + 1 and the bounds of c + 2 are issued before
   // c's member records are awaited, so of the bounds -> items -> records chain only the last
   // load is exposed per bin.
-  auto bounds = [&](long long c, int& b0, int& b1) {
+  auto bounds = [&](bin_t c, int& b0, int& b1) {
     b0 = b1 = 0;
     if (c < ncell) {
       b0 = a.cell_start[c];
       b1 = a.cell_start[c + 1];
     }
   };
-  const long long cfirst = it;
+  const bin_t cfirst = it;
   int k0c, k1c, k0n, k1n;
   bounds(it, k0c, k1c);
   advance();
-  long long cnext = it;
+  bin_t cnext = it;
   bounds(it, k0n, k1n);
   int itA = lane < k1c - k0c ? a.items[k0c + lane] : 0;
   int itB = lane + 32 < k1c - k0c ? a.items[k0c + 32 + lane] : 0;
-  for (long long cid = cfirst; cid < ncell;) {
+  for (bin_t cid = cfirst; cid < ncell;) {
     const int k0 = k0c;
     const int m = k1c - k0c;
     const int curA = itA, curB = itB;
@@ -695,7 +715,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
     cnext = it;
     bounds(it, k0n, k1n);
 #else
-  for (long long cid = it; cid < ncell; advance(), cid = it) {
+  for (bin_t cid = it; cid < ncell; advance(), cid = it) {
     const int k0 = a.cell_start[cid];
     const int m = a.cell_start[cid + 1] - k0;
     const int curA = lane < m ? a.items[k0 + lane] : 0;
@@ -841,12 +861,21 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
           for (int base = 0; base < total; base += 32) {
             const unsigned word = D.bmap[base >> 5];
             const int p = base + lane;
+#if DEM_PAIRS_NODIV
+            // every lane runs the pair code (no divergent branch around it): a lane past the bin's
+            // last pair reads a clamped in-range slot and its result is masked off
+            int ia = 0, ib = 0;
+            const int d = D.desc[before + __popc(word & le) - 1];
+            const bool hit =
+                flat_pair<kGhosts, kMargin>(a, A, d & 0xff, min(p + (d >> 8), kFlatMax - 1), ia, ib, p < total);
+#else
             bool hit = false;
             int ia = 0, ib = 0;
             if (p < total) {
               const int d = D.desc[before + __popc(word & le) - 1];
               hit = flat_pair<kGhosts, kMargin>(a, A, d & 0xff, p + (d >> 8), ia, ib);
             }
+#endif
             before += __popc(word);
             push_hits<kMargin>(a, bf, nbuf, hit, ia, ib, lane);
           }

@@ -1111,7 +1111,7 @@ static dem_status grid_layout(dem_system* sys, double cell, const double* box_lo
     G.n[d] = (int)nd;
     ncell *= nd;
   }
-  if (ncell > (1LL << 31) - 2) {
+  if (ncell > (1LL << 31) - (1LL << 24)) {  // (k_pairs iterates bins in 32 bits, with overshoot)
     sys->err = "too many bins; increase cell_size";
     return DEM_ERR_INVALID_ARG;
   }
