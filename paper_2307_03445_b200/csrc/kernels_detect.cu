@@ -297,6 +297,7 @@ struct Members {
     const float fr = __double2float_rn(p.w + 0.5 * margin);
     const float eta = 1e-5f * (fabsf(fx) + fabsf(fy) + fabsf(fz) + fr + __double2float_ru(margin));
     f[q] = make_float4(fx, fy, fz, fr + eta);
+    if (DEM_PAIRS_F32 == 2) put(q, p);  // the fp64 record for the exact test in the pass
 #else
     put(q, p);
 #endif
@@ -417,7 +418,7 @@ __device__ DEM_FLUSH_ATTR void flush_pairs(const FlushCtx a, const int2* bf, int
   int2 v[kPer];
   int sa[kPer], sb[kPer];
   long long ka[kPer], kb[kPer];
-#if DEM_PAIRS_F32
+#if DEM_PAIRS_F32 == 1
   // the exact predicate (R14) of each buffered pair, on its two records in global memory (the
   // passes only applied the conservative fp32 pre-test; the clump tests are done)
   bool ok[kPer];
@@ -434,7 +435,7 @@ __device__ DEM_FLUSH_ATTR void flush_pairs(const FlushCtx a, const int2* bf, int
 #pragma unroll
   for (int j = 0; j < kPer; ++j) {
     const int k = lane + 32 * j;
-#if DEM_PAIRS_F32
+#if DEM_PAIRS_F32 == 1
     if (ok[j]) {
 #else
     if (k < n) {
@@ -450,7 +451,7 @@ __device__ DEM_FLUSH_ATTR void flush_pairs(const FlushCtx a, const int2* bf, int
   }
 #pragma unroll
   for (int j = 0; j < kPer; ++j) {
-#if DEM_PAIRS_F32
+#if DEM_PAIRS_F32 == 1
     if (ok[j]) {
 #else
     if (lane + 32 * j < n) {
@@ -508,14 +509,18 @@ template <bool kGhosts, bool kMargin>
 __device__ __forceinline__ bool flat_pair(const StepArgs& a, const Members& A, int i, int j, int& ia, int& ib,
                                           bool valid = true) {
 #if DEM_PAIRS_F32
-  // different clumps, at least one owned, and the conservative fp32 pre-test (exact test at the flush)
+  // different clumps, at least one owned, and the conservative fp32 pre-test on the 16-byte records
   const int ci = A.clump[i], cj = A.clump[j];
   const float4 u = A.f[i], v = A.f[j];
   const float dx = v.x - u.x, dy = v.y - u.y, dz = v.z - u.z;
   const float s = u.w + v.w;
   const float d2 = dx * dx + dy * dy + dz * dz;
   // (bitwise &: no short-circuit branch around the arithmetic)
-  const bool hit = (ci != cj) & (!kGhosts || min(ci, cj) < a.n_own) & (d2 <= s * s);
+  bool hit = valid & (ci != cj) & (!kGhosts || min(ci, cj) < a.n_own) & (d2 <= s * s);
+#if DEM_PAIRS_F32 == 2
+  // the exact predicate (R14) on the fp64 records, for the few lanes the pre-test let through
+  if (hit) hit = exact_pair<kMargin>(a.margin, A.get(i), A.get(j));
+#endif
   if (hit) {
     ia = A.item[i];
     ib = A.item[j];

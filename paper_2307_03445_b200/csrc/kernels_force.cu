@@ -41,6 +41,12 @@ constexpr int kPairStride = 8;  // doubles per material pair in Tables::pair
 #ifndef DEM_FORCE_PRO
 #define DEM_FORCE_PRO 1  // batched prologue loads + the first chunk's entries issued before the barrier
 #endif
+#ifndef DEM_FORCE_PRO_EPI
+#define DEM_FORCE_PRO_EPI 0  // 1: the epilogue's q, Omega, template id loaded in the batched prologue (shared)
+#endif
+#if DEM_FORCE_PRO_EPI && !DEM_FORCE_PRO
+#error "DEM_FORCE_PRO_EPI needs DEM_FORCE_PRO"
+#endif
 #ifndef DEM_FORCE_EPI_EARLY
 #define DEM_FORCE_EPI_EARLY 0  // 1: q, Omega, template id cp.async-ed into own_p during the last sums (A/B on C5: force 3.84 -> 3.94 ms)
 #endif
@@ -122,6 +128,8 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
   __shared__ double acc[6][kMaxS];
   __shared__ unsigned char own_of[DEM_FORCE_OWNER ? kFT : 1];  // entry of the chunk -> its own sphere
   __shared__ double cq[DEM_FORCE_ASYNC_EPI ? 10 : 1][kFC];     // own clumps' q, Omega_body, inertia (Eq. 4)
+  __shared__ double cqe[DEM_FORCE_PRO_EPI ? 7 : 1][kFC];       // own clumps' q, Omega_body (batched prologue)
+  __shared__ int cte[DEM_FORCE_PRO_EPI ? kFC : 1];             // and template ids
   // mesh wrench (kMesh): per entry the mesh id (-1: not a mesh entry) and torque about its X
   __shared__ int emesh[kMesh ? kFT : 1];
   __shared__ double mtq[3][kMesh ? kFT : 1];
@@ -156,6 +164,8 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
   Entry ent_first;
   ent_first.partner = -1;
   ent_first.prev = -1;
+  int pcl_first = 0;  // (DEM_FORCE_PRO == 3) the first chunk's partner clump, loaded before the barrier
+  (void)pcl_first;
   {
     const double2* src = reinterpret_cast<const double2*>(a.kin + (size_t)kKin * c0);
     int r0v[2], r1v[2], mv[2], cv[2];
@@ -176,9 +186,20 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
         kv[u] = src[c * (kKin / 2) + r];
       }
     }
+#if DEM_FORCE_PRO_EPI
+    // the integrating thread's q, Omega and template id: loaded with the staging, kept in shared memory
+    double eqv[7];
+    int etv = 0;
+    if (tid < ncl) {
+      const int c = c0 + tid;
+      eqv[0] = a.cur.qw[c]; eqv[1] = a.cur.qx[c]; eqv[2] = a.cur.qy[c]; eqv[3] = a.cur.qz[c];
+      eqv[4] = a.cur.wx[c]; eqv[5] = a.cur.wy[c]; eqv[6] = a.cur.wz[c];
+      etv = a.tid[c];
+    }
+#endif
     const int E1g = a.rows.row_ptr[s0 + nsph];
     if (E0g + tid < E1g) ent_first = a.rows.ent[E0g + tid];
-#if DEM_FORCE_PRO >= 2
+#if DEM_FORCE_PRO == 2
     // and the first chunk's partner sphere record, clump and material, copied into this thread's
     // column of part[] in the background (written by this thread only after it read them)
     if (ent_first.partner >= 0) {
@@ -211,6 +232,16 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
       }
       if (k < ncl * (kKinUsed / 2)) reinterpret_cast<double2*>(ck)[k] = kv[u];
     }
+#if DEM_FORCE_PRO == 3
+    if (ent_first.partner >= 0) pcl_first = a.s_clump[ent_first.partner];
+#endif
+#if DEM_FORCE_PRO_EPI
+    if (tid < ncl) {
+#pragma unroll
+      for (int q = 0; q < 7; ++q) cqe[q][tid] = eqv[q];
+      cte[tid] = etv;
+    }
+#endif
   }
 #else
   for (int k = tid; k <= nsph; k += kFT) {
@@ -357,7 +388,11 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
         rbar = ri;
         mbar = Mi;
       } else if (!wall) {
-#if DEM_FORCE_PRO >= 2
+#if DEM_FORCE_PRO == 3
+        const double4 pj = ldg256(a.spos + t);
+        const double* kjp = a.kin + (size_t)kKin * (c0e == E0 ? pcl_first : a.s_clump[t]);
+        mj = a.s_mat[t];
+#elif DEM_FORCE_PRO == 2
         double4 pj;
         const double* kjp;
         if (c0e == E0) {  // the prologue's copies of this partner
@@ -595,6 +630,11 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
   const double I0 = cq[7][tid], I1 = cq[8][tid], I2 = cq[9][tid];
   const double qw = cq[0][tid], qx = cq[1][tid], qy = cq[2][tid], qz = cq[3][tid];
   const double w0 = cq[4][tid], w1 = cq[5][tid], w2 = cq[6][tid];
+#elif DEM_FORCE_PRO_EPI
+  const int et = cte[tid];
+  const double I0 = a.tab.tpl_inertia[3 * et], I1 = a.tab.tpl_inertia[3 * et + 1], I2 = a.tab.tpl_inertia[3 * et + 2];
+  const double qw = cqe[0][tid], qx = cqe[1][tid], qy = cqe[2][tid], qz = cqe[3][tid];
+  const double w0 = cqe[4][tid], w1 = cqe[5][tid], w2 = cqe[6][tid];
 #elif DEM_FORCE_EPI_EARLY
   double eq[7];
   int et;
