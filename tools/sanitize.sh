@@ -9,7 +9,7 @@ mkdir -p "$OUT"
 python -c "import paper_2307_03445_b200 as d; d.load_library()" || exit 1
 CS=/usr/local/cuda/bin/compute-sanitizer
 for tool in memcheck synccheck initcheck racecheck; do
-  for case in c1 deferred overlap mesh peer2 regrow; do
+  for case in c1 deferred overlap mesh peer2 regrow empty; do
     extra=""
     [ "$tool" = memcheck ] && extra="--leak-check full"
     [ "$tool" = racecheck ] && extra="--racecheck-report all"

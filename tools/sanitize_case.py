@@ -4,7 +4,8 @@
 
 Cases: c1 (C1 box, k = 1), deferred (C1, k = 5 with margin), overlap (k = 4, second stream),
 mesh (a cone pushed into a settled patch), peer2 (LOOPBACK_PEER slab group, P = 2, with a
-coordinated regrow and a neighbour-only migration), regrow (a bed started with too-small capacities so every regrow path runs).
+coordinated regrow and a neighbour-only migration), regrow (a bed started with too-small capacities so every regrow path runs),
+empty (a system without owned clumps, then a lone clump).
 Device memory comes from cudaMallocAsync (use_torch_allocator=False) so the sanitizer sees
 every allocation at its true size instead of a caching-allocator slab.
 """
@@ -83,7 +84,22 @@ def regrow():
     g.close()
 
 
-CASES = dict(c1=c1, deferred=deferred, overlap=overlap, mesh=mesh, peer2=peer2, regrow=regrow)
+def empty():
+    # a system without owned clumps (the step-count tick kernel), then a lone clump
+    s = w.c1_box()
+    g = dem.system_from_scene(s.subset(np.array([], dtype=int)), use_torch_allocator=False)
+    g.dem_step(5)
+    g.dem_synchronize()
+    g.close()
+    one = s.subset(np.array([500]))
+    g = dem.system_from_scene(one, use_torch_allocator=False)
+    g.dem_step(5)
+    g.dem_synchronize()
+    print("empty", g.dem_get_stats()["steps"])
+    g.close()
+
+
+CASES = dict(c1=c1, deferred=deferred, overlap=overlap, mesh=mesh, peer2=peer2, regrow=regrow, empty=empty)
 
 if __name__ == "__main__":
     import torch
