@@ -14,6 +14,7 @@
 //   slots         fixed-width candidate partner lists per owned sphere (i32), filled by the per-bin warps
 //   rows (x2)     CSR by own sphere: row_ptr (i32, ns+1), partner (i32), key (i64), u_t (3 fp64 AoS)
 #pragma once
+#include <utility>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -227,7 +228,41 @@ struct StepArgs {
   Record rec;
   int record;
   Ctl* ctl;
+  int pdl;                   // launch the step's kernels after the first with programmatic serialization
 };
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// The step kernels after the first are launched with programmatic stream serialization (captured
+// into the step graphs as programmatic edges): a kernel's CTAs may become resident while its
+// predecessor's last wave drains, and wait at their very first instruction (griddepcontrol.wait,
+// which returns once the predecessor grid has completed and its memory is visible) — the launch
+// and ramp-up overlap the tail; no data is read early.  Each kernel lets its dependent launch as
+// soon as it started (launch_dependents).  Without the attribute both are no-ops.
+#ifndef DEM_PDL
+#define DEM_PDL 0  // A/B (tools/ab_sizes.sh): C5 and a C5/8 slab unchanged, a C5/45 slab +4%, C3 -1%: off
+#endif
+__device__ __forceinline__ void pdl_wait_and_release() {
+#if DEM_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" :::);
+#endif
+}
+// host: launch `kern` on `s`, with programmatic serialization when `pdl`
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, cudaStream_t s, bool pdl,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (DEM_PDL && pdl) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // ---------------------------------------------------------------- error latch
 __device__ __forceinline__ void raise_error(Ctl* ctl, int code, long long key, long long key2) {

@@ -193,6 +193,7 @@ void launch_pose_count(const StepArgs& a, cudaStream_t s) {
 // Slots are taken by decrementing the counts, which leaves cell_count all-zero for the
 // next step.  The order inside a bin is irrelevant: rows are sorted by partner key.
 __global__ void __launch_bounds__(DEM_SCATTER_LB) k_bin_scatter(StepArgs a) {
+  pdl_wait_and_release();
   if (*a.abort || a.ctl->abort) return;  // (an error in the steps running beside an ahead detection)
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.ns) return;
@@ -648,6 +649,7 @@ __device__ __forceinline__ void member_row(int l, int m, int n7, int n6, int n5,
 
 template <bool kGhosts, bool kMargin>
 __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepArgs a) {
+  pdl_wait_and_release();
   __shared__ Members smA[kPairWarps];
   __shared__ int2 sbuf[kPairWarps][kPairBuf];
 #if DEM_PAIRS_ROWDEC
@@ -977,6 +979,7 @@ __device__ __forceinline__ int prev_index(const Rows& prev, int pb, int pe, long
 #define DEM_ROWS_MINB (2048 / DEM_ROWS_TPB)  // 32 registers (a few spilled): 1.69 ms vs 1.80 at 40, 2.07 at 48
 #endif
 __global__ void __launch_bounds__(DEM_ROWS_TPB, DEM_ROWS_MINB) k_rows_finish(StepArgs a) {
+  pdl_wait_and_release();
   if (*a.abort || a.ctl->abort) return;  // (an error in the steps running beside an ahead detection)
   const int total = a.rows.row_ptr[a.ns];
   if ((long long)total > a.cap_entries) {
@@ -1110,7 +1113,7 @@ __global__ void __launch_bounds__(DEM_ROWS_TPB, DEM_ROWS_MINB) k_rows_finish(Ste
 
 // host launchers
 void launch_bin_scatter(const StepArgs& a, cudaStream_t s) {
-  if (a.ns) k_bin_scatter<<<(a.ns + DEM_SCATTER_TPB - 1) / DEM_SCATTER_TPB, DEM_SCATTER_TPB, 0, s>>>(a);
+  if (a.ns) launch_k(k_bin_scatter, (a.ns + DEM_SCATTER_TPB - 1) / DEM_SCATTER_TPB, DEM_SCATTER_TPB, s, a.pdl, a);
 }
 void launch_pairs(const StepArgs& a, cudaStream_t s, int n_sm) {
   long long warps = a.ncell;
@@ -1120,16 +1123,16 @@ void launch_pairs(const StepArgs& a, cudaStream_t s, int n_sm) {
   if (blocks < 1) blocks = 1;
   const bool ghosts = a.n_own < a.n, margin = a.margin != 0.0;
   if (ghosts && margin)
-    k_pairs<true, true><<<(unsigned)blocks, kPairWarps * 32, 0, s>>>(a);
+    launch_k(k_pairs<true, true>, (unsigned)blocks, kPairWarps * 32, s, a.pdl, a);
   else if (ghosts)
-    k_pairs<true, false><<<(unsigned)blocks, kPairWarps * 32, 0, s>>>(a);
+    launch_k(k_pairs<true, false>, (unsigned)blocks, kPairWarps * 32, s, a.pdl, a);
   else if (margin)
-    k_pairs<false, true><<<(unsigned)blocks, kPairWarps * 32, 0, s>>>(a);
+    launch_k(k_pairs<false, true>, (unsigned)blocks, kPairWarps * 32, s, a.pdl, a);
   else
-    k_pairs<false, false><<<(unsigned)blocks, kPairWarps * 32, 0, s>>>(a);
+    launch_k(k_pairs<false, false>, (unsigned)blocks, kPairWarps * 32, s, a.pdl, a);
 }
 void launch_rows_finish(const StepArgs& a, cudaStream_t s) {
-  if (a.ns) k_rows_finish<<<(a.ns + DEM_ROWS_TPB - 1) / DEM_ROWS_TPB, DEM_ROWS_TPB, 0, s>>>(a);
+  if (a.ns) launch_k(k_rows_finish, (a.ns + DEM_ROWS_TPB - 1) / DEM_ROWS_TPB, DEM_ROWS_TPB, s, a.pdl, a);
 }
 
 }  // namespace dem

@@ -135,6 +135,7 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
   __shared__ double mtq[3][kMesh ? kFT : 1];
   __shared__ double cw[kMesh ? kMaxMeshes : 1][6];
   __shared__ int chunk_mesh, cta_mesh;  // this chunk / this CTA holds mesh entries
+  pdl_wait_and_release();
   const int tid = threadIdx.x;
   const int2 b0 = a.cta_clump[blockIdx.x], b1 = a.cta_clump[blockIdx.x + 1];
   const int c0 = b0.x, c1 = b1.x;
@@ -753,11 +754,12 @@ static void force_carveout() {
 
 // a system that holds no owned clump (empty, or a rank whose slab is empty) still counts its steps
 __global__ void k_step_tick(Ctl* ctl) {
+  pdl_wait_and_release();
   if (!ctl->abort) ctl->step += 1;
 }
 void launch_force_integrate(const StepArgs& a, cudaStream_t s) {
   if (a.n_cta <= 0) {
-    k_step_tick<<<1, 1, 0, s>>>(a.ctl);
+    launch_k(k_step_tick, 1, 1, s, a.pdl, a.ctl);
     return;
   }
   force_carveout<true, true>();
@@ -766,9 +768,11 @@ void launch_force_integrate(const StepArgs& a, cudaStream_t s) {
   force_carveout<false, false>();
   const bool peer = a.peer_state[0] || a.peer_state[1];
   if (a.n_tri)
-    peer ? k_force_integrate<true, true><<<a.n_cta, kFT, 0, s>>>(a) : k_force_integrate<true, false><<<a.n_cta, kFT, 0, s>>>(a);
+    peer ? launch_k(k_force_integrate<true, true>, a.n_cta, kFT, s, a.pdl, a)
+         : launch_k(k_force_integrate<true, false>, a.n_cta, kFT, s, a.pdl, a);
   else
-    peer ? k_force_integrate<false, true><<<a.n_cta, kFT, 0, s>>>(a) : k_force_integrate<false, false><<<a.n_cta, kFT, 0, s>>>(a);
+    peer ? launch_k(k_force_integrate<false, true>, a.n_cta, kFT, s, a.pdl, a)
+         : launch_k(k_force_integrate<false, false>, a.n_cta, kFT, s, a.pdl, a);
 }
 void launch_count_canonical(const Rows& r, const long long* s_key, int ns, unsigned long long* out, cudaStream_t s) {
   if (ns) k_count_canonical<<<(ns + 255) / 256, 256, 0, s>>>(r, s_key, ns, out);

@@ -49,6 +49,7 @@ __device__ __forceinline__ int block_excl_scan(int v, int* total) {
 __global__ void __launch_bounds__(kScanThreads) k_scan_tiles(const int* __restrict__ in, int* __restrict__ out,
                                                              int* __restrict__ tile_sums, long long n,
                                                              const int* abort, const int* abort2, int packed) {
+  pdl_wait_and_release();
   if ((abort && *abort) || (abort2 && *abort2)) return;
   const long long base = (long long)blockIdx.x * kScanTile + (long long)threadIdx.x * kScanItems;
   int v[kScanItems];
@@ -82,6 +83,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_tiles(const int* __restri
 
 __global__ void __launch_bounds__(kScanThreads) k_scan_sums(int* tile_sums, int n_tiles, int* out_total,
                                                             const int* abort, const int* abort2) {
+  pdl_wait_and_release();
   if ((abort && *abort) || (abort2 && *abort2)) return;
   int carry = 0;
   for (int b = 0; b < n_tiles; b += kScanThreads) {
@@ -97,6 +99,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_sums(int* tile_sums, int 
 
 __global__ void __launch_bounds__(kScanThreads) k_scan_add(int* out, const int* tile_sums, long long n,
                                                            const int* abort, const int* abort2) {
+  pdl_wait_and_release();
   if ((abort && *abort) || (abort2 && *abort2)) return;
   const int add = tile_sums[blockIdx.x];
   if (add == 0) return;
@@ -118,15 +121,15 @@ long long scan_tiles_needed(long long n) { return (n + kScanTile - 1) / kScanTil
 
 // out must hold n + 1 ints; tmp must hold scan_tiles_needed(n) ints
 void launch_excl_scan(const int* in, int* out, long long n, int* tmp, const int* abort, cudaStream_t s,
-                      const int* abort2, int packed) {
+                      const int* abort2, int packed, bool pdl) {
   long long tiles = scan_tiles_needed(n);
   if (tiles == 0) {
     cudaMemsetAsync(out, 0, sizeof(int), s);
     return;
   }
-  k_scan_tiles<<<(unsigned)tiles, kScanThreads, 0, s>>>(in, out, tmp, n, abort, abort2, packed);
-  k_scan_sums<<<1, kScanThreads, 0, s>>>(tmp, (int)tiles, out + n, abort, abort2);
-  k_scan_add<<<(unsigned)tiles, kScanThreads, 0, s>>>(out, tmp, n, abort, abort2);
+  launch_k(k_scan_tiles, (unsigned)tiles, kScanThreads, s, pdl, in, out, tmp, n, abort, abort2, packed);
+  launch_k(k_scan_sums, 1, kScanThreads, s, pdl, tmp, (int)tiles, out + n, abort, abort2);
+  launch_k(k_scan_add, (unsigned)tiles, kScanThreads, s, pdl, out, tmp, n, abort, abort2);
 }
 
 }  // namespace dem

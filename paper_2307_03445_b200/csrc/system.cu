@@ -28,7 +28,7 @@ int force_cta_clumps();
 int force_cta_spheres();
 long long scan_tiles_needed(long long n);
 void launch_excl_scan(const int* in, int* out, long long n, int* tmp, const int* abort, cudaStream_t s,
-                      const int* abort2, int packed = 0);
+                      const int* abort2, int packed = 0, bool pdl = false);
 void launch_count_canonical(const Rows& r, const long long* s_key, int ns, unsigned long long* out, cudaStream_t s);
 void launch_pack(const State& st, const int* idx, int n, double* buf, cudaStream_t s);
 void launch_unpack(const State& st, const int* idx, int n, const double* buf, cudaStream_t s);
@@ -125,6 +125,7 @@ struct dem_system {
   cudaStream_t det_stream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_det = nullptr;
   int fault_ahead = 0;
+  int no_pdl = 0;  // env DEM_NO_PDL=1: plain stream serialization between the step kernels
   bool debug_serial_det = false;  // debug (env DEM_DEBUG_SERIAL_DET=1): the force steps wait for the ahead detection
   // kinematic triangle meshes (NEXT-3)
   int n_mesh = 0, n_tri = 0;
@@ -326,6 +327,9 @@ static StepArgs make_args(dem_system* sys, int kind, bool det = false) {
   a.xref = sys->d_xref;
   a.drift_max = sys->dist ? sys->P.drift_max : 0.0;
   a.cell_count = sys->d_cell_count;
+  // programmatic serialization only for graph-launched steps (the in-line profiling pass times the
+  // stages between events, one after the other); DEM_NO_PDL=1 turns it off
+  a.pdl = (!sys->profiling && !sys->no_pdl) ? 1 : 0;
   a.irank = sys->d_irank;
   a.cell_start = sys->d_cell_start;
   a.items = sys->d_items;
@@ -428,14 +432,14 @@ static void enqueue_detect(dem_system* sys, int kind, cudaStream_t s, cudaEvent_
   const int* abort2 = &sys->d_ctl->abort;
   if (run && sys->n_tri) cudaMemsetAsync(a.mlist_out_n, 0, sizeof(int), s);
   if (run) launch_excl_scan(sys->d_cell_count, sys->d_cell_start, sys->ncell, sys->d_scan_tmp, abort, s, abort2,
-                           DEM_SCATTER_RANKS);
+                           DEM_SCATTER_RANKS, a.pdl);
   if (ev) cudaEventRecord(ev[2], s);
   if (run) launch_bin_scatter(a, s);
   if (run) launch_mesh_pairs(a, s);
   if (ev) cudaEventRecord(ev[3], s);
   if (run) launch_pairs(a, s, sys->n_sm);
   if (ev) cudaEventRecord(ev[4], s);
-  if (run) launch_excl_scan(sys->d_row_cnt, a.rows.row_ptr, sys->ns, sys->d_scan_tmp, abort, s, abort2);
+  if (run) launch_excl_scan(sys->d_row_cnt, a.rows.row_ptr, sys->ns, sys->d_scan_tmp, abort, s, abort2, 0, a.pdl);
   if (ev) cudaEventRecord(ev[5], s);
   if (run) launch_rows_finish(a, s);
   if (ev) cudaEventRecord(ev[6], s);
@@ -624,6 +628,7 @@ extern "C" dem_status dem_create(const dem_params* params, const dem_material* m
   dem_system* sys = new dem_system();
   sys->P = *params;
   if (const char* fi = std::getenv("DEM_FAULT_AHEAD_OVERFLOW")) sys->fault_ahead = std::atoi(fi);
+  if (const char* np = std::getenv("DEM_NO_PDL")) sys->no_pdl = std::atoi(np) ? 1 : 0;
   if (const char* sd = std::getenv("DEM_DEBUG_SERIAL_DET")) sys->debug_serial_det = std::atoi(sd) != 0;
   sys->stream = (cudaStream_t)cuda_stream;
   sys->n_mat = n_mat;
