@@ -60,6 +60,13 @@ constexpr int kPairStride = 8;  // doubles per material pair in Tables::pair
 #define DEM_FORCE_MAXS (DEM_FORCE_FT * 9 / 8)  // 144: force 4.30 ms vs 4.84 at 160 (entry-cut CTAs)
 #endif
 constexpr int kFT = DEM_FORCE_FT;      // threads per CTA (= entries per chunk)
+// Skewed slots of the per-entry partials: entry q at q + q/16, so the per-sphere sums (lane l reads
+// entry ~ c l + b, rows of a few entries) spread over all bank pairs instead of every c-th
+#ifndef DEM_FORCE_SKEW
+#define DEM_FORCE_SKEW 0  // A/B on C5: force 3.835 -> 3.85 ms (the index arithmetic costs more than the conflicts): off
+#endif
+constexpr int kPartW = DEM_FORCE_SKEW ? kFT + kFT / 16 : kFT;
+__device__ __forceinline__ int pslot(int q) { return DEM_FORCE_SKEW ? q + (q >> 4) : q; }
 constexpr int kFC = DEM_FORCE_FC;      // max clumps per CTA (host partition, see system.cu)
 constexpr int kMaxS = DEM_FORCE_MAXS;  // max spheres per CTA
 int force_cta_clumps() { return kFC; }
@@ -124,7 +131,7 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
   __shared__ int own_mat[kMaxS];
   __shared__ int own_lc[kMaxS];
   __shared__ __align__(16) double ck[kFC * kKinUsed];
-  __shared__ double part[6][kFT];
+  __shared__ double part[6][kPartW];
   __shared__ double acc[6][kMaxS];
   __shared__ unsigned char own_of[DEM_FORCE_OWNER ? kFT : 1];  // entry of the chunk -> its own sphere
   __shared__ double cq[DEM_FORCE_ASYNC_EPI ? 10 : 1][kFC];     // own clumps' q, Omega_body, inertia (Eq. 4)
@@ -208,10 +215,10 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
       const double* ps = reinterpret_cast<const double*>(a.spos + t);
 #pragma unroll
       for (int d = 0; d < 4; ++d) {
-        const unsigned dst = (unsigned)__cvta_generic_to_shared(&part[d][tid]);
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(&part[d][pslot(tid)]);
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(ps + d) : "memory");
       }
-      int* pi = reinterpret_cast<int*>(&part[4][tid]);
+      int* pi = reinterpret_cast<int*>(&part[4][pslot(tid)]);
       const unsigned d0 = (unsigned)__cvta_generic_to_shared(pi), d1 = (unsigned)__cvta_generic_to_shared(pi + 1);
       asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d0), "l"(a.s_clump + t) : "memory");
       asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d1), "l"(a.s_mat + t) : "memory");
@@ -336,7 +343,7 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
         const double* u = a.prev.ut + (size_t)kUt * pidx;
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-          const unsigned dst = (unsigned)__cvta_generic_to_shared(&part[d][tid]);
+          const unsigned dst = (unsigned)__cvta_generic_to_shared(&part[d][pslot(tid)]);
           asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(u + d) : "memory");
         }
       }
@@ -398,8 +405,8 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
         const double* kjp;
         if (c0e == E0) {  // the prologue's copies of this partner
           asm volatile("cp.async.wait_all;" ::: "memory");
-          pj = make_double4(part[0][tid], part[1][tid], part[2][tid], part[3][tid]);
-          const int* pi = reinterpret_cast<const int*>(&part[4][tid]);
+          pj = make_double4(part[0][pslot(tid)], part[1][pslot(tid)], part[2][pslot(tid)], part[3][pslot(tid)]);
+          const int* pi = reinterpret_cast<const int*>(&part[4][pslot(tid)]);
           kjp = a.kin + (size_t)kKin * pi[0];
           mj = pi[1];
         } else {
@@ -492,8 +499,8 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
           const double vtx = vrx - vn * nx, vty = vry - vn * ny, vtz = vrz - vn * nz;
 #if DEM_FORCE_UT_ASYNC
           asm volatile("cp.async.wait_all;" ::: "memory");
-          const double ux = pidx >= 0 ? part[0][tid] : 0.0, uy = pidx >= 0 ? part[1][tid] : 0.0,
-                       uz = pidx >= 0 ? part[2][tid] : 0.0;
+          const double ux = pidx >= 0 ? part[0][pslot(tid)] : 0.0, uy = pidx >= 0 ? part[1][pslot(tid)] : 0.0,
+                       uz = pidx >= 0 ? part[2][pslot(tid)] : 0.0;
 #endif
           const double upx = ux + h * vtx, upy = uy + h * vty, upz = uz + h * vtz;
           const double upn = upx * nx + upy * ny + upz * nz;
@@ -542,12 +549,12 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
 #if DEM_FORCE_UT_ASYNC
       asm volatile("cp.async.wait_all;" ::: "memory");  // (the u_t copy into these slots has landed)
 #endif
-      part[0][tid] = fx;
-      part[1][tid] = fy;
-      part[2][tid] = fz;
-      part[3][tid] = __fma_rn(riy, fz, -__dmul_rn(riz, fy));
-      part[4][tid] = __fma_rn(riz, fx, -__dmul_rn(rix, fz));
-      part[5][tid] = __fma_rn(rix, fy, -__dmul_rn(riy, fx));
+      part[0][pslot(tid)] = fx;
+      part[1][pslot(tid)] = fy;
+      part[2][pslot(tid)] = fz;
+      part[3][pslot(tid)] = __fma_rn(riy, fz, -__dmul_rn(riz, fy));
+      part[4][pslot(tid)] = __fma_rn(riz, fx, -__dmul_rn(rix, fz));
+      part[5][pslot(tid)] = __fma_rn(rix, fy, -__dmul_rn(riy, fx));
       if (kMesh && mesh >= 0) {
         // reaction on the mesh: +F at p, torque (p - X_m) x F
         const double mx = px - Xjx, my = py - Xjy, mz = pz - Xjz;
@@ -589,7 +596,7 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
       for (int q = 0; q < kFT; ++q) {
         const int m = emesh[q];
         if (m < 0) continue;
-        cw[m][0] -= part[0][q]; cw[m][1] -= part[1][q]; cw[m][2] -= part[2][q];
+        cw[m][0] -= part[0][pslot(q)]; cw[m][1] -= part[1][pslot(q)]; cw[m][2] -= part[2][pslot(q)];
         cw[m][3] += mtq[0][q]; cw[m][4] += mtq[1][q]; cw[m][5] += mtq[2][q];
       }
     }
@@ -605,7 +612,7 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
         for (int d = 0; d < 6; ++d) sum[d] = acc[d][ls];
         for (int q = b - c0e; q < en - c0e; ++q) {
 #pragma unroll
-          for (int d = 0; d < 6; ++d) sum[d] += part[d][q];
+          for (int d = 0; d < 6; ++d) sum[d] += part[d][pslot(q)];
         }
 #pragma unroll
         for (int d = 0; d < 6; ++d) acc[d][ls] = sum[d];
