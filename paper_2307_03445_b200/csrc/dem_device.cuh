@@ -229,6 +229,7 @@ struct StepArgs {
   int record;
   Ctl* ctl;
   int pdl;                   // launch the step's kernels after the first with programmatic serialization
+  int tiny;                  // k_pairs with the small-bin pass (sparse bins: fewer than 2 spheres per bin)
 };
 
 // ---------------------------------------------------------------- programmatic dependent launch

@@ -256,6 +256,10 @@ constexpr int kPairBuf = DEM_PAIRS_BUF;
 // axis d", the pair belongs to C iff (g_a | g_b) == 7: that is how each pair is found in
 // exactly one bin.
 constexpr int kFlatMax = 64;  // bins up to this size: member groups + flat pair enumeration
+#ifndef DEM_PAIRS_TINY
+#define DEM_PAIRS_TINY 1
+#endif
+constexpr int kTiny = 8;      // bins up to this size: every pair in one pass with the per-pair group test
 #ifndef DEM_PAIRS_SOA
 #define DEM_PAIRS_SOA 1
 #endif
@@ -647,7 +651,7 @@ __device__ __forceinline__ void member_row(int l, int m, int n7, int n6, int n5,
   }
 }
 
-template <bool kGhosts, bool kMargin>
+template <bool kGhosts, bool kMargin, bool kTinyOn>
 __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepArgs a) {
   pdl_wait_and_release();
   __shared__ Members smA[kPairWarps];
@@ -729,7 +733,26 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
     const int curB = lane + 32 < m ? a.items[k0 + 32 + lane] : 0;
 #endif
     if (m >= 2) {
-      if (m <= kFlatMax) {
+      if (kTinyOn && m <= kTiny) {
+        // Small bins (sparse regions: a falling column, a bed's free surface): all m (m - 1) / 2 <= 28
+        // pairs in one pass, the own-bin rule applied per pair ((g_a | g_b) == 7) — no group ranking
+        // and no row descriptors, which cost ~200 instructions per bin whatever its size
+        if (lane < m) {
+          const int idx = curA & 0x1fffffff;
+          A.put(lane, ldg256(a.dpos + idx));
+          A.meta_put(lane, make_int2(a.s_clump[idx], curA));
+        }
+        __syncwarp();
+        int i, j;
+        decode_tri(min(lane, kTiny * (kTiny - 1) / 2 - 1), i, j);
+        i = min(i, m - 1);
+        j = min(j, m - 1);
+        const int2 mu = A.meta_get(i), mv = A.meta_get(j);
+        const bool own = (lane < (m * (m - 1)) / 2) & ((((unsigned)(mu.y | mv.y)) >> 29) == 7u);
+        const bool hit = own & candidate<kGhosts, kMargin>(a, mu, mv, A.get(i), A.get(j));
+        push_hits<kMargin>(a, bf, nbuf, hit, mu.y & 0x1fffffff, mv.y & 0x1fffffff, lane);
+        __syncwarp();
+      } else if (m <= kFlatMax) {
         // Lane l loads members l and l + 32 and stores them at their place in the group order
         // (a 64-bit warp scan of one-hot byte counters gives every member its rank in its group
         // and every group its start); then the warp enumerates the pair blocks flat, 32 pairs
@@ -1122,14 +1145,21 @@ void launch_pairs(const StepArgs& a, cudaStream_t s, int n_sm) {
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   const bool ghosts = a.n_own < a.n, margin = a.margin != 0.0;
-  if (ghosts && margin)
-    launch_k(k_pairs<true, true>, (unsigned)blocks, kPairWarps * 32, s, a.pdl, a);
-  else if (ghosts)
-    launch_k(k_pairs<true, false>, (unsigned)blocks, kPairWarps * 32, s, a.pdl, a);
-  else if (margin)
-    launch_k(k_pairs<false, true>, (unsigned)blocks, kPairWarps * 32, s, a.pdl, a);
-  else
-    launch_k(k_pairs<false, false>, (unsigned)blocks, kPairWarps * 32, s, a.pdl, a);
+  // the small-bin pass only where bins are sparse (a.tiny, set from spheres per bin): in a dense bed
+  // nearly no bin takes it and the extra branch per bin costs ~0.3%
+  const bool tiny = DEM_PAIRS_TINY && a.tiny;
+  const unsigned g = (unsigned)blocks, t = kPairWarps * 32;
+  if (tiny) {
+    if (ghosts && margin) launch_k(k_pairs<true, true, true>, g, t, s, a.pdl, a);
+    else if (ghosts) launch_k(k_pairs<true, false, true>, g, t, s, a.pdl, a);
+    else if (margin) launch_k(k_pairs<false, true, true>, g, t, s, a.pdl, a);
+    else launch_k(k_pairs<false, false, true>, g, t, s, a.pdl, a);
+  } else {
+    if (ghosts && margin) launch_k(k_pairs<true, true, false>, g, t, s, a.pdl, a);
+    else if (ghosts) launch_k(k_pairs<true, false, false>, g, t, s, a.pdl, a);
+    else if (margin) launch_k(k_pairs<false, true, false>, g, t, s, a.pdl, a);
+    else launch_k(k_pairs<false, false, false>, g, t, s, a.pdl, a);
+  }
 }
 void launch_rows_finish(const StepArgs& a, cudaStream_t s) {
   if (a.ns) launch_k(k_rows_finish, (a.ns + DEM_ROWS_TPB - 1) / DEM_ROWS_TPB, DEM_ROWS_TPB, s, a.pdl, a);

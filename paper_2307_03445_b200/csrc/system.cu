@@ -126,6 +126,7 @@ struct dem_system {
   cudaEvent_t ev_fork = nullptr, ev_det = nullptr;
   int fault_ahead = 0;
   int no_pdl = 0;  // env DEM_NO_PDL=1: plain stream serialization between the step kernels
+  int tiny_force = -1;  // env DEM_PAIRS_TINY=0/1: the small-bin pass of k_pairs off / on (else by density)
   bool debug_serial_det = false;  // debug (env DEM_DEBUG_SERIAL_DET=1): the force steps wait for the ahead detection
   // kinematic triangle meshes (NEXT-3)
   int n_mesh = 0, n_tri = 0;
@@ -330,6 +331,9 @@ static StepArgs make_args(dem_system* sys, int kind, bool det = false) {
   // programmatic serialization only for graph-launched steps (the in-line profiling pass times the
   // stages between events, one after the other); DEM_NO_PDL=1 turns it off
   a.pdl = (!sys->profiling && !sys->no_pdl) ? 1 : 0;
+  // sparse bins (a falling column, C3: 0.5 spheres per bin; the C5 bed: 5): k_pairs takes the
+  // small-bin pass for bins of at most 8 members (env DEM_PAIRS_TINY=0/1 forces it off/on)
+  a.tiny = sys->tiny_force >= 0 ? sys->tiny_force : ((double)sys->ns < 2.0 * (double)sys->ncell ? 1 : 0);
   a.irank = sys->d_irank;
   a.cell_start = sys->d_cell_start;
   a.items = sys->d_items;
@@ -629,6 +633,7 @@ extern "C" dem_status dem_create(const dem_params* params, const dem_material* m
   sys->P = *params;
   if (const char* fi = std::getenv("DEM_FAULT_AHEAD_OVERFLOW")) sys->fault_ahead = std::atoi(fi);
   if (const char* np = std::getenv("DEM_NO_PDL")) sys->no_pdl = std::atoi(np) ? 1 : 0;
+  if (const char* tp = std::getenv("DEM_PAIRS_TINY")) sys->tiny_force = std::atoi(tp) ? 1 : 0;
   if (const char* sd = std::getenv("DEM_DEBUG_SERIAL_DET")) sys->debug_serial_det = std::atoi(sd) != 0;
   sys->stream = (cudaStream_t)cuda_stream;
   sys->n_mat = n_mat;

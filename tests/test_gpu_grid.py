@@ -77,3 +77,19 @@ def test_bin_region_is_the_occupied_box(dem):
     sa, sb = a.dem_get_state(), b.dem_get_state()
     for k in ("pos", "quat", "vel", "omega"):
         assert np.array_equal(sa[k], sb[k]), k
+
+
+@pytest.mark.parametrize("tiny", ["0", "1"])
+def test_small_bin_pass_and_group_ranking_agree(dem, monkeypatch, tiny):
+    """k_pairs tests bins of at most 8 members in one pass with the own-bin rule per pair (the
+    small-bin pass, chosen where bins are sparse) or through the group ranking and row descriptors;
+    both give the oracle's contact set and forces on a scene with every bin size up to the large-bin
+    path (forced on and off here; by density the scene would take the small-bin pass)."""
+    monkeypatch.setenv("DEM_PAIRS_TINY", tiny)
+    scene = w.random_clumps(63, 1500, box=0.04, types=[0, 3, 6])
+    g = dem.system_from_scene(scene, record_contacts=True)
+    o = oracle.Oracle(scene)
+    g.dem_step(1)
+    o.step(1)
+    assert_same_contact_set(g.dem_get_contacts(), o.contacts())
+    assert_forces_close(g.dem_get_contacts(), o.contacts(), scene)
