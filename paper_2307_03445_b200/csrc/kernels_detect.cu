@@ -260,6 +260,11 @@ constexpr int kFlatMax = 64;  // bins up to this size: member groups + flat pair
 #define DEM_PAIRS_TINY 1
 #endif
 constexpr int kTiny = 8;      // bins up to this size: every pair in one pass with the per-pair group test
+#ifndef DEM_PAIRS_SMALL_DENSE
+#define DEM_PAIRS_SMALL_DENSE 0   // the same per-pair pass in the dense instantiation, bins up to this size (<= 32)
+#endif
+constexpr int kSmallDense = DEM_PAIRS_SMALL_DENSE;
+static_assert(kSmallDense <= 32, "the small-bin pass loads one member per lane");
 #ifndef DEM_PAIRS_SOA
 #define DEM_PAIRS_SOA 1
 #endif
@@ -733,9 +738,9 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
     const int curB = lane + 32 < m ? a.items[k0 + 32 + lane] : 0;
 #endif
     if (m >= 2) {
-      if (kTinyOn && m <= kTiny) {
-        // Small bins (sparse regions: a falling column, a bed's free surface): all m (m - 1) / 2 <= 28
-        // pairs in one pass, the own-bin rule applied per pair ((g_a | g_b) == 7) — no group ranking
+      if (m <= (kTinyOn ? kTiny : kSmallDense)) {
+        // Small bins (sparse regions: a falling column, a bed's free surface): all m (m - 1) / 2 pairs
+        // in passes of 32, the own-bin rule applied per pair ((g_a | g_b) == 7) — no group ranking
         // and no row descriptors, which cost ~200 instructions per bin whatever its size
         if (lane < m) {
           const int idx = curA & 0x1fffffff;
@@ -743,14 +748,16 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
           A.meta_put(lane, make_int2(a.s_clump[idx], curA));
         }
         __syncwarp();
-        int i, j;
-        decode_tri(min(lane, kTiny * (kTiny - 1) / 2 - 1), i, j);
-        i = min(i, m - 1);
-        j = min(j, m - 1);
-        const int2 mu = A.meta_get(i), mv = A.meta_get(j);
-        const bool own = (lane < (m * (m - 1)) / 2) & ((((unsigned)(mu.y | mv.y)) >> 29) == 7u);
-        const bool hit = own & candidate<kGhosts, kMargin>(a, mu, mv, A.get(i), A.get(j));
-        push_hits<kMargin>(a, bf, nbuf, hit, mu.y & 0x1fffffff, mv.y & 0x1fffffff, lane);
+        const int np = (m * (m - 1)) / 2;
+        for (int base = 0; base < np; base += 32) {
+          const int p = base + lane;
+          int i, j;
+          decode_tri(min(p, np - 1), i, j);
+          const int2 mu = A.meta_get(i), mv = A.meta_get(j);
+          const bool own = (p < np) & ((((unsigned)(mu.y | mv.y)) >> 29) == 7u);
+          const bool hit = own & candidate<kGhosts, kMargin>(a, mu, mv, A.get(i), A.get(j));
+          push_hits<kMargin>(a, bf, nbuf, hit, mu.y & 0x1fffffff, mv.y & 0x1fffffff, lane);
+        }
         __syncwarp();
       } else if (m <= kFlatMax) {
         // Lane l loads members l and l + 32 and stores them at their place in the group order
