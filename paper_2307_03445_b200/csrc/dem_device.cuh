@@ -230,6 +230,7 @@ struct StepArgs {
   Ctl* ctl;
   int pdl;                   // launch the step's kernels after the first with programmatic serialization
   int tiny;                  // k_pairs with the small-bin pass (sparse bins: fewer than 2 spheres per bin)
+  int pairs_contig;          // k_pairs: bins per warp in a CTA span (set by launch_pairs)
 };
 
 // ---------------------------------------------------------------- programmatic dependent launch

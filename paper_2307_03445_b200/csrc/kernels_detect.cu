@@ -241,6 +241,12 @@ __global__ void __launch_bounds__(DEM_SCATTER_LB) k_bin_scatter(StepArgs a) {
 #ifndef DEM_PAIRS_MINB
 #define DEM_PAIRS_MINB 8  // 64 registers
 #endif
+#ifndef DEM_PAIRS_ADAPT
+#define DEM_PAIRS_ADAPT 1  // span length from the grid size (launch_pairs) instead of DEM_PAIRS_CONTIG
+#endif
+#ifndef DEM_PAIRS_SPANS_PER_SLOT
+#define DEM_PAIRS_SPANS_PER_SLOT 4
+#endif
 #ifndef DEM_PAIRS_CONTIG
 #define DEM_PAIRS_CONTIG 64  // bins per warp in a CTA span
 #endif
@@ -688,7 +694,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
   // — so the slot writes that follow — stay spatially local.
   // (32-bit bin ids: ncell + the overshoot of the last spans < 2^31, checked by grid_layout)
   using bin_t = int;
-  constexpr bin_t kSpan = (bin_t)kPairWarps * DEM_PAIRS_CONTIG;
+  // (bins per warp in a span: DEM_PAIRS_CONTIG, fewer on a small grid so every SM gets spans: a.pairs_contig)
+  const bin_t kSpan = (bin_t)kPairWarps * (DEM_PAIRS_ADAPT ? a.pairs_contig : DEM_PAIRS_CONTIG);
   const bin_t ncell = (bin_t)a.ncell;
   bin_t it = (bin_t)blockIdx.x * kSpan + w, it_stop = min(ncell, (bin_t)blockIdx.x * kSpan + kSpan);
   auto advance = [&]() {
@@ -1151,21 +1158,30 @@ void launch_pairs(const StepArgs& a, cudaStream_t s, int n_sm) {
   long long cap = (long long)n_sm * 8 * 16;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
+  // span length: DEM_PAIRS_CONTIG bins per warp on a large grid; on a small one (one rank's slab of
+  // a decomposition, a small bed) shorter, so that there are at least 4 spans per resident CTA slot
+  StepArgs b = a;
+  {
+    long long contig = DEM_PAIRS_CONTIG;
+    const long long slots = (long long)n_sm * DEM_PAIRS_MINB;
+    while (contig > 4 && a.ncell < DEM_PAIRS_SPANS_PER_SLOT * slots * kPairWarps * contig) contig >>= 1;
+    b.pairs_contig = (int)contig;
+  }
   const bool ghosts = a.n_own < a.n, margin = a.margin != 0.0;
   // the small-bin pass only where bins are sparse (a.tiny, set from spheres per bin): in a dense bed
   // nearly no bin takes it and the extra branch per bin costs ~0.3%
   const bool tiny = DEM_PAIRS_TINY && a.tiny;
   const unsigned g = (unsigned)blocks, t = kPairWarps * 32;
   if (tiny) {
-    if (ghosts && margin) launch_k(k_pairs<true, true, true>, g, t, s, a.pdl, a);
-    else if (ghosts) launch_k(k_pairs<true, false, true>, g, t, s, a.pdl, a);
-    else if (margin) launch_k(k_pairs<false, true, true>, g, t, s, a.pdl, a);
-    else launch_k(k_pairs<false, false, true>, g, t, s, a.pdl, a);
+    if (ghosts && margin) launch_k(k_pairs<true, true, true>, g, t, s, a.pdl, b);
+    else if (ghosts) launch_k(k_pairs<true, false, true>, g, t, s, a.pdl, b);
+    else if (margin) launch_k(k_pairs<false, true, true>, g, t, s, a.pdl, b);
+    else launch_k(k_pairs<false, false, true>, g, t, s, a.pdl, b);
   } else {
-    if (ghosts && margin) launch_k(k_pairs<true, true, false>, g, t, s, a.pdl, a);
-    else if (ghosts) launch_k(k_pairs<true, false, false>, g, t, s, a.pdl, a);
-    else if (margin) launch_k(k_pairs<false, true, false>, g, t, s, a.pdl, a);
-    else launch_k(k_pairs<false, false, false>, g, t, s, a.pdl, a);
+    if (ghosts && margin) launch_k(k_pairs<true, true, false>, g, t, s, a.pdl, b);
+    else if (ghosts) launch_k(k_pairs<true, false, false>, g, t, s, a.pdl, b);
+    else if (margin) launch_k(k_pairs<false, true, false>, g, t, s, a.pdl, b);
+    else launch_k(k_pairs<false, false, false>, g, t, s, a.pdl, b);
   }
 }
 void launch_rows_finish(const StepArgs& a, cudaStream_t s) {
