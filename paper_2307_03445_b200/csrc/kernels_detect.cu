@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(DEM_SCATTER_LB) k_bin_scatter(StepArgs a) {
 #define DEM_PAIRS_BUF 32  // A/B: 32 beats 64 by 4% (96, 128 much slower)
 #endif
 #ifndef DEM_PAIRS_MINB
-#define DEM_PAIRS_MINB 8  // 64 registers
+#define DEM_PAIRS_MINB 7  // ptxas stays at 64 registers; A/B round 2 vs 8: pairs 4.49 -> 4.43 ms on C5, C3 -1.4% (6: 4.61)
 #endif
 #ifndef DEM_PAIRS_ADAPT
 #define DEM_PAIRS_ADAPT 1  // span length from the grid size (launch_pairs) instead of DEM_PAIRS_CONTIG
