@@ -27,7 +27,7 @@ namespace dem {
 
 constexpr int kPairStride = 8;  // doubles per material pair in Tables::pair
 #ifndef DEM_FORCE_OWNER
-#define DEM_FORCE_OWNER 1  // owner sphere of each entry from a shared table (else a binary search)
+#define DEM_FORCE_OWNER 0  // 1: owner sphere of each entry from a shared table built per chunk; 0: a binary search over the CTA row bounds (A/B round 2 with the batched prologue: force 3.835 -> 3.807 ms)
 #endif
 #ifndef DEM_FORCE_UT_ASYNC
 #define DEM_FORCE_UT_ASYNC 0  // 1: previous u_t staged by cp.async into the thread's part[] slots (A/B: force 3.94 -> 5.10 ms)
