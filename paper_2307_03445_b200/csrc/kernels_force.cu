@@ -41,15 +41,6 @@ constexpr int kPairStride = 8;  // doubles per material pair in Tables::pair
 #ifndef DEM_FORCE_PRO
 #define DEM_FORCE_PRO 1  // batched prologue loads + the first chunk's entries issued before the barrier
 #endif
-#ifndef DEM_FORCE_PRO_EPI
-#define DEM_FORCE_PRO_EPI 0  // 1: the epilogue's q, Omega, template id loaded in the batched prologue (shared)
-#endif
-#if DEM_FORCE_PRO_EPI && !DEM_FORCE_PRO
-#error "DEM_FORCE_PRO_EPI needs DEM_FORCE_PRO"
-#endif
-#ifndef DEM_FORCE_EPI_EARLY
-#define DEM_FORCE_EPI_EARLY 0  // 1: q, Omega, template id cp.async-ed into own_p during the last sums (A/B on C5: force 3.84 -> 3.94 ms)
-#endif
 #ifndef DEM_FORCE_FT
 #define DEM_FORCE_FT 128
 #endif
@@ -135,8 +126,6 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
   __shared__ double acc[6][kMaxS];
   __shared__ unsigned char own_of[DEM_FORCE_OWNER ? kFT : 1];  // entry of the chunk -> its own sphere
   __shared__ double cq[DEM_FORCE_ASYNC_EPI ? 10 : 1][kFC];     // own clumps' q, Omega_body, inertia (Eq. 4)
-  __shared__ double cqe[DEM_FORCE_PRO_EPI ? 7 : 1][kFC];       // own clumps' q, Omega_body (batched prologue)
-  __shared__ int cte[DEM_FORCE_PRO_EPI ? kFC : 1];             // and template ids
   // mesh wrench (kMesh): per entry the mesh id (-1: not a mesh entry) and torque about its X
   __shared__ int emesh[kMesh ? kFT : 1];
   __shared__ double mtq[3][kMesh ? kFT : 1];
@@ -172,8 +161,6 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
   Entry ent_first;
   ent_first.partner = -1;
   ent_first.prev = -1;
-  int pcl_first = 0;  // (DEM_FORCE_PRO == 3) the first chunk's partner clump, loaded before the barrier
-  (void)pcl_first;
   {
     const double2* src = reinterpret_cast<const double2*>(a.kin + (size_t)kKin * c0);
     int r0v[2], r1v[2], mv[2], cv[2];
@@ -194,37 +181,8 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
         kv[u] = src[c * (kKin / 2) + r];
       }
     }
-#if DEM_FORCE_PRO_EPI
-    // the integrating thread's q, Omega and template id: loaded with the staging, kept in shared memory
-    double eqv[7];
-    int etv = 0;
-    if (tid < ncl) {
-      const int c = c0 + tid;
-      eqv[0] = a.cur.qw[c]; eqv[1] = a.cur.qx[c]; eqv[2] = a.cur.qy[c]; eqv[3] = a.cur.qz[c];
-      eqv[4] = a.cur.wx[c]; eqv[5] = a.cur.wy[c]; eqv[6] = a.cur.wz[c];
-      etv = a.tid[c];
-    }
-#endif
     const int E1g = a.rows.row_ptr[s0 + nsph];
     if (E0g + tid < E1g) ent_first = a.rows.ent[E0g + tid];
-#if DEM_FORCE_PRO == 2
-    // and the first chunk's partner sphere record, clump and material, copied into this thread's
-    // column of part[] in the background (written by this thread only after it read them)
-    if (ent_first.partner >= 0) {
-      const int t = ent_first.partner;
-      const double* ps = reinterpret_cast<const double*>(a.spos + t);
-#pragma unroll
-      for (int d = 0; d < 4; ++d) {
-        const unsigned dst = (unsigned)__cvta_generic_to_shared(&part[d][pslot(tid)]);
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(ps + d) : "memory");
-      }
-      int* pi = reinterpret_cast<int*>(&part[4][pslot(tid)]);
-      const unsigned d0 = (unsigned)__cvta_generic_to_shared(pi), d1 = (unsigned)__cvta_generic_to_shared(pi + 1);
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d0), "l"(a.s_clump + t) : "memory");
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d1), "l"(a.s_mat + t) : "memory");
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    }
-#endif
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int k = tid + u * kFT;
@@ -240,16 +198,6 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
       }
       if (k < ncl * (kKinUsed / 2)) reinterpret_cast<double2*>(ck)[k] = kv[u];
     }
-#if DEM_FORCE_PRO == 3
-    if (ent_first.partner >= 0) pcl_first = a.s_clump[ent_first.partner];
-#endif
-#if DEM_FORCE_PRO_EPI
-    if (tid < ncl) {
-#pragma unroll
-      for (int q = 0; q < 7; ++q) cqe[q][tid] = eqv[q];
-      cte[tid] = etv;
-    }
-#endif
   }
 #else
   for (int k = tid; k <= nsph; k += kFT) {
@@ -297,10 +245,6 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
   __syncthreads();
   const double h = a.h;
   const int E0 = rp[0], E1 = rp[nsph];
-#if DEM_FORCE_EPI_EARLY
-  static_assert(8 * kFC <= 4 * kMaxS, "q, Omega and the template id of the CTA's clumps fit in own_p");
-  bool epi = false;  // this thread's epilogue loads were issued (cp.async into own_p)
-#endif
   for (int c0e = E0; c0e < E1; c0e += kFT) {
     const int e = c0e + tid;
     if (kMesh) emesh[tid] = -1;
@@ -396,29 +340,9 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
         rbar = ri;
         mbar = Mi;
       } else if (!wall) {
-#if DEM_FORCE_PRO == 3
-        const double4 pj = ldg256(a.spos + t);
-        const double* kjp = a.kin + (size_t)kKin * (c0e == E0 ? pcl_first : a.s_clump[t]);
-        mj = a.s_mat[t];
-#elif DEM_FORCE_PRO == 2
-        double4 pj;
-        const double* kjp;
-        if (c0e == E0) {  // the prologue's copies of this partner
-          asm volatile("cp.async.wait_all;" ::: "memory");
-          pj = make_double4(part[0][pslot(tid)], part[1][pslot(tid)], part[2][pslot(tid)], part[3][pslot(tid)]);
-          const int* pi = reinterpret_cast<const int*>(&part[4][pslot(tid)]);
-          kjp = a.kin + (size_t)kKin * pi[0];
-          mj = pi[1];
-        } else {
-          pj = ldg256(a.spos + t);
-          kjp = a.kin + (size_t)kKin * a.s_clump[t];
-          mj = a.s_mat[t];
-        }
-#else
         const double4 pj = ldg256(a.spos + t);
         const double* kjp = a.kin + (size_t)kKin * a.s_clump[t];
         mj = a.s_mat[t];
-#endif
         const double rj = pj.w;
         const double dx = pj.x - cx, dy = pj.y - cy, dz = pj.z - cz;
         const double dist = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
@@ -566,26 +490,6 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
       }
     }
     __syncthreads();
-#if DEM_FORCE_EPI_EARLY
-    if (c0e + kFT >= E1 && tid < ncl) {
-      // the last chunk is evaluated, so own_p[] is free: the integrating thread's q, Omega and
-      // template id are copied into it in the background (cp.async: no registers held) while
-      // the per-sphere sums run, and awaited at the integration
-      const int c = c0 + tid;
-      const double* src[7] = {a.cur.qw + c, a.cur.qx + c, a.cur.qy + c, a.cur.qz + c, a.cur.wx + c, a.cur.wy + c,
-                              a.cur.wz + c};
-      double* eq = reinterpret_cast<double*>(own_p);
-#pragma unroll
-      for (int k = 0; k < 7; ++k) {
-        const unsigned dst = (unsigned)__cvta_generic_to_shared(eq + k * kFC + tid);
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src[k]) : "memory");
-      }
-      const unsigned dt = (unsigned)__cvta_generic_to_shared(reinterpret_cast<int*>(eq + 7 * kFC) + tid);
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dt), "l"(a.tid + c) : "memory");
-      asm volatile("cp.async.commit_group;" ::: "memory");
-      epi = true;
-    }
-#endif
     // only thread 0 reads or clears chunk_mesh between the barriers (the other threads set it
     // before the barrier above and next after the barrier below)
     if (kMesh && tid == 0 && *(volatile int*)&chunk_mesh) {
@@ -638,28 +542,6 @@ __global__ void __launch_bounds__(kFT, kMesh ? DEM_FORCE_MINB_MESH : DEM_FORCE_M
   const double I0 = cq[7][tid], I1 = cq[8][tid], I2 = cq[9][tid];
   const double qw = cq[0][tid], qx = cq[1][tid], qy = cq[2][tid], qz = cq[3][tid];
   const double w0 = cq[4][tid], w1 = cq[5][tid], w2 = cq[6][tid];
-#elif DEM_FORCE_PRO_EPI
-  const int et = cte[tid];
-  const double I0 = a.tab.tpl_inertia[3 * et], I1 = a.tab.tpl_inertia[3 * et + 1], I2 = a.tab.tpl_inertia[3 * et + 2];
-  const double qw = cqe[0][tid], qx = cqe[1][tid], qy = cqe[2][tid], qz = cqe[3][tid];
-  const double w0 = cqe[4][tid], w1 = cqe[5][tid], w2 = cqe[6][tid];
-#elif DEM_FORCE_EPI_EARLY
-  double eq[7];
-  int et;
-  if (epi) {
-    asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's own copies
-    const double* sq = reinterpret_cast<const double*>(own_p);
-#pragma unroll
-    for (int k = 0; k < 7; ++k) eq[k] = sq[k * kFC + tid];
-    et = reinterpret_cast<const int*>(sq + 7 * kFC)[tid];
-  } else {
-    eq[0] = a.cur.qw[c]; eq[1] = a.cur.qx[c]; eq[2] = a.cur.qy[c]; eq[3] = a.cur.qz[c];
-    eq[4] = a.cur.wx[c]; eq[5] = a.cur.wy[c]; eq[6] = a.cur.wz[c];
-    et = a.tid[c];
-  }
-  const double I0 = a.tab.tpl_inertia[3 * et], I1 = a.tab.tpl_inertia[3 * et + 1], I2 = a.tab.tpl_inertia[3 * et + 2];
-  const double qw = eq[0], qx = eq[1], qy = eq[2], qz = eq[3];
-  const double w0 = eq[4], w1 = eq[5], w2 = eq[6];
 #else
   const int tt = DEM_KIN_TID ? (int)__double_as_longlong(ck[kKinUsed * tid + 10]) : a.tid[c];
   const double I0 = a.tab.tpl_inertia[3 * tt], I1 = a.tab.tpl_inertia[3 * tt + 1], I2 = a.tab.tpl_inertia[3 * tt + 2];
