@@ -280,20 +280,7 @@ static_assert(kSmallDense <= 32, "the small-bin pass loads one member per lane")
 #ifndef DEM_PAIRS_PIPE
 #define DEM_PAIRS_PIPE 1
 #endif
-// fp32 pre-test of the flat path (DEM_PAIRS_F32): members staged as float (x, y, z) relative to
-// one member's centre and w = r + margin/2 + eta, eta = 1e-5 (|x| + |y| + |z| + r + margin) of the
-// relative coordinates — a slack ~50x the worst fp32 rounding of |d| and of r_a + r_b, so a pair
-// the exact fp64 predicate (R14) accepts always passes |d~|^2 <= (w_a + w_b)^2.  The passes test
-// 16-byte records (half the shared-memory wavefronts of the 32-byte fp64 ones) in fp32, and the
-// exact fp64 predicate runs once per buffered pair at the flush, on the records in global memory:
-// the candidate set stays bit-exact.
-#ifndef DEM_PAIRS_F32
-#define DEM_PAIRS_F32 0  // A/B on C5: pairs 4.62 -> 5.51 ms (the fp32 pre-test costs more issue than the wavefronts it saves)
-#endif
 struct Members {
-#if DEM_PAIRS_F32
-  float4 f[kFlatMax];  // relative centre + inflated radius (flat path)
-#endif
 #if DEM_PAIRS_SOA
   // x, y | z, r in two 16-byte arrays: consecutive members hit consecutive bank quads (a
   // 32-byte double4 stride makes the 128-bit loads of 8 consecutive members conflict 2-way)
@@ -305,18 +292,6 @@ struct Members {
   __device__ __forceinline__ void put(int q, const double4& p) {
     xy[q] = make_double2(p.x, p.y);
     zr[q] = make_double2(p.z, p.w);
-  }
-  // a member of the flat path: its fp32 pre-test record relative to (rx, ry, rz) (DEM_PAIRS_F32)
-  __device__ __forceinline__ void stage(int q, const double4& p, double rx, double ry, double rz, double margin) {
-#if DEM_PAIRS_F32
-    const float fx = __double2float_rn(p.x - rx), fy = __double2float_rn(p.y - ry), fz = __double2float_rn(p.z - rz);
-    const float fr = __double2float_rn(p.w + 0.5 * margin);
-    const float eta = 1e-5f * (fabsf(fx) + fabsf(fy) + fabsf(fz) + fr + __double2float_ru(margin));
-    f[q] = make_float4(fx, fy, fz, fr + eta);
-    if (DEM_PAIRS_F32 == 2) put(q, p);  // the fp64 record for the exact test in the pass
-#else
-    put(q, p);
-#endif
   }
 #else
   double4 p[kFlatMax];  // x, y, z, r
@@ -372,15 +347,6 @@ __device__ __forceinline__ void decode_tri(int p, int& i, int& j) {
   i = p - jj * (jj - 1) / 2;
 }
 
-// the distance part of the candidate predicate (R14), explicit roundings
-template <bool kMargin>
-__device__ __forceinline__ bool exact_pair(double margin, const double4& pi, const double4& pj) {
-  const double dx = sub(pj.x, pi.x), dy = sub(pj.y, pi.y), dz = sub(pj.z, pi.z);
-  const double d2 = add(add(mul(dx, dx), mul(dy, dy)), mul(dz, dz));
-  const double s = kMargin ? add(add(pi.w, pj.w), margin) : add(pi.w, pj.w);
-  return d2 <= mul(s, s);
-}
-
 // one directed candidate: partner t in slot `slot` of own's row (slot -1: own is a ghost,
 // evaluated by its owner); a slot beyond the row width asks the host for wider rows
 __device__ __noinline__ void slot_overflow(Ctl* ctl, int* abort, int slot) {
@@ -388,8 +354,7 @@ __device__ __noinline__ void slot_overflow(Ctl* ctl, int* abort, int slot) {
   atomicExch(abort, 1);
 }
 
-// what a flush needs of the step arguments, by value (a non-inlined flush taking the kernel's
-// parameter block by reference would copy all of it to the stack)
+// what a flush needs of the step arguments
 struct FlushCtx {
   int* row_cnt;
   int* slots;
@@ -418,45 +383,19 @@ __device__ __forceinline__ void put_slot(const FlushCtx& a, int own, int slot, i
 // Flush a warp's buffered pairs: the per-row counting atomics that hand out each entry's
 // slot in its row (walls come first), 2 x kPairBuf/32 independent ones per lane so their
 // latency overlaps, then both directed candidates written into the spheres' slot lists.
-#ifndef DEM_FLUSH_NOINLINE
-#define DEM_FLUSH_NOINLINE 0  // 1: the flush's gathers and exact tests kept out of the pass loop's registers
-#endif
-#if DEM_FLUSH_NOINLINE
-#define DEM_FLUSH_ATTR __noinline__
-#else
-#define DEM_FLUSH_ATTR __forceinline__
-#endif
 template <bool kMargin>
-__device__ DEM_FLUSH_ATTR void flush_pairs(const FlushCtx a, const int2* bf, int n, int lane) {
+__device__ __forceinline__ void flush_pairs(const FlushCtx a, const int2* bf, int n, int lane) {
   __syncwarp();
   if (n == 0) return;
   constexpr int kPer = kPairBuf / 32;
   int2 v[kPer];
   int sa[kPer], sb[kPer];
   long long ka[kPer], kb[kPer];
-#if DEM_PAIRS_F32 == 1
-  // the exact predicate (R14) of each buffered pair, on its two records in global memory (the
-  // passes only applied the conservative fp32 pre-test; the clump tests are done)
-  bool ok[kPer];
 #pragma unroll
   for (int j = 0; j < kPer; ++j) {
     const int k = lane + 32 * j;
-    ok[j] = false;
     if (k < n) {
       v[j] = bf[k];
-      ok[j] = exact_pair<kMargin>(a.margin, ldg256(a.dpos + v[j].x), ldg256(a.dpos + v[j].y));
-    }
-  }
-#endif
-#pragma unroll
-  for (int j = 0; j < kPer; ++j) {
-    const int k = lane + 32 * j;
-#if DEM_PAIRS_F32 == 1
-    if (ok[j]) {
-#else
-    if (k < n) {
-      v[j] = bf[k];
-#endif
       sa[j] = v[j].x < a.ns_own ? atomicAdd(&a.row_cnt[v[j].x], 1) : -1;  // -1: ghost, no row
       sb[j] = v[j].y < a.ns_own ? atomicAdd(&a.row_cnt[v[j].y], 1) : -1;
       if (DEM_SLOT_KEYS) {  // the partners' keys, gathered here beside the atomics' latency
@@ -467,11 +406,7 @@ __device__ DEM_FLUSH_ATTR void flush_pairs(const FlushCtx a, const int2* bf, int
   }
 #pragma unroll
   for (int j = 0; j < kPer; ++j) {
-#if DEM_PAIRS_F32 == 1
-    if (ok[j]) {
-#else
     if (lane + 32 * j < n) {
-#endif
       put_slot(a, v[j].x, sa[j], v[j].y, DEM_SLOT_KEYS ? kb[j] : 0);
       put_slot(a, v[j].y, sb[j], v[j].x, DEM_SLOT_KEYS ? ka[j] : 0);
     }
@@ -524,24 +459,7 @@ __constant__ float c_rcp[kFlatMax + 8] = {1.0f,      DEM_R8(1),  DEM_R8(9),  DEM
 template <bool kGhosts, bool kMargin>
 __device__ __forceinline__ bool flat_pair(const StepArgs& a, const Members& A, int i, int j, int& ia, int& ib,
                                           bool valid = true) {
-#if DEM_PAIRS_F32
-  // different clumps, at least one owned, and the conservative fp32 pre-test on the 16-byte records
-  const int ci = A.clump[i], cj = A.clump[j];
-  const float4 u = A.f[i], v = A.f[j];
-  const float dx = v.x - u.x, dy = v.y - u.y, dz = v.z - u.z;
-  const float s = u.w + v.w;
-  const float d2 = dx * dx + dy * dy + dz * dz;
-  // (bitwise &: no short-circuit branch around the arithmetic)
-  bool hit = valid & (ci != cj) & (!kGhosts || min(ci, cj) < a.n_own) & (d2 <= s * s);
-#if DEM_PAIRS_F32 == 2
-  // the exact predicate (R14) on the fp64 records, for the few lanes the pre-test let through
-  if (hit) hit = exact_pair<kMargin>(a.margin, A.get(i), A.get(j));
-#endif
-  if (hit) {
-    ia = A.item[i];
-    ib = A.item[j];
-  }
-#elif DEM_PAIRS_SPLIT
+#if DEM_PAIRS_SPLIT
   const int2 mi = make_int2(A.clump[i], 0), mj = make_int2(A.clump[j], 0);
   const bool hit = valid & candidate<kGhosts, kMargin>(a, mi, mj, A.get(i), A.get(j));
   if (hit) {
@@ -797,10 +715,6 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
           v1 = 1ull << (8 * pos1);
 #endif
         }
-        // reference point of the fp32 records: member 0's centre (m >= 2, so lane 0 holds one)
-        const double rfx = DEM_PAIRS_F32 ? __shfl_sync(0xffffffffu, u0.x, 0) : 0.0;
-        const double rfy = DEM_PAIRS_F32 ? __shfl_sync(0xffffffffu, u0.y, 0) : 0.0;
-        const double rfz = DEM_PAIRS_F32 ? __shfl_sync(0xffffffffu, u0.z, 0) : 0.0;
 #if DEM_PAIRS_BALLOT
         // Group order by bit-plane ballots: A_k (B_k) = lanes of the first (second) member half
         // whose position has bit k set.  The size of position p is the popcount of the lanes whose
@@ -835,13 +749,13 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
         if (lane < m) {
           const int q = __popc(below(V0, A0, A1, A2, pos0)) + __popc(below(V1, B0, B1, B2, pos0)) +
                         __popc(at(V0, A0, A1, A2, pos0) & lt);
-          A.stage(q, u0, rfx, rfy, rfz, a.margin);
+          A.put(q, u0);
           A.meta_put(q, mt0);
         }
         if (lane + 32 < m) {
           const int q = __popc(below(V0, A0, A1, A2, pos1)) + __popc(below(V1, B0, B1, B2, pos1)) +
                         __popc(at(V0, A0, A1, A2, pos1)) + __popc(at(V1, B0, B1, B2, pos1) & lt);
-          A.stage(q, u1, rfx, rfy, rfz, a.margin);
+          A.put(q, u1);
           A.meta_put(q, mt1);
         }
 #else
@@ -857,12 +771,12 @@ __global__ void __launch_bounds__(kPairWarps * 32, DEM_PAIRS_MINB) k_pairs(StepA
         __syncwarp();
         if (lane < m) {
           const int q = byte_of(st, pos0) + byte_of(x0 - v0, pos0);
-          A.stage(q, u0, rfx, rfy, rfz, a.margin);
+          A.put(q, u0);
           A.meta_put(q, mt0);
         }
         if (lane + 32 < m) {
           const int q = byte_of(st, pos1) + byte_of(t0, pos1) + byte_of(x1 - v1, pos1);
-          A.stage(q, u1, rfx, rfy, rfz, a.margin);
+          A.put(q, u1);
           A.meta_put(q, mt1);
         }
 #endif
